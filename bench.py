@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the mini-batch ego-network generator (seeds -> blocks + features).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one pass of the whole hot path over one mini-batch: sample every hop
+(sampling + compaction kernels) and gather the input vertices' feature rows.
+Inputs (graph shard, feature shard, the seeds of every step) are resident in HBM
+before the timed region.  Each rank samples its own batches (global batch
+g = b * N + rank); the graph and features are range-sharded over the N GPUs and
+peer shards are read over NVLink.  Timing: W untimed warm-up steps, then K steps
+bracketed by barrier + synchronize, CUDA events on the context's stream, max over
+ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain single-threaded C) on the
+host, on the same workload and metric (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = ("sampled edges/sec + mini-batches/sec (seeds→blocks+features) at 1/2/4/8 B200; gather GB/s")
+UNIT = "sampled edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def workload(cfg, world):
+    return {"workload": f"{cfg.name}: {cfg.description}", "batch_per_rank": cfg.batch, "fanouts": cfg.fanouts,
+            "n_vertices": int(cfg.vt_counts.sum()), "n_edges": int(sum(r[3] for r in cfg.rels)),
+            "ranks": world, "partition": "per-type vertex range, floor(p*N_t/P)",
+            "l2": "inputs larger than L2 (feature store %.2f GB, random rows)" % (
+                sum(cfg.row_bytes(u) * int(cfg.vt_counts[u]) for u in cfg.feats) / 1e9)}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+
+def time_oracle(cfg, graph, host_rows, batches, budget_s, min_batches=1):
+    """The oracle as it stands (single-threaded C), sample + gather per batch."""
+    import oracle
+    import synth
+    t0 = time.perf_counter()
+    n_edges = 0
+    n = 0
+    gathered = 0
+    for g in batches:
+        seeds = synth.batch_seeds(cfg, g)
+        res = oracle.sample(graph, seeds, cfg.fanouts, synth.rng_seed(cfg, g))
+        n_edges += sum(len(b.eids) for hop in res.blocks for b in hop)
+        for u in cfg.feats:
+            gathered += oracle.gather(res, cfg.vt_counts, u, host_rows[u]).nbytes
+        n += 1
+        if n >= min_batches and time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"batches": n, "seconds": dt, "edges": n_edges, "bytes": gathered}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import synth
+    graph = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    for b in range(args.warmup):
+        time_oracle(cfg, graph, rows, [b * world], 0.0)
+    per_step = []
+    edges = 0
+    nbytes = 0
+    for b in range(args.warmup, args.warmup + args.steps):
+        r = time_oracle(cfg, graph, rows, [b * world], 0.0)
+        per_step.append(r["seconds"])
+        edges += r["edges"]
+        nbytes += r["bytes"]
+    total = sum(per_step)
+    value = edges / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/bytes",
+            "data": "synthetic", "config": workload(cfg, 1),
+            "minibatches_per_s": args.steps / total, "gather_GBps": nbytes / total / 1e9,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full {cfg.name} batches (sample+compact+gather), one step "
+                                       f"= one batch, single-threaded C oracle on {cpu_model()}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(args, line)
+
+
+def emit(args, line):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(s + "\n")
+
+
+# ----------------------------------------------------------------------------- our path
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "gather_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg_name)
+    except Exception:
+        return None
+
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import synth
+    from synth.device import load_context
+    from paper_2112_15345_b200 import Context
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(dev)
+    graph = synth.build_host_graph(cfg, materialize_indices=cfg.name in ("C1", "C2", "C3"))
+    t_load = time.perf_counter()
+    ctx = Context(rank, world, local_rank, stream)
+    shard = load_context(ctx, graph, world, rank, dev)
+    if world > 1:
+        ctx.connect_peers()
+    t_load = time.perf_counter() - t_load
+    W, K = args.warmup, args.steps
+    steps = W + K
+    seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
+    rngs = [synth.rng_seed(cfg, b * world + rank) for b in range(steps)]
+    seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
+    fanouts = np.array(cfg.fanouts, np.int32)
+    # feature outputs: preallocated at the batch upper bound, reused every step
+    caps_nodes, _ = __import__("paper_2112_15345_b200").batch_caps(
+        cfg.vt_counts, [r[1] for r in cfg.rels], [r[2] for r in cfg.rels], [r[3] for r in cfg.rels],
+        [cfg.dmax(r) for r in range(cfg.n_rel)], cfg.batch, fanouts)
+    outs = [None] * cfg.n_vt
+    for u in cfg.feats:
+        dim, dt = cfg.feats[u]
+        outs[u] = torch.empty((int(caps_nodes[u]), dim), dtype=torch.float32 if dt == 0 else torch.float16,
+                              device=dev)
+    row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
+    torch.cuda.synchronize(dev)
+
+    def step(b):
+        blocks = ctx.sample_blocks(seeds_dev[b], fanouts, rngs[b])
+        ctx.gather_features(blocks, out=outs)
+        e = blocks.nnz()
+        rows = [blocks.n_inputs(u) for u in range(cfg.n_vt)]
+        blocks.free()
+        return e, rows
+
+    with torch.cuda.stream(stream):
+        for b in range(W):
+            step(b)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        ctx.profile()                                   # drain
+        ctx.set_profiling(True)
+        clocks = ClockSampler(local_rank)
+        clocks.start()
+        launches0 = ctx.kernel_launches()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record(stream)
+        edges = 0
+        gbytes = 0
+        for b in range(W, steps):
+            e, rows = step(b)
+            edges += e
+            gbytes += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = ctx.kernel_launches() - launches0
+        clk = clocks.stop()
+        ctx.set_profiling(False)
+        prof = ctx.profile()
+
+    totals = torch.tensor([ms, float(edges), float(gbytes), float(K)], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        mx = totals.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(totals[1:], op=dist.ReduceOp.SUM)
+        ms = float(mx[0])
+        edges = float(totals[1])
+    value = edges / (ms / 1e3)
+
+    # e2e: host seeds in (pinned), features out to pinned host memory, through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        pinned_seeds = [torch.from_numpy(s).pin_memory() for s in seeds_host]
+        host_outs = [None] * cfg.n_vt
+        for u in cfg.feats:
+            host_outs[u] = torch.empty(tuple(outs[u].shape), dtype=outs[u].dtype).pin_memory()
+        with torch.cuda.stream(stream):
+            for b in range(min(W, 2)):
+                bl = ctx.sample_blocks(pinned_seeds[b], fanouts, rngs[b])
+                ctx.gather_features(bl, out=host_outs)
+                bl.free()
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                torch.distributed.barrier()
+            h2d = d2h = 0
+            e_edges = 0
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for b in range(W, steps):
+                bl = ctx.sample_blocks(pinned_seeds[b], fanouts, rngs[b])
+                ctx.gather_features(bl, out=host_outs)
+                e_edges += bl.nnz()
+                h2d += pinned_seeds[b].numel() * 8
+                d2h += sum(bl.n_inputs(u) * row_bytes[u] for u in cfg.feats) + 576
+                bl.free()
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+            ems = t0.elapsed_time(t1)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ems, float(e_edges)], dtype=torch.float64, device=dev)
+            m = t.clone()
+            dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            ems, e_edges = float(m[0]), float(t[1])
+        e2e = {"value": e_edges / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
+               "d2h_bytes_per_step": d2h // K,
+               "note": "seeds from pinned host memory in, gathered feature rows out to pinned host memory "
+                       "(blocks stay device-resident), through eg_sample_blocks / eg_gather_features"}
+
+    # roofline of the gather kernel (events inside the library, on its stream, timed region)
+    peak, peak_src = load_peaks()
+    gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])
+    sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])
+    achieved = (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
+    tr = load_traffic(cfg.name)
+    roofline = {"kernel": "gather_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "algorithmic_bytes_per_launch": gbytes / K,
+                "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id)",
+                "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_batch": sample_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows_h = {u: synth.host_features(cfg, u) for u in cfg.feats} if cfg.name in ("C1", "C2", "C3") else None
+        if rows_h is not None:
+            r = time_oracle(cfg, graph, rows_h, range(1000, 100000), args.cpu_seconds)
+            cpu = {"value": r["edges"] / r["seconds"], "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": f"{r['batches']} full {cfg.name} batches (sample+compact+gather) in "
+                             f"{r['seconds']:.1f} s, single-threaded C oracle on {cpu_model()} "
+                             f"({host_cores()} cores available)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "int32 ids / raw feature bytes (%s)" % ",".join(
+                    sorted({"fp32" if cfg.feats[u][1] == 0 else "fp16" for u in cfg.feats})),
+                "data": "synthetic (seeded generator, synth/)", "config": workload(cfg, world),
+                "minibatches_per_s": world * K / (ms / 1e3),
+                "gather_GBps": (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else None,
+                "sampled_edges_per_batch": edges / (world * K),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk, "load_seconds": t_load, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+        emit(args, line)
+    ctx.close()
+    del shard
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if world != args.gpus:
+        world = args.gpus if world == 1 and args.gpus == 1 else world
+    import synth
+    cfg = synth.config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    run_ours(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/*
+ * egonet.h -- C ABI of the B200-native mini-batch ego-network generator
+ * (the data-parallel hot path of DistDGLv2, arxiv 2112.15345).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n
+ * (the reference is not needed at run time; the citations are for readers).
+ *
+ * The three calls follow the paper's problem statement:
+ *   eg_load_partition   a partitioned heterogeneous graph: per edge type a CSC,
+ *                       per vertex type a range of owned vertices and their
+ *                       feature rows (homogenized type-contiguous ids P:409-415;
+ *                       KVStore id space per type with a partition policy P:465-475).
+ *   eg_sample_blocks    vertex-wise neighbour sampling from seeds, at most
+ *                       fanout[hop][etype] in-neighbours per target,
+ *                       hop by hop with the frontier = unique set,
+ *                       each hop compacted into a block.
+ *   eg_gather_features  the feature rows of the input vertices of the blocks
+ *                       (CPU/GPU feature copy P:563-565; KVStore pull S:217-225).
+ *
+ * Conventions
+ *   - gid = homogenized global vertex id: gid = off[t] + tid, off = prefix sums of
+ *     vt_counts; tid = type-local id.  All gids must be < 2^31.
+ *   - Relation r has src type s(r) and dst type t(r).  Its CSC is the in-edge
+ *     list of each dst vertex (CSC = grouped by dst), src ids are TYPE-LOCAL tids.
+ *   - Partition: vertex type t is split in ranges bounds[t][p] <= tid <
+ *     bounds[t][p+1]; rank p owns the CSC rows of its dst vertices (edge owner =
+ *     dst owner) and the feature rows of its vertices.
+ *   - All calls are stream-ordered on the context's stream.  Device pointers are
+ *     CUDA device pointers of the context's device; "host" marks host pointers.
+ *   - Results are defined by the key32 reading of the paper and are
+ *     independent of world size, stream overlap and launch configuration.
+ *
+ * Errors: every call returns eg_status; on failure eg_last_error() has a message.
+ *   EG_EINVAL bad argument (checked before any device work unless stated),
+ *   EG_ERANGE a vertex id outside its id space (range error before any
+ *             transfer), EG_ENOMEM device allocation failed, EG_ECUDA a CUDA error
+ *   (the context becomes unusable: EG_ESTATE thereafter), EG_EPEER peer shard
+ *   metadata inconsistent.
+ */
+#ifndef EGONET_H
+#define EGONET_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define EG_API __attribute__((visibility("default")))
+#else
+#define EG_API
+#endif
+
+#define EG_MAX_VT 8
+#define EG_MAX_REL 8
+#define EG_MAX_RANKS 8
+#define EG_MAX_HOPS 8
+
+typedef enum {
+    EG_OK = 0,
+    EG_EINVAL = -1,
+    EG_ERANGE = -2,
+    EG_ENOMEM = -3,
+    EG_ECUDA = -4,
+    EG_EPEER = -6,
+    EG_ESTATE = -7
+} eg_status;
+
+typedef struct eg_ctx eg_ctx;
+typedef struct eg_blocks eg_blocks;
+
+/* One relation's shard on this rank (borrowed, device memory, must outlive the ctx). */
+typedef struct {
+    int32_t src_vt, dst_vt;
+    const int64_t *indptr;   /* device, n_local_dst + 1 entries, indptr[0] == 0,
+                                n_local_dst = bounds[dst_vt][rank+1] - bounds[dst_vt][rank] */
+    const int32_t *indices;  /* device, n_local_edges src tids (type s(r)) */
+    int64_t n_local_edges;   /* == indptr[n_local_dst] */
+    int64_t edge_base;       /* global CSC position of local edge 0 (edge ids = base + local pos) */
+} eg_relation;
+
+/* One vertex type's feature shard on this rank (borrowed, device memory). */
+typedef struct {
+    const void *rows;        /* device, n_local_rows x row_bytes, row-major; NULL: no features */
+    int64_t row_bytes;       /* multiple of 16 (or 0 when rows == NULL) */
+} eg_features;
+
+/* A block (hop h) as host struct of device pointers.  hop 0 is the seeds' block
+ * (DGL's list order is the reverse).  dst_nodes[u] is a prefix of src_nodes[u]
+ * (dst-in-src convention).  indptr[r] has n_dst[t(r)] + 1 entries (starting at
+ * 0); indices[r] are local ids into src_nodes[s(r)]; eids[r] are positions in
+ * the relation's unsharded CSC. */
+typedef struct {
+    int32_t hop, n_vt, n_rel, _pad;
+    const int64_t *dst_nodes[EG_MAX_VT];
+    int64_t n_dst[EG_MAX_VT];
+    const int64_t *src_nodes[EG_MAX_VT];
+    int64_t n_src[EG_MAX_VT];
+    const int32_t *indptr[EG_MAX_REL];
+    const int32_t *indices[EG_MAX_REL];
+    const int64_t *eids[EG_MAX_REL];
+    int64_t nnz[EG_MAX_REL];
+} eg_block_view;
+
+/* Library version string. */
+EG_API const char *eg_version(void);
+
+/* Create a context for rank `rank` of `world` (1 <= world <= EG_MAX_RANKS) on CUDA
+ * device `device`; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Fails with EG_ECUDA when no usable sm_100 device is present. */
+EG_API eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, eg_ctx **out);
+
+/* Change the stream subsequent calls are ordered on. */
+EG_API eg_status eg_set_stream(eg_ctx *ctx, void *stream);
+
+/* Load this rank's shard.  vt_counts: host [n_vt] (N_t);
+ * bounds: host [n_vt][world+1] non-decreasing with bounds[t][0]=0 and
+ * bounds[t][world]=N_t, or NULL for the fixed policy bounds[t][p] = floor(p*N_t/world);
+ * rels: host [n_rel]; feats: host [n_vt].  The buffers are BORROWED (not copied).
+ * Validates shapes and ranges of the metadata; device contents are trusted.
+ * Allocates the per-context compaction state (4 B per global vertex + a bitmap). */
+EG_API eg_status eg_load_partition(eg_ctx *ctx, int32_t n_vt, const int64_t *vt_counts, const int64_t *bounds,
+                            int32_t n_rel, const eg_relation *rels, const eg_features *feats);
+
+/* world > 1 only.  Peer mapping over NVLink: every rank exports a host blob
+ * describing its shard (CUDA IPC handles of the borrowed buffers + metadata),
+ * the caller all-gathers the blobs with its own transport (e.g. a torch process
+ * group), and every rank imports all of them.  After import, the kernels read
+ * peer CSC rows and feature rows directly over NVLink / NVSwitch.
+ * eg_export_shard: buf == NULL returns the size in *len.
+ * eg_import_shards: blobs = world blobs, `stride` bytes apart, in rank order.
+ * EG_EPEER when the peers' metadata disagrees (types, counts, bounds, edge bases). */
+EG_API eg_status eg_export_shard(const eg_ctx *ctx, void *buf, size_t *len);
+EG_API eg_status eg_import_shards(eg_ctx *ctx, const void *blobs, size_t stride);
+
+/* Single-process alternative to export/import: attach the shard of `peer`, a
+ * context of the same world loaded in this process (same device or another
+ * device with peer access).  Once every other rank is attached the context is
+ * ready.  Lets one process drive several ranks (and tests emulate world > 1 on
+ * one GPU). */
+EG_API eg_status eg_attach_peer(eg_ctx *ctx, const eg_ctx *peer);
+
+/* Sample L = n_hops blocks from `seeds` (gids, unique, any vertex types, caller
+ * order; host or device pointer; n_seeds may be 0).  fanouts: host [n_hops][n_rel],
+ * row 0 = hop at the seeds; -1 = all in-neighbours, 0 = none, k > 0 = at most k,
+ * uniformly without replacement, per edge type.  rng_seed keys the
+ * draws: the result is a pure function of (graph, seeds, fanouts, rng_seed).
+ * EG_ERANGE: a seed outside [0, N_total); EG_EINVAL: duplicate seeds, bad fanout,
+ * n_hops outside [1, EG_MAX_HOPS].  The id checks run on the device; the call
+ * returns after the batch's sizes are known (one device->host read). */
+EG_API eg_status eg_sample_blocks(eg_ctx *ctx, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
+                           const int32_t *fanouts, uint64_t rng_seed, eg_blocks **out);
+
+/* Host view of block `hop` (0 <= hop < n_hops).  Pointers stay valid until
+ * eg_blocks_free. */
+EG_API eg_status eg_block_view_get(const eg_blocks *blocks, int32_t hop, eg_block_view *out);
+
+/* n_hops of a blocks handle, and the number of input vertices (src nodes of
+ * the last block) of type u. */
+EG_API int32_t eg_blocks_n_hops(const eg_blocks *blocks);
+EG_API int64_t eg_blocks_n_inputs(const eg_blocks *blocks, int32_t u);
+
+/* Gather the feature rows of the input vertices (src nodes of the last block):
+ * out[u] (host array [n_vt]) points to n_inputs(u) x row_bytes(u) bytes, device
+ * or host memory; NULL skips u.  Rows are copied verbatim in input order
+ * (S:217-225); rows owned by peers are read over NVLink.  Host out pointers are
+ * staged through device memory and the call synchronizes. */
+EG_API eg_status eg_gather_features(eg_ctx *ctx, const eg_blocks *blocks, void *const *out);
+
+/* Release a blocks handle (stream-ordered on the context's stream). */
+EG_API eg_status eg_blocks_free(eg_blocks *blocks);
+
+/* Destroy the context (closes peer mappings, frees its state; the borrowed
+ * shard buffers are untouched). */
+EG_API eg_status eg_destroy(eg_ctx *ctx);
+
+/* Message of the last error on this context (thread-unsafe, never NULL). */
+EG_API const char *eg_last_error(const eg_ctx *ctx);
+
+/* Instrumentation.  When enabled, each sample/gather call records CUDA events on
+ * the context's stream around its device work; eg_get_profile synchronizes and
+ * returns {sample_ms_total, gather_ms_total, n_sample_calls, n_gather_calls}.
+ * eg_kernel_launches returns the number of kernels this context has launched. */
+EG_API eg_status eg_set_profiling(eg_ctx *ctx, int32_t enable);
+EG_API eg_status eg_get_profile(eg_ctx *ctx, double out[4]);
+EG_API int64_t eg_kernel_launches(const eg_ctx *ctx);
+
+/* Host-only helpers (no device work; usable without a GPU). */
+/* bounds[p] = floor(p * n / world), p = 0..world. */
+EG_API eg_status eg_range_bounds(int64_t n, int32_t world, int64_t *bounds);
+/* Upper bound of the nodes / edges of a batch (what eg_sample_blocks allocates):
+ * caps_nodes [n_vt] for the input vertices, caps_edges [n_hops][n_rel]. */
+EG_API eg_status eg_batch_caps(int32_t n_vt, const int64_t *vt_counts, int32_t n_rel, const int32_t *rel_src_vt,
+                        const int32_t *rel_dst_vt, const int64_t *rel_n_edges, const int64_t *rel_max_degree,
+                        int64_t n_seeds, int32_t n_hops, const int32_t *fanouts, int64_t *caps_nodes,
+                        int64_t *caps_edges);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EGONET_H */

@@ -1,0 +1,169 @@
+// common.cuh -- device-side descriptors and primitives of the egonet sm_100a path.
+// Product code: shares nothing with oracle/ (see DESIGN.md §1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/egonet.h"
+
+namespace eg {
+
+constexpr int kWarp = 32;
+constexpr int kSMs = 148;                 // B200
+constexpr int kChunkWords = 8192;         // bitmap words per compaction chunk
+constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
+constexpr int kScanBlocks = 256;          // blocks per relation in the two-phase scan
+constexpr int kSelCap = 512;              // candidate slots per warp (selection)
+constexpr int kSelMaxK = 112;             // fast selection path for k <= this
+
+// Error bits written by kernels into meta[kMetaErr].
+enum : int32_t { kErrSeedRange = 1, kErrSeedDup = 2, kErrCapacity = 4 };
+
+// One relation as the kernels see it: per owner rank, the CSC shard pointers
+// (own shard or a peer's, mapped over NVLink).
+struct RelDev {
+    const int64_t *indptr[EG_MAX_RANKS];
+    const int32_t *indices[EG_MAX_RANKS];
+    int64_t edge_base[EG_MAX_RANKS];
+    int32_t src_vt, dst_vt;
+};
+
+struct GraphDev {
+    int32_t n_vt, n_rel, world, rank;
+    int64_t off[EG_MAX_VT + 1];                       // gid = off[t] + tid
+    int64_t bounds[EG_MAX_VT][EG_MAX_RANKS + 1];      // owned tid ranges per rank
+    int64_t boff[EG_MAX_VT + 1];                      // bitmap bit offset per type (chunk aligned)
+    RelDev rel[EG_MAX_REL];
+};
+
+struct FeatDev {
+    const uint8_t *rows[EG_MAX_VT][EG_MAX_RANKS];
+    int64_t row_bytes[EG_MAX_VT];
+};
+
+// Device counters of one batch (int32 slots in one small array).
+//   nodes(l, u): |level l of type u|, l = 0 seeds, l = h+1 src nodes of block h
+//   nnz(h, r):   edges of relation r in block h
+constexpr int kMetaNodes = 0;
+constexpr int kMetaNnz = kMetaNodes + (EG_MAX_HOPS + 1) * EG_MAX_VT;
+constexpr int kMetaErr = kMetaNnz + EG_MAX_HOPS * EG_MAX_REL;
+constexpr int kMetaSize = kMetaErr + 8;
+
+// Everything a hop's kernels touch.
+struct HopDev {
+    int32_t h;
+    uint32_t seed_lo, seed_hi;
+    int32_t fanout[EG_MAX_REL];
+    int64_t *nodes[EG_MAX_VT];       // cumulative node array per type
+    int32_t *indptr[EG_MAX_REL];     // block CSC per relation
+    int32_t *indices[EG_MAX_REL];
+    int64_t *eids[EG_MAX_REL];
+    uint32_t *src[EG_MAX_REL];       // sampled src gids (scratch)
+    int32_t *meta;                   // batch counters
+    int32_t *partial;                // scan scratch [EG_MAX_REL][kScanBlocks]
+    int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
+    uint32_t *bitmap;                // new-vertex bitmap
+    int32_t *chunk_cnt;              // popcount per bitmap chunk
+    int32_t cap_nodes[EG_MAX_VT];    // capacity of nodes[u]
+};
+
+__device__ __forceinline__ int32_t *meta_nodes(int32_t *meta, int l) { return meta + kMetaNodes + l * EG_MAX_VT; }
+__device__ __forceinline__ int32_t *meta_nnz(int32_t *meta, int h) { return meta + kMetaNnz + h * EG_MAX_REL; }
+
+// ------------------------------------------------------------------ ids / partition
+
+__device__ __forceinline__ int owner_of(const GraphDev &g, int t, int64_t tid)
+{
+    int p = 0;
+    while (p < g.world - 1 && tid >= g.bounds[t][p + 1]) ++p;
+    return p;
+}
+
+// ------------------------------------------------------------------ warp / block scans
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v)
+{
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane_id() >= o) v += n;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide exclusive scan; returns the exclusive prefix, *total = block sum.
+// `sh` needs blockDim.x/32 + 1 slots.  All threads must call.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T *sh, T *total)
+{
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T inc = warp_incl_scan(v);
+    if (lane_id() == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        T x = lane_id() < nw ? sh[lane_id()] : T(0);
+        T xi = warp_incl_scan(x);
+        if (lane_id() < nw) sh[lane_id()] = xi - x;
+        if (lane_id() == nw - 1) sh[nw] = xi;
+    }
+    __syncthreads();
+    T res = sh[w] + inc - v;
+    *total = sh[nw];
+    __syncthreads();
+    return res;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T *sh)
+{
+    T t;
+    block_excl_scan(v, sh, &t);
+    return t;
+}
+
+// ------------------------------------------------------------------ Philox4x32-10
+// Counter-based generator of Salmon et al. (SC'11), 10 rounds.  Used only through
+// key32: ctr = {j>>2, lo32(v), hi32(v), (h<<16)|r}, key = seed.
+
+__device__ __forceinline__ void philox4x32_10(uint32_t &c0, uint32_t &c1, uint32_t &c2, uint32_t &c3,
+                                              uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+// ------------------------------------------------------------------ memory helpers
+
+__device__ __forceinline__ int4 ld_nc_v4(const void *p)
+{
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(void *p, const int4 &v)
+{
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+}  // namespace eg

@@ -1,0 +1,825 @@
+// egonet.cu -- the C ABI (include/egonet.h): context, store, per-batch orchestration.
+//
+// Per batch (eg_sample_blocks), all on the context's stream, no host sync until the
+// end (sizes live on the device; buffers are sized by host-computed upper bounds):
+//   seed_split                                  F_0 per type, pos[] of the seeds
+//   for each hop h:
+//     count -> scan                             block indptr (min(d,k) per dst)
+//     sample                                    warp per (dst, relation), key32
+//     mark -> bitcount -> emit -> relabel       frontier + compaction
+//   reset                                       pos[] back to -1
+//   one D2H of the batch counters (+ error bits)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace eg;
+
+namespace {
+
+const char *kVersion = "egonet 0.1.0 (sm_100a)";
+
+struct ShardRel {
+    int32_t src_vt, dst_vt;
+    int64_t n_local_dst, n_local_edges, edge_base, max_degree;
+    cudaIpcMemHandle_t indptr_h, indices_h;
+    int64_t indptr_off, indices_off;
+};
+
+struct ShardFeat {
+    int64_t row_bytes, n_rows;
+    cudaIpcMemHandle_t h;
+    int64_t off;
+    int32_t has;
+};
+
+struct ShardBlob {
+    uint32_t magic, version;
+    int32_t rank, world, n_vt, n_rel;
+    int64_t vt_counts[EG_MAX_VT];
+    int64_t bounds[EG_MAX_VT][EG_MAX_RANKS + 1];
+    ShardRel rel[EG_MAX_REL];
+    ShardFeat feat[EG_MAX_VT];
+};
+constexpr uint32_t kBlobMagic = 0x45474F4E;  // 'EGON'
+
+struct TimedPair {
+    cudaEvent_t a, b;
+    int kind;  // 0 sample, 1 gather
+};
+
+}  // namespace
+
+struct eg_ctx {
+    int32_t rank = 0, world = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    bool broken = false, loaded = false, peers_ready = false;
+    std::string err = "ok";
+    GraphDev g{};
+    FeatDev f{};
+    int64_t vt_counts[EG_MAX_VT] = {};
+    int64_t rel_edges_total[EG_MAX_REL] = {};
+    int64_t rel_max_degree[EG_MAX_REL] = {};
+    int64_t n_total = 0;
+    // own shard (for export)
+    eg_relation own_rel[EG_MAX_REL] = {};
+    eg_features own_feat[EG_MAX_VT] = {};
+    // compaction state
+    int32_t *pos = nullptr;
+    uint32_t *bitmap = nullptr;
+    int32_t *chunk_cnt = nullptr;
+    int32_t *partial = nullptr;
+    int32_t n_chunks = 0;
+    int32_t *h_meta = nullptr;   // pinned
+    std::vector<void *> ipc_bases;
+    uint32_t attached = 0;                          // bit p: rank p's shard is mapped
+    int64_t peer_edges[EG_MAX_RANKS][EG_MAX_REL] = {};
+    int64_t peer_ebase[EG_MAX_RANKS][EG_MAX_REL] = {};
+    int64_t peer_maxdeg[EG_MAX_RANKS][EG_MAX_REL] = {};
+    // instrumentation
+    bool prof = false;
+    std::vector<TimedPair> timed;
+    double prof_ms[2] = {0, 0};
+    int64_t prof_n[2] = {0, 0};
+    int64_t launches = 0;
+};
+
+struct eg_blocks {
+    eg_ctx *ctx = nullptr;
+    int32_t n_hops = 0, n_vt = 0, n_rel = 0;
+    void *mem = nullptr;
+    int64_t *nodes[EG_MAX_VT] = {};
+    int32_t *indptr[EG_MAX_HOPS][EG_MAX_REL] = {};
+    int32_t *indices[EG_MAX_HOPS][EG_MAX_REL] = {};
+    int64_t *eids[EG_MAX_HOPS][EG_MAX_REL] = {};
+    int32_t *meta = nullptr;  // device
+    int64_t n_nodes[EG_MAX_HOPS + 1][EG_MAX_VT] = {};
+    int64_t nnz[EG_MAX_HOPS][EG_MAX_REL] = {};
+};
+
+namespace {
+
+eg_status fail(eg_ctx *c, eg_status s, const std::string &msg)
+{
+    if (c) {
+        c->err = msg;
+        if (s == EG_ECUDA) c->broken = true;
+    }
+    return s;
+}
+
+#define EG_CUDA(ctx, call)                                                                        \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(ctx, EG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+eg_status enter(eg_ctx *c)
+{
+    if (!c) return EG_EINVAL;
+    if (c->broken) return fail(c, EG_ESTATE, "context unusable after an earlier CUDA error: " + c->err);
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return EG_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+typedef CUresult (*PFN_addr_range)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+eg_status ipc_export(eg_ctx *c, const void *p, cudaIpcMemHandle_t *h, int64_t *off)
+{
+    static PFN_addr_range fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *sym = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &sym, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !sym)
+            return fail(c, EG_ECUDA, "cuMemGetAddressRange entry point unavailable");
+        fn = (PFN_addr_range)sym;
+    }
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    if (fn(&base, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return fail(c, EG_ECUDA, "cuMemGetAddressRange failed");
+    EG_CUDA(c, cudaIpcGetMemHandle(h, (void *)base));
+    *off = (int64_t)((const char *)p - (const char *)base);
+    return EG_OK;
+}
+
+void record_start(eg_ctx *c, TimedPair *tp, int kind)
+{
+    if (!c->prof) return;
+    cudaEventCreate(&tp->a);
+    cudaEventCreate(&tp->b);
+    tp->kind = kind;
+    cudaEventRecord(tp->a, c->stream);
+}
+
+void record_end(eg_ctx *c, TimedPair *tp)
+{
+    if (!c->prof) return;
+    cudaEventRecord(tp->b, c->stream);
+    c->timed.push_back(*tp);
+}
+
+void drain_timing(eg_ctx *c)
+{
+    for (auto &tp : c->timed) {
+        cudaEventSynchronize(tp.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tp.a, tp.b);
+        c->prof_ms[tp.kind] += ms;
+        c->prof_n[tp.kind] += 1;
+        cudaEventDestroy(tp.a);
+        cudaEventDestroy(tp.b);
+    }
+    c->timed.clear();
+}
+
+// Upper bounds of a batch (host arithmetic shared with eg_batch_caps).
+eg_status compute_caps(int32_t n_vt, const int64_t *vt_counts, int32_t n_rel, const int32_t *src_vt,
+                       const int32_t *dst_vt, const int64_t *n_edges, const int64_t *maxdeg, int64_t n_seeds,
+                       int32_t n_hops, const int32_t *fanouts, int64_t capF[][EG_MAX_VT],
+                       int64_t capE[][EG_MAX_REL])
+{
+    for (int u = 0; u < n_vt; ++u) capF[0][u] = std::min(vt_counts[u], n_seeds);
+    for (int h = 0; h < n_hops; ++h) {
+        for (int u = 0; u < n_vt; ++u) capF[h + 1][u] = capF[h][u];
+        for (int r = 0; r < n_rel; ++r) {
+            const int64_t k = fanouts[h * n_rel + r];
+            const int64_t kc = k < 0 ? maxdeg[r] : std::min(k, maxdeg[r]);
+            const int64_t t = capF[h][dst_vt[r]];
+            capE[h][r] = (kc > 0 && t > 0) ? std::min(n_edges[r], (t > INT64_MAX / kc) ? INT64_MAX : t * kc) : 0;
+            capF[h + 1][src_vt[r]] += capE[h][r];
+        }
+        for (int u = 0; u < n_vt; ++u) capF[h + 1][u] = std::min(capF[h + 1][u], vt_counts[u]);
+    }
+    return EG_OK;
+}
+
+
+// Metadata part of a shard blob (no IPC handles).
+void fill_meta(const eg_ctx *c, ShardBlob *b)
+{
+    memset(b, 0, sizeof(*b));
+    b->magic = kBlobMagic;
+    b->version = 1;
+    b->rank = c->rank;
+    b->world = c->world;
+    b->n_vt = c->g.n_vt;
+    b->n_rel = c->g.n_rel;
+    for (int t = 0; t < b->n_vt; ++t) {
+        b->vt_counts[t] = c->vt_counts[t];
+        for (int p = 0; p <= c->world; ++p) b->bounds[t][p] = c->g.bounds[t][p];
+        const eg_features &F = c->own_feat[t];
+        b->feat[t].row_bytes = F.rows ? F.row_bytes : 0;
+        b->feat[t].n_rows = c->g.bounds[t][c->rank + 1] - c->g.bounds[t][c->rank];
+        b->feat[t].has = F.rows != nullptr && b->feat[t].n_rows > 0;
+    }
+    for (int r = 0; r < b->n_rel; ++r) {
+        const eg_relation &R = c->own_rel[r];
+        ShardRel &sr = b->rel[r];
+        sr.src_vt = R.src_vt;
+        sr.dst_vt = R.dst_vt;
+        sr.n_local_dst = c->g.bounds[R.dst_vt][c->rank + 1] - c->g.bounds[R.dst_vt][c->rank];
+        sr.n_local_edges = R.n_local_edges;
+        sr.edge_base = R.edge_base;
+        sr.max_degree = c->rel_max_degree[r];
+    }
+}
+
+eg_status check_peer(eg_ctx *c, const ShardBlob &b, int p)
+{
+    const std::string who = "peer " + std::to_string(p) + ": ";
+    if (b.magic != kBlobMagic || b.version != 1 || b.rank != p || b.world != c->world || b.n_vt != c->g.n_vt ||
+        b.n_rel != c->g.n_rel)
+        return fail(c, EG_EPEER, who + "header mismatch (rank / world / type counts)");
+    for (int t = 0; t < b.n_vt; ++t) {
+        if (b.vt_counts[t] != c->vt_counts[t]) return fail(c, EG_EPEER, who + "vertex counts differ");
+        for (int q = 0; q <= c->world; ++q)
+            if (b.bounds[t][q] != c->g.bounds[t][q]) return fail(c, EG_EPEER, who + "partition bounds differ");
+        if ((b.feat[t].row_bytes != 0) != (c->f.row_bytes[t] != 0) ||
+            (b.feat[t].row_bytes && b.feat[t].row_bytes != c->f.row_bytes[t]))
+            return fail(c, EG_EPEER, who + "feature row size differs");
+    }
+    for (int r = 0; r < b.n_rel; ++r)
+        if (b.rel[r].src_vt != c->g.rel[r].src_vt || b.rel[r].dst_vt != c->g.rel[r].dst_vt)
+            return fail(c, EG_EPEER, who + "relation types differ");
+    for (int r = 0; r < b.n_rel; ++r) {
+        c->peer_edges[p][r] = b.rel[r].n_local_edges;
+        c->peer_ebase[p][r] = b.rel[r].edge_base;
+        c->peer_maxdeg[p][r] = b.rel[r].max_degree;
+    }
+    return EG_OK;
+}
+
+// All ranks mapped: global edge counts / max degrees, contiguity of edge bases.
+eg_status finalize_peers(eg_ctx *c)
+{
+    for (int r = 0; r < c->g.n_rel; ++r) {
+        int64_t total = 0, mx = 0;
+        for (int p = 0; p < c->world; ++p) {
+            if (c->peer_ebase[p][r] != total)
+                return fail(c, EG_EPEER, "relation " + std::to_string(r) + ": edge bases not contiguous");
+            total += c->peer_edges[p][r];
+            mx = std::max(mx, c->peer_maxdeg[p][r]);
+        }
+        c->rel_edges_total[r] = total;
+        c->rel_max_degree[r] = mx;
+    }
+    c->peers_ready = true;
+    return EG_OK;
+}
+}  // namespace
+
+// =============================================================================== ABI
+
+extern "C" {
+
+const char *eg_version(void) { return kVersion; }
+
+const char *eg_last_error(const eg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t eg_kernel_launches(const eg_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+eg_status eg_range_bounds(int64_t n, int32_t world, int64_t *bounds)
+{
+    if (n < 0 || world < 1 || !bounds) return EG_EINVAL;
+    for (int p = 0; p <= world; ++p) bounds[p] = (int64_t)((__int128)p * n / world);
+    return EG_OK;
+}
+
+eg_status eg_batch_caps(int32_t n_vt, const int64_t *vt_counts, int32_t n_rel, const int32_t *rel_src_vt,
+                        const int32_t *rel_dst_vt, const int64_t *rel_n_edges, const int64_t *rel_max_degree,
+                        int64_t n_seeds, int32_t n_hops, const int32_t *fanouts, int64_t *caps_nodes,
+                        int64_t *caps_edges)
+{
+    if (n_vt < 1 || n_vt > EG_MAX_VT || n_rel < 1 || n_rel > EG_MAX_REL || n_hops < 1 || n_hops > EG_MAX_HOPS ||
+        n_seeds < 0)
+        return EG_EINVAL;
+    int64_t capF[EG_MAX_HOPS + 1][EG_MAX_VT], capE[EG_MAX_HOPS][EG_MAX_REL];
+    compute_caps(n_vt, vt_counts, n_rel, rel_src_vt, rel_dst_vt, rel_n_edges, rel_max_degree, n_seeds, n_hops,
+                 fanouts, capF, capE);
+    for (int u = 0; u < n_vt; ++u) caps_nodes[u] = capF[n_hops][u];
+    for (int h = 0; h < n_hops; ++h)
+        for (int r = 0; r < n_rel; ++r) caps_edges[h * n_rel + r] = capE[h][r];
+    return EG_OK;
+}
+
+eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, eg_ctx **out)
+{
+    if (!out) return EG_EINVAL;
+    *out = nullptr;
+    if (world < 1 || world > EG_MAX_RANKS || rank < 0 || rank >= world || device < 0) return EG_EINVAL;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n) {
+        cudaGetLastError();
+        return EG_ECUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return EG_ECUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return EG_ECUDA;
+    eg_ctx *c = new eg_ctx();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    if (cudaMallocHost(&c->h_meta, sizeof(int32_t) * kMetaSize) != cudaSuccess) {
+        delete c;
+        return EG_ENOMEM;
+    }
+    // stream-ordered allocations of the batches: keep freed blocks cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+    return EG_OK;
+}
+
+eg_status eg_set_stream(eg_ctx *ctx, void *stream)
+{
+    if (!ctx) return EG_EINVAL;
+    ctx->stream = (cudaStream_t)stream;
+    return EG_OK;
+}
+
+eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, const int64_t *bounds,
+                            int32_t n_rel, const eg_relation *rels, const eg_features *feats)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (c->loaded) return fail(c, EG_EINVAL, "partition already loaded");
+    if (n_vt < 1 || n_vt > EG_MAX_VT || n_rel < 1 || n_rel > EG_MAX_REL || !vt_counts || !rels)
+        return fail(c, EG_EINVAL, "n_vt / n_rel out of range or null arrays");
+    GraphDev &g = c->g;
+    g = GraphDev{};
+    g.n_vt = n_vt;
+    g.n_rel = n_rel;
+    g.world = c->world;
+    g.rank = c->rank;
+    g.off[0] = 0;
+    for (int t = 0; t < n_vt; ++t) {
+        if (vt_counts[t] < 0) return fail(c, EG_EINVAL, "negative vertex count");
+        c->vt_counts[t] = vt_counts[t];
+        g.off[t + 1] = g.off[t] + vt_counts[t];
+    }
+    c->n_total = g.off[n_vt];
+    if (c->n_total >= (int64_t)1 << 31) return fail(c, EG_EINVAL, "total vertex count must be < 2^31");
+    for (int t = 0; t < n_vt; ++t) {
+        for (int p = 0; p <= c->world; ++p)
+            g.bounds[t][p] = bounds ? bounds[t * (c->world + 1) + p] : (int64_t)((__int128)p * vt_counts[t] / c->world);
+        if (g.bounds[t][0] != 0 || g.bounds[t][c->world] != vt_counts[t])
+            return fail(c, EG_EINVAL, "bounds must start at 0 and end at N_t");
+        for (int p = 0; p < c->world; ++p)
+            if (g.bounds[t][p + 1] < g.bounds[t][p]) return fail(c, EG_EINVAL, "bounds must be non-decreasing");
+    }
+    // bitmap layout: one chunk-aligned bit range per type
+    g.boff[0] = 0;
+    for (int t = 0; t < n_vt; ++t) g.boff[t + 1] = g.boff[t] + (int64_t)align_up((size_t)vt_counts[t], kChunkBits);
+    c->n_chunks = (int32_t)(g.boff[n_vt] / kChunkBits);
+
+    unsigned long long *d_max = nullptr;
+    EG_CUDA(c, cudaMalloc(&d_max, sizeof(unsigned long long) * EG_MAX_REL));
+    EG_CUDA(c, cudaMemsetAsync(d_max, 0, sizeof(unsigned long long) * EG_MAX_REL, c->stream));
+    for (int r = 0; r < n_rel; ++r) {
+        const eg_relation &R = rels[r];
+        if (R.src_vt < 0 || R.src_vt >= n_vt || R.dst_vt < 0 || R.dst_vt >= n_vt)
+            return fail(c, EG_EINVAL, "relation vertex type out of range");
+        const int64_t n_local_dst = g.bounds[R.dst_vt][c->rank + 1] - g.bounds[R.dst_vt][c->rank];
+        if (!R.indptr || (R.n_local_edges > 0 && !R.indices) || R.n_local_edges < 0 || R.edge_base < 0)
+            return fail(c, EG_EINVAL, "relation shard pointers / sizes invalid");
+        if (vt_counts[R.src_vt] == 0 && R.n_local_edges > 0)
+            return fail(c, EG_EINVAL, "edges into an empty source type");
+        g.rel[r].src_vt = R.src_vt;
+        g.rel[r].dst_vt = R.dst_vt;
+        g.rel[r].indptr[c->rank] = R.indptr;
+        g.rel[r].indices[c->rank] = R.indices;
+        g.rel[r].edge_base[c->rank] = R.edge_base;
+        c->own_rel[r] = R;
+        c->rel_edges_total[r] = R.n_local_edges;
+        launch_max_degree(R.indptr, n_local_dst, d_max + r, c->stream);
+        ++c->launches;
+    }
+    c->f = FeatDev{};
+    for (int t = 0; t < n_vt; ++t) {
+        eg_features F = feats ? feats[t] : eg_features{nullptr, 0};
+        if (F.rows && (F.row_bytes <= 0 || F.row_bytes % 16))
+            return fail(c, EG_EINVAL, "row_bytes must be a positive multiple of 16");
+        c->f.rows[t][c->rank] = (const uint8_t *)F.rows;
+        c->f.row_bytes[t] = F.rows ? F.row_bytes : 0;
+        c->own_feat[t] = F;
+    }
+    unsigned long long h_max[EG_MAX_REL] = {};
+    EG_CUDA(c, cudaMemcpyAsync(h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, c->stream));
+    EG_CUDA(c, cudaStreamSynchronize(c->stream));
+    EG_CUDA(c, cudaFree(d_max));
+    for (int r = 0; r < n_rel; ++r) c->rel_max_degree[r] = (int64_t)h_max[r];
+
+    EG_CUDA(c, cudaMalloc(&c->pos, sizeof(int32_t) * std::max<int64_t>(1, c->n_total)));
+    EG_CUDA(c, cudaMemsetAsync(c->pos, 0xFF, sizeof(int32_t) * std::max<int64_t>(1, c->n_total), c->stream));
+    EG_CUDA(c, cudaMalloc(&c->bitmap, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, g.boff[n_vt] / 32)));
+    EG_CUDA(c, cudaMemsetAsync(c->bitmap, 0, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, g.boff[n_vt] / 32),
+                               c->stream));
+    EG_CUDA(c, cudaMalloc(&c->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&c->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    EG_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->loaded = true;
+    {
+        ShardBlob self_meta;
+        fill_meta(c, &self_meta);
+        if ((st = check_peer(c, self_meta, c->rank))) return st;
+    }
+    c->attached = 1u << c->rank;
+    c->peers_ready = false;
+    if (c->world == 1) return finalize_peers(c);
+    return EG_OK;
+}
+
+eg_status eg_export_shard(const eg_ctx *cc, void *buf, size_t *len)
+{
+    eg_ctx *c = const_cast<eg_ctx *>(cc);
+    if (!c || !len) return EG_EINVAL;
+    if (!buf) {
+        *len = sizeof(ShardBlob);
+        return EG_OK;
+    }
+    if (*len < sizeof(ShardBlob)) return fail(c, EG_EINVAL, "export buffer too small");
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
+    ShardBlob b;
+    fill_meta(c, &b);
+    for (int t = 0; t < b.n_vt; ++t)
+        if (b.feat[t].has && (st = ipc_export(c, c->own_feat[t].rows, &b.feat[t].h, &b.feat[t].off))) return st;
+    for (int r = 0; r < b.n_rel; ++r) {
+        const eg_relation &R = c->own_rel[r];
+        ShardRel &sr = b.rel[r];
+        if ((st = ipc_export(c, R.indptr, &sr.indptr_h, &sr.indptr_off))) return st;
+        if (R.n_local_edges > 0 && (st = ipc_export(c, R.indices, &sr.indices_h, &sr.indices_off))) return st;
+    }
+    memcpy(buf, &b, sizeof(b));
+    *len = sizeof(b);
+    return EG_OK;
+}
+
+eg_status eg_import_shards(eg_ctx *c, const void *blobs, size_t stride)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
+    if (!blobs || stride < sizeof(ShardBlob)) return fail(c, EG_EINVAL, "blob stride too small");
+    std::vector<ShardBlob> all(c->world);
+    for (int p = 0; p < c->world; ++p) memcpy(&all[p], (const char *)blobs + p * stride, sizeof(ShardBlob));
+    for (int p = 0; p < c->world; ++p)
+        if ((st = check_peer(c, all[p], p))) return st;
+    // map the peers' shards (deduplicate allocations shared by several buffers)
+    for (int p = 0; p < c->world; ++p) {
+        if (p == c->rank) continue;
+        std::map<std::string, char *> opened;
+        auto open = [&](const cudaIpcMemHandle_t &h, int64_t off, const void **outp) -> eg_status {
+            std::string key((const char *)&h, sizeof(h));
+            auto it = opened.find(key);
+            char *base = nullptr;
+            if (it == opened.end()) {
+                void *bp = nullptr;
+                cudaError_t e = cudaIpcOpenMemHandle(&bp, h, cudaIpcMemLazyEnablePeerAccess);
+                if (e != cudaSuccess)
+                    return fail(c, EG_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+                c->ipc_bases.push_back(bp);
+                base = (char *)bp;
+                opened[key] = base;
+            } else {
+                base = it->second;
+            }
+            *outp = base + off;
+            return EG_OK;
+        };
+        const ShardBlob &b = all[p];
+        for (int r = 0; r < b.n_rel; ++r) {
+            const void *ip = nullptr, *ix = nullptr;
+            if ((st = open(b.rel[r].indptr_h, b.rel[r].indptr_off, &ip))) return st;
+            if (b.rel[r].n_local_edges > 0 && (st = open(b.rel[r].indices_h, b.rel[r].indices_off, &ix))) return st;
+            c->g.rel[r].indptr[p] = (const int64_t *)ip;
+            c->g.rel[r].indices[p] = (const int32_t *)ix;
+            c->g.rel[r].edge_base[p] = b.rel[r].edge_base;
+        }
+        for (int t = 0; t < b.n_vt; ++t) {
+            if (!b.feat[t].has) continue;
+            const void *rp = nullptr;
+            if ((st = open(b.feat[t].h, b.feat[t].off, &rp))) return st;
+            c->f.rows[t][p] = (const uint8_t *)rp;
+        }
+    }
+    c->attached = (1u << c->world) - 1;
+    return finalize_peers(c);
+}
+
+eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!peer || !c->loaded || !peer->loaded) return fail(c, EG_EINVAL, "both contexts must be loaded");
+    const int p = peer->rank;
+    if (peer->world != c->world || p == c->rank) return fail(c, EG_EINVAL, "peer must be another rank of the same world");
+    ShardBlob b;
+    fill_meta(peer, &b);
+    if ((st = check_peer(c, b, p))) return st;
+    if (peer->device != c->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(c, EG_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+    for (int r = 0; r < c->g.n_rel; ++r) {
+        c->g.rel[r].indptr[p] = peer->own_rel[r].indptr;
+        c->g.rel[r].indices[p] = peer->own_rel[r].indices;
+        c->g.rel[r].edge_base[p] = peer->own_rel[r].edge_base;
+    }
+    for (int t = 0; t < c->g.n_vt; ++t) c->f.rows[t][p] = (const uint8_t *)peer->own_feat[t].rows;
+    c->attached |= 1u << p;
+    if (c->attached == (1u << c->world) - 1) return finalize_peers(c);
+    return EG_OK;
+}
+
+eg_status eg_sample_blocks(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
+                           const int32_t *fanouts, uint64_t rng_seed, eg_blocks **out)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!out) return fail(c, EG_EINVAL, "out is null");
+    *out = nullptr;
+    if (!c->loaded || !c->peers_ready) return fail(c, EG_EINVAL, "partition not loaded / peers not imported");
+    if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
+    if (n_seeds < 0 || (n_seeds > 0 && !seeds)) return fail(c, EG_EINVAL, "bad seeds");
+    if (!fanouts) return fail(c, EG_EINVAL, "fanouts is null");
+    const GraphDev &g = c->g;
+    const int V = g.n_vt, R = g.n_rel, L = n_hops;
+    for (int i = 0; i < L * R; ++i)
+        if (fanouts[i] < -1) return fail(c, EG_EINVAL, "fanout must be >= -1");
+
+    int32_t src_vt[EG_MAX_REL], dst_vt[EG_MAX_REL];
+    for (int r = 0; r < R; ++r) {
+        src_vt[r] = g.rel[r].src_vt;
+        dst_vt[r] = g.rel[r].dst_vt;
+    }
+    int64_t capF[EG_MAX_HOPS + 1][EG_MAX_VT], capE[EG_MAX_HOPS][EG_MAX_REL];
+    compute_caps(V, c->vt_counts, R, src_vt, dst_vt, c->rel_edges_total, c->rel_max_degree, n_seeds, L, fanouts,
+                 capF, capE);
+    for (int h = 0; h <= L; ++h)
+        for (int u = 0; u < V; ++u)
+            if (capF[h][u] >= INT32_MAX) return fail(c, EG_EINVAL, "batch exceeds 2^31 vertices of one type");
+    for (int h = 0; h < L; ++h)
+        for (int r = 0; r < R; ++r)
+            if (capE[h][r] >= INT32_MAX) return fail(c, EG_EINVAL, "batch exceeds 2^31 edges of one relation");
+
+    // one stream-ordered allocation for the whole batch
+    const bool host_seeds = n_seeds > 0 && !is_device_ptr(seeds);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + std::max<size_t>(bytes, 1), 256);
+        return o;
+    };
+    const size_t o_meta = take(sizeof(int32_t) * kMetaSize);
+    const size_t o_seeds = host_seeds ? take(sizeof(int64_t) * n_seeds) : 0;
+    size_t o_nodes[EG_MAX_VT], o_ip[EG_MAX_HOPS][EG_MAX_REL], o_ix[EG_MAX_HOPS][EG_MAX_REL],
+        o_ei[EG_MAX_HOPS][EG_MAX_REL], o_src[EG_MAX_HOPS][EG_MAX_REL];
+    for (int u = 0; u < V; ++u) o_nodes[u] = take(sizeof(int64_t) * capF[L][u]);
+    for (int h = 0; h < L; ++h)
+        for (int r = 0; r < R; ++r) {
+            o_ip[h][r] = take(sizeof(int32_t) * (capF[h][dst_vt[r]] + 1));
+            o_ix[h][r] = take(sizeof(int32_t) * capE[h][r]);
+            o_ei[h][r] = take(sizeof(int64_t) * capE[h][r]);
+            o_src[h][r] = take(sizeof(uint32_t) * capE[h][r]);
+        }
+    eg_blocks *b = new eg_blocks();
+    b->ctx = c;
+    b->n_hops = L;
+    b->n_vt = V;
+    b->n_rel = R;
+    cudaError_t e = cudaMallocAsync(&b->mem, off, c->stream);
+    if (e != cudaSuccess) {
+        delete b;
+        cudaGetLastError();
+        return fail(c, EG_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    char *base = (char *)b->mem;
+    b->meta = (int32_t *)(base + o_meta);
+    for (int u = 0; u < V; ++u) b->nodes[u] = (int64_t *)(base + o_nodes[u]);
+    uint32_t *srcbuf[EG_MAX_HOPS][EG_MAX_REL];
+    for (int h = 0; h < L; ++h)
+        for (int r = 0; r < R; ++r) {
+            b->indptr[h][r] = (int32_t *)(base + o_ip[h][r]);
+            b->indices[h][r] = (int32_t *)(base + o_ix[h][r]);
+            b->eids[h][r] = (int64_t *)(base + o_ei[h][r]);
+            srcbuf[h][r] = (uint32_t *)(base + o_src[h][r]);
+        }
+    TimedPair tp;
+    record_start(c, &tp, 0);
+    const int64_t *d_seeds = seeds;
+    if (host_seeds) {
+        d_seeds = (const int64_t *)(base + o_seeds);
+        EG_CUDA(c, cudaMemcpyAsync((void *)d_seeds, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice,
+                                   c->stream));
+    }
+    EG_CUDA(c, cudaMemsetAsync(b->meta, 0, sizeof(int32_t) * kMetaSize, c->stream));
+
+    HopDev hd{};
+    hd.seed_lo = (uint32_t)rng_seed;
+    hd.seed_hi = (uint32_t)(rng_seed >> 32);
+    for (int u = 0; u < V; ++u) {
+        hd.nodes[u] = b->nodes[u];
+        hd.cap_nodes[u] = (int32_t)capF[L][u];
+    }
+    hd.meta = b->meta;
+    hd.partial = c->partial;
+    hd.pos = c->pos;
+    hd.bitmap = c->bitmap;
+    hd.chunk_cnt = c->chunk_cnt;
+    launch_seed_split(g, d_seeds, n_seeds, hd, c->stream);
+    c->launches += 1;
+    for (int h = 0; h < L; ++h) {
+        hd.h = h;
+        for (int r = 0; r < R; ++r) {
+            hd.fanout[r] = fanouts[h * R + r];
+            hd.indptr[r] = b->indptr[h][r];
+            hd.indices[r] = b->indices[h][r];
+            hd.eids[r] = b->eids[h][r];
+            hd.src[r] = srcbuf[h][r];
+        }
+        launch_count(g, hd, c->stream);
+        launch_scan(g, hd, c->stream);
+        launch_sample(g, hd, c->stream);
+        launch_mark(g, hd, c->stream);
+        launch_bitcount(g, hd, c->n_chunks, c->stream);
+        launch_emit(g, hd, c->n_chunks, c->stream);
+        launch_relabel(g, hd, c->stream);
+        c->launches += 7;
+    }
+    launch_reset(g, hd, L, c->stream);
+    c->launches += 1;
+    EG_CUDA(c, cudaGetLastError());
+    record_end(c, &tp);
+    EG_CUDA(c, cudaMemcpyAsync(c->h_meta, b->meta, sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, c->stream));
+    EG_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int32_t errbits = c->h_meta[kMetaErr];
+    for (int l = 0; l <= L; ++l)
+        for (int u = 0; u < V; ++u) b->n_nodes[l][u] = c->h_meta[kMetaNodes + l * EG_MAX_VT + u];
+    for (int h = 0; h < L; ++h)
+        for (int r = 0; r < R; ++r) b->nnz[h][r] = c->h_meta[kMetaNnz + h * EG_MAX_REL + r];
+    if (errbits) {
+        cudaFreeAsync(b->mem, c->stream);
+        delete b;
+        if (errbits & kErrSeedRange) return fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
+        if (errbits & kErrSeedDup) return fail(c, EG_EINVAL, "duplicate seeds");
+        return fail(c, EG_EINVAL, "internal capacity overflow");
+    }
+    *out = b;
+    return EG_OK;
+}
+
+int32_t eg_blocks_n_hops(const eg_blocks *b) { return b ? b->n_hops : 0; }
+
+int64_t eg_blocks_n_inputs(const eg_blocks *b, int32_t u)
+{
+    if (!b || u < 0 || u >= b->n_vt) return -1;
+    return b->n_nodes[b->n_hops][u];
+}
+
+eg_status eg_block_view_get(const eg_blocks *b, int32_t hop, eg_block_view *v)
+{
+    if (!b || !v || hop < 0 || hop >= b->n_hops) return EG_EINVAL;
+    memset(v, 0, sizeof(*v));
+    v->hop = hop;
+    v->n_vt = b->n_vt;
+    v->n_rel = b->n_rel;
+    for (int u = 0; u < b->n_vt; ++u) {
+        v->dst_nodes[u] = b->nodes[u];
+        v->n_dst[u] = b->n_nodes[hop][u];
+        v->src_nodes[u] = b->nodes[u];
+        v->n_src[u] = b->n_nodes[hop + 1][u];
+    }
+    for (int r = 0; r < b->n_rel; ++r) {
+        v->indptr[r] = b->indptr[hop][r];
+        v->indices[r] = b->indices[hop][r];
+        v->eids[r] = b->eids[hop][r];
+        v->nnz[r] = b->nnz[hop][r];
+    }
+    return EG_OK;
+}
+
+eg_status eg_gather_features(eg_ctx *c, const eg_blocks *b, void *const *out)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!b || !out || b->ctx != c) return fail(c, EG_EINVAL, "bad blocks / out");
+    GatherDev gd{};
+    gd.meta = b->meta;
+    gd.level = b->n_hops;
+    void *staging[EG_MAX_VT] = {};
+    bool any = false;
+    for (int u = 0; u < b->n_vt; ++u) {
+        gd.nodes[u] = b->nodes[u];
+        if (!out[u]) continue;
+        if (!c->f.row_bytes[u]) return fail(c, EG_EINVAL, "vertex type " + std::to_string(u) + " has no features");
+        const int64_t bytes = b->n_nodes[b->n_hops][u] * c->f.row_bytes[u];
+        if (bytes == 0) continue;
+        if ((uint64_t)(bytes / 16) >= (1ull << 32)) return fail(c, EG_EINVAL, "gather too large");
+        if (is_device_ptr(out[u])) {
+            gd.out[u] = (uint8_t *)out[u];
+        } else {
+            EG_CUDA(c, cudaMallocAsync(&staging[u], bytes, c->stream));
+            gd.out[u] = (uint8_t *)staging[u];
+        }
+        any = true;
+    }
+    if (!any) return EG_OK;
+    TimedPair tp;
+    record_start(c, &tp, 1);
+    launch_gather(c->g, c->f, gd, c->stream);
+    c->launches += 1;
+    EG_CUDA(c, cudaGetLastError());
+    record_end(c, &tp);
+    bool staged = false;
+    for (int u = 0; u < b->n_vt; ++u)
+        if (staging[u]) {
+            EG_CUDA(c, cudaMemcpyAsync(out[u], staging[u], b->n_nodes[b->n_hops][u] * c->f.row_bytes[u],
+                                       cudaMemcpyDeviceToHost, c->stream));
+            EG_CUDA(c, cudaFreeAsync(staging[u], c->stream));
+            staged = true;
+        }
+    if (staged) EG_CUDA(c, cudaStreamSynchronize(c->stream));
+    return EG_OK;
+}
+
+eg_status eg_blocks_free(eg_blocks *b)
+{
+    if (!b) return EG_OK;
+    eg_ctx *c = b->ctx;
+    if (c && !c->broken) {
+        cudaSetDevice(c->device);
+        cudaFreeAsync(b->mem, c->stream);
+    }
+    delete b;
+    return EG_OK;
+}
+
+eg_status eg_set_profiling(eg_ctx *c, int32_t enable)
+{
+    if (!c) return EG_EINVAL;
+    c->prof = enable != 0;
+    return EG_OK;
+}
+
+eg_status eg_get_profile(eg_ctx *c, double out[4])
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    drain_timing(c);
+    out[0] = c->prof_ms[0];
+    out[1] = c->prof_ms[1];
+    out[2] = (double)c->prof_n[0];
+    out[3] = (double)c->prof_n[1];
+    c->prof_ms[0] = c->prof_ms[1] = 0;
+    c->prof_n[0] = c->prof_n[1] = 0;
+    return EG_OK;
+}
+
+eg_status eg_destroy(eg_ctx *c)
+{
+    if (!c) return EG_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    drain_timing(c);
+    for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
+    cudaFree(c->pos);
+    cudaFree(c->bitmap);
+    cudaFree(c->chunk_cnt);
+    cudaFree(c->partial);
+    cudaFreeHost(c->h_meta);
+    delete c;
+    return EG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,380 @@
+"""Python binding of the egonet C ABI (include/egonet.h).
+
+Argument marshalling only: every step of the hot path runs in libegonet.so's
+sm_100a kernels.  PyTorch provides device memory (shards, outputs), streams and
+the process group used to all-gather the peer-shard blobs.  There is no CPU
+fallback: if libegonet.so cannot be loaded, or no B200 is visible, calls fail.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libegonet.so")
+
+EG_MAX_VT = 8
+EG_MAX_REL = 8
+EG_MAX_RANKS = 8
+EG_MAX_HOPS = 8
+
+STATUS = {0: "EG_OK", -1: "EG_EINVAL", -2: "EG_ERANGE", -3: "EG_ENOMEM", -4: "EG_ECUDA", -6: "EG_EPEER",
+          -7: "EG_ESTATE"}
+
+ABI_SYMBOLS = [
+    "eg_version", "eg_create", "eg_set_stream", "eg_load_partition", "eg_export_shard", "eg_import_shards",
+    "eg_sample_blocks", "eg_block_view_get", "eg_blocks_n_hops", "eg_blocks_n_inputs", "eg_gather_features",
+    "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
+    "eg_range_bounds", "eg_batch_caps", "eg_attach_peer",
+]
+
+
+class EgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Relation(ctypes.Structure):
+    _fields_ = [("src_vt", ctypes.c_int32), ("dst_vt", ctypes.c_int32), ("indptr", ctypes.c_void_p),
+                ("indices", ctypes.c_void_p), ("n_local_edges", ctypes.c_int64), ("edge_base", ctypes.c_int64)]
+
+
+class Features(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_void_p), ("row_bytes", ctypes.c_int64)]
+
+
+class BlockView(ctypes.Structure):
+    _fields_ = [("hop", ctypes.c_int32), ("n_vt", ctypes.c_int32), ("n_rel", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("dst_nodes", ctypes.c_void_p * EG_MAX_VT), ("n_dst", ctypes.c_int64 * EG_MAX_VT),
+                ("src_nodes", ctypes.c_void_p * EG_MAX_VT), ("n_src", ctypes.c_int64 * EG_MAX_VT),
+                ("indptr", ctypes.c_void_p * EG_MAX_REL), ("indices", ctypes.c_void_p * EG_MAX_REL),
+                ("eids", ctypes.c_void_p * EG_MAX_REL), ("nnz", ctypes.c_int64 * EG_MAX_REL)]
+
+
+_lib = None
+
+
+def lib(build_if_missing: bool = True):
+    """Load libegonet.so (building it with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is None:
+        if build_if_missing:
+            from . import build as _b
+            _b.build()
+        if not os.path.exists(_SO):
+            raise RuntimeError(f"{_SO} missing: run paper_2112_15345_b200/build.py (no CPU fallback exists)")
+        L = ctypes.CDLL(_SO)
+        c = ctypes
+        P = c.POINTER
+        vp = c.c_void_p
+        L.eg_version.restype = c.c_char_p
+        L.eg_last_error.argtypes = [vp]
+        L.eg_last_error.restype = c.c_char_p
+        L.eg_create.argtypes = [c.c_int32, c.c_int32, c.c_int32, vp, P(vp)]
+        L.eg_set_stream.argtypes = [vp, vp]
+        L.eg_load_partition.argtypes = [vp, c.c_int32, vp, vp, c.c_int32, vp, vp]
+        L.eg_export_shard.argtypes = [vp, vp, P(c.c_size_t)]
+        L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
+        L.eg_attach_peer.argtypes = [vp, vp]
+        L.eg_sample_blocks.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, P(vp)]
+        L.eg_block_view_get.argtypes = [vp, c.c_int32, P(BlockView)]
+        L.eg_blocks_n_hops.argtypes = [vp]
+        L.eg_blocks_n_hops.restype = c.c_int32
+        L.eg_blocks_n_inputs.argtypes = [vp, c.c_int32]
+        L.eg_blocks_n_inputs.restype = c.c_int64
+        L.eg_gather_features.argtypes = [vp, vp, vp]
+        L.eg_blocks_free.argtypes = [vp]
+        L.eg_destroy.argtypes = [vp]
+        L.eg_set_profiling.argtypes = [vp, c.c_int32]
+        L.eg_get_profile.argtypes = [vp, P(c.c_double)]
+        L.eg_kernel_launches.argtypes = [vp]
+        L.eg_kernel_launches.restype = c.c_int64
+        L.eg_range_bounds.argtypes = [c.c_int64, c.c_int32, vp]
+        L.eg_batch_caps.argtypes = [c.c_int32, vp, c.c_int32, vp, vp, vp, vp, c.c_int64, c.c_int32, vp, vp, vp]
+        for name in ABI_SYMBOLS:
+            if name not in ("eg_version", "eg_last_error", "eg_blocks_n_hops", "eg_blocks_n_inputs",
+                            "eg_kernel_launches"):
+                getattr(L, name).restype = c.c_int
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().eg_version().decode()
+
+
+def range_bounds(n: int, world: int) -> np.ndarray:
+    out = np.empty(world + 1, dtype=np.int64)
+    rc = lib().eg_range_bounds(n, world, out.ctypes.data)
+    if rc:
+        raise EgError(rc, "eg_range_bounds")
+    return out
+
+
+def batch_caps(vt_counts, rel_src, rel_dst, rel_edges, rel_maxdeg, n_seeds, fanouts):
+    vtc = np.ascontiguousarray(vt_counts, np.int64)
+    rs, rd = np.ascontiguousarray(rel_src, np.int32), np.ascontiguousarray(rel_dst, np.int32)
+    re_, rm = np.ascontiguousarray(rel_edges, np.int64), np.ascontiguousarray(rel_maxdeg, np.int64)
+    fo = np.ascontiguousarray(fanouts, np.int32)
+    cn = np.empty(len(vtc), np.int64)
+    ce = np.empty(fo.shape, np.int64)
+    rc = lib().eg_batch_caps(len(vtc), vtc.ctypes.data, len(rs), rs.ctypes.data, rd.ctypes.data, re_.ctypes.data,
+                             rm.ctypes.data, n_seeds, fo.shape[0], fo.ctypes.data, cn.ctypes.data, ce.ctypes.data)
+    if rc:
+        raise EgError(rc, "eg_batch_caps")
+    return cn, ce
+
+
+# ----------------------------------------------------------------------------- device wrappers
+
+def _torch():
+    import torch
+    return torch
+
+
+class _DevArray:
+    """__cuda_array_interface__ over library-owned device memory; keeps the owning
+    Blocks alive for as long as any tensor built from it lives."""
+
+    def __init__(self, ptr, n, typestr, owner, device):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+        self._owner = owner
+        self._device = device
+
+
+def _wrap(ptr, n, typestr, owner, device):
+    torch = _torch()
+    if n == 0 or not ptr:
+        dt = {"<i8": torch.int64, "<i4": torch.int32}[typestr]
+        return torch.empty(0, dtype=dt, device=device)
+    with torch.cuda.device(device):
+        return torch.as_tensor(_DevArray(ptr, n, typestr, owner, device), device=device)
+
+
+class Block:
+    """One hop's block: DGL-style bipartite CSC per relation (dst-in-src prefix)."""
+
+    def __init__(self, view: BlockView, owner, device):
+        self.hop = view.hop
+        V, R = view.n_vt, view.n_rel
+        self.n_dst = [int(view.n_dst[u]) for u in range(V)]
+        self.n_src = [int(view.n_src[u]) for u in range(V)]
+        self.nnz = [int(view.nnz[r]) for r in range(R)]
+        self.dst_nodes = [_wrap(view.dst_nodes[u], self.n_dst[u], "<i8", owner, device) for u in range(V)]
+        self.src_nodes = [_wrap(view.src_nodes[u], self.n_src[u], "<i8", owner, device) for u in range(V)]
+        self.indptr = [None] * R
+        self.indices = [_wrap(view.indices[r], self.nnz[r], "<i4", owner, device) for r in range(R)]
+        self.eids = [_wrap(view.eids[r], self.nnz[r], "<i8", owner, device) for r in range(R)]
+        self._view = view
+        self._owner = owner
+        self._device = device
+
+    def set_indptr(self, rel_dst):
+        for r, t in enumerate(rel_dst):
+            self.indptr[r] = _wrap(self._view.indptr[r], self.n_dst[t] + 1, "<i4", self._owner, self._device)
+
+
+class Blocks:
+    """Handle of one sampled mini-batch (eg_blocks).  Per-hop tensors are built
+    lazily (zero-copy views of library memory) on first access."""
+
+    def __init__(self, ctx: "Context", handle: int):
+        self._ctx = ctx
+        self._h = handle
+        self.n_hops = lib().eg_blocks_n_hops(handle)
+        self.views = []
+        for h in range(self.n_hops):
+            v = BlockView()
+            rc = lib().eg_block_view_get(handle, h, ctypes.byref(v))
+            if rc:
+                raise EgError(rc, "eg_block_view_get")
+            self.views.append(v)
+        self._blocks = [None] * self.n_hops
+
+    def __getitem__(self, h) -> Block:
+        if self._blocks[h] is None:
+            b = Block(self.views[h], self, self._ctx.device)
+            b.set_indptr(self._ctx.rel_dst)
+            self._blocks[h] = b
+        return self._blocks[h]
+
+    def __len__(self):
+        return self.n_hops
+
+    def nnz(self, h=None) -> int:
+        hops = range(self.n_hops) if h is None else [h]
+        return sum(int(self.views[x].nnz[r]) for x in hops for r in range(self.views[x].n_rel))
+
+    def n_inputs(self, u) -> int:
+        return int(lib().eg_blocks_n_inputs(self._h, u))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        """Release the library memory now (tensors obtained from this handle must
+        no longer be used).  Otherwise it is released when the handle and all its
+        tensors are garbage."""
+        if self._h:
+            lib().eg_blocks_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One rank's view of the partitioned graph (eg_ctx)."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device: int = 0, stream=None):
+        torch = _torch()
+        self.rank, self.world, self.device = rank, world, device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        rc = lib().eg_create(rank, world, device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if rc:
+            raise EgError(rc, "eg_create (needs an sm_100 GPU; there is no CPU fallback)")
+        self._h = h
+        self._keep = []
+        self.rel_dst = []
+        self.vt_counts = None
+        self.row_bytes = []
+
+    def _check(self, rc, what):
+        if rc:
+            raise EgError(rc, f"{what}: {lib().eg_last_error(self._h).decode()}")
+
+    def set_stream(self, stream):
+        self.stream = stream
+        self._check(lib().eg_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)), "eg_set_stream")
+
+    def load_partition(self, vt_counts, rels, feats, bounds=None):
+        """rels: list of dicts {src_vt, dst_vt, indptr (cuda int64), indices (cuda int32), edge_base};
+        feats: list (per type) of cuda tensors [n_local_rows, ...] or None."""
+        vtc = np.ascontiguousarray(vt_counts, np.int64)
+        self.vt_counts = vtc
+        R = len(rels)
+        carr = (Relation * R)()
+        for r, d in enumerate(rels):
+            ip, ix = d["indptr"], d["indices"]
+            assert ip.dtype.itemsize == 8 and ix.dtype.itemsize == 4 and ip.is_cuda and ix.is_cuda
+            carr[r] = Relation(d["src_vt"], d["dst_vt"], ip.data_ptr(), ix.data_ptr() if ix.numel() else None,
+                               ix.numel(), int(d["edge_base"]))
+            self._keep += [ip, ix]
+        farr = (Features * len(vtc))()
+        self.row_bytes = []
+        for u in range(len(vtc)):
+            t = feats[u] if feats is not None and u < len(feats) else None
+            if t is None:
+                farr[u] = Features(None, 0)
+                self.row_bytes.append(0)
+            else:
+                assert t.is_cuda and t.is_contiguous()
+                rb = t.stride(0) * t.element_size() if t.dim() > 1 else t.element_size()
+                farr[u] = Features(t.data_ptr() if t.numel() else None, rb if t.numel() else 0)
+                self.row_bytes.append(rb)
+                self._keep.append(t)
+        self.rel_dst = [int(d["dst_vt"]) for d in rels]
+        self.rel_src = [int(d["src_vt"]) for d in rels]
+        self.feat_dtypes = [None if (feats is None or u >= len(feats) or feats[u] is None) else feats[u].dtype
+                            for u in range(len(vtc))]
+        self.feat_shapes = [None if (feats is None or u >= len(feats) or feats[u] is None) else tuple(feats[u].shape[1:])
+                            for u in range(len(vtc))]
+        b = None
+        if bounds is not None:
+            b = np.ascontiguousarray(bounds, np.int64)
+            self._keep.append(b)
+        self._check(lib().eg_load_partition(self._h, len(vtc), vtc.ctypes.data, b.ctypes.data if b is not None else None,
+                                            R, ctypes.cast(carr, ctypes.c_void_p), ctypes.cast(farr, ctypes.c_void_p)),
+                    "eg_load_partition")
+
+    def export_shard(self) -> bytes:
+        n = ctypes.c_size_t(0)
+        self._check(lib().eg_export_shard(self._h, None, ctypes.byref(n)), "eg_export_shard")
+        buf = ctypes.create_string_buffer(n.value)
+        self._check(lib().eg_export_shard(self._h, buf, ctypes.byref(n)), "eg_export_shard")
+        return buf.raw[:n.value]
+
+    def attach_peer(self, peer: "Context"):
+        """Single-process peer mapping (another rank's context in this process)."""
+        self._check(lib().eg_attach_peer(self._h, peer._h), "eg_attach_peer")
+
+    def import_shards(self, blobs):
+        stride = len(blobs[0])
+        assert all(len(b) == stride for b in blobs)
+        joined = ctypes.create_string_buffer(b"".join(blobs), stride * len(blobs))
+        self._check(lib().eg_import_shards(self._h, joined, stride), "eg_import_shards")
+
+    def connect_peers(self, group=None):
+        """All-gather the shard blobs over a torch.distributed group and map the peers."""
+        import torch.distributed as dist
+        blob = self.export_shard()
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, blob, group=group)
+        self.import_shards(blobs)
+
+    def sample_blocks(self, seeds, fanouts, rng_seed: int) -> Blocks:
+        """seeds: cuda int64 tensor (or host numpy int64 / pinned tensor); fanouts [hop][rel]."""
+        torch = _torch()
+        fo = np.ascontiguousarray(fanouts, np.int32)
+        if isinstance(seeds, np.ndarray):
+            seeds = np.ascontiguousarray(seeds, np.int64)
+            ptr, n = seeds.ctypes.data, len(seeds)
+        else:
+            assert seeds.dtype == torch.int64 and seeds.is_contiguous()
+            ptr, n = seeds.data_ptr(), seeds.numel()
+        h = ctypes.c_void_p()
+        self._check(lib().eg_sample_blocks(self._h, ptr if n else None, n, fo.shape[0], fo.ctypes.data,
+                                           rng_seed & (2**64 - 1), ctypes.byref(h)), "eg_sample_blocks")
+        return Blocks(self, h.value)
+
+    def gather_features(self, blocks: Blocks, out=None, types=None):
+        """Feature rows of the input vertices per type (None for types without
+        features).  `out` may give preallocated (device or host) tensors / arrays."""
+        torch = _torch()
+        V = len(self.vt_counts)
+        types = range(V) if types is None else types
+        outs = [None] * V
+        ptrs = (ctypes.c_void_p * V)()
+        for u in types:
+            if not self.row_bytes[u]:
+                continue
+            if out is not None and out[u] is not None:
+                o = out[u]
+            else:
+                o = torch.empty((blocks.n_inputs(u),) + self.feat_shapes[u], dtype=self.feat_dtypes[u],
+                                device=self.device)
+            outs[u] = o
+            ptrs[u] = o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data
+        self._check(lib().eg_gather_features(self._h, blocks.handle, ptrs), "eg_gather_features")
+        return outs
+
+    def set_profiling(self, on: bool):
+        self._check(lib().eg_set_profiling(self._h, 1 if on else 0), "eg_set_profiling")
+
+    def profile(self):
+        out = (ctypes.c_double * 4)()
+        self._check(lib().eg_get_profile(self._h, out), "eg_get_profile")
+        return {"sample_ms": out[0], "gather_ms": out[1], "n_sample": int(out[2]), "n_gather": int(out[3])}
+
+    def kernel_launches(self) -> int:
+        return int(lib().eg_kernel_launches(self._h))
+
+    def close(self):
+        if self._h:
+            lib().eg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

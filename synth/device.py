@@ -1,0 +1,71 @@
+"""Put a rank's shard of a synthetic graph on its GPU (input plumbing, untimed).
+
+CSC rows come from the host generator (sliced per rank); src tids of huge
+relations and all feature rows are generated directly on the device by
+synth_dev.cu with the same formulas as the host (byte-identical, tested).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import (HostGraph, NP_DTYPE, Config, dev_lib, shard)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def feature_shard(cfg: Config, u: int, lo: int, hi: int, device):
+    torch = _torch()
+    dim, dt = cfg.feats[u]
+    tdt = torch.float32 if dt == 0 else torch.float16
+    t = torch.empty((hi - lo, dim), dtype=tdt, device=device)
+    if hi > lo:
+        s = torch.cuda.current_stream(device)
+        rc = dev_lib().sy_features_dev(cfg.gen_seed, u, lo, hi, dim, dt, ctypes.c_void_p(t.data_ptr()),
+                                       ctypes.c_void_p(s.cuda_stream))
+        if rc:
+            raise RuntimeError(f"sy_features_dev failed: {rc}")
+    return t
+
+
+def device_shard(graph: HostGraph, world: int, rank: int, device, features: bool = True):
+    """Returns dict(vt_counts, bounds, rels=[{src_vt,dst_vt,indptr,indices,edge_base}], feats=[tensor|None])."""
+    torch = _torch()
+    cfg = graph.cfg
+    materialized = bool(graph.indices) and all(x is not None for x in graph.indices)
+    bounds, rels = shard(graph, world, rank, with_indices=materialized)
+    out_rels = []
+    s = torch.cuda.current_stream(device)
+    for r, rs in enumerate(rels):
+        ip = torch.from_numpy(rs.indptr).to(device)
+        if rs.indices is not None:
+            ix = torch.from_numpy(np.ascontiguousarray(rs.indices, np.int32)).to(device)
+        else:
+            ix = torch.empty(rs.e_hi - rs.e_lo, dtype=torch.int32, device=device)
+            if rs.e_hi > rs.e_lo:
+                n_src = int(cfg.vt_counts[rs.src_vt])
+                rc = dev_lib().sy_indices_dev(cfg.gen_seed, r, n_src, rs.e_lo, rs.e_hi,
+                                              ctypes.c_void_p(ix.data_ptr()), ctypes.c_void_p(s.cuda_stream))
+                if rc:
+                    raise RuntimeError(f"sy_indices_dev failed: {rc}")
+        out_rels.append({"src_vt": rs.src_vt, "dst_vt": rs.dst_vt, "indptr": ip, "indices": ix,
+                         "edge_base": rs.e_lo})
+    feats = []
+    for u in range(cfg.n_vt):
+        if features and u in cfg.feats:
+            feats.append(feature_shard(cfg, u, int(bounds[u][rank]), int(bounds[u][rank + 1]), device))
+        else:
+            feats.append(None)
+    torch.cuda.synchronize(device)
+    return {"vt_counts": cfg.vt_counts, "bounds": bounds, "rels": out_rels, "feats": feats}
+
+
+def load_context(ctx, graph: HostGraph, world: int, rank: int, device, features: bool = True):
+    """device_shard + Context.load_partition; returns the shard dict (keep it alive)."""
+    sh = device_shard(graph, world, rank, device, features)
+    ctx.load_partition(sh["vt_counts"], sh["rels"], sh["feats"], bounds=sh["bounds"])
+    return sh

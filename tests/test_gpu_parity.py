@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Sampled edge lists (eids + relabelled src ids), block CSCs, node lists and
+gathered feature bytes are compared element by element on the same seeded
+inputs (synth/), for the configs' own shapes and fanouts and for the edge cases
+of the method (fanout -1 / 0, d <= k, k > the fast-path limit, hubs, empty and
+mixed-type seeds, errors), and at world sizes 1..8 (P-invariance, DESIGN §3 #13).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_same_batch, assert_same_features, run_and_compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(graph, world=1, rank=0, features=True):
+    from paper_2112_15345_b200 import Context
+    from synth.device import load_context
+    ctx = Context(rank, world, 0)
+    shard = load_context(ctx, graph, world, rank, "cuda:0", features=features)
+    ctx._shard = shard
+    return ctx
+
+
+def _world(graph, world, features=True):
+    """All ranks of a world in this process on one GPU, mapped to each other."""
+    ctxs = [_ctx(graph, world, p, features) for p in range(world)]
+    for a in ctxs:
+        for b in ctxs:
+            if a is not b:
+                a.attach_peer(b)
+    return ctxs
+
+
+@pytest.fixture(scope="module")
+def c1():
+    cfg = synth.config("C1")
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    return cfg, g, rows, _ctx(g)
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cfg = synth.config("C2")
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    return cfg, g, rows, _ctx(g)
+
+
+# ----------------------------------------------------------------------------- C1
+
+@pytest.mark.parametrize("g_idx", range(6))
+def test_c1_batches(c1, g_idx):
+    cfg, g, rows, ctx = c1
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, g_idx), cfg.fanouts, synth.rng_seed(cfg, g_idx), rows,
+                    check_invariants=True)
+
+
+@pytest.mark.parametrize("fanouts", [
+    [[-1, -1, -1], [-1, -1, -1]],          # full neighbourhoods (BFS closed form)
+    [[0, 0, 0]],                           # no edges
+    [[-1, 3, 0], [2, -1, 5]],              # mixed
+    [[1, 1, 1], [1, 1, 1], [1, 1, 1]],     # 3 hops of k = 1
+    [[150, 150, 150]],                     # k > fast-path limit (generic selection)
+    [[113, 40, 112]],                      # around the fast-path boundary
+])
+def test_c1_fanouts(c1, fanouts):
+    cfg, g, rows, ctx = c1
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 3)[:32], fanouts, 777, rows, check_invariants=True)
+
+
+def test_c1_mixed_type_seeds_and_order(c1):
+    cfg, g, rows, ctx = c1
+    seeds = np.array([6000 + 5, 17, 6000 + 1, 3, 5999, 6000 + 3999, 0], np.int64)
+    run_and_compare(ctx, g, cfg, seeds, cfg.fanouts, 9, rows, check_invariants=True)
+
+
+def test_c1_empty_and_single(c1):
+    cfg, g, rows, ctx = c1
+    run_and_compare(ctx, g, cfg, np.zeros(0, np.int64), cfg.fanouts, 1, rows)
+    run_and_compare(ctx, g, cfg, np.array([42], np.int64), cfg.fanouts, 2, rows)
+
+
+def test_c1_large_batch_all_type_a(c1):
+    # every type-A vertex as a seed: many tiles in every kernel
+    cfg, g, rows, ctx = c1
+    seeds = np.random.default_rng(0).permutation(6000).astype(np.int64)
+    run_and_compare(ctx, g, cfg, seeds, cfg.fanouts, 31337, rows, check_invariants=True)
+
+
+def test_c1_errors_then_recovers(c1):
+    from paper_2112_15345_b200 import EgError
+    import torch
+    cfg, g, rows, ctx = c1
+    with pytest.raises(EgError) as e:
+        ctx.sample_blocks(torch.tensor([5, 10_000], device="cuda:0"), cfg.fanouts, 0)
+    assert e.value.code == -2                                  # EG_ERANGE
+    with pytest.raises(EgError) as e:
+        ctx.sample_blocks(torch.tensor([5, 7, 5], device="cuda:0"), cfg.fanouts, 0)
+    assert e.value.code == -1                                  # EG_EINVAL (duplicate)
+    with pytest.raises(EgError):
+        ctx.sample_blocks(torch.tensor([5], device="cuda:0"), [[5, -2, 5]], 0)
+    # the per-context compaction state is clean again
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 1), cfg.fanouts, synth.rng_seed(cfg, 1), rows)
+
+
+def test_c1_host_seeds_and_host_output(c1):
+    cfg, g, rows, ctx = c1
+    seeds = synth.batch_seeds(cfg, 4)
+    rs = synth.rng_seed(cfg, 4)
+    res = oracle.sample(g, seeds, cfg.fanouts, rs)
+    blocks = ctx.sample_blocks(seeds, cfg.fanouts, rs)            # numpy host seeds
+    assert_same_batch(res, blocks, cfg.n_vt, cfg.n_rel)
+    outs = [np.empty((blocks.n_inputs(u), 16), np.float32) for u in range(2)]
+    ctx.gather_features(blocks, out=outs)                          # host outputs
+    for u in range(2):
+        assert outs[u].tobytes() == oracle.gather(res, cfg.vt_counts, u, rows[u]).tobytes()
+
+
+def test_c1_deterministic(c1):
+    import torch
+    cfg, g, rows, ctx = c1
+    s = torch.from_numpy(synth.batch_seeds(cfg, 5)).cuda()
+    a = ctx.sample_blocks(s, cfg.fanouts, 5)
+    b = ctx.sample_blocks(s, cfg.fanouts, 5)
+    for h in range(2):
+        for r in range(3):
+            assert torch.equal(a[h].eids[r], b[h].eids[r]) and torch.equal(a[h].indices[r], b[h].indices[r])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_c1_world_invariance(c1, world):
+    cfg, g, rows, _ = c1
+    ctxs = _world(g, world)
+    for p, ctx in enumerate(ctxs):
+        gi = p + 10
+        run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi), rows)
+
+
+# ----------------------------------------------------------------------------- C2 (bench workload)
+
+@pytest.mark.parametrize("g_idx", range(3))
+def test_c2_full_batches(c2, g_idx):
+    cfg, g, rows, ctx = c2
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, g_idx), cfg.fanouts, synth.rng_seed(cfg, g_idx), rows,
+                    check_invariants=(g_idx == 0))
+
+
+def test_c2_world4_invariance(c2):
+    cfg, g, rows, _ = c2
+    ctxs = _world(g, 4)
+    for p in (0, 3):
+        run_and_compare(ctxs[p], g, cfg, synth.batch_seeds(cfg, 20 + p), cfg.fanouts, synth.rng_seed(cfg, 20 + p),
+                        rows)
+
+
+# ----------------------------------------------------------------------------- C3 (3 hops, hub of degree 618k)
+
+def test_c3_full_batch():
+    cfg = synth.config("C3")
+    g = synth.build_host_graph(cfg)
+    rows = {0: synth.host_features(cfg, 0)}
+    ctx = _ctx(g)
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 0), cfg.fanouts, synth.rng_seed(cfg, 0), rows)
+    # the hub (max in-degree) as a seed: selection over 6e5 keys
+    hub = int(np.argmax(np.diff(g.indptr[0])))
+    run_and_compare(ctx, g, cfg, np.array([hub, 1, 2], np.int64), cfg.fanouts, 123, rows)
+
+
+def test_device_features_match_host_generator():
+    import torch
+    from synth.device import feature_shard
+    for name in ("C1", "C4"):
+        cfg = synth.config(name)
+        t = feature_shard(cfg, 0, 1000, 3000, "cuda:0")
+        torch.cuda.synchronize()
+        assert t.cpu().numpy().tobytes() == synth.host_features(cfg, 0, 1000, 3000).tobytes()
