@@ -242,29 +242,28 @@ def run_ours(args, cfg, rank, world, local_rank):
     rngs = [synth.rng_seed(cfg, b * world + rank) for b in range(steps)]
     seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
     fanouts = np.array(cfg.fanouts, np.int32)
-    # feature outputs: preallocated at the batch upper bound, reused every step
-    caps_nodes, _ = __import__("paper_2112_15345_b200").batch_caps(
-        cfg.vt_counts, [r[1] for r in cfg.rels], [r[2] for r in cfg.rels], [r[3] for r in cfg.rels],
-        [cfg.dmax(r) for r in range(cfg.n_rel)], cfg.batch, fanouts)
-    outs = [None] * cfg.n_vt
-    for u in cfg.feats:
-        dim, dt = cfg.feats[u]
-        outs[u] = torch.empty((int(caps_nodes[u]), dim), dtype=torch.float32 if dt == 0 else torch.float16,
-                              device=dev)
     row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
     torch.cuda.synchronize(dev)
 
-    def step(b):
-        blocks = ctx.sample_blocks(seeds_dev[b], fanouts, rngs[b])
-        ctx.gather_features(blocks, out=outs)
-        e = blocks.nnz()
-        rows = [blocks.n_inputs(u) for u in range(cfg.n_vt)]
-        blocks.free()
+    def launch(b, seeds):
+        # one CUDA-graph launch: sample + compact all hops + gather features; no host sync
+        return ctx.sample_minibatch(seeds[b], fanouts, rngs[b], features=True, async_=True)
+
+    def retire(bl):
+        bl.wait()
+        e = bl.nnz()
+        rows = [bl.n_inputs(u) for u in range(cfg.n_vt)]
         return e, rows
 
     with torch.cuda.stream(stream):
-        for b in range(W):
-            step(b)
+        pend = launch(0, seeds_dev)
+        for b in range(1, W):
+            nxt = launch(b, seeds_dev)
+            retire(pend)
+            pend.free()
+            pend = nxt
+        retire(pend)
+        pend.free()
         torch.cuda.synchronize(dev)
         if world > 1:
             torch.distributed.barrier()
@@ -280,10 +279,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         ev0.record(stream)
         edges = 0
         gbytes = 0
+        pend = launch(W, seeds_dev)
         for b in range(W, steps):
-            e, rows = step(b)
+            nxt = launch(b + 1, seeds_dev) if b + 1 < steps else None
+            e, rows = retire(pend)
+            pend.free()
             edges += e
             gbytes += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
+            pend = nxt
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -308,15 +311,29 @@ def run_ours(args, cfg, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         pinned_seeds = [torch.from_numpy(s).pin_memory() for s in seeds_host]
+        caps_nodes, _ = __import__("paper_2112_15345_b200").batch_caps(
+            cfg.vt_counts, [r[1] for r in cfg.rels], [r[2] for r in cfg.rels], [r[3] for r in cfg.rels],
+            [cfg.dmax(r) for r in range(cfg.n_rel)], cfg.batch, fanouts)
         host_outs = [None] * cfg.n_vt
         for u in cfg.feats:
-            host_outs[u] = torch.empty(tuple(outs[u].shape), dtype=outs[u].dtype).pin_memory()
+            dim, dt = cfg.feats[u]
+            host_outs[u] = torch.empty((int(caps_nodes[u]), dim),
+                                       dtype=torch.float32 if dt == 0 else torch.float16).pin_memory()
+
+        def e2e_retire(bl):
+            e, rows = retire(bl)
+            nbytes = 0
+            for u in cfg.feats:
+                f = bl.features(u)
+                host_outs[u][:rows[u]].copy_(f, non_blocking=True)
+                nbytes += rows[u] * row_bytes[u]
+            return e, nbytes
+
         with torch.cuda.stream(stream):
-            for b in range(min(W, 2)):
-                bl = ctx.sample_blocks(pinned_seeds[b], fanouts, rngs[b])
-                ctx.gather_features(bl, out=host_outs)
-                bl.free()
+            pend = launch(0, pinned_seeds)
+            e2e_retire(pend)
             torch.cuda.synchronize(dev)
+            pend.free()
             if world > 1:
                 torch.distributed.barrier()
             h2d = d2h = 0
@@ -324,15 +341,22 @@ def run_ours(args, cfg, rank, world, local_rank):
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
+            pend = launch(W, pinned_seeds)
+            done = []
             for b in range(W, steps):
-                bl = ctx.sample_blocks(pinned_seeds[b], fanouts, rngs[b])
-                ctx.gather_features(bl, out=host_outs)
-                e_edges += bl.nnz()
+                nxt = launch(b + 1, pinned_seeds) if b + 1 < steps else None
+                e, nb = e2e_retire(pend)
+                e_edges += e
                 h2d += pinned_seeds[b].numel() * 8
-                d2h += sum(bl.n_inputs(u) * row_bytes[u] for u in cfg.feats) + 576
-                bl.free()
+                d2h += nb + 576
+                done.append(pend)
+                if len(done) > 1:
+                    done.pop(0).free()
+                pend = nxt
             t1.record(stream)
             torch.cuda.synchronize(dev)
+            for bl in done:
+                bl.free()
             ems = t0.elapsed_time(t1)
         if world > 1:
             import torch.distributed as dist
@@ -343,13 +367,13 @@ def run_ours(args, cfg, rank, world, local_rank):
             ems, e_edges = float(m[0]), float(t[1])
         e2e = {"value": e_edges / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
                "d2h_bytes_per_step": d2h // K,
-               "note": "seeds from pinned host memory in, gathered feature rows out to pinned host memory "
-                       "(blocks stay device-resident), through eg_sample_blocks / eg_gather_features"}
+               "note": "seeds from pinned host memory in (H2D inside eg_sample_minibatch), gathered feature rows "
+                       "out to pinned host memory (D2H), per-batch counters read back; blocks stay device-resident"}
 
     # roofline of the gather kernel (events inside the library, on its stream, timed region)
     peak, peak_src = load_peaks()
-    gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])
-    sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])
+    gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])      # gather kernel node, graph-internal events
+    sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])      # sampling + compaction nodes
     achieved = (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     tr = load_traffic(cfg.name)
     roofline = {"kernel": "gather_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

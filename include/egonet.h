@@ -152,6 +152,31 @@ EG_API eg_status eg_attach_peer(eg_ctx *ctx, const eg_ctx *peer);
 EG_API eg_status eg_sample_blocks(eg_ctx *ctx, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
                            const int32_t *fanouts, uint64_t rng_seed, eg_blocks **out);
 
+/* Flags of eg_sample_minibatch. */
+#define EG_FEATURES 1   /* also gather the input vertices' feature rows (library-owned) */
+#define EG_ASYNC 2      /* return right after enqueueing; sizes are resolved by eg_blocks_wait */
+
+/* One whole mini-batch as ONE CUDA-graph launch: sampling + compaction of every hop
+ * and, with EG_FEATURES, the feature gather of the input vertices into buffers the
+ * blocks handle owns (eg_blocks_features).  Same semantics and errors as
+ * eg_sample_blocks (which is this call with flags = 0).  With EG_ASYNC the call
+ * returns after enqueueing on the context's stream (no host synchronisation), so a
+ * caller can enqueue batch b+1 before reading batch b; seed errors are then
+ * reported by eg_blocks_wait (or any accessor).  Batch memory comes from a ring of
+ * slots per (n_hops, fanouts, seed capacity): one device allocation and one
+ * captured graph per slot, reused after eg_blocks_free. */
+EG_API eg_status eg_sample_minibatch(eg_ctx *ctx, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
+                                     const int32_t *fanouts, uint64_t rng_seed, int32_t flags, eg_blocks **out);
+
+/* Wait for an EG_ASYNC batch; returns its status (EG_ERANGE / EG_EINVAL for bad seeds). */
+EG_API eg_status eg_blocks_wait(eg_blocks *blocks);
+
+/* Feature rows gathered by eg_sample_minibatch(EG_FEATURES) for type u (device
+ * pointer, n_rows x row_bytes, valid until eg_blocks_free; NULL / 0 if the type has
+ * no features or the batch was sampled without EG_FEATURES). */
+EG_API eg_status eg_blocks_features(const eg_blocks *blocks, int32_t u, const void **rows, int64_t *n_rows,
+                                    int64_t *row_bytes);
+
 /* Host view of block `hop` (0 <= hop < n_hops).  Pointers stay valid until
  * eg_blocks_free. */
 EG_API eg_status eg_block_view_get(const eg_blocks *blocks, int32_t hop, eg_block_view *out);

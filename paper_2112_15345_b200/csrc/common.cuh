@@ -10,7 +10,7 @@ namespace eg {
 
 constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
-constexpr int kChunkWords = 8192;         // bitmap words per compaction chunk
+constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one CTA)
 constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
 constexpr int kScanBlocks = 256;          // blocks per relation in the two-phase scan
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
@@ -52,7 +52,6 @@ constexpr int kMetaSize = kMetaErr + 8;
 // Everything a hop's kernels touch.
 struct HopDev {
     int32_t h;
-    uint32_t seed_lo, seed_hi;
     int32_t fanout[EG_MAX_REL];
     int64_t *nodes[EG_MAX_VT];       // cumulative node array per type
     int32_t *indptr[EG_MAX_REL];     // block CSC per relation
@@ -64,6 +63,11 @@ struct HopDev {
     int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
     uint32_t *bitmap;                // new-vertex bitmap
     int32_t *chunk_cnt;              // popcount per bitmap chunk
+    int32_t *chunk_pre;              // exclusive prefix of chunk_cnt within the chunk's type
+    uint32_t *ticket;                // last-block-done counter of bitcount_kernel
+    int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
+    int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
+    const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
     int32_t cap_nodes[EG_MAX_VT];    // capacity of nodes[u]
 };
 

@@ -44,23 +44,50 @@ __global__ void __launch_bounds__(256) mark_kernel(const __grid_constant__ Graph
     }
 }
 
-// Popcount of each bitmap chunk.
-__global__ void __launch_bounds__(256) bitcount_kernel(const __grid_constant__ HopDev hd)
+// Popcount of each bitmap chunk (one CTA, one uint4 per thread); the last CTA to
+// finish turns the counts into per-type exclusive prefixes (chunk_pre).
+__global__ void __launch_bounds__(256) bitcount_kernel(const __grid_constant__ GraphDev g,
+                                                       const __grid_constant__ HopDev hd, int32_t n_chunks)
 {
+    static_assert(kChunkWords == 4 * 256, "one uint4 per thread");
     __shared__ int32_t sh[33];
-    const uint4 *w = reinterpret_cast<const uint4 *>(hd.bitmap + (int64_t)blockIdx.x * kChunkWords);
-    int32_t c = 0;
-#pragma unroll 4
-    for (int i = threadIdx.x; i < kChunkWords / 4; i += blockDim.x) {
-        const uint4 x = w[i];
-        c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-    }
+    __shared__ bool last;
+    const uint4 x = reinterpret_cast<const uint4 *>(hd.bitmap + (int64_t)blockIdx.x * kChunkWords)[threadIdx.x];
+    int32_t c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
     c = block_sum(c, sh);
-    if (threadIdx.x == 0) hd.chunk_cnt[blockIdx.x] = c;
+    if (threadIdx.x == 0) {
+        hd.chunk_cnt[blockIdx.x] = c;
+        __threadfence();
+        last = atomicAdd(hd.ticket, 1u) == (uint32_t)n_chunks - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // exclusive scan over all chunks, then rebase each type at its first chunk
+    __shared__ int32_t type_base[EG_MAX_VT];
+    int32_t carry = 0;
+    for (int c0 = 0; c0 < n_chunks; c0 += blockDim.x) {
+        const int ci = c0 + threadIdx.x;
+        const int32_t v = ci < n_chunks ? *((volatile int32_t *)hd.chunk_cnt + ci) : 0;
+        int32_t tot;
+        const int32_t ex = block_excl_scan(v, sh, &tot);
+        if (ci < n_chunks) hd.chunk_pre[ci] = carry + ex;
+        carry += tot;
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (threadIdx.x < g.n_vt) type_base[threadIdx.x] = hd.chunk_pre[g.boff[threadIdx.x] / kChunkBits];
+    __syncthreads();
+    for (int ci = threadIdx.x; ci < n_chunks; ci += blockDim.x) {
+        int u = 0;
+        while ((int64_t)ci * kChunkBits >= g.boff[u + 1]) ++u;
+        hd.chunk_pre[ci] -= type_base[u];
+    }
+    if (threadIdx.x == 0) *hd.ticket = 0;   // ready for the next hop
 }
 
 // New vertices of each chunk, in gid order: append to the node array of their type,
-// set pos[], clear the bitmap words.
+// set pos[], clear the bitmap words.  One CTA per chunk, 4 words per thread.
 __global__ void __launch_bounds__(256) emit_kernel(const __grid_constant__ GraphDev g,
                                                    const __grid_constant__ HopDev hd)
 {
@@ -71,29 +98,26 @@ __global__ void __launch_bounds__(256) emit_kernel(const __grid_constant__ Graph
     const int64_t bit0 = (int64_t)c * kChunkBits;
     int u = 0;
     while (bit0 >= g.boff[u + 1]) ++u;
-    const int fc = (int)(g.boff[u] / kChunkBits);
-    int32_t s = 0;
-    for (int j = fc + threadIdx.x; j < c; j += blockDim.x) s += hd.chunk_cnt[j];
-    const int32_t prior = block_sum(s, sh);
+    const int32_t prior = hd.chunk_pre[c];
     const int32_t nF = meta_nodes(hd.meta, hd.h)[u];
-    const int64_t goff = g.off[u] - g.boff[u];   // gid = goff + bit index
-    int64_t *nodes = hd.nodes[u];
-    const int32_t cap = hd.cap_nodes[u];
-    int32_t running = 0;
-    for (int tile = 0; tile < kChunkWords / 256; ++tile) {
-        const int64_t wi = (int64_t)c * kChunkWords + tile * 256 + threadIdx.x;
-        uint32_t word = hd.bitmap[wi];
-        int32_t tot;
-        const int32_t ex = block_excl_scan((int32_t)__popc(word), sh, &tot);
-        if (tot == 0) continue;
-        if (word) {
-            int32_t position = nF + prior + running + ex;
-            const int64_t gbase = goff + wi * 32;
-            hd.bitmap[wi] = 0;
+    const int64_t wi = (int64_t)c * kChunkWords + 4 * threadIdx.x;
+    uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + wi);
+    const uint4 x = *wp;
+    uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    const int32_t pc = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+    int32_t tot;
+    int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
+    if (pc) {
+        const int64_t gbase = (g.off[u] - g.boff[u]) + wi * 32;   // gid of bit 0 of word wi
+        int64_t *nodes = hd.nodes[u];
+        const int32_t cap = hd.cap_nodes[u];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t word = w[q];
             while (word) {
                 const int b = __ffs(word) - 1;
                 word &= word - 1;
-                const int64_t gid = gbase + b;
+                const int64_t gid = gbase + 32 * q + b;
                 if (position < cap) {
                     nodes[position] = gid;
                     hd.pos[gid] = position;
@@ -103,7 +127,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const __grid_constant__ Graph
                 ++position;
             }
         }
-        running += tot;
+        *wp = make_uint4(0, 0, 0, 0);
     }
     if (threadIdx.x == 0) atomicAdd(meta_nodes(hd.meta, hd.h + 1) + u, mine);
 }
@@ -145,9 +169,9 @@ void launch_mark(const GraphDev &g, const HopDev &hd, cudaStream_t s)
     mark_kernel<<<kSMs * 8, 256, 0, s>>>(g, hd);
 }
 
-void launch_bitcount(const GraphDev &, const HopDev &hd, int32_t n_chunks, cudaStream_t s)
+void launch_bitcount(const GraphDev &g, const HopDev &hd, int32_t n_chunks, cudaStream_t s)
 {
-    bitcount_kernel<<<n_chunks, 256, 0, s>>>(hd);
+    bitcount_kernel<<<n_chunks, 256, 0, s>>>(g, hd, n_chunks);
 }
 
 void launch_emit(const GraphDev &g, const HopDev &hd, int32_t n_chunks, cudaStream_t s)

@@ -58,6 +58,37 @@ struct TimedPair {
 
 }  // namespace
 
+// A batch "plan": everything fixed by (hops, fanouts, seed capacity, features):
+// upper bounds, the memory layout of one batch, and its slots.
+struct Slot;
+struct Plan {
+    int32_t n_hops = 0;
+    int32_t fanouts[EG_MAX_HOPS * EG_MAX_REL] = {};
+    int64_t n_cap = 0;
+    bool features = false;
+    int64_t capF[EG_MAX_HOPS + 1][EG_MAX_VT] = {};
+    int64_t capE[EG_MAX_HOPS][EG_MAX_REL] = {};
+    size_t o_meta = 0, o_dyn = 0, o_seeds = 0, total = 0;
+    size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
+    size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
+           o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {};
+    int32_t n_kernels = 0;
+    std::vector<Slot *> slots;
+};
+
+// One batch's worth of device memory with its captured CUDA graph:
+//   H2D {rng_seed, n_seeds} -> memset counters -> seed_split -> per hop (count, scan,
+//   sample, mark, bitcount, emit, relabel) -> reset -> [gather] -> D2H counters.
+struct Slot {
+    Plan *plan = nullptr;
+    char *mem = nullptr;
+    int32_t *h_meta = nullptr;   // pinned
+    uint64_t *h_dyn = nullptr;   // pinned
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t done = nullptr, s0 = nullptr, s1 = nullptr, g0 = nullptr, g1 = nullptr;
+    bool busy = false, used = false, timed = false;
+};
+
 struct eg_ctx {
     int32_t rank = 0, world = 1, device = 0;
     cudaStream_t stream = nullptr;
@@ -76,7 +107,10 @@ struct eg_ctx {
     int32_t *pos = nullptr;
     uint32_t *bitmap = nullptr;
     int32_t *chunk_cnt = nullptr;
+    int32_t *chunk_pre = nullptr;
+    uint32_t *ticket = nullptr;
     int32_t *partial = nullptr;
+    uint64_t *h_dyn = nullptr;   // pinned {rng_seed, n_seeds}
     int32_t n_chunks = 0;
     int32_t *h_meta = nullptr;   // pinned
     std::vector<void *> ipc_bases;
@@ -90,13 +124,19 @@ struct eg_ctx {
     double prof_ms[2] = {0, 0};
     int64_t prof_n[2] = {0, 0};
     int64_t launches = 0;
+    // batch plans (CUDA graphs)
+    std::vector<Plan *> plans;
+    cudaStream_t cap_stream = nullptr;
 };
 
 struct eg_blocks {
     eg_ctx *ctx = nullptr;
+    Slot *slot = nullptr;
     int32_t n_hops = 0, n_vt = 0, n_rel = 0;
-    void *mem = nullptr;
+    bool ready = false;
+    eg_status status = EG_OK;
     int64_t *nodes[EG_MAX_VT] = {};
+    uint8_t *feat[EG_MAX_VT] = {};
     int32_t *indptr[EG_MAX_HOPS][EG_MAX_REL] = {};
     int32_t *indices[EG_MAX_HOPS][EG_MAX_REL] = {};
     int64_t *eids[EG_MAX_HOPS][EG_MAX_REL] = {};
@@ -104,6 +144,8 @@ struct eg_blocks {
     int64_t n_nodes[EG_MAX_HOPS + 1][EG_MAX_VT] = {};
     int64_t nnz[EG_MAX_HOPS][EG_MAX_REL] = {};
 };
+
+
 
 namespace {
 
@@ -343,11 +385,16 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
     c->world = world;
     c->device = device;
     c->stream = (cudaStream_t)stream;
-    if (cudaMallocHost(&c->h_meta, sizeof(int32_t) * kMetaSize) != cudaSuccess) {
+    if (cudaMallocHost(&c->h_meta, sizeof(int32_t) * kMetaSize) != cudaSuccess ||
+        cudaMallocHost(&c->h_dyn, sizeof(uint64_t) * 2) != cudaSuccess) {
         delete c;
         return EG_ENOMEM;
     }
-    // stream-ordered allocations of the batches: keep freed blocks cached in the pool
+    if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return EG_ECUDA;
+    }
+    // stream-ordered allocations (host-output staging): keep freed blocks cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
@@ -442,6 +489,9 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     EG_CUDA(c, cudaMemsetAsync(c->bitmap, 0, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, g.boff[n_vt] / 32),
                                c->stream));
     EG_CUDA(c, cudaMalloc(&c->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&c->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&c->ticket, sizeof(uint32_t)));
+    EG_CUDA(c, cudaMemsetAsync(c->ticket, 0, sizeof(uint32_t), c->stream));
     EG_CUDA(c, cudaMalloc(&c->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
@@ -562,141 +612,325 @@ eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
     return EG_OK;
 }
 
-eg_status eg_sample_blocks(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
-                           const int32_t *fanouts, uint64_t rng_seed, eg_blocks **out)
-{
-    eg_status st = enter(c);
-    if (st) return st;
-    if (!out) return fail(c, EG_EINVAL, "out is null");
-    *out = nullptr;
-    if (!c->loaded || !c->peers_ready) return fail(c, EG_EINVAL, "partition not loaded / peers not imported");
-    if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
-    if (n_seeds < 0 || (n_seeds > 0 && !seeds)) return fail(c, EG_EINVAL, "bad seeds");
-    if (!fanouts) return fail(c, EG_EINVAL, "fanouts is null");
-    const GraphDev &g = c->g;
-    const int V = g.n_vt, R = g.n_rel, L = n_hops;
-    for (int i = 0; i < L * R; ++i)
-        if (fanouts[i] < -1) return fail(c, EG_EINVAL, "fanout must be >= -1");
+}  // extern "C"
 
+namespace {
+
+eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, bool features, Plan **out)
+{
+    const GraphDev &g = c->g;
+    const int V = g.n_vt, R = g.n_rel;
+    for (Plan *p : c->plans)
+        if (p->n_hops == L && p->n_cap == n_cap && p->features == features &&
+            !memcmp(p->fanouts, fanouts, sizeof(int32_t) * L * R)) {
+            *out = p;
+            return EG_OK;
+        }
+    Plan *p = new Plan();
+    p->n_hops = L;
+    memcpy(p->fanouts, fanouts, sizeof(int32_t) * L * R);
+    p->n_cap = n_cap;
+    p->features = features;
     int32_t src_vt[EG_MAX_REL], dst_vt[EG_MAX_REL];
     for (int r = 0; r < R; ++r) {
         src_vt[r] = g.rel[r].src_vt;
         dst_vt[r] = g.rel[r].dst_vt;
     }
-    int64_t capF[EG_MAX_HOPS + 1][EG_MAX_VT], capE[EG_MAX_HOPS][EG_MAX_REL];
-    compute_caps(V, c->vt_counts, R, src_vt, dst_vt, c->rel_edges_total, c->rel_max_degree, n_seeds, L, fanouts,
-                 capF, capE);
+    compute_caps(V, c->vt_counts, R, src_vt, dst_vt, c->rel_edges_total, c->rel_max_degree, n_cap, L, fanouts,
+                 p->capF, p->capE);
     for (int h = 0; h <= L; ++h)
         for (int u = 0; u < V; ++u)
-            if (capF[h][u] >= INT32_MAX) return fail(c, EG_EINVAL, "batch exceeds 2^31 vertices of one type");
+            if (p->capF[h][u] >= INT32_MAX) {
+                delete p;
+                return fail(c, EG_EINVAL, "batch exceeds 2^31 vertices of one type");
+            }
     for (int h = 0; h < L; ++h)
         for (int r = 0; r < R; ++r)
-            if (capE[h][r] >= INT32_MAX) return fail(c, EG_EINVAL, "batch exceeds 2^31 edges of one relation");
-
-    // one stream-ordered allocation for the whole batch
-    const bool host_seeds = n_seeds > 0 && !is_device_ptr(seeds);
+            if (p->capE[h][r] >= INT32_MAX) {
+                delete p;
+                return fail(c, EG_EINVAL, "batch exceeds 2^31 edges of one relation");
+            }
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
         off = align_up(off + std::max<size_t>(bytes, 1), 256);
         return o;
     };
-    const size_t o_meta = take(sizeof(int32_t) * kMetaSize);
-    const size_t o_seeds = host_seeds ? take(sizeof(int64_t) * n_seeds) : 0;
-    size_t o_nodes[EG_MAX_VT], o_ip[EG_MAX_HOPS][EG_MAX_REL], o_ix[EG_MAX_HOPS][EG_MAX_REL],
-        o_ei[EG_MAX_HOPS][EG_MAX_REL], o_src[EG_MAX_HOPS][EG_MAX_REL];
-    for (int u = 0; u < V; ++u) o_nodes[u] = take(sizeof(int64_t) * capF[L][u]);
+    p->o_meta = take(sizeof(int32_t) * kMetaSize);
+    p->o_dyn = take(sizeof(uint64_t) * 2);
+    p->o_seeds = take(sizeof(int64_t) * n_cap);
+    for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
     for (int h = 0; h < L; ++h)
         for (int r = 0; r < R; ++r) {
-            o_ip[h][r] = take(sizeof(int32_t) * (capF[h][dst_vt[r]] + 1));
-            o_ix[h][r] = take(sizeof(int32_t) * capE[h][r]);
-            o_ei[h][r] = take(sizeof(int64_t) * capE[h][r]);
-            o_src[h][r] = take(sizeof(uint32_t) * capE[h][r]);
+            const int64_t nd = p->capF[h][dst_vt[r]] + 1;
+            p->o_ip[h][r] = take(sizeof(int32_t) * nd);
+            p->o_ix[h][r] = take(sizeof(int32_t) * p->capE[h][r]);
+            p->o_ei[h][r] = take(sizeof(int64_t) * p->capE[h][r]);
+            p->o_src[h][r] = take(sizeof(uint32_t) * p->capE[h][r]);
+            p->o_ib[h][r] = take(sizeof(int64_t) * nd);
+            p->o_id[h][r] = take(sizeof(int32_t) * nd);
         }
-    eg_blocks *b = new eg_blocks();
-    b->ctx = c;
-    b->n_hops = L;
-    b->n_vt = V;
-    b->n_rel = R;
-    cudaError_t e = cudaMallocAsync(&b->mem, off, c->stream);
-    if (e != cudaSuccess) {
-        delete b;
-        cudaGetLastError();
-        return fail(c, EG_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
-    }
-    char *base = (char *)b->mem;
-    b->meta = (int32_t *)(base + o_meta);
-    for (int u = 0; u < V; ++u) b->nodes[u] = (int64_t *)(base + o_nodes[u]);
-    uint32_t *srcbuf[EG_MAX_HOPS][EG_MAX_REL];
-    for (int h = 0; h < L; ++h)
-        for (int r = 0; r < R; ++r) {
-            b->indptr[h][r] = (int32_t *)(base + o_ip[h][r]);
-            b->indices[h][r] = (int32_t *)(base + o_ix[h][r]);
-            b->eids[h][r] = (int64_t *)(base + o_ei[h][r]);
-            srcbuf[h][r] = (uint32_t *)(base + o_src[h][r]);
-        }
-    TimedPair tp;
-    record_start(c, &tp, 0);
-    const int64_t *d_seeds = seeds;
-    if (host_seeds) {
-        d_seeds = (const int64_t *)(base + o_seeds);
-        EG_CUDA(c, cudaMemcpyAsync((void *)d_seeds, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice,
-                                   c->stream));
-    }
-    EG_CUDA(c, cudaMemsetAsync(b->meta, 0, sizeof(int32_t) * kMetaSize, c->stream));
+    if (features)
+        for (int u = 0; u < V; ++u)
+            if (c->f.row_bytes[u]) p->o_feat[u] = take((size_t)(p->capF[L][u] * c->f.row_bytes[u]));
+    p->total = off;
+    c->plans.push_back(p);
+    *out = p;
+    return EG_OK;
+}
 
-    HopDev hd{};
-    hd.seed_lo = (uint32_t)rng_seed;
-    hd.seed_hi = (uint32_t)(rng_seed >> 32);
-    for (int u = 0; u < V; ++u) {
-        hd.nodes[u] = b->nodes[u];
-        hd.cap_nodes[u] = (int32_t)capF[L][u];
+void fill_views(const Plan *p, char *base, eg_blocks *b)
+{
+    b->meta = (int32_t *)(base + p->o_meta);
+    for (int u = 0; u < b->n_vt; ++u) {
+        b->nodes[u] = (int64_t *)(base + p->o_nodes[u]);
+        b->feat[u] = p->o_feat[u] ? (uint8_t *)(base + p->o_feat[u]) : nullptr;
     }
-    hd.meta = b->meta;
+    for (int h = 0; h < p->n_hops; ++h)
+        for (int r = 0; r < b->n_rel; ++r) {
+            b->indptr[h][r] = (int32_t *)(base + p->o_ip[h][r]);
+            b->indices[h][r] = (int32_t *)(base + p->o_ix[h][r]);
+            b->eids[h][r] = (int64_t *)(base + p->o_ei[h][r]);
+        }
+}
+
+// Record the whole batch into a CUDA graph (once per slot).
+eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
+{
+    const GraphDev &g = c->g;
+    const int V = g.n_vt, R = g.n_rel, L = p->n_hops;
+    char *base = sl->mem;
+    cudaStream_t cs = c->cap_stream;
+    HopDev hd{};
+    hd.dyn = (const uint64_t *)(base + p->o_dyn);
+    hd.meta = (int32_t *)(base + p->o_meta);
     hd.partial = c->partial;
     hd.pos = c->pos;
     hd.bitmap = c->bitmap;
     hd.chunk_cnt = c->chunk_cnt;
-    launch_seed_split(g, d_seeds, n_seeds, hd, c->stream);
-    c->launches += 1;
+    hd.chunk_pre = c->chunk_pre;
+    hd.ticket = c->ticket;
+    for (int u = 0; u < V; ++u) {
+        hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
+        hd.cap_nodes[u] = (int32_t)p->capF[L][u];
+    }
+    int nk = 0;
+    EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    cudaMemcpyAsync((void *)hd.dyn, sl->h_dyn, sizeof(uint64_t) * 2, cudaMemcpyHostToDevice, cs);
+    cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
+    cudaMemsetAsync(hd.meta, 0, sizeof(int32_t) * kMetaSize, cs);
+    launch_seed_split(g, (const int64_t *)(base + p->o_seeds), hd, cs);
+    ++nk;
     for (int h = 0; h < L; ++h) {
         hd.h = h;
         for (int r = 0; r < R; ++r) {
-            hd.fanout[r] = fanouts[h * R + r];
-            hd.indptr[r] = b->indptr[h][r];
-            hd.indices[r] = b->indices[h][r];
-            hd.eids[r] = b->eids[h][r];
-            hd.src[r] = srcbuf[h][r];
+            hd.fanout[r] = p->fanouts[h * R + r];
+            hd.indptr[r] = (int32_t *)(base + p->o_ip[h][r]);
+            hd.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
+            hd.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
+            hd.src[r] = (uint32_t *)(base + p->o_src[h][r]);
+            hd.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
+            hd.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
         }
-        launch_count(g, hd, c->stream);
-        launch_scan(g, hd, c->stream);
-        launch_sample(g, hd, c->stream);
-        launch_mark(g, hd, c->stream);
-        launch_bitcount(g, hd, c->n_chunks, c->stream);
-        launch_emit(g, hd, c->n_chunks, c->stream);
-        launch_relabel(g, hd, c->stream);
-        c->launches += 7;
+        launch_count(g, hd, cs);
+        launch_scan(g, hd, cs);
+        launch_sample(g, hd, cs);
+        launch_mark(g, hd, cs);
+        launch_bitcount(g, hd, c->n_chunks, cs);
+        launch_emit(g, hd, c->n_chunks, cs);
+        launch_relabel(g, hd, cs);
+        nk += 7;
     }
-    launch_reset(g, hd, L, c->stream);
-    c->launches += 1;
-    EG_CUDA(c, cudaGetLastError());
-    record_end(c, &tp);
-    EG_CUDA(c, cudaMemcpyAsync(c->h_meta, b->meta, sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, c->stream));
-    EG_CUDA(c, cudaStreamSynchronize(c->stream));
-    const int32_t errbits = c->h_meta[kMetaErr];
-    for (int l = 0; l <= L; ++l)
-        for (int u = 0; u < V; ++u) b->n_nodes[l][u] = c->h_meta[kMetaNodes + l * EG_MAX_VT + u];
-    for (int h = 0; h < L; ++h)
-        for (int r = 0; r < R; ++r) b->nnz[h][r] = c->h_meta[kMetaNnz + h * EG_MAX_REL + r];
-    if (errbits) {
-        cudaFreeAsync(b->mem, c->stream);
-        delete b;
-        if (errbits & kErrSeedRange) return fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
-        if (errbits & kErrSeedDup) return fail(c, EG_EINVAL, "duplicate seeds");
-        return fail(c, EG_EINVAL, "internal capacity overflow");
+    launch_reset(g, hd, L, cs);
+    ++nk;
+    cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
+    if (p->features) {
+        GatherDev gd{};
+        gd.meta = hd.meta;
+        gd.level = L;
+        bool any = false;
+        for (int u = 0; u < V; ++u) {
+            gd.nodes[u] = hd.nodes[u];
+            gd.out[u] = p->o_feat[u] ? (uint8_t *)(base + p->o_feat[u]) : nullptr;
+            any |= gd.out[u] != nullptr;
+        }
+        cudaEventRecordWithFlags(sl->g0, cs, cudaEventRecordExternal);
+        if (any) {
+            launch_gather(g, c->f, gd, cs);
+            ++nk;
+        }
+        cudaEventRecordWithFlags(sl->g1, cs, cudaEventRecordExternal);
+    }
+    cudaMemcpyAsync(sl->h_meta, hd.meta, sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, cs);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&sl->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    p->n_kernels = nk;
+    return EG_OK;
+}
+
+eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
+{
+    for (Slot *sl : p->slots)
+        if (!sl->busy) {
+            if (sl->used) EG_CUDA(c, cudaEventSynchronize(sl->done));   // its last run has retired
+            sl->busy = true;
+            *out = sl;
+            return EG_OK;
+        }
+    Slot *sl = new Slot();
+    sl->plan = p;
+    cudaError_t e = cudaMalloc(&sl->mem, p->total);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete sl;
+        return fail(c, EG_ENOMEM, std::string("batch slot cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    EG_CUDA(c, cudaMallocHost(&sl->h_meta, sizeof(int32_t) * kMetaSize));
+    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 2));
+    EG_CUDA(c, cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming));
+    EG_CUDA(c, cudaEventCreate(&sl->s0));
+    EG_CUDA(c, cudaEventCreate(&sl->s1));
+    EG_CUDA(c, cudaEventCreate(&sl->g0));
+    EG_CUDA(c, cudaEventCreate(&sl->g1));
+    p->slots.push_back(sl);
+    eg_status st = capture_slot(c, p, sl);
+    if (st) return st;
+    sl->busy = true;
+    *out = sl;
+    return EG_OK;
+}
+
+void destroy_plans(eg_ctx *c)
+{
+    for (Plan *p : c->plans) {
+        for (Slot *sl : p->slots) {
+            if (sl->exec) cudaGraphExecDestroy(sl->exec);
+            cudaFree(sl->mem);
+            cudaFreeHost(sl->h_meta);
+            cudaFreeHost(sl->h_dyn);
+            for (cudaEvent_t ev : {sl->done, sl->s0, sl->s1, sl->g0, sl->g1})
+                if (ev) cudaEventDestroy(ev);
+            delete sl;
+        }
+        delete p;
+    }
+    c->plans.clear();
+}
+
+// Resolve a pending batch: wait for its counters, read sizes and error bits.
+eg_status finish(eg_blocks *b)
+{
+    if (b->ready) return b->status;
+    eg_ctx *c = b->ctx;
+    Slot *sl = b->slot;
+    cudaError_t e = cudaEventSynchronize(sl->done);
+    b->ready = true;
+    if (e != cudaSuccess) return b->status = fail(c, EG_ECUDA, std::string("batch: ") + cudaGetErrorString(e));
+    const int32_t *m = sl->h_meta;
+    for (int l = 0; l <= b->n_hops; ++l)
+        for (int u = 0; u < b->n_vt; ++u) b->n_nodes[l][u] = m[kMetaNodes + l * EG_MAX_VT + u];
+    for (int h = 0; h < b->n_hops; ++h)
+        for (int r = 0; r < b->n_rel; ++r) b->nnz[h][r] = m[kMetaNnz + h * EG_MAX_REL + r];
+    if (sl->timed) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, sl->s0, sl->s1) == cudaSuccess) {
+            c->prof_ms[0] += ms;
+            c->prof_n[0] += 1;
+        }
+        if (sl->plan->features && cudaEventElapsedTime(&ms, sl->g0, sl->g1) == cudaSuccess) {
+            c->prof_ms[1] += ms;
+            c->prof_n[1] += 1;
+        }
+        sl->timed = false;
+    }
+    const int32_t errbits = m[kMetaErr];
+    if (errbits & kErrSeedRange) return b->status = fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
+    if (errbits & kErrSeedDup) return b->status = fail(c, EG_EINVAL, "duplicate seeds");
+    if (errbits) return b->status = fail(c, EG_EINVAL, "internal capacity overflow");
+    return b->status = EG_OK;
+}
+
+int64_t round_cap(int64_t n)
+{
+    int64_t c = 64;
+    while (c < n) c <<= 1;
+    return c;
+}
+
+eg_status enqueue_batch(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops, const int32_t *fanouts,
+                        uint64_t rng_seed, bool features, eg_blocks **out)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!out) return fail(c, EG_EINVAL, "out is null");
+    *out = nullptr;
+    if (!c->loaded || !c->peers_ready) return fail(c, EG_EINVAL, "partition not loaded / peers not mapped");
+    if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
+    if (n_seeds < 0 || (n_seeds > 0 && !seeds)) return fail(c, EG_EINVAL, "bad seeds");
+    if (!fanouts) return fail(c, EG_EINVAL, "fanouts is null");
+    for (int i = 0; i < n_hops * c->g.n_rel; ++i)
+        if (fanouts[i] < -1) return fail(c, EG_EINVAL, "fanout must be >= -1");
+    Plan *p = nullptr;
+    if ((st = get_plan(c, n_hops, fanouts, round_cap(n_seeds), features, &p))) return st;
+    Slot *sl = nullptr;
+    if ((st = acquire_slot(c, p, &sl))) return st;
+    if (n_seeds > 0)
+        EG_CUDA(c, cudaMemcpyAsync(sl->mem + p->o_seeds, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyDefault,
+                                   c->stream));
+    sl->h_dyn[0] = rng_seed;
+    sl->h_dyn[1] = (uint64_t)n_seeds;
+    sl->timed = c->prof;
+    EG_CUDA(c, cudaGraphLaunch(sl->exec, c->stream));
+    EG_CUDA(c, cudaEventRecord(sl->done, c->stream));
+    sl->used = true;
+    c->launches += p->n_kernels;
+    eg_blocks *b = new eg_blocks();
+    b->ctx = c;
+    b->slot = sl;
+    b->n_hops = n_hops;
+    b->n_vt = c->g.n_vt;
+    b->n_rel = c->g.n_rel;
+    fill_views(p, sl->mem, b);
+    *out = b;
+    return EG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+eg_status eg_sample_blocks(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
+                           const int32_t *fanouts, uint64_t rng_seed, eg_blocks **out)
+{
+    return eg_sample_minibatch(c, seeds, n_seeds, n_hops, fanouts, rng_seed, 0, out);
+}
+
+eg_status eg_sample_minibatch(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
+                              const int32_t *fanouts, uint64_t rng_seed, int32_t flags, eg_blocks **out)
+{
+    eg_blocks *b = nullptr;
+    eg_status st = enqueue_batch(c, seeds, n_seeds, n_hops, fanouts, rng_seed, (flags & EG_FEATURES) != 0, &b);
+    if (st) return st;
+    if (!(flags & EG_ASYNC)) {
+        st = finish(b);
+        if (st) {
+            eg_blocks_free(b);
+            return st;
+        }
     }
     *out = b;
     return EG_OK;
+}
+
+eg_status eg_blocks_wait(eg_blocks *b)
+{
+    if (!b) return EG_EINVAL;
+    cudaSetDevice(b->ctx->device);
+    return finish(b);
 }
 
 int32_t eg_blocks_n_hops(const eg_blocks *b) { return b ? b->n_hops : 0; }
@@ -704,12 +938,16 @@ int32_t eg_blocks_n_hops(const eg_blocks *b) { return b ? b->n_hops : 0; }
 int64_t eg_blocks_n_inputs(const eg_blocks *b, int32_t u)
 {
     if (!b || u < 0 || u >= b->n_vt) return -1;
+    if (finish(const_cast<eg_blocks *>(b))) return -1;
     return b->n_nodes[b->n_hops][u];
 }
 
-eg_status eg_block_view_get(const eg_blocks *b, int32_t hop, eg_block_view *v)
+eg_status eg_block_view_get(const eg_blocks *cb, int32_t hop, eg_block_view *v)
 {
-    if (!b || !v || hop < 0 || hop >= b->n_hops) return EG_EINVAL;
+    if (!cb || !v || hop < 0 || hop >= cb->n_hops) return EG_EINVAL;
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    eg_status st = finish(b);
+    if (st) return st;
     memset(v, 0, sizeof(*v));
     v->hop = hop;
     v->n_vt = b->n_vt;
@@ -729,11 +967,25 @@ eg_status eg_block_view_get(const eg_blocks *b, int32_t hop, eg_block_view *v)
     return EG_OK;
 }
 
-eg_status eg_gather_features(eg_ctx *c, const eg_blocks *b, void *const *out)
+eg_status eg_blocks_features(const eg_blocks *cb, int32_t u, const void **rows, int64_t *n_rows, int64_t *row_bytes)
+{
+    if (!cb || u < 0 || u >= cb->n_vt || !rows || !n_rows || !row_bytes) return EG_EINVAL;
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    eg_status st = finish(b);
+    if (st) return st;
+    *rows = b->feat[u];
+    *n_rows = b->feat[u] ? b->n_nodes[b->n_hops][u] : 0;
+    *row_bytes = b->feat[u] ? b->ctx->f.row_bytes[u] : 0;
+    return EG_OK;
+}
+
+eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
 {
     eg_status st = enter(c);
     if (st) return st;
-    if (!b || !out || b->ctx != c) return fail(c, EG_EINVAL, "bad blocks / out");
+    if (!cb || !out || cb->ctx != c) return fail(c, EG_EINVAL, "bad blocks / out");
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    if ((st = finish(b))) return st;
     GatherDev gd{};
     gd.meta = b->meta;
     gd.level = b->n_hops;
@@ -776,11 +1028,7 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *b, void *const *out)
 eg_status eg_blocks_free(eg_blocks *b)
 {
     if (!b) return EG_OK;
-    eg_ctx *c = b->ctx;
-    if (c && !c->broken) {
-        cudaSetDevice(c->device);
-        cudaFreeAsync(b->mem, c->stream);
-    }
+    if (b->slot) b->slot->busy = false;   // reuse waits for the slot's last run to retire
     delete b;
     return EG_OK;
 }
@@ -812,10 +1060,15 @@ eg_status eg_destroy(eg_ctx *c)
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     drain_timing(c);
+    destroy_plans(c);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
     cudaFree(c->pos);
     cudaFree(c->bitmap);
     cudaFree(c->chunk_cnt);
+    cudaFree(c->chunk_pre);
+    cudaFree(c->ticket);
+    cudaFreeHost(c->h_dyn);
     cudaFree(c->partial);
     cudaFreeHost(c->h_meta);
     delete c;

@@ -5,7 +5,7 @@
 namespace eg {
 
 // sample.cu
-void launch_seed_split(const GraphDev &g, const int64_t *seeds, int64_t n, const HopDev &hd, cudaStream_t s);
+void launch_seed_split(const GraphDev &g, const int64_t *seeds, const HopDev &hd, cudaStream_t s);
 void launch_count(const GraphDev &g, const HopDev &hd, cudaStream_t s);
 void launch_scan(const GraphDev &g, const HopDev &hd, cudaStream_t s);
 void launch_sample(const GraphDev &g, const HopDev &hd, cudaStream_t s);

@@ -15,9 +15,10 @@ namespace eg {
 // Seeds (caller order, mixed types) -> F_0[u] (stable per type) + pos[] for the
 // dst-prefix relabel; flags out-of-range and duplicate seeds.  One CTA.
 __global__ void __launch_bounds__(1024) seed_split_kernel(const __grid_constant__ GraphDev g,
-                                                          const int64_t *__restrict__ seeds, int64_t n,
+                                                          const int64_t *__restrict__ seeds,
                                                           const __grid_constant__ HopDev hd)
 {
+    const int64_t n = (int64_t)hd.dyn[1];
     __shared__ int32_t sh[33];
     __shared__ int32_t base[EG_MAX_VT];
     if (threadIdx.x < EG_MAX_VT) base[threadIdx.x] = 0;
@@ -57,9 +58,9 @@ __global__ void __launch_bounds__(1024) seed_split_kernel(const __grid_constant_
         meta_nodes(hd.meta, 0)[threadIdx.x] = min(base[threadIdx.x], hd.cap_nodes[threadIdx.x]);
 }
 
-void launch_seed_split(const GraphDev &g, const int64_t *seeds, int64_t n, const HopDev &hd, cudaStream_t s)
+void launch_seed_split(const GraphDev &g, const int64_t *seeds, const HopDev &hd, cudaStream_t s)
 {
-    seed_split_kernel<<<1, 1024, 0, s>>>(g, seeds, n, hd);
+    seed_split_kernel<<<1, 1024, 0, s>>>(g, seeds, hd);
 }
 
 // ----------------------------------------------------------------------------- counts + scan
@@ -88,8 +89,10 @@ __global__ void __launch_bounds__(256) count_kernel(const __grid_constant__ Grap
             const int p = owner_of(g, t, tid);
             const int64_t x = tid - g.bounds[t][p];
             const int64_t *ip = R.indptr[p];
-            const int64_t d = ip[x + 1] - ip[x];
+            const int64_t b0 = ip[x], d = ip[x + 1] - b0;
             c = (int32_t)((k < 0 || d <= k) ? d : k);
+            hd.ibase[r][i] = ((int64_t)p << 56) | b0;
+            hd.ideg[r][i] = (int32_t)d;
         }
         hd.indptr[r][i] = c;
         sum += c;
@@ -166,7 +169,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 // Generic exact selection for any k < d: binary search of the k-th smallest key
 // value T (33 counting passes over the d keys), then one ascending-j emission
 // pass taking key < T and the first (k - #{key < T}) offsets with key == T.
-__device__ void select_generic(const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
+__device__ __noinline__ void select_generic(const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
                                uint32_t k0, uint32_t k1)
 {
     const int64_t nq = (d + 3) >> 2;
@@ -279,53 +282,95 @@ __device__ void select_fast(const Item &it, int64_t d, int k, uint32_t v_lo, uin
 
 constexpr int kSampleWarps = 8;
 
-__global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const __grid_constant__ GraphDev g,
+// The items of a hop are the (relation, dst) pairs, relation-major.  A warp takes 32
+// consecutive items at a time: lane l loads item l's block row (pos0, cnt) and the
+// CSC row start / degree the count kernel recorded.  Items that take their whole
+// neighbourhood (d <= k or k = -1; most of a power-law graph) are copied as one
+// segmented copy spread over all 32 lanes; items that need a selection (d > k) are
+// then processed one at a time by the whole warp.
+__global__ void __launch_bounds__(kSampleWarps * 32, 4) sample_kernel(const __grid_constant__ GraphDev g,
                                                                    const __grid_constant__ HopDev hd)
 {
     __shared__ uint64_t s_cand[kSampleWarps][kSelCap];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
+    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
     int64_t cum[EG_MAX_REL + 1];
     cum[0] = 0;
     for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + (hd.fanout[r] != 0 ? nF[g.rel[r].dst_vt] : 0);
     const int64_t total = cum[g.n_rel];
-    for (int64_t w = (int64_t)blockIdx.x * kSampleWarps + warp; w < total; w += (int64_t)gridDim.x * kSampleWarps) {
+    for (int64_t g0 = ((int64_t)blockIdx.x * kSampleWarps + warp) * 32; g0 < total;
+         g0 += (int64_t)gridDim.x * kSampleWarps * 32) {
+        const int64_t it = g0 + lane;
         int r = 0;
-        while (w >= cum[r + 1]) ++r;
-        const int64_t i = w - cum[r];
-        const int32_t pos0 = hd.indptr[r][i];
-        const int32_t cnt = hd.indptr[r][i + 1] - pos0;
-        if (cnt == 0) continue;
-        const RelDev &R = g.rel[r];
-        const int t = R.dst_vt;
-        const int64_t v = hd.nodes[t][i];
-        const int64_t tid = v - g.off[t];
-        const int p = owner_of(g, t, tid);
-        const int64_t x = tid - g.bounds[t][p];
-        int64_t base = 0, end = 0;
-        if (lane == 0) {
-            base = R.indptr[p][x];
-            end = R.indptr[p][x + 1];
+        int32_t pos0 = 0, cnt = 0, d = 0;
+        int64_t ib = 0, i = 0;
+        if (it < total) {
+            while (it >= cum[r + 1]) ++r;
+            i = it - cum[r];
+            pos0 = hd.indptr[r][i];
+            cnt = hd.indptr[r][i + 1] - pos0;
+            if (cnt > 0) {
+                ib = hd.ibase[r][i];
+                d = hd.ideg[r][i];
+            }
         }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        end = __shfl_sync(0xffffffffu, end, 0);
-        const int64_t d = end - base;
-        Item it;
-        it.soff = (uint32_t)g.off[R.src_vt];
-        it.ebase = R.edge_base[p] + base;
-        it.ix = R.indices[p] + base;
-        it.src_out = hd.src[r] + pos0;
-        it.eid_out = hd.eids[r] + pos0;
         const int k = hd.fanout[r];
-        if (k < 0 || d <= k) {
-            for (int64_t j = lane; j < d; j += 32) emit_edge(it, (int32_t)j, j);
-        } else {
-            const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
-            if (k <= kSelMaxK)
-                select_fast(it, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, hd.seed_lo, hd.seed_hi,
+        const bool sel = cnt > 0 && k >= 0 && d > k;
+        // ---- segmented copy of the full neighbourhoods of this group
+        const int32_t c = (cnt > 0 && !sel) ? cnt : 0;
+        const int32_t incl = warp_incl_scan(c);
+        const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int32_t excl = incl - c;
+        for (int32_t b = 0; b < tot; b += 32) {
+            const int32_t s = b + lane;
+            int L = 0;   // the lane whose item holds output slot s: last lane with excl <= s
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = L + step;
+                const int32_t ex = __shfl_sync(0xffffffffu, excl, cand & 31);
+                if (cand < 32 && ex <= s) L = cand;
+            }
+            const int32_t exL = __shfl_sync(0xffffffffu, excl, L);
+            const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
+            const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
+            const int rL = __shfl_sync(0xffffffffu, r, L);
+            if (s < tot) {
+                const int p = (int)(ibL >> 56);
+                const int64_t base = ibL & ((1ll << 56) - 1);
+                const int32_t j = s - exL;
+                const RelDev &R = g.rel[rL];
+                hd.src[rL][posL + j] = (uint32_t)g.off[R.src_vt] + (uint32_t)__ldg(R.indices[p] + base + j);
+                hd.eids[rL][posL + j] = R.edge_base[p] + base + j;
+            }
+        }
+        // ---- items that need a selection: one at a time, whole warp
+        uint32_t selmask = __ballot_sync(0xffffffffu, sel);
+        while (selmask) {
+            const int L = __ffs(selmask) - 1;
+            selmask &= selmask - 1;
+            const int rL = __shfl_sync(0xffffffffu, r, L);
+            const int64_t iL = __shfl_sync(0xffffffffu, i, L);
+            const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
+            const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
+            const int32_t dL = __shfl_sync(0xffffffffu, d, L);
+            const RelDev &R = g.rel[rL];
+            const int p = (int)(ibL >> 56);
+            const int64_t base = ibL & ((1ll << 56) - 1);
+            const int64_t v = hd.nodes[R.dst_vt][iL];
+            Item itm;
+            itm.soff = (uint32_t)g.off[R.src_vt];
+            itm.ebase = R.edge_base[p] + base;
+            itm.ix = R.indices[p] + base;
+            itm.src_out = hd.src[rL] + posL;
+            itm.eid_out = hd.eids[rL] + posL;
+            const int kL = hd.fanout[rL];
+            const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)rL;
+            if (kL <= kSelMaxK)
+                select_fast(itm, dL, kL, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi,
                             s_cand[warp]);
             else
-                select_generic(it, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, hd.seed_lo, hd.seed_hi);
+                select_generic(itm, dL, kL, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
         }
     }
 }

@@ -27,8 +27,12 @@ ABI_SYMBOLS = [
     "eg_version", "eg_create", "eg_set_stream", "eg_load_partition", "eg_export_shard", "eg_import_shards",
     "eg_sample_blocks", "eg_block_view_get", "eg_blocks_n_hops", "eg_blocks_n_inputs", "eg_gather_features",
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
-    "eg_range_bounds", "eg_batch_caps", "eg_attach_peer",
+    "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
+    "eg_blocks_features",
 ]
+
+EG_FEATURES = 1
+EG_ASYNC = 2
 
 
 class EgError(RuntimeError):
@@ -81,6 +85,9 @@ def lib(build_if_missing: bool = True):
         L.eg_attach_peer.argtypes = [vp, vp]
         L.eg_sample_blocks.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, P(vp)]
         L.eg_block_view_get.argtypes = [vp, c.c_int32, P(BlockView)]
+        L.eg_sample_minibatch.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, c.c_int32, P(vp)]
+        L.eg_blocks_wait.argtypes = [vp]
+        L.eg_blocks_features.argtypes = [vp, c.c_int32, P(vp), P(c.c_int64), P(c.c_int64)]
         L.eg_blocks_n_hops.argtypes = [vp]
         L.eg_blocks_n_hops.restype = c.c_int32
         L.eg_blocks_n_inputs.argtypes = [vp, c.c_int32]
@@ -179,21 +186,36 @@ class Block:
 
 
 class Blocks:
-    """Handle of one sampled mini-batch (eg_blocks).  Per-hop tensors are built
-    lazily (zero-copy views of library memory) on first access."""
+    """Handle of one sampled mini-batch (eg_blocks).  Sizes are resolved on first
+    use (waiting for an EG_ASYNC batch); per-hop tensors are zero-copy views of
+    library memory built lazily."""
 
     def __init__(self, ctx: "Context", handle: int):
         self._ctx = ctx
         self._h = handle
         self.n_hops = lib().eg_blocks_n_hops(handle)
-        self.views = []
-        for h in range(self.n_hops):
-            v = BlockView()
-            rc = lib().eg_block_view_get(handle, h, ctypes.byref(v))
-            if rc:
-                raise EgError(rc, "eg_block_view_get")
-            self.views.append(v)
+        self._views = None
         self._blocks = [None] * self.n_hops
+
+    def wait(self):
+        rc = lib().eg_blocks_wait(self._h)
+        if rc:
+            raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        return self
+
+    @property
+    def views(self):
+        if self._views is None:
+            self.wait()
+            vs = []
+            for h in range(self.n_hops):
+                v = BlockView()
+                rc = lib().eg_block_view_get(self._h, h, ctypes.byref(v))
+                if rc:
+                    raise EgError(rc, "eg_block_view_get")
+                vs.append(v)
+            self._views = vs
+        return self._views
 
     def __getitem__(self, h) -> Block:
         if self._blocks[h] is None:
@@ -206,20 +228,38 @@ class Blocks:
         return self.n_hops
 
     def nnz(self, h=None) -> int:
+        vs = self.views
         hops = range(self.n_hops) if h is None else [h]
-        return sum(int(self.views[x].nnz[r]) for x in hops for r in range(self.views[x].n_rel))
+        return sum(int(vs[x].nnz[r]) for x in hops for r in range(vs[x].n_rel))
 
     def n_inputs(self, u) -> int:
+        self.views
         return int(lib().eg_blocks_n_inputs(self._h, u))
+
+    def features(self, u):
+        """Feature rows of the input vertices of type u gathered in the same graph
+        launch (sample_minibatch(features=True)); zero-copy tensor or None."""
+        torch = _torch()
+        self.views
+        ptr, n, rb = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+        rc = lib().eg_blocks_features(self._h, u, ctypes.byref(ptr), ctypes.byref(n), ctypes.byref(rb))
+        if rc:
+            raise EgError(rc, "eg_blocks_features")
+        if not ptr.value and n.value == 0 and not self._ctx.row_bytes[u]:
+            return None
+        dt, shape = self._ctx.feat_dtypes[u], self._ctx.feat_shapes[u]
+        if n.value == 0:
+            return torch.empty((0,) + shape, dtype=dt, device=self._ctx.device)
+        raw = _wrap(ptr.value, n.value * rb.value // 4, "<i4", self, self._ctx.device)
+        return raw.view(dt).view((n.value,) + shape)
 
     @property
     def handle(self):
         return self._h
 
     def free(self):
-        """Release the library memory now (tensors obtained from this handle must
-        no longer be used).  Otherwise it is released when the handle and all its
-        tensors are garbage."""
+        """Release the batch's slot now (tensors obtained from this handle must no
+        longer be used).  Otherwise it is released when the handle is garbage."""
         if self._h:
             lib().eg_blocks_free(self._h)
             self._h = None
@@ -334,6 +374,24 @@ class Context:
         h = ctypes.c_void_p()
         self._check(lib().eg_sample_blocks(self._h, ptr if n else None, n, fo.shape[0], fo.ctypes.data,
                                            rng_seed & (2**64 - 1), ctypes.byref(h)), "eg_sample_blocks")
+        return Blocks(self, h.value)
+
+    def sample_minibatch(self, seeds, fanouts, rng_seed: int, features: bool = True, async_: bool = False) -> Blocks:
+        """One CUDA-graph launch: sample + compact every hop (+ gather features into
+        library-owned buffers, Blocks.features(u)).  async_=True returns after
+        enqueueing; sizes are resolved on first use."""
+        torch = _torch()
+        fo = np.ascontiguousarray(fanouts, np.int32)
+        if isinstance(seeds, np.ndarray):
+            seeds = np.ascontiguousarray(seeds, np.int64)
+            ptr, n = seeds.ctypes.data, len(seeds)
+        else:
+            assert seeds.dtype == torch.int64 and seeds.is_contiguous()
+            ptr, n = seeds.data_ptr(), seeds.numel()
+        flags = (EG_FEATURES if features else 0) | (EG_ASYNC if async_ else 0)
+        h = ctypes.c_void_p()
+        self._check(lib().eg_sample_minibatch(self._h, ptr if n else None, n, fo.shape[0], fo.ctypes.data,
+                                              rng_seed & (2**64 - 1), flags, ctypes.byref(h)), "eg_sample_minibatch")
         return Blocks(self, h.value)
 
     def gather_features(self, blocks: Blocks, out=None, types=None):

@@ -179,3 +179,61 @@ def test_device_features_match_host_generator():
         t = feature_shard(cfg, 0, 1000, 3000, "cuda:0")
         torch.cuda.synchronize()
         assert t.cpu().numpy().tobytes() == synth.host_features(cfg, 0, 1000, 3000).tobytes()
+
+
+# ----------------------------------------------------------------------------- one-graph mini-batch path
+
+def _features_of(blocks, cfg):
+    return [blocks.features(u) if u in cfg.feats else None for u in range(cfg.n_vt)]
+
+
+@pytest.mark.parametrize("g_idx", range(3))
+def test_c1_minibatch_graph_with_features(c1, g_idx):
+    cfg, g, rows, ctx = c1
+    seeds = synth.batch_seeds(cfg, g_idx)
+    rs = synth.rng_seed(cfg, g_idx)
+    res = oracle.sample(g, seeds, cfg.fanouts, rs)
+    import torch
+    b = ctx.sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+    assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+    assert_same_features(res, _features_of(b, cfg), cfg, rows)
+    b.free()
+
+
+def test_c2_async_pipeline(c2):
+    """Several batches in flight (EG_ASYNC), each bit-exact; slots are reused."""
+    import torch
+    cfg, g, rows, ctx = c2
+    idx = list(range(30, 36))
+    seeds = [torch.from_numpy(synth.batch_seeds(cfg, i)).cuda() for i in idx]
+    pend = [ctx.sample_minibatch(s, cfg.fanouts, synth.rng_seed(cfg, i), features=True, async_=True)
+            for s, i in zip(seeds[:3], idx[:3])]
+    for k, i in enumerate(idx):
+        b = pend.pop(0)
+        res = oracle.sample(g, synth.batch_seeds(cfg, i), cfg.fanouts, synth.rng_seed(cfg, i))
+        assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+        assert_same_features(res, _features_of(b, cfg), cfg, rows)
+        b.free()
+        if k + 3 < len(idx):
+            pend.append(ctx.sample_minibatch(seeds[k + 3], cfg.fanouts, synth.rng_seed(cfg, idx[k + 3]),
+                                             features=True, async_=True))
+
+
+def test_c1_async_error_reported_at_wait(c1):
+    from paper_2112_15345_b200 import EgError
+    import torch
+    cfg, g, rows, ctx = c1
+    b = ctx.sample_minibatch(torch.tensor([3, 99999], device="cuda:0"), cfg.fanouts, 1, async_=True)
+    with pytest.raises(EgError) as e:
+        b.wait()
+    assert e.value.code == -2
+    b.free()
+    run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 2), cfg.fanouts, synth.rng_seed(cfg, 2), rows)
+
+
+def test_c1_batch_sizes_share_and_split_plans(c1):
+    """Different seed counts / fanouts use different plans; results stay exact."""
+    cfg, g, rows, ctx = c1
+    for n, fo in [(1, cfg.fanouts), (63, cfg.fanouts), (65, cfg.fanouts), (200, [[2, 3, 4], [4, 3, 2]]),
+                  (64, cfg.fanouts)]:
+        run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 7, batch=n), fo, 1000 + n, rows)
