@@ -296,6 +296,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         clk = clocks.stop()
         ctx.set_profiling(False)
         prof = ctx.profile()
+        trace = {k: round(1e3 * ms / max(1, n), 2) for k, (ms, n) in ctx.trace().items()}
 
     totals = torch.tensor([ms, float(edges), float(gbytes), float(K)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -403,7 +404,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "gather_GBps": (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk, "load_seconds": t_load, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+                "clocks": clk, "load_seconds": t_load, "stage_us": trace or None, "host": {"cores": host_cores(), "cpu": cpu_model()}}
         emit(args, line)
     ctx.close()
     del shard

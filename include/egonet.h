@@ -211,7 +211,35 @@ EG_API eg_status eg_set_profiling(eg_ctx *ctx, int32_t enable);
 EG_API eg_status eg_get_profile(eg_ctx *ctx, double out[4]);
 EG_API int64_t eg_kernel_launches(const eg_ctx *ctx);
 
+/* Tracing: with EG_TRACE=1 in the environment at eg_create, every captured batch
+ * graph carries an event after each stage (seed split; per hop count, scan,
+ * sample+select, bitcount, emit, relabel; reset; gather) and, while profiling is
+ * enabled, finished batches accumulate per-stage device time.  Returns the number
+ * of stages; entry i (if in range) is copied to name / total_ms / count. */
+EG_API int32_t eg_trace_get(const eg_ctx *ctx, int32_t i, char *name, size_t name_len, double *total_ms,
+                            int64_t *count);
+
 /* Host-only helpers (no device work; usable without a GPU). */
+
+/* What one rank publishes about its shard (no device pointers): the global schema,
+ * the partition bounds, its CSC shard extents and its feature row size. */
+typedef struct {
+    int32_t rank, world, n_vt, n_rel;
+    int64_t vt_counts[EG_MAX_VT];
+    int64_t bounds[EG_MAX_VT][EG_MAX_RANKS + 1];
+    int32_t rel_src_vt[EG_MAX_REL], rel_dst_vt[EG_MAX_REL];
+    int64_t rel_n_local_edges[EG_MAX_REL], rel_edge_base[EG_MAX_REL], rel_max_degree[EG_MAX_REL];
+    int64_t row_bytes[EG_MAX_VT];
+} eg_shard_meta;
+
+/* Check that `world` shard metas (rank order) describe ONE partition: same schema,
+ * vertex counts, bounds (0 .. N_t, non-decreasing) and row sizes everywhere; rank p's
+ * relation shards start at edge_base = sum of the lower ranks' edge counts.  On
+ * success fills rel_edges[r] = |E_r| and rel_max_degree[r] (either may be NULL).
+ * EG_EPEER (with a reason in msg, if given) otherwise.  eg_import_shards and
+ * eg_attach_peer run the same check. */
+EG_API eg_status eg_check_shard_metas(int32_t world, const eg_shard_meta *metas, int64_t *rel_edges,
+                                      int64_t *rel_max_degree, char *msg, size_t msg_len);
 /* bounds[p] = floor(p * n / world), p = 0..world. */
 EG_API eg_status eg_range_bounds(int64_t n, int32_t world, int64_t *bounds);
 /* Upper bound of the nodes / edges of a batch (what eg_sample_blocks allocates):

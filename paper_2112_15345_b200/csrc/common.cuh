@@ -46,7 +46,8 @@ struct FeatDev {
 //   nnz(h, r):   edges of relation r in block h
 constexpr int kMetaNodes = 0;
 constexpr int kMetaNnz = kMetaNodes + (EG_MAX_HOPS + 1) * EG_MAX_VT;
-constexpr int kMetaErr = kMetaNnz + EG_MAX_HOPS * EG_MAX_REL;
+constexpr int kMetaSel = kMetaNnz + EG_MAX_HOPS * EG_MAX_REL;   // selection-queue length per hop
+constexpr int kMetaErr = kMetaSel + EG_MAX_HOPS;
 constexpr int kMetaSize = kMetaErr + 8;
 
 // Everything a hop's kernels touch.
@@ -68,6 +69,7 @@ struct HopDev {
     int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
     int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
+    uint64_t *selq;                  // items that need a selection: (r << 32) | i
     int32_t cap_nodes[EG_MAX_VT];    // capacity of nodes[u]
 };
 

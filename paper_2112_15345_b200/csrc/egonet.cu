@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -71,7 +72,8 @@ struct Plan {
     size_t o_meta = 0, o_dyn = 0, o_seeds = 0, total = 0;
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {};
+           o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
+           o_selq[EG_MAX_HOPS] = {};
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
 };
@@ -87,6 +89,8 @@ struct Slot {
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t done = nullptr, s0 = nullptr, s1 = nullptr, g0 = nullptr, g1 = nullptr;
     bool busy = false, used = false, timed = false;
+    std::vector<cudaEvent_t> tev;        // EG_TRACE: one event after each stage of the graph
+    std::vector<std::string> tlab;
 };
 
 struct eg_ctx {
@@ -115,9 +119,7 @@ struct eg_ctx {
     int32_t *h_meta = nullptr;   // pinned
     std::vector<void *> ipc_bases;
     uint32_t attached = 0;                          // bit p: rank p's shard is mapped
-    int64_t peer_edges[EG_MAX_RANKS][EG_MAX_REL] = {};
-    int64_t peer_ebase[EG_MAX_RANKS][EG_MAX_REL] = {};
-    int64_t peer_maxdeg[EG_MAX_RANKS][EG_MAX_REL] = {};
+    eg_shard_meta metas[EG_MAX_RANKS] = {};          // every rank's published shard metadata
     // instrumentation
     bool prof = false;
     std::vector<TimedPair> timed;
@@ -127,6 +129,10 @@ struct eg_ctx {
     // batch plans (CUDA graphs)
     std::vector<Plan *> plans;
     cudaStream_t cap_stream = nullptr;
+    bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
+    std::vector<std::string> trace_names;
+    std::vector<double> trace_ms;
+    std::vector<int64_t> trace_n;
 };
 
 struct eg_blocks {
@@ -273,7 +279,7 @@ void fill_meta(const eg_ctx *c, ShardBlob *b)
         b->vt_counts[t] = c->vt_counts[t];
         for (int p = 0; p <= c->world; ++p) b->bounds[t][p] = c->g.bounds[t][p];
         const eg_features &F = c->own_feat[t];
-        b->feat[t].row_bytes = F.rows ? F.row_bytes : 0;
+        b->feat[t].row_bytes = F.row_bytes;
         b->feat[t].n_rows = c->g.bounds[t][c->rank + 1] - c->g.bounds[t][c->rank];
         b->feat[t].has = F.rows != nullptr && b->feat[t].n_rows > 0;
     }
@@ -289,45 +295,82 @@ void fill_meta(const eg_ctx *c, ShardBlob *b)
     }
 }
 
+void to_meta(const ShardBlob &b, eg_shard_meta *m)
+{
+    memset(m, 0, sizeof(*m));
+    m->rank = b.rank;
+    m->world = b.world;
+    m->n_vt = b.n_vt;
+    m->n_rel = b.n_rel;
+    for (int t = 0; t < EG_MAX_VT; ++t) {
+        m->vt_counts[t] = b.vt_counts[t];
+        for (int q = 0; q <= EG_MAX_RANKS; ++q) m->bounds[t][q] = b.bounds[t][q];
+        m->row_bytes[t] = b.feat[t].row_bytes;
+    }
+    for (int r = 0; r < EG_MAX_REL; ++r) {
+        m->rel_src_vt[r] = b.rel[r].src_vt;
+        m->rel_dst_vt[r] = b.rel[r].dst_vt;
+        m->rel_n_local_edges[r] = b.rel[r].n_local_edges;
+        m->rel_edge_base[r] = b.rel[r].edge_base;
+        m->rel_max_degree[r] = b.rel[r].max_degree;
+    }
+}
+
+// The one consistency check of a partition's published metadata.
+bool check_metas(int world, const eg_shard_meta *m, int64_t *edges, int64_t *maxdeg, std::string *why)
+{
+    if (world < 1 || world > EG_MAX_RANKS) return *why = "world out of range", false;
+    const eg_shard_meta &a = m[0];
+    if (a.n_vt < 1 || a.n_vt > EG_MAX_VT || a.n_rel < 1 || a.n_rel > EG_MAX_REL)
+        return *why = "schema size out of range", false;
+    for (int p = 0; p < world; ++p) {
+        const eg_shard_meta &b = m[p];
+        const std::string who = "rank " + std::to_string(p) + ": ";
+        if (b.rank != p || b.world != world) return *why = who + "rank / world mismatch", false;
+        if (b.n_vt != a.n_vt || b.n_rel != a.n_rel) return *why = who + "schema differs", false;
+        for (int t = 0; t < a.n_vt; ++t) {
+            if (b.vt_counts[t] != a.vt_counts[t]) return *why = who + "vertex counts differ", false;
+            if (b.row_bytes[t] != a.row_bytes[t]) return *why = who + "feature row size differs", false;
+            if (b.bounds[t][0] != 0 || b.bounds[t][world] != b.vt_counts[t])
+                return *why = who + "bounds must span [0, N_t]", false;
+            for (int q = 0; q <= world; ++q) {
+                if (b.bounds[t][q] != a.bounds[t][q]) return *why = who + "partition bounds differ", false;
+                if (q < world && b.bounds[t][q + 1] < b.bounds[t][q]) return *why = who + "bounds decrease", false;
+            }
+        }
+        for (int r = 0; r < a.n_rel; ++r)
+            if (b.rel_src_vt[r] != a.rel_src_vt[r] || b.rel_dst_vt[r] != a.rel_dst_vt[r])
+                return *why = who + "relation types differ", false;
+    }
+    for (int r = 0; r < a.n_rel; ++r) {
+        int64_t total = 0, mx = 0;
+        for (int p = 0; p < world; ++p) {
+            if (m[p].rel_edge_base[r] != total || m[p].rel_n_local_edges[r] < 0)
+                return *why = "relation " + std::to_string(r) + ": edge bases not contiguous at rank " +
+                              std::to_string(p), false;
+            total += m[p].rel_n_local_edges[r];
+            mx = std::max(mx, m[p].rel_max_degree[r]);
+        }
+        if (edges) edges[r] = total;
+        if (maxdeg) maxdeg[r] = mx;
+    }
+    return true;
+}
+
 eg_status check_peer(eg_ctx *c, const ShardBlob &b, int p)
 {
-    const std::string who = "peer " + std::to_string(p) + ": ";
-    if (b.magic != kBlobMagic || b.version != 1 || b.rank != p || b.world != c->world || b.n_vt != c->g.n_vt ||
-        b.n_rel != c->g.n_rel)
-        return fail(c, EG_EPEER, who + "header mismatch (rank / world / type counts)");
-    for (int t = 0; t < b.n_vt; ++t) {
-        if (b.vt_counts[t] != c->vt_counts[t]) return fail(c, EG_EPEER, who + "vertex counts differ");
-        for (int q = 0; q <= c->world; ++q)
-            if (b.bounds[t][q] != c->g.bounds[t][q]) return fail(c, EG_EPEER, who + "partition bounds differ");
-        if ((b.feat[t].row_bytes != 0) != (c->f.row_bytes[t] != 0) ||
-            (b.feat[t].row_bytes && b.feat[t].row_bytes != c->f.row_bytes[t]))
-            return fail(c, EG_EPEER, who + "feature row size differs");
-    }
-    for (int r = 0; r < b.n_rel; ++r)
-        if (b.rel[r].src_vt != c->g.rel[r].src_vt || b.rel[r].dst_vt != c->g.rel[r].dst_vt)
-            return fail(c, EG_EPEER, who + "relation types differ");
-    for (int r = 0; r < b.n_rel; ++r) {
-        c->peer_edges[p][r] = b.rel[r].n_local_edges;
-        c->peer_ebase[p][r] = b.rel[r].edge_base;
-        c->peer_maxdeg[p][r] = b.rel[r].max_degree;
-    }
+    if (b.magic != kBlobMagic || b.version != 1 || b.rank != p || b.world != c->world)
+        return fail(c, EG_EPEER, "peer blob " + std::to_string(p) + ": header mismatch");
+    to_meta(b, &c->metas[p]);
     return EG_OK;
 }
 
-// All ranks mapped: global edge counts / max degrees, contiguity of edge bases.
+// All ranks mapped: validate the partition, global edge counts / max degrees.
 eg_status finalize_peers(eg_ctx *c)
 {
-    for (int r = 0; r < c->g.n_rel; ++r) {
-        int64_t total = 0, mx = 0;
-        for (int p = 0; p < c->world; ++p) {
-            if (c->peer_ebase[p][r] != total)
-                return fail(c, EG_EPEER, "relation " + std::to_string(r) + ": edge bases not contiguous");
-            total += c->peer_edges[p][r];
-            mx = std::max(mx, c->peer_maxdeg[p][r]);
-        }
-        c->rel_edges_total[r] = total;
-        c->rel_max_degree[r] = mx;
-    }
+    std::string why;
+    if (!check_metas(c->world, c->metas, c->rel_edges_total, c->rel_max_degree, &why))
+        return fail(c, EG_EPEER, why);
     c->peers_ready = true;
     return EG_OK;
 }
@@ -348,6 +391,19 @@ eg_status eg_range_bounds(int64_t n, int32_t world, int64_t *bounds)
     if (n < 0 || world < 1 || !bounds) return EG_EINVAL;
     for (int p = 0; p <= world; ++p) bounds[p] = (int64_t)((__int128)p * n / world);
     return EG_OK;
+}
+
+eg_status eg_check_shard_metas(int32_t world, const eg_shard_meta *metas, int64_t *rel_edges,
+                               int64_t *rel_max_degree, char *msg, size_t msg_len)
+{
+    if (!metas) return EG_EINVAL;
+    std::string why;
+    const bool ok = check_metas(world, metas, rel_edges, rel_max_degree, &why);
+    if (msg && msg_len) {
+        strncpy(msg, ok ? "ok" : why.c_str(), msg_len - 1);
+        msg[msg_len - 1] = 0;
+    }
+    return ok ? EG_OK : EG_EPEER;
 }
 
 eg_status eg_batch_caps(int32_t n_vt, const int64_t *vt_counts, int32_t n_rel, const int32_t *rel_src_vt,
@@ -389,6 +445,10 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
         cudaMallocHost(&c->h_dyn, sizeof(uint64_t) * 2) != cudaSuccess) {
         delete c;
         return EG_ENOMEM;
+    }
+    {
+        const char *tr = getenv("EG_TRACE");
+        c->trace = tr && tr[0] == '1';
     }
     if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
@@ -471,10 +531,13 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     c->f = FeatDev{};
     for (int t = 0; t < n_vt; ++t) {
         eg_features F = feats ? feats[t] : eg_features{nullptr, 0};
-        if (F.rows && (F.row_bytes <= 0 || F.row_bytes % 16))
+        const int64_t n_rows = g.bounds[t][c->rank + 1] - g.bounds[t][c->rank];
+        if (F.row_bytes < 0 || F.row_bytes % 16 || (F.rows && F.row_bytes == 0))
             return fail(c, EG_EINVAL, "row_bytes must be a positive multiple of 16");
+        if (!F.rows && F.row_bytes > 0 && n_rows > 0)
+            return fail(c, EG_EINVAL, "feature rows missing for a non-empty local range");
         c->f.rows[t][c->rank] = (const uint8_t *)F.rows;
-        c->f.row_bytes[t] = F.rows ? F.row_bytes : 0;
+        c->f.row_bytes[t] = F.row_bytes;
         c->own_feat[t] = F;
     }
     unsigned long long h_max[EG_MAX_REL] = {};
@@ -670,6 +733,11 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
             p->o_ib[h][r] = take(sizeof(int64_t) * nd);
             p->o_id[h][r] = take(sizeof(int32_t) * nd);
         }
+    for (int h = 0; h < L; ++h) {
+        int64_t items = 0;
+        for (int r = 0; r < R; ++r) items += p->capF[h][dst_vt[r]];
+        p->o_selq[h] = take(sizeof(uint64_t) * items);
+    }
     if (features)
         for (int u = 0; u < V; ++u)
             if (c->f.row_bytes[u]) p->o_feat[u] = take((size_t)(p->capF[L][u] * c->f.row_bytes[u]));
@@ -715,12 +783,22 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.cap_nodes[u] = (int32_t)p->capF[L][u];
     }
     int nk = 0;
+    auto mark = [&](const std::string &label) {
+        if (!c->trace) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecordWithFlags(ev, cs, cudaEventRecordExternal);
+        sl->tev.push_back(ev);
+        sl->tlab.push_back(label);
+    };
     EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     cudaMemcpyAsync((void *)hd.dyn, sl->h_dyn, sizeof(uint64_t) * 2, cudaMemcpyHostToDevice, cs);
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     cudaMemsetAsync(hd.meta, 0, sizeof(int32_t) * kMetaSize, cs);
+    mark("start");
     launch_seed_split(g, (const int64_t *)(base + p->o_seeds), hd, cs);
     ++nk;
+    mark("seed_split");
     for (int h = 0; h < L; ++h) {
         hd.h = h;
         for (int r = 0; r < R; ++r) {
@@ -732,17 +810,25 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             hd.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
             hd.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
         }
+        hd.selq = (uint64_t *)(base + p->o_selq[h]);
+        const std::string hs = "h" + std::to_string(h) + ".";
         launch_count(g, hd, cs);
+        mark(hs + "count");
         launch_scan(g, hd, cs);
-        launch_sample(g, hd, cs);
-        launch_mark(g, hd, cs);
+        mark(hs + "scan");
+        launch_sample(g, hd, cs);          // sample + select (marks new sources)
+        mark(hs + "sample+select");
         launch_bitcount(g, hd, c->n_chunks, cs);
+        mark(hs + "bitcount");
         launch_emit(g, hd, c->n_chunks, cs);
+        mark(hs + "emit");
         launch_relabel(g, hd, cs);
+        mark(hs + "relabel");
         nk += 7;
     }
     launch_reset(g, hd, L, cs);
     ++nk;
+    mark("reset");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
         GatherDev gd{};
@@ -759,6 +845,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             launch_gather(g, c->f, gd, cs);
             ++nk;
         }
+        mark("gather");
         cudaEventRecordWithFlags(sl->g1, cs, cudaEventRecordExternal);
     }
     cudaMemcpyAsync(sl->h_meta, hd.meta, sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, cs);
@@ -814,6 +901,7 @@ void destroy_plans(eg_ctx *c)
             cudaFreeHost(sl->h_dyn);
             for (cudaEvent_t ev : {sl->done, sl->s0, sl->s1, sl->g0, sl->g1})
                 if (ev) cudaEventDestroy(ev);
+            for (cudaEvent_t ev : sl->tev) cudaEventDestroy(ev);
             delete sl;
         }
         delete p;
@@ -846,6 +934,21 @@ eg_status finish(eg_blocks *b)
             c->prof_n[1] += 1;
         }
         sl->timed = false;
+    }
+    if (c->trace && c->prof && sl->tev.size() > 1) {
+        for (size_t k = 1; k < sl->tev.size(); ++k) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, sl->tev[k - 1], sl->tev[k]);
+            size_t idx = 0;
+            while (idx < c->trace_names.size() && c->trace_names[idx] != sl->tlab[k]) ++idx;
+            if (idx == c->trace_names.size()) {
+                c->trace_names.push_back(sl->tlab[k]);
+                c->trace_ms.push_back(0);
+                c->trace_n.push_back(0);
+            }
+            c->trace_ms[idx] += ms;
+            c->trace_n[idx] += 1;
+        }
     }
     const int32_t errbits = m[kMetaErr];
     if (errbits & kErrSeedRange) return b->status = fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
@@ -1031,6 +1134,21 @@ eg_status eg_blocks_free(eg_blocks *b)
     if (b->slot) b->slot->busy = false;   // reuse waits for the slot's last run to retire
     delete b;
     return EG_OK;
+}
+
+int32_t eg_trace_get(const eg_ctx *c, int32_t i, char *name, size_t name_len, double *total_ms, int64_t *count)
+{
+    if (!c) return 0;
+    const int32_t n = (int32_t)c->trace_names.size();
+    if (i >= 0 && i < n) {
+        if (name && name_len) {
+            strncpy(name, c->trace_names[i].c_str(), name_len - 1);
+            name[name_len - 1] = 0;
+        }
+        if (total_ms) *total_ms = c->trace_ms[i];
+        if (count) *count = c->trace_n[i];
+    }
+    return n;
 }
 
 eg_status eg_set_profiling(eg_ctx *c, int32_t enable)

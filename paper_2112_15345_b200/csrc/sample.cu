@@ -142,6 +142,7 @@ void launch_scan(const GraphDev &g, const HopDev &hd, cudaStream_t s)
 // ----------------------------------------------------------------------------- sampling
 
 struct Item {
+    int64_t bit_base;       // boff[s(r)] - off[s(r)]: bitmap bit of gid = bit_base + gid
     uint32_t soff;          // off[s(r)]
     int64_t ebase;          // global CSC position of this dst's first edge
     const int32_t *ix;      // src tids of this dst's in-edges
@@ -149,10 +150,24 @@ struct Item {
     int64_t *eid_out;
 };
 
-__device__ __forceinline__ void emit_edge(const Item &it, int32_t slot, int64_t j)
+// Write one sampled edge and, if its source is not yet in the batch, mark it in
+// the new-vertex bitmap (the first step of the hop's compaction, fused here).
+__device__ __forceinline__ void mark_new(const HopDev &hd, uint32_t gid, int64_t bit_base)
 {
-    it.src_out[slot] = it.soff + (uint32_t)__ldg(it.ix + j);
+    if (__ldg(hd.pos + gid) < 0) {
+        const int64_t bit = bit_base + gid;
+        const uint32_t m = 1u << (bit & 31);
+        uint32_t *wp = hd.bitmap + (bit >> 5);
+        if (!(*wp & m)) atomicOr(wp, m);
+    }
+}
+
+__device__ __forceinline__ void emit_edge(const HopDev &hd, const Item &it, int32_t slot, int64_t j)
+{
+    const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
+    it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
+    mark_new(hd, gid, it.bit_base);
 }
 
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
@@ -169,7 +184,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 // Generic exact selection for any k < d: binary search of the k-th smallest key
 // value T (33 counting passes over the d keys), then one ascending-j emission
 // pass taking key < T and the first (k - #{key < T}) offsets with key == T.
-__device__ __noinline__ void select_generic(const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
+__device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
                                uint32_t k0, uint32_t k1)
 {
     const int64_t nq = (d + 3) >> 2;
@@ -220,7 +235,7 @@ __device__ __noinline__ void select_generic(const Item &it, int64_t d, int k, ui
         int slot = out + ex;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            if (sel >> t & 1) emit_edge(it, slot++, 4 * q + t);
+            if (sel >> t & 1) emit_edge(hd, it, slot++, 4 * q + t);
         out += __shfl_sync(0xffffffffu, ex + cs, 31);
     }
 }
@@ -230,7 +245,7 @@ __device__ __noinline__ void select_generic(const Item &it, int64_t d, int k, ui
 // the k smallest composites among them are found by rank counting and emitted in
 // ascending j.  Falls back to select_generic if the candidate count is < k or
 // exceeds the slots (both astronomically rare; the result is identical).
-__device__ void select_fast(const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
+__device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi, uint32_t hr,
                             uint32_t k0, uint32_t k1, uint64_t *cand)
 {
     const uint64_t E = 2ull * (uint64_t)k + 32;
@@ -259,7 +274,7 @@ __device__ void select_fast(const Item &it, int64_t d, int k, uint32_t v_lo, uin
     }
     __syncwarp();
     if (m < k || m > kSelCap) {
-        select_generic(it, d, k, v_lo, v_hi, hr, k0, k1);
+        select_generic(hd, it, d, k, v_lo, v_hi, hr, k0, k1);
         return;
     }
     int32_t out = 0;
@@ -274,7 +289,7 @@ __device__ void select_fast(const Item &it, int64_t d, int k, uint32_t v_lo, uin
             sel = rank < k;
         }
         const uint32_t b = __ballot_sync(0xffffffffu, sel);
-        if (sel) emit_edge(it, out + __popc(b & lanemask_lt()), (int64_t)(uint32_t)mine);
+        if (sel) emit_edge(hd, it, out + __popc(b & lanemask_lt()), (int64_t)(uint32_t)mine);
         out += __popc(b);
     }
     __syncwarp();
@@ -287,14 +302,12 @@ constexpr int kSampleWarps = 8;
 // CSC row start / degree the count kernel recorded.  Items that take their whole
 // neighbourhood (d <= k or k = -1; most of a power-law graph) are copied as one
 // segmented copy spread over all 32 lanes; items that need a selection (d > k) are
-// then processed one at a time by the whole warp.
-__global__ void __launch_bounds__(kSampleWarps * 32, 4) sample_kernel(const __grid_constant__ GraphDev g,
+// appended to the hop's selection queue, drained warp-per-item by select_kernel.
+__global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(const __grid_constant__ GraphDev g,
                                                                    const __grid_constant__ HopDev hd)
 {
-    __shared__ uint64_t s_cand[kSampleWarps][kSelCap];
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
-    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
     int64_t cum[EG_MAX_REL + 1];
     cum[0] = 0;
     for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + (hd.fanout[r] != 0 ? nF[g.rel[r].dst_vt] : 0);
@@ -317,6 +330,14 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 4) sample_kernel(const __gr
         }
         const int k = hd.fanout[r];
         const bool sel = cnt > 0 && k >= 0 && d > k;
+        // ---- items that need a selection -> queue (one atomic per warp)
+        const uint32_t selmask = __ballot_sync(0xffffffffu, sel);
+        if (selmask) {
+            uint32_t qbase = 0;
+            if (lane == 0) qbase = atomicAdd((uint32_t *)(hd.meta + kMetaSel + hd.h), (uint32_t)__popc(selmask));
+            qbase = __shfl_sync(0xffffffffu, qbase, 0);
+            if (sel) hd.selq[qbase + __popc(selmask & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
+        }
         // ---- segmented copy of the full neighbourhoods of this group
         const int32_t c = (cnt > 0 && !sel) ? cnt : 0;
         const int32_t incl = warp_incl_scan(c);
@@ -340,44 +361,54 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 4) sample_kernel(const __gr
                 const int64_t base = ibL & ((1ll << 56) - 1);
                 const int32_t j = s - exL;
                 const RelDev &R = g.rel[rL];
-                hd.src[rL][posL + j] = (uint32_t)g.off[R.src_vt] + (uint32_t)__ldg(R.indices[p] + base + j);
+                const uint32_t gid = (uint32_t)g.off[R.src_vt] + (uint32_t)__ldg(R.indices[p] + base + j);
+                hd.src[rL][posL + j] = gid;
                 hd.eids[rL][posL + j] = R.edge_base[p] + base + j;
+                mark_new(hd, gid, g.boff[R.src_vt] - g.off[R.src_vt]);
             }
         }
-        // ---- items that need a selection: one at a time, whole warp
-        uint32_t selmask = __ballot_sync(0xffffffffu, sel);
-        while (selmask) {
-            const int L = __ffs(selmask) - 1;
-            selmask &= selmask - 1;
-            const int rL = __shfl_sync(0xffffffffu, r, L);
-            const int64_t iL = __shfl_sync(0xffffffffu, i, L);
-            const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
-            const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
-            const int32_t dL = __shfl_sync(0xffffffffu, d, L);
-            const RelDev &R = g.rel[rL];
-            const int p = (int)(ibL >> 56);
-            const int64_t base = ibL & ((1ll << 56) - 1);
-            const int64_t v = hd.nodes[R.dst_vt][iL];
-            Item itm;
-            itm.soff = (uint32_t)g.off[R.src_vt];
-            itm.ebase = R.edge_base[p] + base;
-            itm.ix = R.indices[p] + base;
-            itm.src_out = hd.src[rL] + posL;
-            itm.eid_out = hd.eids[rL] + posL;
-            const int kL = hd.fanout[rL];
-            const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)rL;
-            if (kL <= kSelMaxK)
-                select_fast(itm, dL, kL, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi,
-                            s_cand[warp]);
-            else
-                select_generic(itm, dL, kL, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
-        }
+    }
+}
+
+// Selection items (d > k): one warp per item, any order (each item owns its slots).
+__global__ void __launch_bounds__(kSampleWarps * 32) select_kernel(const __grid_constant__ GraphDev g,
+                                                                   const __grid_constant__ HopDev hd)
+{
+    __shared__ uint64_t s_cand[kSampleWarps][kSelCap];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
+    const int64_t n = *(const uint32_t *)(hd.meta + kMetaSel + hd.h);
+    for (int64_t w = (int64_t)blockIdx.x * kSampleWarps + warp; w < n; w += (int64_t)gridDim.x * kSampleWarps) {
+        const uint64_t e = hd.selq[w];
+        const int r = (int)(e >> 32);
+        const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+        const RelDev &R = g.rel[r];
+        const int32_t pos0 = hd.indptr[r][i];
+        const int64_t ib = hd.ibase[r][i];
+        const int64_t d = hd.ideg[r][i];
+        const int64_t v = hd.nodes[R.dst_vt][i];
+        const int p = (int)(ib >> 56);
+        const int64_t base = ib & ((1ll << 56) - 1);
+        Item itm;
+        itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
+        itm.soff = (uint32_t)g.off[R.src_vt];
+        itm.ebase = R.edge_base[p] + base;
+        itm.ix = R.indices[p] + base;
+        itm.src_out = hd.src[r] + pos0;
+        itm.eid_out = hd.eids[r] + pos0;
+        const int k = hd.fanout[r];
+        const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
+        if (k <= kSelMaxK)
+            select_fast(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi, s_cand[warp]);
+        else
+            select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
     }
 }
 
 void launch_sample(const GraphDev &g, const HopDev &hd, cudaStream_t s)
 {
     sample_kernel<<<kSMs * 8, kSampleWarps * 32, 0, s>>>(g, hd);
+    select_kernel<<<kSMs * 4, kSampleWarps * 32, 0, s>>>(g, hd);
 }
 
 }  // namespace eg

@@ -28,7 +28,7 @@ ABI_SYMBOLS = [
     "eg_sample_blocks", "eg_block_view_get", "eg_blocks_n_hops", "eg_blocks_n_inputs", "eg_gather_features",
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
-    "eg_blocks_features",
+    "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get",
 ]
 
 EG_FEATURES = 1
@@ -48,6 +48,48 @@ class Relation(ctypes.Structure):
 
 class Features(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_void_p), ("row_bytes", ctypes.c_int64)]
+
+
+class ShardMeta(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("n_vt", ctypes.c_int32), ("n_rel", ctypes.c_int32),
+                ("vt_counts", ctypes.c_int64 * EG_MAX_VT),
+                ("bounds", (ctypes.c_int64 * (EG_MAX_RANKS + 1)) * EG_MAX_VT),
+                ("rel_src_vt", ctypes.c_int32 * EG_MAX_REL), ("rel_dst_vt", ctypes.c_int32 * EG_MAX_REL),
+                ("rel_n_local_edges", ctypes.c_int64 * EG_MAX_REL), ("rel_edge_base", ctypes.c_int64 * EG_MAX_REL),
+                ("rel_max_degree", ctypes.c_int64 * EG_MAX_REL), ("row_bytes", ctypes.c_int64 * EG_MAX_VT)]
+
+
+def shard_meta(rank, world, vt_counts, bounds, rels, row_bytes):
+    """Build an eg_shard_meta (host only).  rels: list of dicts with src_vt, dst_vt,
+    n_local_edges, edge_base, max_degree."""
+    m = ShardMeta()
+    m.rank, m.world, m.n_vt, m.n_rel = rank, world, len(vt_counts), len(rels)
+    for t, n in enumerate(vt_counts):
+        m.vt_counts[t] = int(n)
+        m.row_bytes[t] = int(row_bytes[t])
+        for q in range(world + 1):
+            m.bounds[t][q] = int(bounds[t][q])
+    for r, d in enumerate(rels):
+        m.rel_src_vt[r], m.rel_dst_vt[r] = int(d["src_vt"]), int(d["dst_vt"])
+        m.rel_n_local_edges[r], m.rel_edge_base[r] = int(d["n_local_edges"]), int(d["edge_base"])
+        m.rel_max_degree[r] = int(d.get("max_degree", 0))
+    return m
+
+
+def check_shard_metas(metas):
+    """eg_check_shard_metas over a list of ShardMeta (rank order); returns
+    (rel_edges, rel_max_degree) or raises EgError(EG_EPEER)."""
+    world = len(metas)
+    arr = (ShardMeta * world)(*metas)
+    edges = np.zeros(EG_MAX_REL, np.int64)
+    mx = np.zeros(EG_MAX_REL, np.int64)
+    msg = ctypes.create_string_buffer(256)
+    rc = lib().eg_check_shard_metas(world, ctypes.cast(arr, ctypes.c_void_p), edges.ctypes.data, mx.ctypes.data,
+                                    msg, 256)
+    if rc:
+        raise EgError(rc, msg.value.decode())
+    n_rel = metas[0].n_rel
+    return edges[:n_rel], mx[:n_rel]
 
 
 class BlockView(ctypes.Structure):
@@ -83,6 +125,9 @@ def lib(build_if_missing: bool = True):
         L.eg_export_shard.argtypes = [vp, vp, P(c.c_size_t)]
         L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
         L.eg_attach_peer.argtypes = [vp, vp]
+        L.eg_trace_get.argtypes = [vp, c.c_int32, c.c_char_p, c.c_size_t, P(c.c_double), P(c.c_int64)]
+        L.eg_trace_get.restype = c.c_int32
+        L.eg_check_shard_metas.argtypes = [c.c_int32, vp, vp, vp, c.c_char_p, c.c_size_t]
         L.eg_sample_blocks.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, P(vp)]
         L.eg_block_view_get.argtypes = [vp, c.c_int32, P(BlockView)]
         L.eg_sample_minibatch.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, c.c_int32, P(vp)]
@@ -103,7 +148,7 @@ def lib(build_if_missing: bool = True):
         L.eg_batch_caps.argtypes = [c.c_int32, vp, c.c_int32, vp, vp, vp, vp, c.c_int64, c.c_int32, vp, vp, vp]
         for name in ABI_SYMBOLS:
             if name not in ("eg_version", "eg_last_error", "eg_blocks_n_hops", "eg_blocks_n_inputs",
-                            "eg_kernel_launches"):
+                            "eg_kernel_launches", "eg_trace_get"):
                 getattr(L, name).restype = c.c_int
         _lib = L
     return _lib
@@ -319,7 +364,7 @@ class Context:
             else:
                 assert t.is_cuda and t.is_contiguous()
                 rb = t.stride(0) * t.element_size() if t.dim() > 1 else t.element_size()
-                farr[u] = Features(t.data_ptr() if t.numel() else None, rb if t.numel() else 0)
+                farr[u] = Features(t.data_ptr() if t.numel() else None, rb)
                 self.row_bytes.append(rb)
                 self._keep.append(t)
         self.rel_dst = [int(d["dst_vt"]) for d in rels]
@@ -422,6 +467,17 @@ class Context:
         out = (ctypes.c_double * 4)()
         self._check(lib().eg_get_profile(self._h, out), "eg_get_profile")
         return {"sample_ms": out[0], "gather_ms": out[1], "n_sample": int(out[2]), "n_gather": int(out[3])}
+
+    def trace(self):
+        """Per-stage device time accumulated with EG_TRACE=1 (ms total, count)."""
+        n = lib().eg_trace_get(self._h, -1, None, 0, None, None)
+        out = {}
+        for i in range(n):
+            name = ctypes.create_string_buffer(64)
+            ms, cnt = ctypes.c_double(), ctypes.c_int64()
+            lib().eg_trace_get(self._h, i, name, 64, ctypes.byref(ms), ctypes.byref(cnt))
+            out[name.value.decode()] = (ms.value, cnt.value)
+        return out
 
     def kernel_launches(self) -> int:
         return int(lib().eg_kernel_launches(self._h))
