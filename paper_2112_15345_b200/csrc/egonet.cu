@@ -73,7 +73,7 @@ struct Plan {
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_selq[EG_MAX_HOPS] = {};
+           o_selq[EG_MAX_HOPS] = {}, o_bd = 0, o_bar = 0;
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
 };
@@ -720,6 +720,8 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         return o;
     };
     p->o_meta = take(sizeof(int32_t) * kMetaSize);
+    p->o_bd = take(sizeof(BatchDev));
+    p->o_bar = take(sizeof(uint32_t) * 2);
     p->o_dyn = take(sizeof(uint64_t) * 2);
     p->o_seeds = take(sizeof(int64_t) * n_cap);
     for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
@@ -782,6 +784,28 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
         hd.cap_nodes[u] = (int32_t)p->capF[L][u];
     }
+    BatchDev bd{};
+    bd.n_hops = L;
+    bd.n_chunks = c->n_chunks;
+    bd.seeds = (const int64_t *)(base + p->o_seeds);
+    bd.bar = (uint32_t *)(base + p->o_bar);
+    for (int h = 0; h < L; ++h) {
+        HopDev x = hd;
+        x.h = h;
+        for (int r = 0; r < R; ++r) {
+            x.fanout[r] = p->fanouts[h * R + r];
+            x.indptr[r] = (int32_t *)(base + p->o_ip[h][r]);
+            x.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
+            x.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
+            x.src[r] = (uint32_t *)(base + p->o_src[h][r]);
+            x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
+            x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
+        }
+        x.selq = (uint64_t *)(base + p->o_selq[h]);
+        bd.hop[h] = x;
+    }
+    EG_CUDA(c, cudaMemcpy(base + p->o_bd, &bd, sizeof(bd), cudaMemcpyHostToDevice));
+    EG_CUDA(c, cudaMemset(base + p->o_bar, 0, sizeof(uint32_t) * 2));
     int nk = 0;
     auto mark = [&](const std::string &label) {
         if (!c->trace) return;
@@ -796,39 +820,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     cudaMemsetAsync(hd.meta, 0, sizeof(int32_t) * kMetaSize, cs);
     mark("start");
-    launch_seed_split(g, (const int64_t *)(base + p->o_seeds), hd, cs);
-    ++nk;
-    mark("seed_split");
-    for (int h = 0; h < L; ++h) {
-        hd.h = h;
-        for (int r = 0; r < R; ++r) {
-            hd.fanout[r] = p->fanouts[h * R + r];
-            hd.indptr[r] = (int32_t *)(base + p->o_ip[h][r]);
-            hd.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
-            hd.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
-            hd.src[r] = (uint32_t *)(base + p->o_src[h][r]);
-            hd.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
-            hd.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
-        }
-        hd.selq = (uint64_t *)(base + p->o_selq[h]);
-        const std::string hs = "h" + std::to_string(h) + ".";
-        launch_count(g, hd, cs);
-        mark(hs + "count");
-        launch_scan(g, hd, cs);
-        mark(hs + "scan");
-        launch_sample(g, hd, cs);          // sample + select (marks new sources)
-        mark(hs + "sample+select");
-        launch_bitcount(g, hd, c->n_chunks, cs);
-        mark(hs + "bitcount");
-        launch_emit(g, hd, c->n_chunks, cs);
-        mark(hs + "emit");
-        launch_relabel(g, hd, cs);
-        mark(hs + "relabel");
-        nk += 7;
-    }
-    launch_reset(g, hd, L, cs);
-    ++nk;
-    mark("reset");
+    nk += launch_batch(g, (const BatchDev *)(base + p->o_bd), L, c->n_chunks, cs);
+    mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
         GatherDev gd{};

@@ -4,18 +4,15 @@
 
 namespace eg {
 
-// sample.cu
-void launch_seed_split(const GraphDev &g, const int64_t *seeds, const HopDev &hd, cudaStream_t s);
-void launch_count(const GraphDev &g, const HopDev &hd, cudaStream_t s);
-void launch_scan(const GraphDev &g, const HopDev &hd, cudaStream_t s);
-void launch_sample(const GraphDev &g, const HopDev &hd, cudaStream_t s);
-
-// compact.cu
-void launch_mark(const GraphDev &g, const HopDev &hd, cudaStream_t s);
-void launch_bitcount(const GraphDev &g, const HopDev &hd, int32_t n_chunks, cudaStream_t s);
-void launch_emit(const GraphDev &g, const HopDev &hd, int32_t n_chunks, cudaStream_t s);
-void launch_relabel(const GraphDev &g, const HopDev &hd, cudaStream_t s);
-void launch_reset(const GraphDev &g, const HopDev &hd, int32_t level, cudaStream_t s);
+// batch.cu: sampling + compaction of a whole batch (one persistent kernel)
+struct BatchDev {
+    int32_t n_hops, n_chunks;
+    const int64_t *seeds;
+    uint32_t *bar;                 // grid barrier {count, generation}, zero-initialised
+    HopDev hop[EG_MAX_HOPS];
+};
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, cudaStream_t s);
+int batch_grid();
 
 // gather.cu
 struct GatherDev {

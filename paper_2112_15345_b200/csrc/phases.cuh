@@ -1,0 +1,506 @@
+// phases.cuh -- the phases of one mini-batch as device functions over a virtual grid.
+//
+// Each phase distributes its work over `nb` blocks (block index `bid`), so the same
+// code runs as one persistent cooperative kernel (batch.cu: grid barriers between
+// phases) or as one kernel per phase (bid = blockIdx.x).
+//
+// Method:
+//   seed split        F_0[u] = seeds of type u in caller order
+//   count             c = min(d, k) (all d if k == -1 or d <= k) per (dst, r)
+//   scan              block CSC indptr = exclusive prefix of c
+//   sample            d <= k: the whole in-neighbourhood in CSC order; d > k: the
+//                     k offsets with the smallest (key32 << 32 | j), ascending j P:284-285
+//   bitcount / emit   new sources of the hop in gid order after the dst prefix
+//   relabel           local src ids = positions in src_nodes
+#pragma once
+#include "common.cuh"
+
+namespace eg {
+
+__device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1u; }
+
+// ============================================================================ seed split
+
+// Seeds (caller order, mixed types) -> F_0[u] (stable per type) + pos[] for the
+// dst-prefix relabel; flags out-of-range and duplicate seeds.  One block.
+__device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ seeds)
+{
+    __shared__ int32_t sh[33];
+    __shared__ int32_t base[EG_MAX_VT];
+    const int64_t n = (int64_t)hd.dyn[1];
+    if (threadIdx.x < EG_MAX_VT) base[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n_total = g.off[g.n_vt];
+    for (int64_t t0 = 0; t0 < n; t0 += blockDim.x) {
+        const int64_t i = t0 + threadIdx.x;
+        int64_t gid = -1;
+        int vt = -1;
+        if (i < n) {
+            gid = seeds[i];
+            if (gid < 0 || gid >= n_total) {
+                atomicOr(hd.meta + kMetaErr, kErrSeedRange);
+            } else {
+                vt = 0;
+                while (gid >= g.off[vt + 1]) ++vt;
+            }
+        }
+        for (int u = 0; u < g.n_vt; ++u) {
+            const int32_t flag = (vt == u);
+            int32_t tot;
+            const int32_t ex = block_excl_scan(flag, sh, &tot);
+            if (flag) {
+                const int32_t p = base[u] + ex;
+                if (p < hd.cap_nodes[u]) {
+                    hd.nodes[u][p] = gid;
+                    if (atomicCAS(hd.pos + gid, -1, p) != -1) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+                } else {
+                    atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                }
+            }
+            if (threadIdx.x == 0) base[u] += tot;
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x < g.n_vt)
+        meta_nodes(hd.meta, 0)[threadIdx.x] = min(base[threadIdx.x], hd.cap_nodes[threadIdx.x]);
+    __syncthreads();
+}
+
+// ============================================================================ count + scan
+
+// Virtual blocks (r, b), b < kScanBlocks: count c for the dst items of chunk b of
+// F_h[t(r)] into the block indptr slots, record (owner, CSC row start) and d for
+// the sampler, enqueue the items that need a selection; per-chunk sums -> partial.
+__device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb)
+{
+    __shared__ int32_t sh[33];
+    const int32_t *nF = meta_nodes(hd.meta, hd.h);
+    if (bid == 0 && threadIdx.x < g.n_vt)   // S_h starts as F_h; emit adds the new ones
+        meta_nodes(hd.meta, hd.h + 1)[threadIdx.x] = nF[threadIdx.x];
+    for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
+        const int r = vb / kScanBlocks, b = vb % kScanBlocks;
+        const RelDev &R = g.rel[r];
+        const int t = R.dst_vt;
+        const int k = hd.fanout[r];
+        const int64_t n = nF[t];
+        const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
+        const int64_t lo = b * chunk, hi = min(n, lo + chunk);
+        int32_t sum = 0;
+        for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {   // block-uniform trip count
+            const int64_t i = t0 + threadIdx.x;
+            bool sel = false;
+            if (i < hi) {
+                int32_t c = 0;
+                if (k != 0) {
+                    const int64_t tid = hd.nodes[t][i] - g.off[t];
+                    const int p = owner_of(g, t, tid);
+                    const int64_t x = tid - g.bounds[t][p];
+                    const int64_t *ip = R.indptr[p];
+                    const int64_t b0 = ip[x], d = ip[x + 1] - b0;
+                    const bool all = (k < 0 || d <= k);
+                    c = (int32_t)(all ? d : k);
+                    sel = !all;
+                    hd.ibase[r][i] = ((int64_t)p << 56) | b0;
+                    hd.ideg[r][i] = (int32_t)d;
+                }
+                hd.indptr[r][i] = c;
+                sum += c;
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, sel);
+            if (m) {
+                uint32_t q = 0;
+                if (lane_id() == 0) q = atomicAdd((uint32_t *)(hd.meta + kMetaSel + hd.h), (uint32_t)__popc(m));
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (sel) hd.selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
+            }
+        }
+        sum = block_sum(sum, sh);
+        if (threadIdx.x == 0) hd.partial[r * kScanBlocks + b] = sum;
+    }
+}
+
+// Exclusive scan of the counts in place -> block indptr; nnz(h, r).  Also clears the
+// chunk-group sums used by this hop's compaction.
+__device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_groups)
+{
+    __shared__ int32_t sh[33];
+    if (bid == 0)
+        for (int i = threadIdx.x; i < n_groups; i += blockDim.x) hd.chunk_pre[i] = 0;
+    for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
+        const int r = vb / kScanBlocks, b = vb % kScanBlocks;
+        const int t = g.rel[r].dst_vt;
+        const int64_t n = meta_nodes(hd.meta, hd.h)[t];
+        const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
+        const int64_t lo = b * chunk, hi = min(n, lo + chunk);
+        int32_t s = 0;
+        for (int j = threadIdx.x; j < b; j += blockDim.x) s += hd.partial[r * kScanBlocks + j];
+        int32_t carry = block_sum(s, sh);
+        int32_t *ip = hd.indptr[r];
+        for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
+            const int64_t i = t0 + threadIdx.x;
+            const int32_t v = i < hi ? ip[i] : 0;
+            int32_t tot;
+            const int32_t ex = block_excl_scan(v, sh, &tot);
+            if (i < hi) ip[i] = carry + ex;
+            carry += tot;
+        }
+        if (b == kScanBlocks - 1 && threadIdx.x == 0) {
+            ip[n] = carry;
+            meta_nnz(hd.meta, hd.h)[r] = carry;
+        }
+    }
+}
+
+// ============================================================================ sampling
+
+struct Item {
+    int64_t bit_base;       // boff[s(r)] - off[s(r)]: bitmap bit of gid = bit_base + gid
+    uint32_t soff;          // off[s(r)]
+    int64_t ebase;          // global CSC position of this dst's first edge
+    const int32_t *ix;      // src tids of this dst's in-edges
+    uint32_t *src_out;      // this item's output slots
+    int64_t *eid_out;
+};
+
+// If the source is not yet in the batch, mark it in the new-vertex bitmap (the
+// first step of the hop's compaction, fused into sampling).
+__device__ __forceinline__ void mark_new(const HopDev &hd, uint32_t gid, int64_t bit_base)
+{
+    if (__ldcg(hd.pos + gid) < 0) {
+        const int64_t bit = bit_base + gid;
+        const uint32_t m = 1u << (bit & 31);
+        uint32_t *wp = hd.bitmap + (bit >> 5);
+        if (!(__ldcg(wp) & m)) atomicOr(wp, m);
+    }
+}
+
+__device__ __forceinline__ void emit_edge(const HopDev &hd, const Item &it, int32_t slot, int64_t j)
+{
+    const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
+    it.src_out[slot] = gid;
+    it.eid_out[slot] = it.ebase + j;
+    mark_new(hd, gid, it.bit_base);
+}
+
+// Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
+__device__ __forceinline__ void keys4(uint32_t q, uint32_t v_lo, uint32_t v_hi, uint32_t hr, uint32_t k0,
+                                      uint32_t k1, uint32_t w[4])
+{
+    uint32_t c0 = q, c1 = v_lo, c2 = v_hi, c3 = hr;
+    philox4x32_10(c0, c1, c2, c3, k0, k1);
+    w[0] = c0; w[1] = c1; w[2] = c2; w[3] = c3;
+}
+
+// Generic exact selection for any k < d: binary search of the k-th smallest key
+// value T (33 counting passes over the d keys), then one ascending-j emission
+// pass taking key < T and the first (k - #{key < T}) offsets with key == T.
+__device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo,
+                                            uint32_t v_hi, uint32_t hr, uint32_t k0, uint32_t k1)
+{
+    const int64_t nq = (d + 3) >> 2;
+    auto count_lt = [&](uint64_t x) -> int64_t {
+        int64_t c = 0;
+        for (int64_t q = lane_id(); q < nq; q += 32) {
+            uint32_t w[4];
+            keys4((uint32_t)q, v_lo, v_hi, hr, k0, k1, w);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) c += (4 * q + t < d && (uint64_t)w[t] < x);
+        }
+        return warp_sum(c);
+    };
+    uint64_t lo = 0, hi = 1ull << 32;   // count_lt(lo) < k <= count_lt(hi)
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (count_lt(mid) < k) lo = mid; else hi = mid;
+    }
+    const uint32_t T = (uint32_t)lo;
+    const int64_t need_eq = k - count_lt(lo);
+    int32_t out = 0;
+    int64_t eq_seen = 0;
+    for (int64_t q0 = 0; q0 < nq; q0 += 32) {
+        const int64_t q = q0 + lane_id();
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (q < nq) keys4((uint32_t)q, v_lo, v_hi, hr, k0, k1, w);
+        uint32_t lt = 0, eq = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (q < nq && 4 * q + t < d) {
+                lt |= (w[t] < T) << t;
+                eq |= (w[t] == T) << t;
+            }
+        const int ceq = __popc(eq);
+        const int eq_ex = warp_incl_scan(ceq) - ceq;
+        uint32_t sel = lt;
+        int er = (int)(eq_seen + eq_ex);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (eq >> t & 1) {
+                if (er < need_eq) sel |= 1u << t;
+                ++er;
+            }
+        eq_seen += __shfl_sync(0xffffffffu, eq_ex + ceq, 31);
+        const int cs = __popc(sel);
+        const int ex = warp_incl_scan(cs) - cs;
+        int slot = out + ex;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (sel >> t & 1) emit_edge(hd, it, slot++, 4 * q + t);
+        out += __shfl_sync(0xffffffffu, ex + cs, 31);
+    }
+}
+
+// Fast selection for k <= kSelMaxK: one pass over the d keys keeps the candidates
+// below a threshold T (expected 2k + 32 of them) in shared memory, in ascending j;
+// the k smallest composites among them are found by rank counting and emitted in
+// ascending j.  Falls back to select_generic if the candidate count is < k or
+// exceeds the slots (both astronomically rare; the result is identical).
+__device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
+                            uint32_t hr, uint32_t k0, uint32_t k1, uint64_t *cand)
+{
+    const uint64_t E = 2ull * (uint64_t)k + 32;
+    const uint64_t T = (E >= (uint64_t)d) ? (1ull << 32) : ((E << 32) / (uint64_t)d);
+    const int64_t nq = (d + 3) >> 2;
+    int m = 0;
+    for (int64_t q0 = 0; q0 < nq; q0 += 32) {
+        const int64_t q = q0 + lane_id();
+        uint32_t w[4] = {0, 0, 0, 0};
+        uint32_t f = 0;
+        if (q < nq) {
+            keys4((uint32_t)q, v_lo, v_hi, hr, k0, k1, w);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) f |= (uint32_t)(4 * q + t < d && (uint64_t)w[t] < T) << t;
+        }
+        const int c = __popc(f);
+        const int ex = warp_incl_scan(c) - c;
+        const int tot = __shfl_sync(0xffffffffu, ex + c, 31);
+        if (m + tot <= kSelCap) {
+            int slot = m + ex;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (f >> t & 1) cand[slot++] = ((uint64_t)w[t] << 32) | (uint64_t)(4 * q + t);
+        }
+        m += tot;
+    }
+    __syncwarp();
+    if (m < k || m > kSelCap) {
+        select_generic(hd, it, d, k, v_lo, v_hi, hr, k0, k1);
+        return;
+    }
+    int32_t out = 0;
+    for (int c0 = 0; c0 < m; c0 += 32) {
+        const int c = c0 + lane_id();
+        bool sel = false;
+        uint64_t mine = 0;
+        if (c < m) {
+            mine = cand[c];
+            int rank = 0;
+            for (int o = 0; o < m; ++o) rank += cand[o] < mine;
+            sel = rank < k;
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, sel);
+        if (sel) emit_edge(hd, it, out + __popc(b & lanemask_lt()), (int64_t)(uint32_t)mine);
+        out += __popc(b);
+    }
+    __syncwarp();
+}
+
+// Sampling of one hop: the selection items (queued by phase_count) one per warp,
+// then the full-neighbourhood items as segmented copies, 32 items per warp.
+// cand: kSelCap slots of this warp in shared memory.
+__device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
+{
+    const int warps = blockDim.x >> 5;
+    const int lane = lane_id();
+    const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
+    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
+    // ---- selections (d > k): warp per item
+    const int64_t nsel = *(const volatile uint32_t *)(hd.meta + kMetaSel + hd.h);
+    for (int64_t w = gw; w < nsel; w += nw) {
+        const uint64_t e = hd.selq[w];
+        const int r = (int)(e >> 32);
+        const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+        const RelDev &R = g.rel[r];
+        const int32_t pos0 = hd.indptr[r][i];
+        const int64_t ib = hd.ibase[r][i];
+        const int64_t d = hd.ideg[r][i];
+        const int64_t v = hd.nodes[R.dst_vt][i];
+        const int p = (int)(ib >> 56);
+        const int64_t base = ib & ((1ll << 56) - 1);
+        Item itm;
+        itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
+        itm.soff = (uint32_t)g.off[R.src_vt];
+        itm.ebase = R.edge_base[p] + base;
+        itm.ix = R.indices[p] + base;
+        itm.src_out = hd.src[r] + pos0;
+        itm.eid_out = hd.eids[r] + pos0;
+        const int k = hd.fanout[r];
+        const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
+        if (k <= kSelMaxK)
+            select_fast(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi, cand);
+        else
+            select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
+    }
+    // ---- full neighbourhoods: segmented copy over groups of 32 items
+    const int32_t *nF = meta_nodes(hd.meta, hd.h);
+    int64_t cum[EG_MAX_REL + 1];
+    cum[0] = 0;
+    for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + (hd.fanout[r] != 0 ? nF[g.rel[r].dst_vt] : 0);
+    const int64_t total = cum[g.n_rel];
+    for (int64_t g0 = gw * 32; g0 < total; g0 += nw * 32) {
+        const int64_t it = g0 + lane;
+        int r = 0;
+        int32_t pos0 = 0, cnt = 0, d = 0;
+        int64_t ib = 0;
+        if (it < total) {
+            while (it >= cum[r + 1]) ++r;
+            const int64_t i = it - cum[r];
+            pos0 = hd.indptr[r][i];
+            cnt = hd.indptr[r][i + 1] - pos0;
+            if (cnt > 0) {
+                ib = hd.ibase[r][i];
+                d = hd.ideg[r][i];
+            }
+        }
+        const int k = hd.fanout[r];
+        const bool copy = cnt > 0 && !(k >= 0 && d > k);
+        const int32_t c = copy ? cnt : 0;
+        const int32_t incl = warp_incl_scan(c);
+        const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int32_t excl = incl - c;
+        for (int32_t b = 0; b < tot; b += 32) {
+            const int32_t s = b + lane;
+            int L = 0;   // the lane whose item holds output slot s: last lane with excl <= s
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand_l = L + step;
+                const int32_t ex = __shfl_sync(0xffffffffu, excl, cand_l & 31);
+                if (cand_l < 32 && ex <= s) L = cand_l;
+            }
+            const int32_t exL = __shfl_sync(0xffffffffu, excl, L);
+            const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
+            const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
+            const int rL = __shfl_sync(0xffffffffu, r, L);
+            if (s < tot) {
+                const int p = (int)(ibL >> 56);
+                const int64_t base = ibL & ((1ll << 56) - 1);
+                const int32_t j = s - exL;
+                const RelDev &R = g.rel[rL];
+                const uint32_t gid = (uint32_t)g.off[R.src_vt] + (uint32_t)__ldg(R.indices[p] + base + j);
+                hd.src[rL][posL + j] = gid;
+                hd.eids[rL][posL + j] = R.edge_base[p] + base + j;
+                mark_new(hd, gid, g.boff[R.src_vt] - g.off[R.src_vt]);
+            }
+        }
+    }
+}
+
+// ============================================================================ compaction
+
+// Popcount of each bitmap chunk (virtual block per chunk, one uint4 per thread) and
+// the sums of groups of kGroupChunks chunks.
+constexpr int kGroupChunks = 256;
+
+__device__ void phase_bitcount(const HopDev &hd, int bid, int nb, int32_t n_chunks)
+{
+    static_assert(kChunkWords == 4 * 256, "one uint4 per thread");
+    __shared__ int32_t sh[33];
+    for (int c = bid; c < n_chunks; c += nb) {
+        const uint4 x = __ldcg(reinterpret_cast<const uint4 *>(hd.bitmap + (int64_t)c * kChunkWords) + threadIdx.x);
+        int32_t v = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        v = block_sum(v, sh);
+        if (threadIdx.x == 0) {
+            hd.chunk_cnt[c] = v;
+            if (v) atomicAdd(hd.chunk_pre + c / kGroupChunks, v);
+        }
+    }
+}
+
+// number of set bits in chunks [0, c): group sums + the chunks of c's group before it
+__device__ __forceinline__ int32_t bits_before(const HopDev &hd, int c, int32_t *sh)
+{
+    const int gi = c / kGroupChunks;
+    int32_t s = 0;
+    for (int j = threadIdx.x; j < gi; j += blockDim.x) s += __ldcg(hd.chunk_pre + j);
+    for (int j = gi * kGroupChunks + threadIdx.x; j < c; j += blockDim.x) s += __ldcg(hd.chunk_cnt + j);
+    return block_sum(s, sh);
+}
+
+// New vertices of each chunk, in gid order: append to the node array of their type,
+// set pos[], clear the bitmap words.  Virtual block per chunk, 4 words per thread.
+__device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+{
+    __shared__ int32_t sh[33];
+    for (int c = bid; c < n_chunks; c += nb) {
+        const int32_t mine = __ldcg(hd.chunk_cnt + c);
+        if (mine == 0) continue;   // block-uniform
+        const int64_t bit0 = (int64_t)c * kChunkBits;
+        int u = 0;
+        while (bit0 >= g.boff[u + 1]) ++u;
+        const int fc = (int)(g.boff[u] / kChunkBits);
+        const int32_t prior = bits_before(hd, c, sh) - bits_before(hd, fc, sh);
+        const int32_t nF = meta_nodes(hd.meta, hd.h)[u];
+        const int64_t wi = (int64_t)c * kChunkWords + 4 * threadIdx.x;
+        uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + wi);
+        const uint4 x = __ldcg(wp);
+        uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        const int32_t pc = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+        int32_t tot;
+        int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
+        if (pc) {
+            const int64_t gbase = (g.off[u] - g.boff[u]) + wi * 32;   // gid of bit 0 of word wi
+            int64_t *nodes = hd.nodes[u];
+            const int32_t cap = hd.cap_nodes[u];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t word = w[q];
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    const int64_t gid = gbase + 32 * q + b;
+                    if (position < cap) {
+                        nodes[position] = gid;
+                        hd.pos[gid] = position;
+                    } else {
+                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                    }
+                    ++position;
+                }
+            }
+            *wp = make_uint4(0, 0, 0, 0);
+        }
+        if (threadIdx.x == 0) atomicAdd(meta_nodes(hd.meta, hd.h + 1) + u, mine);
+    }
+}
+
+// indices = pos[src]: the local id of every sampled src in S_h[s(r)].
+__device__ void phase_relabel(const GraphDev &g, const HopDev &hd, int bid, int nb)
+{
+    const int32_t *nnz = meta_nnz(hd.meta, hd.h);
+    int64_t cum[EG_MAX_REL + 1];
+    cum[0] = 0;
+    for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + nnz[r];
+    const int64_t total = cum[g.n_rel];
+    for (int64_t e = bid * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)nb * blockDim.x) {
+        int r = 0;
+        while (e >= cum[r + 1]) ++r;
+        const int64_t le = e - cum[r];
+        hd.indices[r][le] = __ldcg(hd.pos + hd.src[r][le]);
+    }
+}
+
+// End of batch: pos[] back to -1 for every vertex of the batch.
+__device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, int bid, int nb)
+{
+    const int32_t *n = meta_nodes(hd.meta, level);
+    int64_t cum[EG_MAX_VT + 1];
+    cum[0] = 0;
+    for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
+    for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < cum[g.n_vt]; i += (int64_t)nb * blockDim.x) {
+        int u = 0;
+        while (i >= cum[u + 1]) ++u;
+        const int64_t gid = hd.nodes[u][i - cum[u]];
+        if (gid >= 0 && gid < g.off[g.n_vt]) hd.pos[gid] = -1;
+    }
+}
+
+}  // namespace eg
