@@ -44,7 +44,23 @@ __device__ __forceinline__ void grid_barrier(uint32_t *bar, uint32_t nb)
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 2) batch_kernel(const __grid_constant__ GraphDev g,
+__device__ __forceinline__ uint64_t globaltimer()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Tracing: block 0 stamps the global timer after every barrier into the batch
+// counters (copied to the host with them); phase k lasted stamp[k+1] - stamp[k].
+__device__ __forceinline__ void stamp(const BatchDev *bd, int &k)
+{
+    if (bd->trace && blockIdx.x == 0 && threadIdx.x == 0 && k < kMaxStamps)
+        reinterpret_cast<uint64_t *>(bd->hop[0].meta + kMetaStamps)[k] = globaltimer();
+    ++k;
+}
+
+__global__ void __launch_bounds__(kBatchThreads, 3) batch_kernel(const __grid_constant__ GraphDev g,
                                                                  const BatchDev *__restrict__ bd)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
@@ -52,24 +68,33 @@ __global__ void __launch_bounds__(kBatchThreads, 2) batch_kernel(const __grid_co
     uint32_t *bar = bd->bar;
     const int L = bd->n_hops;
     const int32_t n_groups = (bd->n_chunks + kGroupChunks - 1) / kGroupChunks;
+    int k = 0;
+    stamp(bd, k);
     if (bid == 0) phase_seed_split(g, bd->hop[0], bd->seeds);
     grid_barrier(bar, nb);
+    stamp(bd, k);
     for (int h = 0; h < L; ++h) {
         const HopDev &hd = bd->hop[h];
         phase_count(g, hd, bid, nb);
         if (h > 0) phase_relabel(g, bd->hop[h - 1], bid, nb);
         grid_barrier(bar, nb);
+        stamp(bd, k);
         phase_scan(g, hd, bid, nb, n_groups);
         grid_barrier(bar, nb);
+        stamp(bd, k);
         phase_sample(g, hd, bid, nb, s_cand[threadIdx.x >> 5]);
         grid_barrier(bar, nb);
+        stamp(bd, k);
         phase_bitcount(hd, bid, nb, bd->n_chunks);
         grid_barrier(bar, nb);
+        stamp(bd, k);
         phase_emit(g, hd, bid, nb, bd->n_chunks);
         grid_barrier(bar, nb);
+        stamp(bd, k);
     }
     phase_relabel(g, bd->hop[L - 1], bid, nb);
     grid_barrier(bar, nb);
+    stamp(bd, k);
     phase_reset(g, bd->hop[L - 1], L, bid, nb);
 }
 

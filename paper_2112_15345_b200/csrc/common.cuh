@@ -48,7 +48,9 @@ constexpr int kMetaNodes = 0;
 constexpr int kMetaNnz = kMetaNodes + (EG_MAX_HOPS + 1) * EG_MAX_VT;
 constexpr int kMetaSel = kMetaNnz + EG_MAX_HOPS * EG_MAX_REL;   // selection-queue length per hop
 constexpr int kMetaErr = kMetaSel + EG_MAX_HOPS;
-constexpr int kMetaSize = kMetaErr + 8;
+constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase timestamps (tracing)
+constexpr int kMaxStamps = 64;
+constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
 
 // Everything a hop's kernels touch.
 struct HopDev {

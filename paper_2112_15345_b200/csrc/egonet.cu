@@ -787,6 +787,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     BatchDev bd{};
     bd.n_hops = L;
     bd.n_chunks = c->n_chunks;
+    bd.trace = c->trace ? 1 : 0;
     bd.seeds = (const int64_t *)(base + p->o_seeds);
     bd.bar = (uint32_t *)(base + p->o_bar);
     for (int h = 0; h < L; ++h) {
@@ -927,6 +928,28 @@ eg_status finish(eg_blocks *b)
             c->prof_n[1] += 1;
         }
         sl->timed = false;
+    }
+    if (c->trace && c->prof) {
+        // in-kernel phase stamps (batch_kernel): seed, per hop count/scan/sample/bitcount/emit, relabel
+        const uint64_t *st = reinterpret_cast<const uint64_t *>(m + kMetaStamps);
+        std::vector<std::string> names = {"k.seed"};
+        for (int h = 0; h < b->n_hops; ++h)
+            for (const char *x : {"count", "scan", "sample", "bitcount", "emit"})
+                names.push_back("k.h" + std::to_string(h) + "." + x);
+        names.push_back("k.relabel");
+        for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
+            if (!st[k + 1] || !st[k]) break;
+            const double ms = (double)(st[k + 1] - st[k]) * 1e-6;
+            size_t idx = 0;
+            while (idx < c->trace_names.size() && c->trace_names[idx] != names[k]) ++idx;
+            if (idx == c->trace_names.size()) {
+                c->trace_names.push_back(names[k]);
+                c->trace_ms.push_back(0);
+                c->trace_n.push_back(0);
+            }
+            c->trace_ms[idx] += ms;
+            c->trace_n[idx] += 1;
+        }
     }
     if (c->trace && c->prof && sl->tev.size() > 1) {
         for (size_t k = 1; k < sl->tev.size(); ++k) {

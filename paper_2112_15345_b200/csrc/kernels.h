@@ -6,7 +6,7 @@ namespace eg {
 
 // batch.cu: sampling + compaction of a whole batch (one persistent kernel)
 struct BatchDev {
-    int32_t n_hops, n_chunks;
+    int32_t n_hops, n_chunks, trace, _pad;
     const int64_t *seeds;
     uint32_t *bar;                 // grid barrier {count, generation}, zero-initialised
     HopDev hop[EG_MAX_HOPS];

@@ -164,13 +164,11 @@ struct Item {
 
 // If the source is not yet in the batch, mark it in the new-vertex bitmap (the
 // first step of the hop's compaction, fused into sampling).
-__device__ __forceinline__ void mark_new(const HopDev &hd, uint32_t gid, int64_t bit_base)
+__device__ __forceinline__ void mark_new(const HopDev &hd, uint32_t gid, int32_t pos_of_gid, int64_t bit_base)
 {
-    if (__ldcg(hd.pos + gid) < 0) {
+    if (pos_of_gid < 0) {
         const int64_t bit = bit_base + gid;
-        const uint32_t m = 1u << (bit & 31);
-        uint32_t *wp = hd.bitmap + (bit >> 5);
-        if (!(__ldcg(wp) & m)) atomicOr(wp, m);
+        atomicOr(hd.bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED, no round trip
     }
 }
 
@@ -179,7 +177,7 @@ __device__ __forceinline__ void emit_edge(const HopDev &hd, const Item &it, int3
     const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
     it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
-    mark_new(hd, gid, it.bit_base);
+    mark_new(hd, gid, __ldcg(hd.pos + gid), it.bit_base);
 }
 
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
@@ -367,29 +365,55 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
         const int32_t incl = warp_incl_scan(c);
         const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const int32_t excl = incl - c;
-        for (int32_t b = 0; b < tot; b += 32) {
-            const int32_t s = b + lane;
-            int L = 0;   // the lane whose item holds output slot s: last lane with excl <= s
+        constexpr int U = 4;   // slots per lane per round: U independent load chains in flight
+        for (int32_t b0 = 0; b0 < tot; b0 += 32 * U) {
+            uint32_t gid[U];
+            int32_t posv[U];
+            uint32_t *dsrc[U];
+            int64_t *deid[U];
+            int64_t eid[U], bb[U];
+            const int32_t *ixp[U];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int cand_l = L + step;
-                const int32_t ex = __shfl_sync(0xffffffffu, excl, cand_l & 31);
-                if (cand_l < 32 && ex <= s) L = cand_l;
+            for (int q = 0; q < U; ++q) {
+                const int32_t s = b0 + q * 32 + lane;
+                int L = 0;   // the lane whose item holds output slot s: last lane with excl <= s
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand_l = L + step;
+                    const int32_t ex = __shfl_sync(0xffffffffu, excl, cand_l & 31);
+                    if (cand_l < 32 && ex <= s) L = cand_l;
+                }
+                const int32_t exL = __shfl_sync(0xffffffffu, excl, L);
+                const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
+                const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
+                const int rL = __shfl_sync(0xffffffffu, r, L);
+                dsrc[q] = nullptr;
+                if (s < tot) {
+                    const int p = (int)(ibL >> 56);
+                    const int64_t base = ibL & ((1ll << 56) - 1);
+                    const int32_t j = s - exL;
+                    const RelDev &R = g.rel[rL];
+                    ixp[q] = R.indices[p] + base + j;
+                    gid[q] = (uint32_t)g.off[R.src_vt];
+                    bb[q] = g.boff[R.src_vt] - g.off[R.src_vt];
+                    eid[q] = R.edge_base[p] + base + j;
+                    dsrc[q] = hd.src[rL] + posL + j;
+                    deid[q] = hd.eids[rL] + posL + j;
+                }
             }
-            const int32_t exL = __shfl_sync(0xffffffffu, excl, L);
-            const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
-            const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
-            const int rL = __shfl_sync(0xffffffffu, r, L);
-            if (s < tot) {
-                const int p = (int)(ibL >> 56);
-                const int64_t base = ibL & ((1ll << 56) - 1);
-                const int32_t j = s - exL;
-                const RelDev &R = g.rel[rL];
-                const uint32_t gid = (uint32_t)g.off[R.src_vt] + (uint32_t)__ldg(R.indices[p] + base + j);
-                hd.src[rL][posL + j] = gid;
-                hd.eids[rL][posL + j] = R.edge_base[p] + base + j;
-                mark_new(hd, gid, g.boff[R.src_vt] - g.off[R.src_vt]);
-            }
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (dsrc[q]) gid[q] += (uint32_t)__ldg(ixp[q]);
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (dsrc[q]) posv[q] = __ldcg(hd.pos + gid[q]);
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (dsrc[q]) {
+                    *dsrc[q] = gid[q];
+                    *deid[q] = eid[q];
+                    mark_new(hd, gid[q], posv[q], bb[q]);
+                }
         }
     }
 }
