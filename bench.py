@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--depth", type=int, default=4, help="mini-batches in flight per GPU (pipeline lanes)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
@@ -235,6 +236,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     shard = load_context(ctx, graph, world, rank, dev)
     if world > 1:
         ctx.connect_peers()
+    ctx.set_pipeline(args.depth)
     t_load = time.perf_counter() - t_load
     W, K = args.warmup, args.steps
     steps = W + K
@@ -255,15 +257,31 @@ def run_ours(args, cfg, rank, world, local_rank):
         rows = [bl.n_inputs(u) for u in range(cfg.n_vt)]
         return e, rows
 
+    from collections import deque
+
+    def run(lo, hi, seeds, on_retire):
+        """Launch batches lo..hi-1 keeping `depth` in flight; retire in order."""
+        q = deque()
+        for b in range(lo, hi):
+            q.append(launch(b, seeds))
+            if len(q) >= args.depth:
+                bl = q.popleft()
+                on_retire(bl)
+                bl.free()
+        while q:
+            bl = q.popleft()
+            on_retire(bl)
+            bl.free()
+
+    acc = {"edges": 0, "gbytes": 0}
+
+    def count(bl):
+        e, rows = retire(bl)
+        acc["edges"] += e
+        acc["gbytes"] += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
+
     with torch.cuda.stream(stream):
-        pend = launch(0, seeds_dev)
-        for b in range(1, W):
-            nxt = launch(b, seeds_dev)
-            retire(pend)
-            pend.free()
-            pend = nxt
-        retire(pend)
-        pend.free()
+        run(0, W, seeds_dev, retire)
         torch.cuda.synchronize(dev)
         if world > 1:
             torch.distributed.barrier()
@@ -277,16 +295,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
         ev0.record(stream)
-        edges = 0
-        gbytes = 0
-        pend = launch(W, seeds_dev)
-        for b in range(W, steps):
-            nxt = launch(b + 1, seeds_dev) if b + 1 < steps else None
-            e, rows = retire(pend)
-            pend.free()
-            edges += e
-            gbytes += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
-            pend = nxt
+        run(W, steps, seeds_dev, count)
+        edges, gbytes = acc["edges"], acc["gbytes"]
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -330,35 +340,27 @@ def run_ours(args, cfg, rank, world, local_rank):
                 nbytes += rows[u] * row_bytes[u]
             return e, nbytes
 
+        e2e_acc = {"edges": 0, "h2d": 0, "d2h": 0}
+
+        def e2e_count(bl):
+            e, nb = e2e_retire(bl)
+            e2e_acc["edges"] += e
+            e2e_acc["h2d"] += cfg.batch * 8
+            e2e_acc["d2h"] += nb + 576
+
         with torch.cuda.stream(stream):
-            pend = launch(0, pinned_seeds)
-            e2e_retire(pend)
+            run(0, min(W, 3), pinned_seeds, e2e_retire)
             torch.cuda.synchronize(dev)
-            pend.free()
             if world > 1:
                 torch.distributed.barrier()
-            h2d = d2h = 0
-            e_edges = 0
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-            pend = launch(W, pinned_seeds)
-            done = []
-            for b in range(W, steps):
-                nxt = launch(b + 1, pinned_seeds) if b + 1 < steps else None
-                e, nb = e2e_retire(pend)
-                e_edges += e
-                h2d += pinned_seeds[b].numel() * 8
-                d2h += nb + 576
-                done.append(pend)
-                if len(done) > 1:
-                    done.pop(0).free()
-                pend = nxt
+            run(W, steps, pinned_seeds, e2e_count)
             t1.record(stream)
             torch.cuda.synchronize(dev)
-            for bl in done:
-                bl.free()
             ems = t0.elapsed_time(t1)
+        e_edges, h2d, d2h = e2e_acc["edges"], e2e_acc["h2d"], e2e_acc["d2h"]
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([ems, float(e_edges)], dtype=torch.float64, device=dev)
@@ -404,7 +406,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "gather_GBps": (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk, "load_seconds": t_load, "stage_us": trace or None, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+                "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
+                "pipeline_depth": args.depth, "host": {"cores": host_cores(), "cpu": cpu_model()}}
         emit(args, line)
     ctx.close()
     del shard

@@ -168,6 +168,13 @@ EG_API eg_status eg_sample_blocks(eg_ctx *ctx, const int64_t *seeds, int64_t n_s
 EG_API eg_status eg_sample_minibatch(eg_ctx *ctx, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
                                      const int32_t *fanouts, uint64_t rng_seed, int32_t flags, eg_blocks **out);
 
+/* Pipeline depth: up to `depth` batches run concurrently (round-robin over `depth`
+ * lanes, each with its own stream and compaction state: 4 B per global vertex +
+ * N_total/8 bytes).  Default 1.  Results are unchanged; the caller overlaps batches
+ * by enqueueing with EG_ASYNC before waiting (the asynchronous mini-batch pipeline
+ * of P:548-679, on one GPU). */
+EG_API eg_status eg_set_pipeline(eg_ctx *ctx, int32_t depth);
+
 /* Wait for an EG_ASYNC batch; returns its status (EG_ERANGE / EG_EINVAL for bad seeds). */
 EG_API eg_status eg_blocks_wait(eg_blocks *blocks);
 

@@ -59,6 +59,20 @@ struct TimedPair {
 
 }  // namespace
 
+// A lane: one stream + the per-batch compaction state (gid -> position map, new-vertex
+// bitmap, scan scratch).  Batches on different lanes are independent and run
+// concurrently (the asynchronous mini-batch pipeline); batches on one
+// lane are ordered.
+struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ready = nullptr;     // caller stream -> lane ordering
+    int32_t *pos = nullptr;
+    uint32_t *bitmap = nullptr;
+    int32_t *chunk_cnt = nullptr;
+    int32_t *chunk_pre = nullptr;
+    int32_t *partial = nullptr;
+};
+
 // A batch "plan": everything fixed by (hops, fanouts, seed capacity, features):
 // upper bounds, the memory layout of one batch, and its slots.
 struct Slot;
@@ -89,6 +103,7 @@ struct Slot {
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t done = nullptr, s0 = nullptr, s1 = nullptr, g0 = nullptr, g1 = nullptr;
     bool busy = false, used = false, timed = false;
+    int lane = 0;
     std::vector<cudaEvent_t> tev;        // EG_TRACE: one event after each stage of the graph
     std::vector<std::string> tlab;
 };
@@ -107,13 +122,10 @@ struct eg_ctx {
     // own shard (for export)
     eg_relation own_rel[EG_MAX_REL] = {};
     eg_features own_feat[EG_MAX_VT] = {};
-    // compaction state
-    int32_t *pos = nullptr;
-    uint32_t *bitmap = nullptr;
-    int32_t *chunk_cnt = nullptr;
-    int32_t *chunk_pre = nullptr;
-    uint32_t *ticket = nullptr;
-    int32_t *partial = nullptr;
+    // compaction state, one per lane (pipeline depth)
+    std::vector<Lane> lanes;
+    int next_lane = 0;
+    int depth = 1;
     uint64_t *h_dyn = nullptr;   // pinned {rng_seed, n_seeds}
     int32_t n_chunks = 0;
     int32_t *h_meta = nullptr;   // pinned
@@ -293,6 +305,25 @@ void fill_meta(const eg_ctx *c, ShardBlob *b)
         sr.edge_base = R.edge_base;
         sr.max_degree = c->rel_max_degree[r];
     }
+}
+
+eg_status add_lane(eg_ctx *c)
+{
+    Lane ln;
+    const int64_t nt = std::max<int64_t>(1, c->n_total);
+    const size_t words = (size_t)std::max<int64_t>(1, c->g.boff[c->g.n_vt] / 32);
+    EG_CUDA(c, cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+    EG_CUDA(c, cudaEventCreateWithFlags(&ln.ready, cudaEventDisableTiming));
+    EG_CUDA(c, cudaMalloc(&ln.pos, sizeof(int32_t) * nt));
+    EG_CUDA(c, cudaMemset(ln.pos, 0xFF, sizeof(int32_t) * nt));
+    EG_CUDA(c, cudaMalloc(&ln.bitmap, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMemset(ln.bitmap, 0, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMalloc(&ln.chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&ln.chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&ln.partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    EG_CUDA(c, cudaDeviceSynchronize());
+    c->lanes.push_back(ln);
+    return EG_OK;
 }
 
 void to_meta(const ShardBlob &b, eg_shard_meta *m)
@@ -546,16 +577,7 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     EG_CUDA(c, cudaFree(d_max));
     for (int r = 0; r < n_rel; ++r) c->rel_max_degree[r] = (int64_t)h_max[r];
 
-    EG_CUDA(c, cudaMalloc(&c->pos, sizeof(int32_t) * std::max<int64_t>(1, c->n_total)));
-    EG_CUDA(c, cudaMemsetAsync(c->pos, 0xFF, sizeof(int32_t) * std::max<int64_t>(1, c->n_total), c->stream));
-    EG_CUDA(c, cudaMalloc(&c->bitmap, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, g.boff[n_vt] / 32)));
-    EG_CUDA(c, cudaMemsetAsync(c->bitmap, 0, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, g.boff[n_vt] / 32),
-                               c->stream));
-    EG_CUDA(c, cudaMalloc(&c->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&c->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&c->ticket, sizeof(uint32_t)));
-    EG_CUDA(c, cudaMemsetAsync(c->ticket, 0, sizeof(uint32_t), c->stream));
-    EG_CUDA(c, cudaMalloc(&c->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    if ((st = add_lane(c))) return st;
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
     {
@@ -774,12 +796,13 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     HopDev hd{};
     hd.dyn = (const uint64_t *)(base + p->o_dyn);
     hd.meta = (int32_t *)(base + p->o_meta);
-    hd.partial = c->partial;
-    hd.pos = c->pos;
-    hd.bitmap = c->bitmap;
-    hd.chunk_cnt = c->chunk_cnt;
-    hd.chunk_pre = c->chunk_pre;
-    hd.ticket = c->ticket;
+    const Lane &ln = c->lanes[sl->lane];
+    hd.partial = ln.partial;
+    hd.pos = ln.pos;
+    hd.bitmap = ln.bitmap;
+    hd.chunk_cnt = ln.chunk_cnt;
+    hd.chunk_pre = ln.chunk_pre;
+    hd.ticket = nullptr;
     for (int u = 0; u < V; ++u) {
         hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
         hd.cap_nodes[u] = (int32_t)p->capF[L][u];
@@ -855,8 +878,10 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
 
 eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
 {
+    const int lane = c->next_lane;
+    c->next_lane = (c->next_lane + 1) % c->depth;
     for (Slot *sl : p->slots)
-        if (!sl->busy) {
+        if (!sl->busy && sl->lane == lane) {
             if (sl->used) EG_CUDA(c, cudaEventSynchronize(sl->done));   // its last run has retired
             sl->busy = true;
             *out = sl;
@@ -864,6 +889,7 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
         }
     Slot *sl = new Slot();
     sl->plan = p;
+    sl->lane = lane;
     cudaError_t e = cudaMalloc(&sl->mem, p->total);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -910,6 +936,7 @@ eg_status finish(eg_blocks *b)
     eg_ctx *c = b->ctx;
     Slot *sl = b->slot;
     cudaError_t e = cudaEventSynchronize(sl->done);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, sl->done, 0);
     b->ready = true;
     if (e != cudaSuccess) return b->status = fail(c, EG_ECUDA, std::string("batch: ") + cudaGetErrorString(e));
     const int32_t *m = sl->h_meta;
@@ -997,14 +1024,17 @@ eg_status enqueue_batch(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_
     if ((st = get_plan(c, n_hops, fanouts, round_cap(n_seeds), features, &p))) return st;
     Slot *sl = nullptr;
     if ((st = acquire_slot(c, p, &sl))) return st;
+    Lane &ln = c->lanes[sl->lane];
+    EG_CUDA(c, cudaEventRecord(ln.ready, c->stream));          // seeds produced on the caller's stream
+    EG_CUDA(c, cudaStreamWaitEvent(ln.stream, ln.ready, 0));
     if (n_seeds > 0)
         EG_CUDA(c, cudaMemcpyAsync(sl->mem + p->o_seeds, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyDefault,
-                                   c->stream));
+                                   ln.stream));
     sl->h_dyn[0] = rng_seed;
     sl->h_dyn[1] = (uint64_t)n_seeds;
     sl->timed = c->prof;
-    EG_CUDA(c, cudaGraphLaunch(sl->exec, c->stream));
-    EG_CUDA(c, cudaEventRecord(sl->done, c->stream));
+    EG_CUDA(c, cudaGraphLaunch(sl->exec, ln.stream));
+    EG_CUDA(c, cudaEventRecord(sl->done, ln.stream));
     sl->used = true;
     c->launches += p->n_kernels;
     eg_blocks *b = new eg_blocks();
@@ -1152,6 +1182,20 @@ eg_status eg_blocks_free(eg_blocks *b)
     return EG_OK;
 }
 
+eg_status eg_set_pipeline(eg_ctx *c, int32_t depth)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
+    if (depth < 1 || depth > 16) return fail(c, EG_EINVAL, "pipeline depth must be in [1, 16]");
+    while ((int)c->lanes.size() < depth)
+        if ((st = add_lane(c))) return st;
+    // lanes beyond depth stay allocated but unused
+    c->next_lane = 0;
+    c->depth = depth;
+    return EG_OK;
+}
+
 int32_t eg_trace_get(const eg_ctx *c, int32_t i, char *name, size_t name_len, double *total_ms, int64_t *count)
 {
     if (!c) return 0;
@@ -1197,13 +1241,18 @@ eg_status eg_destroy(eg_ctx *c)
     destroy_plans(c);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
-    cudaFree(c->pos);
-    cudaFree(c->bitmap);
-    cudaFree(c->chunk_cnt);
-    cudaFree(c->chunk_pre);
-    cudaFree(c->ticket);
+    for (Lane &ln : c->lanes) {
+        if (ln.stream) cudaStreamSynchronize(ln.stream);
+        cudaFree(ln.pos);
+        cudaFree(ln.bitmap);
+        cudaFree(ln.chunk_cnt);
+        cudaFree(ln.chunk_pre);
+        cudaFree(ln.partial);
+        if (ln.ready) cudaEventDestroy(ln.ready);
+        if (ln.stream) cudaStreamDestroy(ln.stream);
+    }
+    c->lanes.clear();
     cudaFreeHost(c->h_dyn);
-    cudaFree(c->partial);
     cudaFreeHost(c->h_meta);
     delete c;
     return EG_OK;

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__
 
 // ----------------------------------------------------------------------------- TMA path
 
-constexpr int kStages = 6;
+constexpr int kStages = 4;
 constexpr int kStageBytes = 16384;
 constexpr int kMaxRowsPerTile = 128;
 

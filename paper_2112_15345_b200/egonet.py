@@ -28,7 +28,7 @@ ABI_SYMBOLS = [
     "eg_sample_blocks", "eg_block_view_get", "eg_blocks_n_hops", "eg_blocks_n_inputs", "eg_gather_features",
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
-    "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get",
+    "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline",
 ]
 
 EG_FEATURES = 1
@@ -125,6 +125,7 @@ def lib(build_if_missing: bool = True):
         L.eg_export_shard.argtypes = [vp, vp, P(c.c_size_t)]
         L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
         L.eg_attach_peer.argtypes = [vp, vp]
+        L.eg_set_pipeline.argtypes = [vp, c.c_int32]
         L.eg_trace_get.argtypes = [vp, c.c_int32, c.c_char_p, c.c_size_t, P(c.c_double), P(c.c_int64)]
         L.eg_trace_get.restype = c.c_int32
         L.eg_check_shard_metas.argtypes = [c.c_int32, vp, vp, vp, c.c_char_p, c.c_size_t]
@@ -459,6 +460,10 @@ class Context:
             ptrs[u] = o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data
         self._check(lib().eg_gather_features(self._h, blocks.handle, ptrs), "eg_gather_features")
         return outs
+
+    def set_pipeline(self, depth: int):
+        """Up to `depth` batches in flight (independent lanes / streams)."""
+        self._check(lib().eg_set_pipeline(self._h, depth), "eg_set_pipeline")
 
     def set_profiling(self, on: bool):
         self._check(lib().eg_set_profiling(self._h, 1 if on else 0), "eg_set_profiling")

@@ -237,3 +237,26 @@ def test_c1_batch_sizes_share_and_split_plans(c1):
     for n, fo in [(1, cfg.fanouts), (63, cfg.fanouts), (65, cfg.fanouts), (200, [[2, 3, 4], [4, 3, 2]]),
                   (64, cfg.fanouts)]:
         run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 7, batch=n), fo, 1000 + n, rows)
+
+
+def test_c2_pipeline_depth4_concurrent_lanes(c2):
+    """Four batches in flight on four lanes (streams + compaction state): each bit-exact."""
+    import torch
+    cfg, g, rows, ctx = c2
+    ctx.set_pipeline(4)
+    try:
+        idx = list(range(40, 52))
+        seeds = [torch.from_numpy(synth.batch_seeds(cfg, i)).cuda() for i in idx]
+        pend = []
+        for k, i in enumerate(idx):
+            pend.append((i, ctx.sample_minibatch(seeds[k], cfg.fanouts, synth.rng_seed(cfg, i), features=True,
+                                                 async_=True)))
+            if len(pend) == 4 or k == len(idx) - 1:
+                while pend:
+                    j, b = pend.pop(0)
+                    res = oracle.sample(g, synth.batch_seeds(cfg, j), cfg.fanouts, synth.rng_seed(cfg, j))
+                    assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+                    assert_same_features(res, _features_of(b, cfg), cfg, rows)
+                    b.free()
+    finally:
+        ctx.set_pipeline(1)
