@@ -373,18 +373,42 @@ def run_ours(args, cfg, rank, world, local_rank):
                "note": "seeds from pinned host memory in (H2D inside eg_sample_minibatch), gathered feature rows "
                        "out to pinned host memory (D2H), per-batch counters read back; blocks stay device-resident"}
 
-    # roofline of the gather kernel (events inside the library, on its stream, timed region)
+    # roofline of the gather kernel (events inside the library's graph, on its stream,
+    # timed region).  P = 1: HBM-bound (read row + write row + read id).  P > 1: rows owned
+    # by peers cross NVLink; the remote share is measured on one extra batch.
     peak, peak_src = load_peaks()
-    gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])      # gather kernel node, graph-internal events
+    gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])      # gather kernel node
     sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])      # sampling + compaction nodes
     achieved = (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     tr = load_traffic(cfg.name)
-    roofline = {"kernel": "gather_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    roofline = {"kernel": "gather_tma_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                 "algorithmic_bytes_per_launch": gbytes / K,
                 "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id)",
                 "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_batch": sample_ms}
+    if world > 1:
+        with torch.cuda.stream(stream):
+            bl = ctx.sample_minibatch(seeds_dev[0], fanouts, rngs[0], features=False)
+            remote = 0
+            rows_tot = 0
+            bounds = shard["bounds"]
+            for u in cfg.feats:
+                ids = bl[bl.n_hops - 1].src_nodes[u] - int(cfg.offsets[u])
+                lo, hi = int(bounds[u][rank]), int(bounds[u][rank + 1])
+                n_remote = int(((ids < lo) | (ids >= hi)).sum().item())
+                remote += n_remote * row_bytes[u]
+                rows_tot += ids.numel() * row_bytes[u]
+            bl.free()
+        frac_remote = remote / max(1, rows_tot)
+        nv_bytes = (gbytes / K) / 2 * frac_remote          # row bytes read over NVLink per launch
+        nv_peak = 770.0
+        nv_achieved = nv_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
+        roofline.update({"bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak, "frac": nv_achieved / nv_peak,
+                         "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction per GPU",
+                         "per_unit": "row_bytes per input row owned by a peer (read over NVLink)",
+                         "algorithmic_bytes_per_launch": nv_bytes, "remote_row_fraction": frac_remote,
+                         "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak}})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

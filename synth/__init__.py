@@ -59,6 +59,7 @@ def lib():
         L.sy_indptr.restype = c.c_int
         L.sy_indices.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_void_p]
         L.sy_features.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
+        L.sy_features_ids.argtypes = [c.c_uint64, c.c_int32, c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
         L.sy_select_train.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_uint64, c.c_void_p, c.c_int64]
         L.sy_select_train.restype = c.c_int64
         L.sy_perm_keys.argtypes = [c.c_uint64, c.c_int64, c.c_void_p, c.c_int64, c.c_void_p]
@@ -238,6 +239,25 @@ def host_features(cfg: Config, u: int, lo: int = 0, hi: int | None = None) -> np
     out = np.empty((hi - lo, dim), dtype=NP_DTYPE[dt])
     lib().sy_features(cfg.gen_seed, u, lo, hi, dim, dt, out.ctypes.data)
     return out
+
+
+def host_features_ids(cfg: Config, u: int, tids) -> np.ndarray:
+    """Feature rows of the given type-local ids (no full materialisation)."""
+    dim, dt = cfg.feats[u]
+    tids = np.ascontiguousarray(tids, dtype=np.int64)
+    out = np.empty((len(tids), dim), dtype=NP_DTYPE[dt])
+    lib().sy_features_ids(cfg.gen_seed, u, tids.ctypes.data, len(tids), dim, dt, out.ctypes.data)
+    return out
+
+
+class LazyRows:
+    """Stands in for a [N_u, dim] host feature array: rows[tids] computed on demand."""
+
+    def __init__(self, cfg: Config, u: int):
+        self.cfg, self.u = cfg, u
+
+    def take(self, tids):
+        return host_features_ids(self.cfg, self.u, tids)
 
 
 # ----------------------------------------------------------------------------- partition

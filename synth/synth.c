@@ -119,6 +119,23 @@ void sy_features(uint64_t G, int32_t u, int64_t tid_lo, int64_t tid_hi, int64_t 
     }
 }
 
+/* feature rows of an arbitrary list of tids (rows not materialised on the host) */
+void sy_features_ids(uint64_t G, int32_t u, const int64_t *tids, int64_t n, int64_t dim, int32_t dtype,
+                     void *out)
+{
+    if (dtype == 0) {
+        uint32_t *o = (uint32_t *)out;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t c = 0; c < dim; ++c) o[i * dim + c] = sy_feat_f32(G, u, tids[i], c);
+    } else {
+        uint16_t *o = (uint16_t *)out;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t c = 0; c < dim; ++c) o[i * dim + c] = sy_feat_f16(G, u, tids[i], c);
+    }
+}
+
 /* train ids: tids t in [0, n) with hash(G,'TRN_',t) < thresh (ascending);
  * returns the count (written up to cap). */
 int64_t sy_select_train(uint64_t G, int32_t u, int64_t n, uint64_t thresh, int64_t *out, int64_t cap)

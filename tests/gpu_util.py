@@ -47,7 +47,12 @@ def assert_same_features(res, feats, cfg, host_rows):
         if u not in cfg.feats:
             assert feats[u] is None
             continue
-        want = oracle.gather(res, cfg.vt_counts, u, host_rows[u])
+        rows = host_rows[u]
+        if isinstance(rows, synth.LazyRows):
+            # huge configs: out_u[i] = rows_u[tid_i] with rows_u defined by the generator
+            want = rows.take(res.input_nodes(u) - int(cfg.offsets[u]))
+        else:
+            want = oracle.gather(res, cfg.vt_counts, u, rows)
         got = feats[u].cpu().numpy()
         assert got.shape == want.shape
         assert got.tobytes() == want.tobytes(), f"feature bytes differ for type {u}"
