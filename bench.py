@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--depth", type=int, default=4, help="mini-batches in flight per GPU (pipeline lanes)")
+    ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
+    ap.add_argument("--bundle", type=int, default=4, help="mini-batches per launch (bundled kernels)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
@@ -236,7 +237,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     shard = load_context(ctx, graph, world, rank, dev)
     if world > 1:
         ctx.connect_peers()
-    ctx.set_pipeline(args.depth)
+    ctx.set_pipeline(args.depth, args.bundle)
     t_load = time.perf_counter() - t_load
     W, K = args.warmup, args.steps
     steps = W + K
@@ -247,9 +248,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
     torch.cuda.synchronize(dev)
 
-    def launch(b, seeds):
-        # one CUDA-graph launch: sample + compact all hops + gather features; no host sync
-        return ctx.sample_minibatch(seeds[b], fanouts, rngs[b], features=True, async_=True)
+    def launch(b0, b1, seeds):
+        # one CUDA-graph launch for batches b0..b1-1: sample + compact all hops + gather
+        # features; no host sync
+        if b1 - b0 == 1 and args.bundle == 1:
+            return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=True, async_=True)]
+        return ctx.sample_bundle([seeds[b] for b in range(b0, b1)], fanouts, rngs[b0:b1], features=True,
+                                 async_=True)
 
     def retire(bl):
         bl.wait()
@@ -260,18 +265,18 @@ def run_ours(args, cfg, rank, world, local_rank):
     from collections import deque
 
     def run(lo, hi, seeds, on_retire):
-        """Launch batches lo..hi-1 keeping `depth` in flight; retire in order."""
+        """Launch batches lo..hi-1 in bundles, keeping `depth` launches in flight."""
         q = deque()
-        for b in range(lo, hi):
-            q.append(launch(b, seeds))
+        for b0 in range(lo, hi, args.bundle):
+            q.append(launch(b0, min(hi, b0 + args.bundle), seeds))
             if len(q) >= args.depth:
-                bl = q.popleft()
+                for bl in q.popleft():
+                    on_retire(bl)
+                    bl.free()
+        while q:
+            for bl in q.popleft():
                 on_retire(bl)
                 bl.free()
-        while q:
-            bl = q.popleft()
-            on_retire(bl)
-            bl.free()
 
     acc = {"edges": 0, "gbytes": 0}
 
@@ -379,17 +384,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     peak, peak_src = load_peaks()
     gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])      # gather kernel node
     sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])      # sampling + compaction nodes
-    achieved = (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
+    n_launch = max(1, prof["n_gather"])                             # one gather launch per bundle
+    achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     tr = load_traffic(cfg.name)
     roofline = {"kernel": "gather_tma_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                "algorithmic_bytes_per_launch": gbytes / K,
-                "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id)",
-                "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_batch": sample_ms}
+                "algorithmic_bytes_per_launch": gbytes / n_launch,
+                "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id); one launch gathers "
+                            "the rows of a bundle of %d mini-batches" % args.bundle,
+                "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms}
     if world > 1:
         with torch.cuda.stream(stream):
             bl = ctx.sample_minibatch(seeds_dev[0], fanouts, rngs[0], features=False)
+            bl.wait()
             remote = 0
             rows_tot = 0
             bounds = shard["bounds"]
@@ -401,7 +409,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 rows_tot += ids.numel() * row_bytes[u]
             bl.free()
         frac_remote = remote / max(1, rows_tot)
-        nv_bytes = (gbytes / K) / 2 * frac_remote          # row bytes read over NVLink per launch
+        nv_bytes = (gbytes / n_launch) / 2 * frac_remote   # row bytes read over NVLink per launch
         nv_peak = 770.0
         nv_achieved = nv_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
         roofline.update({"bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak, "frac": nv_achieved / nv_peak,
@@ -427,11 +435,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                     sorted({"fp32" if cfg.feats[u][1] == 0 else "fp16" for u in cfg.feats})),
                 "data": "synthetic (seeded generator, synth/)", "config": workload(cfg, world),
                 "minibatches_per_s": world * K / (ms / 1e3),
-                "gather_GBps": (gbytes / K) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else None,
+                "gather_GBps": achieved if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
-                "pipeline_depth": args.depth, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+                "pipeline_depth": args.depth, "bundle": args.bundle, "host": {"cores": host_cores(), "cpu": cpu_model()}}
         emit(args, line)
     ctx.close()
     del shard

@@ -168,12 +168,23 @@ EG_API eg_status eg_sample_blocks(eg_ctx *ctx, const int64_t *seeds, int64_t n_s
 EG_API eg_status eg_sample_minibatch(eg_ctx *ctx, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
                                      const int32_t *fanouts, uint64_t rng_seed, int32_t flags, eg_blocks **out);
 
-/* Pipeline depth: up to `depth` batches run concurrently (round-robin over `depth`
- * lanes, each with its own stream and compaction state: 4 B per global vertex +
- * N_total/8 bytes).  Default 1.  Results are unchanged; the caller overlaps batches
- * by enqueueing with EG_ASYNC before waiting (the asynchronous mini-batch pipeline
- * of P:548-679, on one GPU). */
-EG_API eg_status eg_set_pipeline(eg_ctx *ctx, int32_t depth);
+/* Pipeline shape.  depth: up to `depth` launches run concurrently (round-robin over
+ * `depth` lanes, each with its own stream); bundle: one launch may carry up to `bundle`
+ * mini-batches (eg_sample_bundle), each phase kernel processing all of them at once
+ * (the paper's bundling of several mini-batches).  Each lane keeps `bundle`
+ * compaction states (4 B per global vertex + N_total/8 bytes each).  Default 1, 1.
+ * Results never change; the caller overlaps launches by enqueueing with EG_ASYNC
+ * before waiting (the asynchronous mini-batch pipeline of P:548-679). */
+EG_API eg_status eg_set_pipeline(eg_ctx *ctx, int32_t depth, int32_t bundle);
+
+/* n_batches (1 <= n <= bundle) independent mini-batches as ONE graph launch: batch b
+ * has seeds[b] (n_seeds[b] gids, host or device), rng_seeds[b]; all share n_hops and
+ * fanouts.  out[b] receives batch b's handle (freed independently).  Same flags and
+ * errors as eg_sample_minibatch; without EG_ASYNC the call returns once all n_batches
+ * are resolved (on an error all handles are released and the first error returned). */
+EG_API eg_status eg_sample_bundle(eg_ctx *ctx, int32_t n_batches, const int64_t *const *seeds,
+                                  const int64_t *n_seeds, int32_t n_hops, const int32_t *fanouts,
+                                  const uint64_t *rng_seeds, int32_t flags, eg_blocks **out);
 
 /* Wait for an EG_ASYNC batch; returns its status (EG_ERANGE / EG_EINVAL for bad seeds). */
 EG_API eg_status eg_blocks_wait(eg_blocks *blocks);

@@ -59,13 +59,9 @@ struct TimedPair {
 
 }  // namespace
 
-// A lane: one stream + the per-batch compaction state (gid -> position map, new-vertex
-// bitmap, scan scratch).  Batches on different lanes are independent and run
-// concurrently (the asynchronous mini-batch pipeline); batches on one
-// lane are ordered.
-struct Lane {
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ready = nullptr;     // caller stream -> lane ordering
+// Compaction state of one batch in flight: gid -> position map, new-vertex bitmap,
+// scan scratch.
+struct BatchState {
     int32_t *pos = nullptr;
     uint32_t *bitmap = nullptr;
     int32_t *chunk_cnt = nullptr;
@@ -73,36 +69,51 @@ struct Lane {
     int32_t *partial = nullptr;
 };
 
-// A batch "plan": everything fixed by (hops, fanouts, seed capacity, features):
-// upper bounds, the memory layout of one batch, and its slots.
+// A lane: one stream + the states of the `bundle` batches one launch carries.  Launches
+// on different lanes are independent and run concurrently (the asynchronous mini-batch
+// pipeline); launches on one lane are ordered.
+struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ready = nullptr;     // caller stream -> lane ordering
+    std::vector<BatchState> st;
+};
+
+// A batch "plan": everything fixed by (hops, fanouts, seed capacity, features, bundle
+// size B): upper bounds, the memory layout of one batch (repeated B times), its slots.
 struct Slot;
 struct Plan {
     int32_t n_hops = 0;
     int32_t fanouts[EG_MAX_HOPS * EG_MAX_REL] = {};
     int64_t n_cap = 0;
     bool features = false;
+    int32_t B = 1;
     int64_t capF[EG_MAX_HOPS + 1][EG_MAX_VT] = {};
     int64_t capE[EG_MAX_HOPS][EG_MAX_REL] = {};
-    size_t o_meta = 0, o_dyn = 0, o_seeds = 0, total = 0;
+    // per-batch layout (offsets inside a batch region of `stride` bytes)
+    size_t o_meta = 0, o_dyn = 0, o_seeds = 0, stride = 0;
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_selq[EG_MAX_HOPS] = {}, o_bd = 0, o_bar = 0;
+           o_selq[EG_MAX_HOPS] = {};
+    size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
+    char *batch_base(char *mem, int b) const { return mem + o_bd + align_bd() + (size_t)b * stride; }
+    static size_t align_bd() { return (sizeof(BatchDev) + 255) / 256 * 256; }
 };
 
-// One batch's worth of device memory with its captured CUDA graph:
-//   H2D {rng_seed, n_seeds} -> memset counters -> seed_split -> per hop (count, scan,
-//   sample, mark, bitcount, emit, relabel) -> reset -> [gather] -> D2H counters.
+// One launch's worth of device memory (B batches) with its captured CUDA graph:
+//   H2D {rng_seed, n_seeds} x B -> memset counters -> seed split -> per hop (count, scan,
+//   sample, bitcount, emit) -> relabel -> reset -> [gather] -> D2H counters.
 struct Slot {
     Plan *plan = nullptr;
     char *mem = nullptr;
-    int32_t *h_meta = nullptr;   // pinned
-    uint64_t *h_dyn = nullptr;   // pinned
+    int32_t *h_meta = nullptr;   // pinned, B x kMetaSize
+    uint64_t *h_dyn = nullptr;   // pinned, B x {rng_seed, n_seeds}
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t done = nullptr, s0 = nullptr, s1 = nullptr, g0 = nullptr, g1 = nullptr;
-    bool busy = false, used = false, timed = false;
+    int refs = 0;                // live eg_blocks handles of the last launch
+    bool used = false, timed = false, finished = false;
     int lane = 0;
     std::vector<cudaEvent_t> tev;        // EG_TRACE: one event after each stage of the graph
     std::vector<std::string> tlab;
@@ -122,10 +133,10 @@ struct eg_ctx {
     // own shard (for export)
     eg_relation own_rel[EG_MAX_REL] = {};
     eg_features own_feat[EG_MAX_VT] = {};
-    // compaction state, one per lane (pipeline depth)
+    // pipeline: `depth` lanes, each carrying bundles of up to `bundle` batches
     std::vector<Lane> lanes;
     int next_lane = 0;
-    int depth = 1;
+    int depth = 1, bundle = 1;
     uint64_t *h_dyn = nullptr;   // pinned {rng_seed, n_seeds}
     int32_t n_chunks = 0;
     int32_t *h_meta = nullptr;   // pinned
@@ -150,6 +161,7 @@ struct eg_ctx {
 struct eg_blocks {
     eg_ctx *ctx = nullptr;
     Slot *slot = nullptr;
+    int32_t bidx = 0;            // batch index within the slot's bundle
     int32_t n_hops = 0, n_vt = 0, n_rel = 0;
     bool ready = false;
     eg_status status = EG_OK;
@@ -307,22 +319,37 @@ void fill_meta(const eg_ctx *c, ShardBlob *b)
     }
 }
 
-eg_status add_lane(eg_ctx *c)
+eg_status alloc_state(eg_ctx *c, BatchState *st)
 {
-    Lane ln;
     const int64_t nt = std::max<int64_t>(1, c->n_total);
     const size_t words = (size_t)std::max<int64_t>(1, c->g.boff[c->g.n_vt] / 32);
-    EG_CUDA(c, cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
-    EG_CUDA(c, cudaEventCreateWithFlags(&ln.ready, cudaEventDisableTiming));
-    EG_CUDA(c, cudaMalloc(&ln.pos, sizeof(int32_t) * nt));
-    EG_CUDA(c, cudaMemset(ln.pos, 0xFF, sizeof(int32_t) * nt));
-    EG_CUDA(c, cudaMalloc(&ln.bitmap, sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMemset(ln.bitmap, 0, sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMalloc(&ln.chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&ln.chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&ln.partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    EG_CUDA(c, cudaMalloc(&st->pos, sizeof(int32_t) * nt));
+    EG_CUDA(c, cudaMemset(st->pos, 0xFF, sizeof(int32_t) * nt));
+    EG_CUDA(c, cudaMalloc(&st->bitmap, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMemset(st->bitmap, 0, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMalloc(&st->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&st->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    return EG_OK;
+}
+
+// At least `depth` lanes with at least `bundle` batch states each.
+eg_status ensure_lanes(eg_ctx *c, int depth, int bundle)
+{
+    eg_status st;
+    while ((int)c->lanes.size() < depth) {
+        Lane ln;
+        EG_CUDA(c, cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+        EG_CUDA(c, cudaEventCreateWithFlags(&ln.ready, cudaEventDisableTiming));
+        c->lanes.push_back(ln);
+    }
+    for (Lane &ln : c->lanes)
+        while ((int)ln.st.size() < bundle) {
+            BatchState bs;
+            if ((st = alloc_state(c, &bs))) return st;
+            ln.st.push_back(bs);
+        }
     EG_CUDA(c, cudaDeviceSynchronize());
-    c->lanes.push_back(ln);
     return EG_OK;
 }
 
@@ -577,7 +604,7 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     EG_CUDA(c, cudaFree(d_max));
     for (int r = 0; r < n_rel; ++r) c->rel_max_degree[r] = (int64_t)h_max[r];
 
-    if ((st = add_lane(c))) return st;
+    if ((st = ensure_lanes(c, 1, 1))) return st;
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
     {
@@ -701,12 +728,13 @@ eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
 
 namespace {
 
-eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, bool features, Plan **out)
+eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, bool features, int32_t B,
+                   Plan **out)
 {
     const GraphDev &g = c->g;
     const int V = g.n_vt, R = g.n_rel;
     for (Plan *p : c->plans)
-        if (p->n_hops == L && p->n_cap == n_cap && p->features == features &&
+        if (p->n_hops == L && p->n_cap == n_cap && p->features == features && p->B == B &&
             !memcmp(p->fanouts, fanouts, sizeof(int32_t) * L * R)) {
             *out = p;
             return EG_OK;
@@ -716,6 +744,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
     memcpy(p->fanouts, fanouts, sizeof(int32_t) * L * R);
     p->n_cap = n_cap;
     p->features = features;
+    p->B = B;
     int32_t src_vt[EG_MAX_REL], dst_vt[EG_MAX_REL];
     for (int r = 0; r < R; ++r) {
         src_vt[r] = g.rel[r].src_vt;
@@ -742,8 +771,6 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         return o;
     };
     p->o_meta = take(sizeof(int32_t) * kMetaSize);
-    p->o_bd = take(sizeof(BatchDev));
-    p->o_bar = take(sizeof(uint32_t) * 2);
     p->o_dyn = take(sizeof(uint64_t) * 2);
     p->o_seeds = take(sizeof(int64_t) * n_cap);
     for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
@@ -765,7 +792,9 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
     if (features)
         for (int u = 0; u < V; ++u)
             if (c->f.row_bytes[u]) p->o_feat[u] = take((size_t)(p->capF[L][u] * c->f.row_bytes[u]));
-    p->total = off;
+    p->stride = off;
+    p->o_bd = 0;
+    p->total = Plan::align_bd() + (size_t)B * p->stride;
     c->plans.push_back(p);
     *out = p;
     return EG_OK;
@@ -786,50 +815,64 @@ void fill_views(const Plan *p, char *base, eg_blocks *b)
         }
 }
 
-// Record the whole batch into a CUDA graph (once per slot).
+// Record one launch of the slot's bundle into a CUDA graph (once per slot).
 eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
 {
     const GraphDev &g = c->g;
-    const int V = g.n_vt, R = g.n_rel, L = p->n_hops;
-    char *base = sl->mem;
+    const int V = g.n_vt, R = g.n_rel, L = p->n_hops, B = p->B;
     cudaStream_t cs = c->cap_stream;
-    HopDev hd{};
-    hd.dyn = (const uint64_t *)(base + p->o_dyn);
-    hd.meta = (int32_t *)(base + p->o_meta);
     const Lane &ln = c->lanes[sl->lane];
-    hd.partial = ln.partial;
-    hd.pos = ln.pos;
-    hd.bitmap = ln.bitmap;
-    hd.chunk_cnt = ln.chunk_cnt;
-    hd.chunk_pre = ln.chunk_pre;
-    hd.ticket = nullptr;
-    for (int u = 0; u < V; ++u) {
-        hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
-        hd.cap_nodes[u] = (int32_t)p->capF[L][u];
-    }
-    BatchDev bd{};
-    bd.n_hops = L;
-    bd.n_chunks = c->n_chunks;
-    bd.trace = c->trace ? 1 : 0;
-    bd.seeds = (const int64_t *)(base + p->o_seeds);
-    bd.bar = (uint32_t *)(base + p->o_bar);
-    for (int h = 0; h < L; ++h) {
-        HopDev x = hd;
-        x.h = h;
-        for (int r = 0; r < R; ++r) {
-            x.fanout[r] = p->fanouts[h * R + r];
-            x.indptr[r] = (int32_t *)(base + p->o_ip[h][r]);
-            x.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
-            x.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
-            x.src[r] = (uint32_t *)(base + p->o_src[h][r]);
-            x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
-            x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
+    BatchDev *bd = new BatchDev();
+    memset(bd, 0, sizeof(BatchDev));
+    bd->n_hops = L;
+    bd->n_chunks = c->n_chunks;
+    bd->trace = c->trace ? 1 : 0;
+    bd->B = B;
+    GatherSet gs{};
+    gs.nb = B;
+    for (int b = 0; b < B; ++b) {
+        char *base = p->batch_base(sl->mem, b);
+        const BatchState &st = ln.st[b];
+        HopDev hd{};
+        hd.dyn = (const uint64_t *)(base + p->o_dyn);
+        hd.meta = (int32_t *)(base + p->o_meta);
+        hd.partial = st.partial;
+        hd.pos = st.pos;
+        hd.bitmap = st.bitmap;
+        hd.chunk_cnt = st.chunk_cnt;
+        hd.chunk_pre = st.chunk_pre;
+        hd.ticket = nullptr;
+        for (int u = 0; u < V; ++u) {
+            hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
+            hd.cap_nodes[u] = (int32_t)p->capF[L][u];
         }
-        x.selq = (uint64_t *)(base + p->o_selq[h]);
-        bd.hop[h] = x;
+        bd->seeds[b] = (const int64_t *)(base + p->o_seeds);
+        for (int h = 0; h < L; ++h) {
+            HopDev x = hd;
+            x.h = h;
+            for (int r = 0; r < R; ++r) {
+                x.fanout[r] = p->fanouts[h * R + r];
+                x.indptr[r] = (int32_t *)(base + p->o_ip[h][r]);
+                x.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
+                x.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
+                x.src[r] = (uint32_t *)(base + p->o_src[h][r]);
+                x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
+                x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
+            }
+            x.selq = (uint64_t *)(base + p->o_selq[h]);
+            bd->hop[b][h] = x;
+        }
+        GatherDev &gd = gs.b[b];
+        gd.meta = hd.meta;
+        gd.level = L;
+        for (int u = 0; u < V; ++u) {
+            gd.nodes[u] = hd.nodes[u];
+            gd.out[u] = p->o_feat[u] ? (uint8_t *)(base + p->o_feat[u]) : nullptr;
+        }
     }
-    EG_CUDA(c, cudaMemcpy(base + p->o_bd, &bd, sizeof(bd), cudaMemcpyHostToDevice));
-    EG_CUDA(c, cudaMemset(base + p->o_bar, 0, sizeof(uint32_t) * 2));
+    cudaError_t e0 = cudaMemcpy(sl->mem + p->o_bd, bd, sizeof(BatchDev), cudaMemcpyHostToDevice);
+    delete bd;
+    if (e0 != cudaSuccess) return fail(c, EG_ECUDA, std::string("BatchDev upload: ") + cudaGetErrorString(e0));
     int nk = 0;
     auto mark = [&](const std::string &label) {
         if (!c->trace) return;
@@ -840,32 +883,30 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         sl->tlab.push_back(label);
     };
     EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
-    cudaMemcpyAsync((void *)hd.dyn, sl->h_dyn, sizeof(uint64_t) * 2, cudaMemcpyHostToDevice, cs);
+    for (int b = 0; b < B; ++b) {
+        char *base = p->batch_base(sl->mem, b);
+        cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + 2 * b, sizeof(uint64_t) * 2, cudaMemcpyHostToDevice, cs);
+        cudaMemsetAsync(base + p->o_meta, 0, sizeof(int32_t) * kMetaSize, cs);
+    }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
-    cudaMemsetAsync(hd.meta, 0, sizeof(int32_t) * kMetaSize, cs);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(base + p->o_bd), L, c->n_chunks, cs);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
-        GatherDev gd{};
-        gd.meta = hd.meta;
-        gd.level = L;
         bool any = false;
-        for (int u = 0; u < V; ++u) {
-            gd.nodes[u] = hd.nodes[u];
-            gd.out[u] = p->o_feat[u] ? (uint8_t *)(base + p->o_feat[u]) : nullptr;
-            any |= gd.out[u] != nullptr;
-        }
+        for (int u = 0; u < V; ++u) any |= p->o_feat[u] != 0;
         cudaEventRecordWithFlags(sl->g0, cs, cudaEventRecordExternal);
         if (any) {
-            launch_gather(g, c->f, gd, cs);
+            launch_gather(g, c->f, gs, cs);
             ++nk;
         }
-        mark("gather");
         cudaEventRecordWithFlags(sl->g1, cs, cudaEventRecordExternal);
+        mark("gather");
     }
-    cudaMemcpyAsync(sl->h_meta, hd.meta, sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, cs);
+    for (int b = 0; b < B; ++b)
+        cudaMemcpyAsync(sl->h_meta + (size_t)b * kMetaSize, p->batch_base(sl->mem, b) + p->o_meta,
+                        sizeof(int32_t) * kMetaSize, cudaMemcpyDeviceToHost, cs);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
     if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
@@ -881,9 +922,8 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
     const int lane = c->next_lane;
     c->next_lane = (c->next_lane + 1) % c->depth;
     for (Slot *sl : p->slots)
-        if (!sl->busy && sl->lane == lane) {
+        if (sl->refs == 0 && sl->lane == lane) {
             if (sl->used) EG_CUDA(c, cudaEventSynchronize(sl->done));   // its last run has retired
-            sl->busy = true;
             *out = sl;
             return EG_OK;
         }
@@ -896,8 +936,8 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
         delete sl;
         return fail(c, EG_ENOMEM, std::string("batch slot cudaMalloc: ") + cudaGetErrorString(e));
     }
-    EG_CUDA(c, cudaMallocHost(&sl->h_meta, sizeof(int32_t) * kMetaSize));
-    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 2));
+    EG_CUDA(c, cudaMallocHost(&sl->h_meta, sizeof(int32_t) * kMetaSize * p->B));
+    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 2 * p->B));
     EG_CUDA(c, cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming));
     EG_CUDA(c, cudaEventCreate(&sl->s0));
     EG_CUDA(c, cudaEventCreate(&sl->s1));
@@ -906,7 +946,6 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
     p->slots.push_back(sl);
     eg_status st = capture_slot(c, p, sl);
     if (st) return st;
-    sl->busy = true;
     *out = sl;
     return EG_OK;
 }
@@ -929,7 +968,56 @@ void destroy_plans(eg_ctx *c)
     c->plans.clear();
 }
 
-// Resolve a pending batch: wait for its counters, read sizes and error bits.
+void trace_add(eg_ctx *c, const std::string &name, double ms)
+{
+    size_t idx = 0;
+    while (idx < c->trace_names.size() && c->trace_names[idx] != name) ++idx;
+    if (idx == c->trace_names.size()) {
+        c->trace_names.push_back(name);
+        c->trace_ms.push_back(0);
+        c->trace_n.push_back(0);
+    }
+    c->trace_ms[idx] += ms;
+    c->trace_n[idx] += 1;
+}
+
+// The slot's last launch has completed (host waited): per-launch timing, once.
+void slot_finished(eg_ctx *c, Slot *sl)
+{
+    if (sl->finished) return;
+    sl->finished = true;
+    if (!sl->timed) return;
+    sl->timed = false;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, sl->s0, sl->s1) == cudaSuccess) {
+        c->prof_ms[0] += ms;
+        c->prof_n[0] += 1;
+    }
+    if (sl->plan->features && cudaEventElapsedTime(&ms, sl->g0, sl->g1) == cudaSuccess) {
+        c->prof_ms[1] += ms;
+        c->prof_n[1] += 1;
+    }
+    if (c->trace) {
+        // in-kernel phase stamps of batch 0: seed, per hop count/scan/sample/bitcount/emit, relabel, reset
+        const uint64_t *st = reinterpret_cast<const uint64_t *>(sl->h_meta + kMetaStamps);
+        std::vector<std::string> names = {"k.seed"};
+        for (int h = 0; h < sl->plan->n_hops; ++h)
+            for (const char *x : {"count", "scan", "sample", "bitcount", "emit"})
+                names.push_back("k.h" + std::to_string(h) + "." + x);
+        names.push_back("k.relabel");
+        for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
+            if (!st[k + 1] || !st[k]) break;
+            trace_add(c, names[k], (double)(st[k + 1] - st[k]) * 1e-6);
+        }
+        for (size_t k = 1; k < sl->tev.size(); ++k) {
+            float e = 0;
+            cudaEventElapsedTime(&e, sl->tev[k - 1], sl->tev[k]);
+            trace_add(c, sl->tlab[k], e);
+        }
+    }
+}
+
+// Resolve a pending batch: wait for its launch, read sizes and error bits.
 eg_status finish(eg_blocks *b)
 {
     if (b->ready) return b->status;
@@ -939,60 +1027,12 @@ eg_status finish(eg_blocks *b)
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, sl->done, 0);
     b->ready = true;
     if (e != cudaSuccess) return b->status = fail(c, EG_ECUDA, std::string("batch: ") + cudaGetErrorString(e));
-    const int32_t *m = sl->h_meta;
+    slot_finished(c, sl);
+    const int32_t *m = sl->h_meta + (size_t)b->bidx * kMetaSize;
     for (int l = 0; l <= b->n_hops; ++l)
         for (int u = 0; u < b->n_vt; ++u) b->n_nodes[l][u] = m[kMetaNodes + l * EG_MAX_VT + u];
     for (int h = 0; h < b->n_hops; ++h)
         for (int r = 0; r < b->n_rel; ++r) b->nnz[h][r] = m[kMetaNnz + h * EG_MAX_REL + r];
-    if (sl->timed) {
-        float ms = 0;
-        if (cudaEventElapsedTime(&ms, sl->s0, sl->s1) == cudaSuccess) {
-            c->prof_ms[0] += ms;
-            c->prof_n[0] += 1;
-        }
-        if (sl->plan->features && cudaEventElapsedTime(&ms, sl->g0, sl->g1) == cudaSuccess) {
-            c->prof_ms[1] += ms;
-            c->prof_n[1] += 1;
-        }
-        sl->timed = false;
-    }
-    if (c->trace && c->prof) {
-        // in-kernel phase stamps (batch_kernel): seed, per hop count/scan/sample/bitcount/emit, relabel
-        const uint64_t *st = reinterpret_cast<const uint64_t *>(m + kMetaStamps);
-        std::vector<std::string> names = {"k.seed"};
-        for (int h = 0; h < b->n_hops; ++h)
-            for (const char *x : {"count", "scan", "sample", "bitcount", "emit"})
-                names.push_back("k.h" + std::to_string(h) + "." + x);
-        names.push_back("k.relabel");
-        for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
-            if (!st[k + 1] || !st[k]) break;
-            const double ms = (double)(st[k + 1] - st[k]) * 1e-6;
-            size_t idx = 0;
-            while (idx < c->trace_names.size() && c->trace_names[idx] != names[k]) ++idx;
-            if (idx == c->trace_names.size()) {
-                c->trace_names.push_back(names[k]);
-                c->trace_ms.push_back(0);
-                c->trace_n.push_back(0);
-            }
-            c->trace_ms[idx] += ms;
-            c->trace_n[idx] += 1;
-        }
-    }
-    if (c->trace && c->prof && sl->tev.size() > 1) {
-        for (size_t k = 1; k < sl->tev.size(); ++k) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, sl->tev[k - 1], sl->tev[k]);
-            size_t idx = 0;
-            while (idx < c->trace_names.size() && c->trace_names[idx] != sl->tlab[k]) ++idx;
-            if (idx == c->trace_names.size()) {
-                c->trace_names.push_back(sl->tlab[k]);
-                c->trace_ms.push_back(0);
-                c->trace_n.push_back(0);
-            }
-            c->trace_ms[idx] += ms;
-            c->trace_n[idx] += 1;
-        }
-    }
     const int32_t errbits = m[kMetaErr];
     if (errbits & kErrSeedRange) return b->status = fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
     if (errbits & kErrSeedDup) return b->status = fail(c, EG_EINVAL, "duplicate seeds");
@@ -1007,44 +1047,62 @@ int64_t round_cap(int64_t n)
     return c;
 }
 
-eg_status enqueue_batch(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops, const int32_t *fanouts,
-                        uint64_t rng_seed, bool features, eg_blocks **out)
+// One launch for nb batches (nb <= the context's bundle size).
+eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, const int64_t *n_seeds,
+                         int32_t n_hops, const int32_t *fanouts, const uint64_t *rng_seeds, bool features,
+                         eg_blocks **out)
 {
     eg_status st = enter(c);
     if (st) return st;
     if (!out) return fail(c, EG_EINVAL, "out is null");
-    *out = nullptr;
     if (!c->loaded || !c->peers_ready) return fail(c, EG_EINVAL, "partition not loaded / peers not mapped");
+    if (nb < 1 || nb > kMaxBundle) return fail(c, EG_EINVAL, "bundle size out of [1, 16]");
+    if (nb > c->bundle) return fail(c, EG_EINVAL, "bundle larger than eg_set_pipeline's bundle size");
     if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
-    if (n_seeds < 0 || (n_seeds > 0 && !seeds)) return fail(c, EG_EINVAL, "bad seeds");
-    if (!fanouts) return fail(c, EG_EINVAL, "fanouts is null");
+    if (!fanouts || !seeds || !n_seeds || !rng_seeds) return fail(c, EG_EINVAL, "null argument");
+    int64_t nmax = 0;
+    for (int b = 0; b < nb; ++b) {
+        out[b] = nullptr;
+        if (n_seeds[b] < 0 || (n_seeds[b] > 0 && !seeds[b])) return fail(c, EG_EINVAL, "bad seeds");
+        nmax = std::max(nmax, n_seeds[b]);
+    }
     for (int i = 0; i < n_hops * c->g.n_rel; ++i)
         if (fanouts[i] < -1) return fail(c, EG_EINVAL, "fanout must be >= -1");
+    // a single batch uses a 1-batch plan; bundles use the context's bundle size
+    const int32_t B = nb == 1 ? 1 : c->bundle;
     Plan *p = nullptr;
-    if ((st = get_plan(c, n_hops, fanouts, round_cap(n_seeds), features, &p))) return st;
+    if ((st = get_plan(c, n_hops, fanouts, round_cap(nmax), features, B, &p))) return st;
     Slot *sl = nullptr;
     if ((st = acquire_slot(c, p, &sl))) return st;
     Lane &ln = c->lanes[sl->lane];
     EG_CUDA(c, cudaEventRecord(ln.ready, c->stream));          // seeds produced on the caller's stream
     EG_CUDA(c, cudaStreamWaitEvent(ln.stream, ln.ready, 0));
-    if (n_seeds > 0)
-        EG_CUDA(c, cudaMemcpyAsync(sl->mem + p->o_seeds, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyDefault,
-                                   ln.stream));
-    sl->h_dyn[0] = rng_seed;
-    sl->h_dyn[1] = (uint64_t)n_seeds;
+    for (int b = 0; b < B; ++b) {
+        const int64_t n = b < nb ? n_seeds[b] : 0;
+        if (n > 0)
+            EG_CUDA(c, cudaMemcpyAsync(p->batch_base(sl->mem, b) + p->o_seeds, seeds[b], sizeof(int64_t) * n,
+                                       cudaMemcpyDefault, ln.stream));
+        sl->h_dyn[2 * b] = b < nb ? rng_seeds[b] : 0;
+        sl->h_dyn[2 * b + 1] = (uint64_t)n;
+    }
     sl->timed = c->prof;
+    sl->finished = false;
     EG_CUDA(c, cudaGraphLaunch(sl->exec, ln.stream));
     EG_CUDA(c, cudaEventRecord(sl->done, ln.stream));
     sl->used = true;
+    sl->refs = nb;
     c->launches += p->n_kernels;
-    eg_blocks *b = new eg_blocks();
-    b->ctx = c;
-    b->slot = sl;
-    b->n_hops = n_hops;
-    b->n_vt = c->g.n_vt;
-    b->n_rel = c->g.n_rel;
-    fill_views(p, sl->mem, b);
-    *out = b;
+    for (int b = 0; b < nb; ++b) {
+        eg_blocks *h = new eg_blocks();
+        h->ctx = c;
+        h->slot = sl;
+        h->bidx = b;
+        h->n_hops = n_hops;
+        h->n_vt = c->g.n_vt;
+        h->n_rel = c->g.n_rel;
+        fill_views(p, p->batch_base(sl->mem, b), h);
+        out[b] = h;
+    }
     return EG_OK;
 }
 
@@ -1061,17 +1119,30 @@ eg_status eg_sample_blocks(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int
 eg_status eg_sample_minibatch(eg_ctx *c, const int64_t *seeds, int64_t n_seeds, int32_t n_hops,
                               const int32_t *fanouts, uint64_t rng_seed, int32_t flags, eg_blocks **out)
 {
-    eg_blocks *b = nullptr;
-    eg_status st = enqueue_batch(c, seeds, n_seeds, n_hops, fanouts, rng_seed, (flags & EG_FEATURES) != 0, &b);
+    return eg_sample_bundle(c, 1, &seeds, &n_seeds, n_hops, fanouts, &rng_seed, flags, out);
+}
+
+eg_status eg_sample_bundle(eg_ctx *c, int32_t n_batches, const int64_t *const *seeds, const int64_t *n_seeds,
+                           int32_t n_hops, const int32_t *fanouts, const uint64_t *rng_seeds, int32_t flags,
+                           eg_blocks **out)
+{
+    eg_status st = enqueue_bundle(c, n_batches, seeds, n_seeds, n_hops, fanouts, rng_seeds,
+                                  (flags & EG_FEATURES) != 0, out);
     if (st) return st;
     if (!(flags & EG_ASYNC)) {
-        st = finish(b);
-        if (st) {
-            eg_blocks_free(b);
-            return st;
+        eg_status first = EG_OK;
+        for (int b = 0; b < n_batches; ++b) {
+            st = finish(out[b]);
+            if (st && !first) first = st;
+        }
+        if (first) {
+            for (int b = 0; b < n_batches; ++b) {
+                eg_blocks_free(out[b]);
+                out[b] = nullptr;
+            }
+            return first;
         }
     }
-    *out = b;
     return EG_OK;
 }
 
@@ -1135,7 +1206,9 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
     if (!cb || !out || cb->ctx != c) return fail(c, EG_EINVAL, "bad blocks / out");
     eg_blocks *b = const_cast<eg_blocks *>(cb);
     if ((st = finish(b))) return st;
-    GatherDev gd{};
+    GatherSet gs{};
+    gs.nb = 1;
+    GatherDev &gd = gs.b[0];
     gd.meta = b->meta;
     gd.level = b->n_hops;
     void *staging[EG_MAX_VT] = {};
@@ -1146,7 +1219,6 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
         if (!c->f.row_bytes[u]) return fail(c, EG_EINVAL, "vertex type " + std::to_string(u) + " has no features");
         const int64_t bytes = b->n_nodes[b->n_hops][u] * c->f.row_bytes[u];
         if (bytes == 0) continue;
-        if ((uint64_t)(bytes / 16) >= (1ull << 32)) return fail(c, EG_EINVAL, "gather too large");
         if (is_device_ptr(out[u])) {
             gd.out[u] = (uint8_t *)out[u];
         } else {
@@ -1158,7 +1230,7 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
     if (!any) return EG_OK;
     TimedPair tp;
     record_start(c, &tp, 1);
-    launch_gather(c->g, c->f, gd, c->stream);
+    launch_gather(c->g, c->f, gs, c->stream);
     c->launches += 1;
     EG_CUDA(c, cudaGetLastError());
     record_end(c, &tp);
@@ -1177,22 +1249,22 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
 eg_status eg_blocks_free(eg_blocks *b)
 {
     if (!b) return EG_OK;
-    if (b->slot) b->slot->busy = false;   // reuse waits for the slot's last run to retire
+    if (b->slot && b->slot->refs > 0) b->slot->refs -= 1;   // reuse waits for the slot's last run
     delete b;
     return EG_OK;
 }
 
-eg_status eg_set_pipeline(eg_ctx *c, int32_t depth)
+eg_status eg_set_pipeline(eg_ctx *c, int32_t depth, int32_t bundle)
 {
     eg_status st = enter(c);
     if (st) return st;
     if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
     if (depth < 1 || depth > 16) return fail(c, EG_EINVAL, "pipeline depth must be in [1, 16]");
-    while ((int)c->lanes.size() < depth)
-        if ((st = add_lane(c))) return st;
-    // lanes beyond depth stay allocated but unused
+    if (bundle < 1 || bundle > kMaxBundle) return fail(c, EG_EINVAL, "bundle size must be in [1, 16]");
+    if ((st = ensure_lanes(c, depth, bundle))) return st;
     c->next_lane = 0;
     c->depth = depth;
+    c->bundle = bundle;
     return EG_OK;
 }
 
@@ -1243,11 +1315,13 @@ eg_status eg_destroy(eg_ctx *c)
     for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
     for (Lane &ln : c->lanes) {
         if (ln.stream) cudaStreamSynchronize(ln.stream);
-        cudaFree(ln.pos);
-        cudaFree(ln.bitmap);
-        cudaFree(ln.chunk_cnt);
-        cudaFree(ln.chunk_pre);
-        cudaFree(ln.partial);
+        for (BatchState &bs : ln.st) {
+            cudaFree(bs.pos);
+            cudaFree(bs.bitmap);
+            cudaFree(bs.chunk_cnt);
+            cudaFree(bs.chunk_pre);
+            cudaFree(bs.partial);
+        }
         if (ln.ready) cudaEventDestroy(ln.ready);
         if (ln.stream) cudaStreamDestroy(ln.stream);
     }

@@ -24,44 +24,80 @@ namespace eg {
 
 // ----------------------------------------------------------------------------- LDG path
 
-constexpr int kUnroll = 8;
+// A warp copies groups of 32 consecutive output rows of one type: one coalesced load of
+// the 32 ids, then "items" of one warp-wide 16-B access each (rows of >= 512 B take
+// ceil(U/32) items per row; shorter rows pack 32/U rows per item), kBatch items in
+// flight per lane before their stores.  Consecutive lanes touch consecutive 16-B units
+// of a row, so every row read and the output write are coalesced.
+constexpr int kBatch = 8;
+
+__device__ __forceinline__ int32_t seg_rows(const GatherSet &gs, int b, int u)
+{
+    const GatherDev &gd = gs.b[b];
+    return gd.out[u] ? gd.meta[kMetaNodes + gd.level * EG_MAX_VT + u] : 0;
+}
 
 __global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__ GraphDev g,
                                                          const __grid_constant__ FeatDev f,
-                                                         const __grid_constant__ GatherDev gd)
+                                                         const __grid_constant__ GatherSet gs)
 {
-    const int32_t *n = gd.meta + kMetaNodes + gd.level * EG_MAX_VT;
-    int64_t cum[EG_MAX_VT + 1];
-    uint32_t units[EG_MAX_VT];
-    cum[0] = 0;
-    for (int u = 0; u < g.n_vt; ++u) {
-        units[u] = (uint32_t)(f.row_bytes[u] >> 4);
-        cum[u + 1] = cum[u] + (gd.out[u] ? (int64_t)n[u] * units[u] : 0);
-    }
-    const int64_t total = cum[g.n_vt];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q0 < total; q0 += stride * kUnroll) {
-        int4 val[kUnroll];
-        uint8_t *dst[kUnroll];
-#pragma unroll
-        for (int k = 0; k < kUnroll; ++k) {
-            const int64_t q = q0 + k * stride;
-            dst[k] = nullptr;
-            if (q < total) {
-                int u = 0;
-                while (q >= cum[u + 1]) ++u;
-                const uint32_t local = (uint32_t)(q - cum[u]);
-                const uint32_t i = local / units[u], c = local - i * units[u];
-                const int64_t tid = __ldg(gd.nodes[u] + i) - g.off[u];
-                const int p = owner_of(g, u, tid);
-                const uint8_t *src = f.rows[u][p] + (tid - g.bounds[u][p]) * f.row_bytes[u] + 16 * (int64_t)c;
-                val[k] = ld_nc_v4(src);
-                dst[k] = gd.out[u] + (int64_t)local * 16;
-            }
+    const int lane = lane_id();
+    const int V = g.n_vt, S = gs.nb * V;                 // segments: (batch, type)
+    int64_t total = 0;
+    for (int sg = 0; sg < S; ++sg) total += ((int64_t)seg_rows(gs, sg / V, sg % V) + 31) / 32;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int sg = 0;
+    int64_t seg_lo = 0, seg_hi = (seg_rows(gs, 0, 0) + 31) / 32;
+    for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); grp < total; grp += nw) {
+        while (grp >= seg_hi) {                          // groups are visited in increasing order
+            ++sg;
+            seg_lo = seg_hi;
+            seg_hi += (seg_rows(gs, sg / V, sg % V) + 31) / 32;
         }
+        const int u = sg % V;
+        const GatherDev &gd = gs.b[sg / V];
+        const int64_t row0 = (grp - seg_lo) * 32;
+        const int nrows = (int)min((int64_t)32, (int64_t)seg_rows(gs, sg / V, u) - row0);
+        const int64_t rb = f.row_bytes[u];
+        const int U = (int)(rb >> 4);
+        const uint8_t *srow = nullptr;
+        if (lane < nrows) {
+            const int64_t tid = __ldg(gd.nodes[u] + row0 + lane) - g.off[u];
+            const int p = owner_of(g, u, tid);
+            srow = f.rows[u][p] + (tid - g.bounds[u][p]) * rb;
+        }
+        uint8_t *dbase = gd.out[u] + row0 * rb;
+        const bool wide = U >= 32;
+        const int cpr = wide ? (U + 31) >> 5 : 1;        // items per row (wide rows)
+        const int rpi = wide ? 1 : 32 / U;               // rows per item (narrow rows)
+        const int lrow = wide ? 0 : lane / U, lunit = wide ? lane : lane % U;
+        const int items = wide ? nrows * cpr : (nrows + rpi - 1) / rpi;
+        for (int k0 = 0; k0 < items; k0 += kBatch) {
+            int4 v[kBatch];
+            uint8_t *dst[kBatch];
 #pragma unroll
-        for (int k = 0; k < kUnroll; ++k)
-            if (dst[k]) st_v4(dst[k], val[k]);
+            for (int q = 0; q < kBatch; ++q) {
+                const int k = k0 + q;
+                int row, unit;
+                if (wide) {
+                    row = k / cpr;
+                    unit = (k - row * cpr) * 32 + lane;
+                } else {
+                    row = k * rpi + lrow;
+                    unit = lunit;
+                }
+                const bool ok = k < items && row < nrows && unit < U && (wide || lane < rpi * U);
+                const uint8_t *sp = (const uint8_t *)__shfl_sync(0xffffffffu, (unsigned long long)srow, row & 31);
+                dst[q] = nullptr;
+                if (ok) {
+                    v[q] = ld_nc_v4(sp + 16 * unit);
+                    dst[q] = dbase + row * rb + 16 * unit;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kBatch; ++q)
+                if (dst[q]) st_v4(dst[q], v[q]);
+        }
     }
 }
 
@@ -118,37 +154,51 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-struct TileMap {
-    int64_t tcum[EG_MAX_VT + 1];   // tiles before type u
-    int32_t rpt[EG_MAX_VT];        // rows per tile
-    int32_t n[EG_MAX_VT];
+// Tiles of consecutive rows of one (batch, type) segment; segments in (batch, type) order.
+struct TileCursor {
+    int sg = 0;
+    int64_t lo = 0, hi = 0;
 };
 
-__device__ __forceinline__ void tile_of(const TileMap &m, int n_vt, int64_t t, int &u, int64_t &row0, int32_t &nrows)
+__device__ __forceinline__ int32_t rows_per_tile(const FeatDev &f, int u)
 {
-    u = 0;
-    while (t >= m.tcum[u + 1]) ++u;
-    row0 = (t - m.tcum[u]) * m.rpt[u];
-    nrows = (int32_t)min((int64_t)m.rpt[u], (int64_t)m.n[u] - row0);
+    const int64_t rb = f.row_bytes[u];
+    return rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
+}
+
+__device__ __forceinline__ int64_t seg_tiles(const GatherSet &gs, const FeatDev &f, int V, int sg)
+{
+    const int32_t n = seg_rows(gs, sg / V, sg % V);
+    const int32_t rpt = rows_per_tile(f, sg % V);
+    return (n + rpt - 1) / rpt;
+}
+
+// tiles are visited in increasing order by each block: advance the cursor
+__device__ __forceinline__ void tile_of(const GatherSet &gs, const FeatDev &f, int V, TileCursor &cur, int64_t t,
+                                        int &b, int &u, int64_t &row0, int32_t &nrows)
+{
+    while (t >= cur.hi) {
+        ++cur.sg;
+        cur.lo = cur.hi;
+        cur.hi += seg_tiles(gs, f, V, cur.sg);
+    }
+    b = cur.sg / V;
+    u = cur.sg % V;
+    const int32_t rpt = rows_per_tile(f, u);
+    row0 = (t - cur.lo) * rpt;
+    nrows = (int32_t)min((int64_t)rpt, (int64_t)seg_rows(gs, b, u) - row0);
 }
 
 __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant__ GraphDev g,
                                                            const __grid_constant__ FeatDev f,
-                                                           const __grid_constant__ GatherDev gd)
+                                                           const __grid_constant__ GatherSet gs)
 {
     extern __shared__ __align__(128) uint8_t stage_mem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     const int warp = threadIdx.x >> 5, lane = lane_id();
-    TileMap m;
-    const int32_t *nn = gd.meta + kMetaNodes + gd.level * EG_MAX_VT;
-    m.tcum[0] = 0;
-    for (int u = 0; u < g.n_vt; ++u) {
-        const int64_t rb = f.row_bytes[u];
-        m.rpt[u] = rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
-        m.n[u] = gd.out[u] ? nn[u] : 0;
-        m.tcum[u + 1] = m.tcum[u] + (m.n[u] + m.rpt[u] - 1) / m.rpt[u];
-    }
-    const int64_t total = m.tcum[g.n_vt];
+    const int V = g.n_vt, S = gs.nb * V;
+    int64_t total = 0;
+    for (int sg = 0; sg < S; ++sg) total += seg_tiles(gs, f, V, sg);
     const int64_t n_my = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -158,21 +208,23 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    TileCursor cur;
+    cur.hi = seg_tiles(gs, f, V, 0);
     if (warp == 0) {
         // producer: ids -> bulk loads of rows into the stage
         for (int64_t j = 0; j < n_my; ++j) {
             const int s = (int)(j % kStages);
             mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));
-            int u;
+            int b, u;
             int64_t row0;
             int32_t nrows;
-            tile_of(m, g.n_vt, blockIdx.x + j * gridDim.x, u, row0, nrows);
+            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, b, u, row0, nrows);
             const int64_t rb = f.row_bytes[u];
             if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nrows * rb));
             __syncwarp();
             uint8_t *dst = stage_mem + s * kStageBytes;
             for (int rr = lane; rr < nrows; rr += 32) {
-                const int64_t tid = __ldg(gd.nodes[u] + row0 + rr) - g.off[u];
+                const int64_t tid = __ldg(gs.b[b].nodes[u] + row0 + rr) - g.off[u];
                 const int p = owner_of(g, u, tid);
                 bulk_g2s(dst + rr * rb, f.rows[u][p] + (tid - g.bounds[u][p]) * rb, (uint32_t)rb, &full[s]);
             }
@@ -182,13 +234,13 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
         for (int64_t j = 0; j < n_my; ++j) {
             const int s = (int)(j % kStages);
             mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
-            int u;
+            int b, u;
             int64_t row0;
             int32_t nrows;
-            tile_of(m, g.n_vt, blockIdx.x + j * gridDim.x, u, row0, nrows);
+            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, b, u, row0, nrows);
             const int64_t rb = f.row_bytes[u];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_s2g(gd.out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
+            bulk_s2g(gs.b[b].out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             mbar_arrive(&empty[s]);
         }
@@ -206,7 +258,7 @@ static int gather_mode()
     return mode;
 }
 
-void launch_gather(const GraphDev &g, const FeatDev &f, const GatherDev &gd, cudaStream_t s)
+void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cudaStream_t s)
 {
     if (gather_mode() == 1) {
         static int blocks = 0;

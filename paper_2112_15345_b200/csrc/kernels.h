@@ -4,24 +4,36 @@
 
 namespace eg {
 
-// batch.cu: sampling + compaction of a whole batch (one persistent kernel)
-struct BatchDev {
-    int32_t n_hops, n_chunks, trace, _pad;
-    const int64_t *seeds;
-    uint32_t *bar;                 // grid barrier {count, generation}, zero-initialised
-    HopDev hop[EG_MAX_HOPS];
-};
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, cudaStream_t s);
-int batch_grid();
+// A bundle of up to kMaxBundle mini-batches runs as one launch of each phase kernel
+// (grid.y = batch of the bundle) and one gather: the paper's bundling of the sampling
+// of several mini-batches.
+constexpr int kMaxBundle = 16;
 
-// gather.cu
 struct GatherDev {
     uint8_t *out[EG_MAX_VT];
     const int64_t *nodes[EG_MAX_VT];
     const int32_t *meta;
     int32_t level;
 };
-void launch_gather(const GraphDev &g, const FeatDev &f, const GatherDev &gd, cudaStream_t s);
+
+// The gathers of one launch: batch b of the bundle is b[b] (kernel parameter).
+struct GatherSet {
+    int32_t nb;
+    GatherDev b[kMaxBundle];
+};
+
+struct BatchDev {
+    int32_t n_hops, n_chunks, trace, B;
+    const int64_t *seeds[kMaxBundle];
+    HopDev hop[kMaxBundle][EG_MAX_HOPS];
+};
+
+// batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
+// returns the number of kernels.
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s);
+
+// gather.cu
+void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);
 
 // store.cu
 void launch_max_degree(const int64_t *indptr, int64_t n, unsigned long long *out, cudaStream_t s);

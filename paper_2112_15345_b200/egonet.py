@@ -28,7 +28,7 @@ ABI_SYMBOLS = [
     "eg_sample_blocks", "eg_block_view_get", "eg_blocks_n_hops", "eg_blocks_n_inputs", "eg_gather_features",
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
-    "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline",
+    "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
 ]
 
 EG_FEATURES = 1
@@ -125,7 +125,8 @@ def lib(build_if_missing: bool = True):
         L.eg_export_shard.argtypes = [vp, vp, P(c.c_size_t)]
         L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
         L.eg_attach_peer.argtypes = [vp, vp]
-        L.eg_set_pipeline.argtypes = [vp, c.c_int32]
+        L.eg_set_pipeline.argtypes = [vp, c.c_int32, c.c_int32]
+        L.eg_sample_bundle.argtypes = [vp, c.c_int32, vp, vp, c.c_int32, vp, vp, c.c_int32, vp]
         L.eg_trace_get.argtypes = [vp, c.c_int32, c.c_char_p, c.c_size_t, P(c.c_double), P(c.c_int64)]
         L.eg_trace_get.restype = c.c_int32
         L.eg_check_shard_metas.argtypes = [c.c_int32, vp, vp, vp, c.c_char_p, c.c_size_t]
@@ -440,6 +441,30 @@ class Context:
                                               rng_seed & (2**64 - 1), flags, ctypes.byref(h)), "eg_sample_minibatch")
         return Blocks(self, h.value)
 
+    def sample_bundle(self, seeds_list, fanouts, rng_seeds, features: bool = True, async_: bool = False):
+        """Several mini-batches as ONE graph launch (bundle); returns one Blocks per batch."""
+        torch = _torch()
+        fo = np.ascontiguousarray(fanouts, np.int32)
+        n = len(seeds_list)
+        ptrs = (ctypes.c_void_p * n)()
+        cnts = np.zeros(n, np.int64)
+        keep = []
+        for i, s in enumerate(seeds_list):
+            if isinstance(s, np.ndarray):
+                s = np.ascontiguousarray(s, np.int64)
+                keep.append(s)
+                ptrs[i], cnts[i] = s.ctypes.data, len(s)
+            else:
+                assert s.dtype == torch.int64 and s.is_contiguous()
+                ptrs[i], cnts[i] = s.data_ptr(), s.numel()
+        rs = np.ascontiguousarray([int(x) & (2**64 - 1) for x in rng_seeds], np.uint64)
+        outs = (ctypes.c_void_p * n)()
+        flags = (EG_FEATURES if features else 0) | (EG_ASYNC if async_ else 0)
+        self._check(lib().eg_sample_bundle(self._h, n, ctypes.cast(ptrs, ctypes.c_void_p), cnts.ctypes.data,
+                                           fo.shape[0], fo.ctypes.data, rs.ctypes.data, flags,
+                                           ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_bundle")
+        return [Blocks(self, outs[i]) for i in range(n)]
+
     def gather_features(self, blocks: Blocks, out=None, types=None):
         """Feature rows of the input vertices per type (None for types without
         features).  `out` may give preallocated (device or host) tensors / arrays."""
@@ -461,9 +486,11 @@ class Context:
         self._check(lib().eg_gather_features(self._h, blocks.handle, ptrs), "eg_gather_features")
         return outs
 
-    def set_pipeline(self, depth: int):
-        """Up to `depth` batches in flight (independent lanes / streams)."""
-        self._check(lib().eg_set_pipeline(self._h, depth), "eg_set_pipeline")
+    def set_pipeline(self, depth: int, bundle: int = 1):
+        """Up to `depth` launches in flight (independent lanes / streams), each carrying up
+        to `bundle` mini-batches (sample_bundle)."""
+        self._check(lib().eg_set_pipeline(self._h, depth, bundle), "eg_set_pipeline")
+        self.bundle = bundle
 
     def set_profiling(self, on: bool):
         self._check(lib().eg_set_profiling(self._h, 1 if on else 0), "eg_set_profiling")

@@ -311,3 +311,39 @@ def test_device_indices_match_host_generator():
                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     assert np.array_equal(t.cpu().numpy(), synth.gen_indices(cfg, 0, lo, hi))
+
+
+def test_c2_bundles_of_4_on_2_lanes(c2):
+    """Bundled launches (4 mini-batches per graph launch, grid.y = batch) on 2 lanes,
+    including an empty batch and a smaller one: every batch bit-exact."""
+    import torch
+    cfg, g, rows, ctx = c2
+    ctx.set_pipeline(2, 4)
+    try:
+        for rnd in range(3):
+            idx = [60 + 4 * rnd + j for j in range(4)]
+            seeds = [synth.batch_seeds(cfg, i) for i in idx]
+            seeds[1] = seeds[1][:100] if rnd == 1 else seeds[1]
+            seeds[2] = seeds[2][:0] if rnd == 2 else seeds[2]
+            rs = [synth.rng_seed(cfg, i) for i in idx]
+            bls = ctx.sample_bundle([torch.from_numpy(s).cuda() for s in seeds], cfg.fanouts, rs, features=True,
+                                    async_=(rnd != 0))
+            for s, r, b in zip(seeds, rs, bls):
+                res = oracle.sample(g, s, cfg.fanouts, r)
+                assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+                assert_same_features(res, _features_of(b, cfg), cfg, rows)
+                b.free()
+        # a partial bundle (3 of 4) and a bad batch inside an async bundle
+        bls = ctx.sample_bundle([torch.from_numpy(synth.batch_seeds(cfg, 90)).cuda(),
+                                 torch.tensor([1, 99999999], device="cuda:0"),
+                                 torch.from_numpy(synth.batch_seeds(cfg, 91)).cuda()], cfg.fanouts, [5, 6, 7],
+                                async_=True)
+        from paper_2112_15345_b200 import EgError
+        with pytest.raises(EgError):
+            bls[1].wait()
+        res = oracle.sample(g, synth.batch_seeds(cfg, 91), cfg.fanouts, 7)
+        assert_same_batch(res, bls[2], cfg.n_vt, cfg.n_rel)
+        for b in bls:
+            b.free()
+    finally:
+        ctx.set_pipeline(1, 1)
