@@ -38,12 +38,12 @@ UNIT = "sampled edges/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=32)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
-    ap.add_argument("--bundle", type=int, default=4, help="mini-batches per launch (bundled kernels)")
+    ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
@@ -252,7 +252,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         # one CUDA-graph launch for batches b0..b1-1: sample + compact all hops + gather
         # features; no host sync
         if b1 - b0 == 1 and args.bundle == 1:
-            return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=True, async_=True)]
+            return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=True, async_=True)]  # noqa
         return ctx.sample_bundle([seeds[b] for b in range(b0, b1)], fanouts, rngs[b0:b1], features=True,
                                  async_=True)
 
@@ -387,7 +387,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     n_launch = max(1, prof["n_gather"])                             # one gather launch per bundle
     achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     tr = load_traffic(cfg.name)
-    roofline = {"kernel": "gather_tma_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    roofline = {"kernel": "gather_ldg_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                 "algorithmic_bytes_per_launch": gbytes / n_launch,
@@ -412,7 +412,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         nv_bytes = (gbytes / n_launch) / 2 * frac_remote   # row bytes read over NVLink per launch
         nv_peak = 770.0
         nv_achieved = nv_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
-        roofline.update({"bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak, "frac": nv_achieved / nv_peak,
+        roofline.update({"kernel": "gather_ldg_kernel", "bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak,
+                         "frac": nv_achieved / nv_peak,
                          "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction per GPU",
                          "per_unit": "row_bytes per input row owned by a peer (read over NVLink)",
                          "algorithmic_bytes_per_launch": nv_bytes, "remote_row_fraction": frac_remote,
