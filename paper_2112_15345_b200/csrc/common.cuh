@@ -12,7 +12,7 @@ constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
 constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one CTA)
 constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
-constexpr int kScanBlocks = 256;          // blocks per relation in the two-phase scan
+constexpr int kScanBlocks = 64;           // virtual blocks per relation in the two-phase scan
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
 
