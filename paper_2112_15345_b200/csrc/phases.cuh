@@ -27,6 +27,10 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
 {
     __shared__ int32_t sh[33];
     __shared__ int32_t base[EG_MAX_VT];
+    // pointers hoisted into registers: HopDev lives in global memory and every store
+    // below could alias it, so reading fields inside the loops would reload them
+    int32_t *const pos = hd.pos;
+    int32_t *const meta = hd.meta;
     const int64_t n = (int64_t)hd.dyn[1];
     if (threadIdx.x < EG_MAX_VT) base[threadIdx.x] = 0;
     __syncthreads();
@@ -38,7 +42,7 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
         if (i < n) {
             gid = seeds[i];
             if (gid < 0 || gid >= n_total) {
-                atomicOr(hd.meta + kMetaErr, kErrSeedRange);
+                atomicOr(meta + kMetaErr, kErrSeedRange);
             } else {
                 vt = 0;
                 while (gid >= g.off[vt + 1]) ++vt;
@@ -52,9 +56,9 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
                 const int32_t p = base[u] + ex;
                 if (p < hd.cap_nodes[u]) {
                     hd.nodes[u][p] = gid;
-                    if (atomicCAS(hd.pos + gid, -1, p) != -1) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+                    if (atomicCAS(pos + gid, -1, p) != -1) atomicOr(meta + kMetaErr, kErrSeedDup);
                 } else {
-                    atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                    atomicOr(meta + kMetaErr, kErrCapacity);
                 }
             }
             if (threadIdx.x == 0) base[u] += tot;
@@ -85,6 +89,12 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
         const int64_t n = nF[t];
         const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
         const int64_t lo = b * chunk, hi = min(n, lo + chunk);
+        const int64_t *const nodes = hd.nodes[t];
+        int64_t *const ibase = hd.ibase[r];
+        int32_t *const ideg = hd.ideg[r];
+        int32_t *const bip = hd.indptr[r];
+        uint64_t *const selq = hd.selq;
+        uint32_t *const selc = (uint32_t *)(hd.meta + kMetaSel + hd.h);
         int32_t sum = 0;
         for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {   // block-uniform trip count
             const int64_t i = t0 + threadIdx.x;
@@ -92,7 +102,7 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
             if (i < hi) {
                 int32_t c = 0;
                 if (k != 0) {
-                    const int64_t tid = hd.nodes[t][i] - g.off[t];
+                    const int64_t tid = nodes[i] - g.off[t];
                     const int p = owner_of(g, t, tid);
                     const int64_t x = tid - g.bounds[t][p];
                     const int64_t *ip = R.indptr[p];
@@ -100,18 +110,18 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
                     const bool all = (k < 0 || d <= k);
                     c = (int32_t)(all ? d : k);
                     sel = !all;
-                    hd.ibase[r][i] = ((int64_t)p << 56) | b0;
-                    hd.ideg[r][i] = (int32_t)d;
+                    ibase[i] = ((int64_t)p << 56) | b0;
+                    ideg[i] = (int32_t)d;
                 }
-                hd.indptr[r][i] = c;
+                bip[i] = c;
                 sum += c;
             }
             const uint32_t m = __ballot_sync(0xffffffffu, sel);
             if (m) {
                 uint32_t q = 0;
-                if (lane_id() == 0) q = atomicAdd((uint32_t *)(hd.meta + kMetaSel + hd.h), (uint32_t)__popc(m));
+                if (lane_id() == 0) q = atomicAdd(selc, (uint32_t)__popc(m));
                 q = __shfl_sync(0xffffffffu, q, 0);
-                if (sel) hd.selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
+                if (sel) selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
             }
         }
         sum = block_sum(sum, sh);
@@ -133,9 +143,10 @@ __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb,
         const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
         const int64_t lo = b * chunk, hi = min(n, lo + chunk);
         int32_t s = 0;
-        for (int j = threadIdx.x; j < b; j += blockDim.x) s += hd.partial[r * kScanBlocks + j];
+        const int32_t *const partial = hd.partial + r * kScanBlocks;
+        for (int j = threadIdx.x; j < b; j += blockDim.x) s += partial[j];
         int32_t carry = block_sum(s, sh);
-        int32_t *ip = hd.indptr[r];
+        int32_t *const ip = hd.indptr[r];
         for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
             const int64_t i = t0 + threadIdx.x;
             const int32_t v = i < hi ? ip[i] : 0;
@@ -154,6 +165,8 @@ __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb,
 // ============================================================================ sampling
 
 struct Item {
+    const int32_t *pos;     // the batch's gid -> position map (read only here)
+    uint32_t *bitmap;       // the batch's new-vertex bitmap
     int64_t bit_base;       // boff[s(r)] - off[s(r)]: bitmap bit of gid = bit_base + gid
     uint32_t soff;          // off[s(r)]
     int64_t ebase;          // global CSC position of this dst's first edge
@@ -164,20 +177,20 @@ struct Item {
 
 // If the source is not yet in the batch, mark it in the new-vertex bitmap (the
 // first step of the hop's compaction, fused into sampling).
-__device__ __forceinline__ void mark_new(const HopDev &hd, uint32_t gid, int32_t pos_of_gid, int64_t bit_base)
+__device__ __forceinline__ void mark_new(uint32_t *bitmap, uint32_t gid, int32_t pos_of_gid, int64_t bit_base)
 {
     if (pos_of_gid < 0) {
         const int64_t bit = bit_base + gid;
-        atomicOr(hd.bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED, no round trip
+        atomicOr(bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED, no round trip
     }
 }
 
-__device__ __forceinline__ void emit_edge(const HopDev &hd, const Item &it, int32_t slot, int64_t j)
+__device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_t slot, int64_t j)
 {
     const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
     it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
-    mark_new(hd, gid, __ldcg(hd.pos + gid), it.bit_base);
+    mark_new(it.bitmap, gid, __ldcg(it.pos + gid), it.bit_base);
 }
 
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
@@ -311,10 +324,13 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
+    const int32_t *const pos = hd.pos;
+    uint32_t *const bitmap = hd.bitmap;
+    const uint64_t *const selq = hd.selq;
     // ---- selections (d > k): warp per item
     const int64_t nsel = *(const volatile uint32_t *)(hd.meta + kMetaSel + hd.h);
     for (int64_t w = gw; w < nsel; w += nw) {
-        const uint64_t e = hd.selq[w];
+        const uint64_t e = selq[w];
         const int r = (int)(e >> 32);
         const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
         const RelDev &R = g.rel[r];
@@ -325,6 +341,8 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
         const int p = (int)(ib >> 56);
         const int64_t base = ib & ((1ll << 56) - 1);
         Item itm;
+        itm.pos = pos;
+        itm.bitmap = bitmap;
         itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
         itm.soff = (uint32_t)g.off[R.src_vt];
         itm.ebase = R.edge_base[p] + base;
@@ -349,15 +367,20 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
         int r = 0;
         int32_t pos0 = 0, cnt = 0, d = 0;
         int64_t ib = 0;
+        uint32_t *srcp = nullptr;
+        int64_t *eidp = nullptr;
         if (it < total) {
             while (it >= cum[r + 1]) ++r;
             const int64_t i = it - cum[r];
-            pos0 = hd.indptr[r][i];
-            cnt = hd.indptr[r][i + 1] - pos0;
+            const int32_t *bip = hd.indptr[r];
+            pos0 = bip[i];
+            cnt = bip[i + 1] - pos0;
             if (cnt > 0) {
                 ib = hd.ibase[r][i];
                 d = hd.ideg[r][i];
             }
+            srcp = hd.src[r] + pos0;
+            eidp = hd.eids[r] + pos0;
         }
         const int k = hd.fanout[r];
         const bool copy = cnt > 0 && !(k >= 0 && d > k);
@@ -384,9 +407,10 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
                     if (cand_l < 32 && ex <= s) L = cand_l;
                 }
                 const int32_t exL = __shfl_sync(0xffffffffu, excl, L);
-                const int32_t posL = __shfl_sync(0xffffffffu, pos0, L);
                 const int64_t ibL = __shfl_sync(0xffffffffu, ib, L);
                 const int rL = __shfl_sync(0xffffffffu, r, L);
+                uint32_t *const srcL = (uint32_t *)__shfl_sync(0xffffffffu, (unsigned long long)srcp, L);
+                int64_t *const eidL = (int64_t *)__shfl_sync(0xffffffffu, (unsigned long long)eidp, L);
                 dsrc[q] = nullptr;
                 if (s < tot) {
                     const int p = (int)(ibL >> 56);
@@ -397,8 +421,8 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
                     gid[q] = (uint32_t)g.off[R.src_vt];
                     bb[q] = g.boff[R.src_vt] - g.off[R.src_vt];
                     eid[q] = R.edge_base[p] + base + j;
-                    dsrc[q] = hd.src[rL] + posL + j;
-                    deid[q] = hd.eids[rL] + posL + j;
+                    dsrc[q] = srcL + j;
+                    deid[q] = eidL + j;
                 }
             }
 #pragma unroll
@@ -406,13 +430,13 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
                 if (dsrc[q]) gid[q] += (uint32_t)__ldg(ixp[q]);
 #pragma unroll
             for (int q = 0; q < U; ++q)
-                if (dsrc[q]) posv[q] = __ldcg(hd.pos + gid[q]);
+                if (dsrc[q]) posv[q] = __ldcg(pos + gid[q]);
 #pragma unroll
             for (int q = 0; q < U; ++q)
                 if (dsrc[q]) {
                     *dsrc[q] = gid[q];
                     *deid[q] = eid[q];
-                    mark_new(hd, gid[q], posv[q], bb[q]);
+                    mark_new(bitmap, gid[q], posv[q], bb[q]);
                 }
         }
     }
@@ -472,7 +496,9 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
         int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
         if (pc) {
             const int64_t gbase = (g.off[u] - g.boff[u]) + wi * 32;   // gid of bit 0 of word wi
-            int64_t *nodes = hd.nodes[u];
+            int64_t *const nodes = hd.nodes[u];
+            int32_t *const pos = hd.pos;
+            int32_t *const meta = hd.meta;
             const int32_t cap = hd.cap_nodes[u];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -483,9 +509,9 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
                     const int64_t gid = gbase + 32 * q + b;
                     if (position < cap) {
                         nodes[position] = gid;
-                        hd.pos[gid] = position;
+                        pos[gid] = position;
                     } else {
-                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                        atomicOr(meta + kMetaErr, kErrCapacity);
                     }
                     ++position;
                 }
@@ -499,16 +525,13 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
 // indices = pos[src]: the local id of every sampled src in S_h[s(r)].
 __device__ void phase_relabel(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
-    const int32_t *nnz = meta_nnz(hd.meta, hd.h);
-    int64_t cum[EG_MAX_REL + 1];
-    cum[0] = 0;
-    for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + nnz[r];
-    const int64_t total = cum[g.n_rel];
-    for (int64_t e = bid * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)nb * blockDim.x) {
-        int r = 0;
-        while (e >= cum[r + 1]) ++r;
-        const int64_t le = e - cum[r];
-        hd.indices[r][le] = __ldcg(hd.pos + hd.src[r][le]);
+    const int32_t *const pos = hd.pos;
+    const int64_t stride = (int64_t)nb * blockDim.x;
+    for (int r = 0; r < g.n_rel; ++r) {
+        const int64_t n = meta_nnz(hd.meta, hd.h)[r];
+        const uint32_t *const src = hd.src[r];
+        int32_t *const idx = hd.indices[r];
+        for (int64_t e = bid * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) idx[e] = __ldcg(pos + src[e]);
     }
 }
 
@@ -519,11 +542,14 @@ __device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, 
     int64_t cum[EG_MAX_VT + 1];
     cum[0] = 0;
     for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
-    for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < cum[g.n_vt]; i += (int64_t)nb * blockDim.x) {
-        int u = 0;
-        while (i >= cum[u + 1]) ++u;
-        const int64_t gid = hd.nodes[u][i - cum[u]];
-        if (gid >= 0 && gid < g.off[g.n_vt]) hd.pos[gid] = -1;
+    int32_t *const pos = hd.pos;
+    for (int u = 0; u < g.n_vt; ++u) {
+        const int64_t *const nodes = hd.nodes[u];
+        const int64_t n = cum[u + 1] - cum[u];
+        for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
+            const int64_t gid = nodes[i];
+            if (gid >= 0 && gid < g.off[g.n_vt]) pos[gid] = -1;
+        }
     }
 }
 
