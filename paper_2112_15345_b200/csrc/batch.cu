@@ -64,10 +64,11 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_sample(const __grid_consta
     phase_sample(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_bitcount(const BatchDev *__restrict__ bd, int h)
+__global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
+                                                            const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 4 + 5 * h);
-    phase_bitcount(bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+    phase_bitcount(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_emit(const __grid_constant__ GraphDev g,
@@ -104,7 +105,7 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_scan<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_sample<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_bitcount<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(bd_dev, h);
+        k_bitcount<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_emit<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         nk += 5;
     }

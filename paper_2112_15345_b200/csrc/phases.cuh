@@ -175,14 +175,14 @@ struct Item {
     int64_t *eid_out;
 };
 
-// If the source is not yet in the batch, mark it in the new-vertex bitmap (the
-// first step of the hop's compaction, fused into sampling).
-__device__ __forceinline__ void mark_new(uint32_t *bitmap, uint32_t gid, int32_t pos_of_gid, int64_t bit_base)
+// Mark the source in the hop's bitmap (the first step of the compaction, fused into
+// sampling).  Fire-and-forget RED.OR, no load: sources already in the batch are
+// cleared from the bitmap by phase_bitcount (one check per unique source instead of
+// a dependent pos[] load per sampled edge).
+__device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t gid, int64_t bit_base)
 {
-    if (pos_of_gid < 0) {
-        const int64_t bit = bit_base + gid;
-        atomicOr(bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED, no round trip
-    }
+    const int64_t bit = bit_base + gid;
+    atomicOr(bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED
 }
 
 __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_t slot, int64_t j)
@@ -190,7 +190,7 @@ __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_
     const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
     it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
-    mark_new(it.bitmap, gid, __ldcg(it.pos + gid), it.bit_base);
+    mark_src(it.bitmap, gid, it.bit_base);
 }
 
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
@@ -324,7 +324,7 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const int32_t *const pos = hd.pos;
+    const int32_t *const pos = hd.pos;     // (relabel reads it; sampling only marks)
     uint32_t *const bitmap = hd.bitmap;
     const uint64_t *const selq = hd.selq;
     // ---- selections (d > k): warp per item
@@ -391,7 +391,6 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
         constexpr int U = 4;   // slots per lane per round: U independent load chains in flight
         for (int32_t b0 = 0; b0 < tot; b0 += 32 * U) {
             uint32_t gid[U];
-            int32_t posv[U];
             uint32_t *dsrc[U];
             int64_t *deid[U];
             int64_t eid[U], bb[U];
@@ -430,13 +429,10 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
                 if (dsrc[q]) gid[q] += (uint32_t)__ldg(ixp[q]);
 #pragma unroll
             for (int q = 0; q < U; ++q)
-                if (dsrc[q]) posv[q] = __ldcg(pos + gid[q]);
-#pragma unroll
-            for (int q = 0; q < U; ++q)
                 if (dsrc[q]) {
                     *dsrc[q] = gid[q];
                     *deid[q] = eid[q];
-                    mark_new(bitmap, gid[q], posv[q], bb[q]);
+                    mark_src(bitmap, gid[q], bb[q]);
                 }
         }
     }
@@ -448,13 +444,38 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
 // the sums of groups of kGroupChunks chunks.
 constexpr int kGroupChunks = 256;
 
-__device__ void phase_bitcount(const HopDev &hd, int bid, int nb, int32_t n_chunks)
+__device__ void phase_bitcount(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
 {
     static_assert(kChunkWords == 4 * 256, "one uint4 per thread");
     __shared__ int32_t sh[33];
+    const int32_t *const pos = hd.pos;
     for (int c = bid; c < n_chunks; c += nb) {
-        const uint4 x = __ldcg(reinterpret_cast<const uint4 *>(hd.bitmap + (int64_t)c * kChunkWords) + threadIdx.x);
-        int32_t v = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + (int64_t)c * kChunkWords) + threadIdx.x;
+        const uint4 x = __ldcg(wp);
+        uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        if (w[0] | w[1] | w[2] | w[3]) {
+            // clear the marked sources that are already in the batch (pos >= 0)
+            const int64_t bit0 = (int64_t)c * kChunkBits;
+            int u = 0;
+            while (bit0 >= g.boff[u + 1]) ++u;
+            const int64_t gbase = (g.off[u] - g.boff[u]) + ((int64_t)c * kChunkWords + 4 * threadIdx.x) * 32;
+            uint32_t drop[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t word = w[q];
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    if (__ldcg(pos + gbase + 32 * q + b) >= 0) drop[q] |= 1u << b;
+                }
+            }
+            if (drop[0] | drop[1] | drop[2] | drop[3]) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w[q] &= ~drop[q];
+                *wp = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        int32_t v = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
         v = block_sum(v, sh);
         if (threadIdx.x == 0) {
             hd.chunk_cnt[c] = v;
