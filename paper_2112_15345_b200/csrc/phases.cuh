@@ -460,15 +460,32 @@ __device__ void phase_bitcount(const GraphDev &g, const HopDev &hd, int bid, int
             while (bit0 >= g.boff[u + 1]) ++u;
             const int64_t gbase = (g.off[u] - g.boff[u]) + ((int64_t)c * kChunkWords + 4 * threadIdx.x) * 32;
             uint32_t drop[4] = {0, 0, 0, 0};
+            // the pos[] checks of this thread's set bits, issued together (independent loads)
+            constexpr int kM = 8;
+            int32_t pv[kM];
+            int16_t at[kM];
+            int nb_ = 0;
+            uint32_t rest[4] = {w[0], w[1], w[2], w[3]};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t word = w[q];
-                while (word) {
-                    const int b = __ffs(word) - 1;
-                    word &= word - 1;
+            for (int q = 0; q < 4; ++q)
+                while (rest[q] && nb_ < kM) {
+                    const int b = __ffs(rest[q]) - 1;
+                    rest[q] &= rest[q] - 1;
+                    at[nb_++] = (int16_t)(32 * q + b);
+                }
+#pragma unroll
+            for (int m = 0; m < kM; ++m)
+                if (m < nb_) pv[m] = __ldcg(pos + gbase + at[m]);
+#pragma unroll
+            for (int m = 0; m < kM; ++m)
+                if (m < nb_ && pv[m] >= 0) drop[at[m] >> 5] |= 1u << (at[m] & 31);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)       // more than kM bits in this thread's words: rare
+                while (rest[q]) {
+                    const int b = __ffs(rest[q]) - 1;
+                    rest[q] &= rest[q] - 1;
                     if (__ldcg(pos + gbase + 32 * q + b) >= 0) drop[q] |= 1u << b;
                 }
-            }
             if (drop[0] | drop[1] | drop[2] | drop[3]) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) w[q] &= ~drop[q];
