@@ -64,7 +64,8 @@ struct HopDev {
     int32_t *meta;                   // batch counters
     int32_t *partial;                // scan scratch [EG_MAX_REL][kScanBlocks]
     int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
-    uint32_t *bitmap;                // new-vertex bitmap
+    uint32_t *bitmap;                // this hop's marks: every sampled source (A)
+    uint32_t *members;               // vertices already in the batch (M); new = A & ~M
     int32_t *chunk_cnt;              // popcount per bitmap chunk
     int32_t *chunk_pre;              // exclusive prefix of chunk_cnt within the chunk's type
     uint32_t *ticket;                // last-block-done counter of bitcount_kernel

@@ -64,6 +64,7 @@ struct TimedPair {
 struct BatchState {
     int32_t *pos = nullptr;
     uint32_t *bitmap = nullptr;
+    uint32_t *members = nullptr;
     int32_t *chunk_cnt = nullptr;
     int32_t *chunk_pre = nullptr;
     int32_t *partial = nullptr;
@@ -327,6 +328,8 @@ eg_status alloc_state(eg_ctx *c, BatchState *st)
     EG_CUDA(c, cudaMemset(st->pos, 0xFF, sizeof(int32_t) * nt));
     EG_CUDA(c, cudaMalloc(&st->bitmap, sizeof(uint32_t) * words));
     EG_CUDA(c, cudaMemset(st->bitmap, 0, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMalloc(&st->members, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMemset(st->members, 0, sizeof(uint32_t) * words));
     EG_CUDA(c, cudaMalloc(&st->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
     EG_CUDA(c, cudaMalloc(&st->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
     EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
@@ -839,6 +842,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.partial = st.partial;
         hd.pos = st.pos;
         hd.bitmap = st.bitmap;
+        hd.members = st.members;
         hd.chunk_cnt = st.chunk_cnt;
         hd.chunk_pre = st.chunk_pre;
         hd.ticket = nullptr;
@@ -1036,7 +1040,10 @@ eg_status finish(eg_blocks *b)
     const int32_t errbits = m[kMetaErr];
     if (errbits & kErrSeedRange) return b->status = fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
     if (errbits & kErrSeedDup) return b->status = fail(c, EG_EINVAL, "duplicate seeds");
-    if (errbits) return b->status = fail(c, EG_EINVAL, "internal capacity overflow");
+    if (errbits) {   // cannot happen with true upper bounds; the batch state is not trustworthy
+        c->broken = true;
+        return b->status = fail(c, EG_ESTATE, "internal capacity overflow");
+    }
     return b->status = EG_OK;
 }
 
@@ -1318,6 +1325,7 @@ eg_status eg_destroy(eg_ctx *c)
         for (BatchState &bs : ln.st) {
             cudaFree(bs.pos);
             cudaFree(bs.bitmap);
+            cudaFree(bs.members);
             cudaFree(bs.chunk_cnt);
             cudaFree(bs.chunk_pre);
             cudaFree(bs.partial);

@@ -25,13 +25,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 // dst-prefix relabel; flags out-of-range and duplicate seeds.  One block.
 __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ seeds)
 {
-    __shared__ int32_t sh[33];
+    __shared__ int32_t wcnt[32][EG_MAX_VT];   // per warp, per type: count, then exclusive offset
     __shared__ int32_t base[EG_MAX_VT];
     // pointers hoisted into registers: HopDev lives in global memory and every store
     // below could alias it, so reading fields inside the loops would reload them
     int32_t *const pos = hd.pos;
     int32_t *const meta = hd.meta;
     const int64_t n = (int64_t)hd.dyn[1];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = lane_id();
     if (threadIdx.x < EG_MAX_VT) base[threadIdx.x] = 0;
     __syncthreads();
     const int64_t n_total = g.off[g.n_vt];
@@ -48,25 +49,40 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
                 while (gid >= g.off[vt + 1]) ++vt;
             }
         }
+        // stable placement per type: ballot ranks within the warp, warp offsets per type
+        int rank = 0;
         for (int u = 0; u < g.n_vt; ++u) {
-            const int32_t flag = (vt == u);
-            int32_t tot;
-            const int32_t ex = block_excl_scan(flag, sh, &tot);
-            if (flag) {
-                const int32_t p = base[u] + ex;
-                if (p < hd.cap_nodes[u]) {
-                    hd.nodes[u][p] = gid;
-                    if (atomicCAS(pos + gid, -1, p) != -1) atomicOr(meta + kMetaErr, kErrSeedDup);
-                } else {
-                    atomicOr(meta + kMetaErr, kErrCapacity);
-                }
-            }
-            if (threadIdx.x == 0) base[u] += tot;
-            __syncthreads();
+            const uint32_t m = __ballot_sync(0xffffffffu, vt == u);
+            if (vt == u) rank = __popc(m & lanemask_lt());
+            if (lane == 0) wcnt[w][u] = __popc(m);
         }
+        __syncthreads();
+        if (threadIdx.x < g.n_vt) {
+            const int u = threadIdx.x;
+            int32_t run = base[u];
+            for (int ww = 0; ww < nw; ++ww) {
+                const int32_t cnt = wcnt[ww][u];
+                wcnt[ww][u] = run;
+                run += cnt;
+            }
+            base[u] = run;
+        }
+        __syncthreads();
+        if (vt >= 0) {
+            const int32_t p = wcnt[w][vt] + rank;
+            if (p < hd.cap_nodes[vt]) {
+                hd.nodes[vt][p] = gid;
+                if (atomicCAS(pos + gid, -1, p) != -1) atomicOr(meta + kMetaErr, kErrSeedDup);
+                const int64_t bit = g.boff[vt] + (gid - g.off[vt]);
+                atomicOr(hd.members + (bit >> 5), 1u << (bit & 31));
+            } else {
+                atomicOr(meta + kMetaErr, kErrCapacity);
+            }
+        }
+        __syncthreads();
     }
     if (threadIdx.x < g.n_vt)
-        meta_nodes(hd.meta, 0)[threadIdx.x] = min(base[threadIdx.x], hd.cap_nodes[threadIdx.x]);
+        meta_nodes(meta, 0)[threadIdx.x] = min(base[threadIdx.x], hd.cap_nodes[threadIdx.x]);
     __syncthreads();
 }
 
@@ -444,55 +460,20 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
 // the sums of groups of kGroupChunks chunks.
 constexpr int kGroupChunks = 256;
 
-__device__ void phase_bitcount(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+__device__ void phase_bitcount(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
 {
     static_assert(kChunkWords == 4 * 256, "one uint4 per thread");
     __shared__ int32_t sh[33];
-    const int32_t *const pos = hd.pos;
     for (int c = bid; c < n_chunks; c += nb) {
-        uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + (int64_t)c * kChunkWords) + threadIdx.x;
-        const uint4 x = __ldcg(wp);
-        uint32_t w[4] = {x.x, x.y, x.z, x.w};
-        if (w[0] | w[1] | w[2] | w[3]) {
-            // clear the marked sources that are already in the batch (pos >= 0)
-            const int64_t bit0 = (int64_t)c * kChunkBits;
-            int u = 0;
-            while (bit0 >= g.boff[u + 1]) ++u;
-            const int64_t gbase = (g.off[u] - g.boff[u]) + ((int64_t)c * kChunkWords + 4 * threadIdx.x) * 32;
-            uint32_t drop[4] = {0, 0, 0, 0};
-            // the pos[] checks of this thread's set bits, issued together (independent loads)
-            constexpr int kM = 8;
-            int32_t pv[kM];
-            int16_t at[kM];
-            int nb_ = 0;
-            uint32_t rest[4] = {w[0], w[1], w[2], w[3]};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                while (rest[q] && nb_ < kM) {
-                    const int b = __ffs(rest[q]) - 1;
-                    rest[q] &= rest[q] - 1;
-                    at[nb_++] = (int16_t)(32 * q + b);
-                }
-#pragma unroll
-            for (int m = 0; m < kM; ++m)
-                if (m < nb_) pv[m] = __ldcg(pos + gbase + at[m]);
-#pragma unroll
-            for (int m = 0; m < kM; ++m)
-                if (m < nb_ && pv[m] >= 0) drop[at[m] >> 5] |= 1u << (at[m] & 31);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)       // more than kM bits in this thread's words: rare
-                while (rest[q]) {
-                    const int b = __ffs(rest[q]) - 1;
-                    rest[q] &= rest[q] - 1;
-                    if (__ldcg(pos + gbase + 32 * q + b) >= 0) drop[q] |= 1u << b;
-                }
-            if (drop[0] | drop[1] | drop[2] | drop[3]) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) w[q] &= ~drop[q];
-                *wp = make_uint4(w[0], w[1], w[2], w[3]);
-            }
+        const int64_t wq = (int64_t)c * (kChunkWords / 4) + threadIdx.x;
+        uint4 *ap = reinterpret_cast<uint4 *>(hd.bitmap) + wq;
+        const uint4 a = __ldcg(ap);
+        int32_t v = 0;
+        if (a.x | a.y | a.z | a.w) {
+            const uint4 m = __ldcg(reinterpret_cast<const uint4 *>(hd.members) + wq);
+            v = __popc(a.x & ~m.x) + __popc(a.y & ~m.y) + __popc(a.z & ~m.z) + __popc(a.w & ~m.w);
+            if (v == 0) *ap = make_uint4(0, 0, 0, 0);   // only members marked: consumed here, emit skips
         }
-        int32_t v = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
         v = block_sum(v, sh);
         if (threadIdx.x == 0) {
             hd.chunk_cnt[c] = v;
@@ -527,8 +508,11 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
         const int32_t nF = meta_nodes(hd.meta, hd.h)[u];
         const int64_t wi = (int64_t)c * kChunkWords + 4 * threadIdx.x;
         uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + wi);
+        uint4 *mp = reinterpret_cast<uint4 *>(hd.members + wi);
         const uint4 x = __ldcg(wp);
-        uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        uint4 mm = make_uint4(0, 0, 0, 0);
+        if (x.x | x.y | x.z | x.w) mm = __ldcg(mp);
+        uint32_t w[4] = {x.x & ~mm.x, x.y & ~mm.y, x.z & ~mm.z, x.w & ~mm.w};
         const int32_t pc = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
         int32_t tot;
         int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
@@ -554,8 +538,9 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
                     ++position;
                 }
             }
-            *wp = make_uint4(0, 0, 0, 0);
+            *mp = make_uint4(mm.x | w[0], mm.y | w[1], mm.z | w[2], mm.w | w[3]);   // now members
         }
+        if (x.x | x.y | x.z | x.w) *wp = make_uint4(0, 0, 0, 0);                    // marks consumed
         if (threadIdx.x == 0) atomicAdd(meta_nodes(hd.meta, hd.h + 1) + u, mine);
     }
 }
@@ -581,12 +566,17 @@ __device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, 
     cum[0] = 0;
     for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
     int32_t *const pos = hd.pos;
+    uint32_t *const members = hd.members;
     for (int u = 0; u < g.n_vt; ++u) {
         const int64_t *const nodes = hd.nodes[u];
         const int64_t n = cum[u + 1] - cum[u];
         for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
             const int64_t gid = nodes[i];
-            if (gid >= 0 && gid < g.off[g.n_vt]) pos[gid] = -1;
+            if (gid >= g.off[u] && gid < g.off[u + 1]) {
+                pos[gid] = -1;
+                const int64_t bit = g.boff[u] + (gid - g.off[u]);
+                atomicAnd(members + (bit >> 5), ~(1u << (bit & 31)));
+            }
         }
     }
 }
