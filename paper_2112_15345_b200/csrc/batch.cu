@@ -34,7 +34,7 @@ __device__ __forceinline__ void stamp(const BatchDev *bd, int k)
         reinterpret_cast<uint64_t *>(bd->hop[blockIdx.y][0].meta + kMetaStamps)[k] = globaltimer();
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_seed(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd)
 {
     stamp(bd, 0);
@@ -56,12 +56,18 @@ __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ 
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, (bd->n_chunks + kGroupChunks - 1) / kGroupChunks);
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 2) k_sample(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, 2) k_select(const __grid_constant__ GraphDev g,
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
     stamp(bd, 3 + 5 * h);
-    phase_sample(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
+    phase_select(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
+}
+
+__global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant__ GraphDev g,
+                                                        const BatchDev *__restrict__ bd, int h)
+{
+    phase_copy(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
@@ -71,7 +77,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constan
     phase_bitcount(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_emit(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kChunkWords, 2) k_emit(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 5 + 5 * h);
@@ -92,22 +98,29 @@ __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__
     phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
 }
 
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s)
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
+                 const Fork &fk)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
     const int wide = kScanBlocks * g.n_rel;        // count / scan: one block per virtual block
     const int samp = (kSMs * 4 + B - 1) / B;
     int nk = 0;
-    k_seed<<<dim3(1, B), kBatchThreads, 0, s>>>(g, bd_dev);
+    k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
     ++nk;
     for (int h = 0; h < n_hops; ++h) {
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_scan<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_sample<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        // selections and full-neighbourhood copies write disjoint slots: two graph branches
+        cudaEventRecord(fk.fork, s);
+        cudaStreamWaitEvent(fk.side, fk.fork, 0);
+        k_copy<<<dim3(per, B), kBatchThreads, 0, fk.side>>>(g, bd_dev, h);
+        cudaEventRecord(fk.join, fk.side);
+        k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        cudaStreamWaitEvent(s, fk.join, 0);
         k_bitcount<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_emit<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        nk += 5;
+        k_emit<<<dim3(n_chunks, B), kChunkWords, 0, s>>>(g, bd_dev, h);
+        nk += 6;
     }
     k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
     k_reset<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);

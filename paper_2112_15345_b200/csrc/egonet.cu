@@ -153,6 +153,7 @@ struct eg_ctx {
     // batch plans (CUDA graphs)
     std::vector<Plan *> plans;
     cudaStream_t cap_stream = nullptr;
+    Fork fork{};                          // capture side stream + events (graph branches)
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
@@ -511,7 +512,10 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
         const char *tr = getenv("EG_TRACE");
         c->trace = tr && tr[0] == '1';
     }
-    if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->fork.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->fork.join, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return EG_ECUDA;
     }
@@ -894,7 +898,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -1319,6 +1323,9 @@ eg_status eg_destroy(eg_ctx *c)
     drain_timing(c);
     destroy_plans(c);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    if (c->fork.side) cudaStreamDestroy(c->fork.side);
+    if (c->fork.fork) cudaEventDestroy(c->fork.fork);
+    if (c->fork.join) cudaEventDestroy(c->fork.join);
     for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
     for (Lane &ln : c->lanes) {
         if (ln.stream) cudaStreamSynchronize(ln.stream);

@@ -28,9 +28,16 @@ struct BatchDev {
     HopDev hop[kMaxBundle][EG_MAX_HOPS];
 };
 
+// A side stream + two events to fork / join independent kernels inside a capture.
+struct Fork {
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+};
+
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
 // returns the number of kernels.
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s);
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
+                 const Fork &fk);
 
 // gather.cu
 void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);

@@ -331,16 +331,14 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
     __syncwarp();
 }
 
-// Sampling of one hop: the selection items (queued by phase_count) one per warp,
-// then the full-neighbourhood items as segmented copies, 32 items per warp.
-// cand: kSelCap slots of this warp in shared memory.
-__device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
+// Sampling of one hop, part 1: the selection items (d > k, queued by phase_count),
+// one warp per item.  cand: kSelCap slots of this warp in shared memory.
+__device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
 {
     const int warps = blockDim.x >> 5;
-    const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const int32_t *const pos = hd.pos;     // (relabel reads it; sampling only marks)
+    const int32_t *const pos = hd.pos;
     uint32_t *const bitmap = hd.bitmap;
     const uint64_t *const selq = hd.selq;
     // ---- selections (d > k): warp per item
@@ -372,6 +370,16 @@ __device__ void phase_sample(const GraphDev &g, const HopDev &hd, int bid, int n
         else
             select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
     }
+}
+
+// Sampling of one hop, part 2: the full-neighbourhood items (d <= k or k = -1) as
+// segmented copies, 32 items per warp, 4 independent load chains per lane.
+__device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
+{
+    const int warps = blockDim.x >> 5;
+    const int lane = lane_id();
+    const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
+    uint32_t *const bitmap = hd.bitmap;
     // ---- full neighbourhoods: segmented copy over groups of 32 items
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
     int64_t cum[EG_MAX_REL + 1];
@@ -493,10 +501,11 @@ __device__ __forceinline__ int32_t bits_before(const HopDev &hd, int c, int32_t 
 }
 
 // New vertices of each chunk, in gid order: append to the node array of their type,
-// set pos[], clear the bitmap words.  Virtual block per chunk, 4 words per thread.
+// set pos[], fold them into the members, clear the marks.  Virtual block per chunk,
+// one word per thread (1024 threads).
 __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
 {
-    __shared__ int32_t sh[33];
+    __shared__ int32_t sh[33];   // blockDim.x == kChunkWords == 1024
     for (int c = bid; c < n_chunks; c += nb) {
         const int32_t mine = __ldcg(hd.chunk_cnt + c);
         if (mine == 0) continue;   // block-uniform
@@ -506,14 +515,14 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
         const int fc = (int)(g.boff[u] / kChunkBits);
         const int32_t prior = bits_before(hd, c, sh) - bits_before(hd, fc, sh);
         const int32_t nF = meta_nodes(hd.meta, hd.h)[u];
-        const int64_t wi = (int64_t)c * kChunkWords + 4 * threadIdx.x;
-        uint4 *wp = reinterpret_cast<uint4 *>(hd.bitmap + wi);
-        uint4 *mp = reinterpret_cast<uint4 *>(hd.members + wi);
-        const uint4 x = __ldcg(wp);
-        uint4 mm = make_uint4(0, 0, 0, 0);
-        if (x.x | x.y | x.z | x.w) mm = __ldcg(mp);
-        uint32_t w[4] = {x.x & ~mm.x, x.y & ~mm.y, x.z & ~mm.z, x.w & ~mm.w};
-        const int32_t pc = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+        // one bitmap word per thread (blockDim.x == kChunkWords)
+        const int64_t wi = (int64_t)c * kChunkWords + threadIdx.x;
+        uint32_t *wp = hd.bitmap + wi;
+        uint32_t *mp = hd.members + wi;
+        const uint32_t x = __ldcg(wp);
+        const uint32_t mm = x ? __ldcg(mp) : 0u;
+        uint32_t word = x & ~mm;
+        const int32_t pc = __popc(word);
         int32_t tot;
         int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
         if (pc) {
@@ -522,25 +531,21 @@ __device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb,
             int32_t *const pos = hd.pos;
             int32_t *const meta = hd.meta;
             const int32_t cap = hd.cap_nodes[u];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t word = w[q];
-                while (word) {
-                    const int b = __ffs(word) - 1;
-                    word &= word - 1;
-                    const int64_t gid = gbase + 32 * q + b;
-                    if (position < cap) {
-                        nodes[position] = gid;
-                        pos[gid] = position;
-                    } else {
-                        atomicOr(meta + kMetaErr, kErrCapacity);
-                    }
-                    ++position;
+            *mp = mm | word;                                          // now members
+            while (word) {
+                const int b = __ffs(word) - 1;
+                word &= word - 1;
+                const int64_t gid = gbase + b;
+                if (position < cap) {
+                    nodes[position] = gid;
+                    pos[gid] = position;
+                } else {
+                    atomicOr(meta + kMetaErr, kErrCapacity);
                 }
+                ++position;
             }
-            *mp = make_uint4(mm.x | w[0], mm.y | w[1], mm.z | w[2], mm.w | w[3]);   // now members
         }
-        if (x.x | x.y | x.z | x.w) *wp = make_uint4(0, 0, 0, 0);                    // marks consumed
+        if (x) *wp = 0u;                                              // marks consumed
         if (threadIdx.x == 0) atomicAdd(meta_nodes(hd.meta, hd.h + 1) + u, mine);
     }
 }
