@@ -67,8 +67,7 @@ struct HopDev {
     uint32_t *bitmap;                // this hop's marks: every sampled source (A)
     uint32_t *members;               // vertices already in the batch (M); new = A & ~M
     int32_t *chunk_cnt;              // popcount per bitmap chunk
-    int32_t *chunk_pre;              // exclusive prefix of chunk_cnt within the chunk's type
-    uint32_t *ticket;                // last-block-done counter of bitcount_kernel
+    int32_t *chunk_pre;              // sums of groups of kGroupChunks chunks
     int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
     int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch

@@ -138,9 +138,7 @@ struct eg_ctx {
     std::vector<Lane> lanes;
     int next_lane = 0;
     int depth = 1, bundle = 1;
-    uint64_t *h_dyn = nullptr;   // pinned {rng_seed, n_seeds}
     int32_t n_chunks = 0;
-    int32_t *h_meta = nullptr;   // pinned
     std::vector<void *> ipc_bases;
     uint32_t attached = 0;                          // bit p: rank p's shard is mapped
     eg_shard_meta metas[EG_MAX_RANKS] = {};          // every rank's published shard metadata
@@ -503,11 +501,6 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
     c->world = world;
     c->device = device;
     c->stream = (cudaStream_t)stream;
-    if (cudaMallocHost(&c->h_meta, sizeof(int32_t) * kMetaSize) != cudaSuccess ||
-        cudaMallocHost(&c->h_dyn, sizeof(uint64_t) * 2) != cudaSuccess) {
-        delete c;
-        return EG_ENOMEM;
-    }
     {
         const char *tr = getenv("EG_TRACE");
         c->trace = tr && tr[0] == '1';
@@ -849,7 +842,6 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.members = st.members;
         hd.chunk_cnt = st.chunk_cnt;
         hd.chunk_pre = st.chunk_pre;
-        hd.ticket = nullptr;
         for (int u = 0; u < V; ++u) {
             hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
             hd.cap_nodes[u] = (int32_t)p->capF[L][u];
@@ -1341,8 +1333,6 @@ eg_status eg_destroy(eg_ctx *c)
         if (ln.stream) cudaStreamDestroy(ln.stream);
     }
     c->lanes.clear();
-    cudaFreeHost(c->h_dyn);
-    cudaFreeHost(c->h_meta);
     delete c;
     return EG_OK;
 }
