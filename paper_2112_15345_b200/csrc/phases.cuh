@@ -278,8 +278,8 @@ __device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, in
 
 // Fast selection for k <= kSelMaxK: one pass over the d keys keeps the candidates
 // below a threshold T (expected 2k + 32 of them) in shared memory, in ascending j;
-// the k smallest composites among them are found by rank counting and emitted in
-// ascending j.  Falls back to select_generic if the candidate count is < k or
+// the k smallest composites among them are found by a register radix select (m <= 128)
+// or rank counting, and emitted in ascending j.  Falls back to select_generic if the candidate count is < k or
 // exceeds the slots (both astronomically rare; the result is identical).
 __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
                             uint32_t hr, uint32_t k0, uint32_t k1, uint64_t *cand)
@@ -314,6 +314,58 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
         return;
     }
     int32_t out = 0;
+    if (m <= 128) {
+        // radix select of the k-th smallest key among the m candidates, held 4 per lane
+        // (slot c = lane + 32 i); two warp reductions per bit, early exit once every
+        // candidate that still matches the decided bits is selected.
+        uint32_t key[4];
+        bool val[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane_id() + 32 * i;
+            val[i] = c < m;
+            key[i] = val[i] ? (uint32_t)(cand[c] >> 32) : 0u;
+        }
+        uint32_t P = 0;          // decided high bits of the threshold key
+        int krem = k;            // selections still to make among keys matching P
+        int s = 32;              // bits [s, 32) are decided
+        while (s > 0) {
+            const int b = s - 1;
+            uint32_t c0 = 0, cm = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const bool match = val[i] && (s == 32 || (key[i] >> s) == (P >> s));
+                cm += match;
+                c0 += match && !((key[i] >> b) & 1u);
+            }
+            cm = __reduce_add_sync(0xffffffffu, cm);
+            if ((int)cm == krem) break;                 // all matching keys are selected
+            c0 = __reduce_add_sync(0xffffffffu, c0);
+            if (krem > (int)c0) {
+                krem -= (int)c0;
+                P |= 1u << b;
+            }
+            s = b;
+        }
+        // selected: key below P on the decided bits, or matching them and among the first
+        // krem such candidates in slot (= ascending j) order
+        int eq_seen = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = lane_id() + 32 * i;
+            const uint32_t hi = s == 32 ? 0u : (key[i] >> s), ph = s == 32 ? 0u : (P >> s);
+            const bool lt = val[i] && hi < ph;
+            const bool eq = val[i] && hi == ph;
+            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+            const bool sel = lt || (eq && eq_seen + __popc(beq & lanemask_lt()) < krem);
+            eq_seen += __popc(beq);
+            const uint32_t bs = __ballot_sync(0xffffffffu, sel);
+            if (sel) emit_edge(hd, it, out + __popc(bs & lanemask_lt()), (int64_t)(uint32_t)cand[c]);
+            out += __popc(bs);
+        }
+        __syncwarp();
+        return;
+    }
     for (int c0 = 0; c0 < m; c0 += 32) {
         const int c = c0 + lane_id();
         bool sel = false;
