@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ 
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, (bd->n_chunks + kGroupChunks - 1) / kGroupChunks);
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 2) k_select(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, 3) k_select(const __grid_constant__ GraphDev g,
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
