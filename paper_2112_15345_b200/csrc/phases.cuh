@@ -276,6 +276,64 @@ __device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, in
     }
 }
 
+// Selection for d <= 128: every key fits in registers (4 consecutive offsets per lane,
+// one Philox call), so the k-th smallest key is found by a radix select over them
+// directly, ties broken by ascending j, and the selected offsets are emitted in
+// ascending j (j = 4 lane + t).
+__device__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
+                             uint32_t hr, uint32_t k0, uint32_t k1)
+{
+    const int lane = lane_id();
+    uint32_t w[4] = {0, 0, 0, 0};
+    uint32_t vm = 0;                                  // valid offsets of this lane
+    if (4 * lane < d) {
+        keys4((uint32_t)lane, v_lo, v_hi, hr, k0, k1, w);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) vm |= (uint32_t)(4 * lane + t < d) << t;
+    }
+    uint32_t P = 0;
+    int krem = k, s = 32;
+    while (s > 0) {
+        const int b = s - 1;
+        uint32_t c0 = 0, cm = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const bool match = (vm >> t & 1) && (s == 32 || (w[t] >> s) == (P >> s));
+            cm += match;
+            c0 += match && !((w[t] >> b) & 1u);
+        }
+        cm = __reduce_add_sync(0xffffffffu, cm);
+        if ((int)cm == krem) break;
+        c0 = __reduce_add_sync(0xffffffffu, c0);
+        if (krem > (int)c0) {
+            krem -= (int)c0;
+            P |= 1u << b;
+        }
+        s = b;
+    }
+    uint32_t ltm = 0, eqm = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t hi = s == 32 ? 0u : (w[t] >> s), ph = s == 32 ? 0u : (P >> s);
+        ltm |= (uint32_t)((vm >> t & 1) && hi < ph) << t;
+        eqm |= (uint32_t)((vm >> t & 1) && hi == ph) << t;
+    }
+    const int ce = __popc(eqm);
+    int er = warp_incl_scan(ce) - ce;                 // equal keys before this lane (ascending j)
+    uint32_t sel = ltm;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (eqm >> t & 1) {
+            if (er < krem) sel |= 1u << t;
+            ++er;
+        }
+    const int cs = __popc(sel);
+    int slot = warp_incl_scan(cs) - cs;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (sel >> t & 1) emit_edge(hd, it, slot++, 4 * lane + t);
+}
+
 // Fast selection for k <= kSelMaxK: one pass over the d keys keeps the candidates
 // below a threshold T (expected 2k + 32 of them) in shared memory, in ascending j;
 // the k smallest composites among them are found by a register radix select (m <= 128)
@@ -284,8 +342,11 @@ __device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, in
 __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
                             uint32_t hr, uint32_t k0, uint32_t k1, uint64_t *cand)
 {
+    // any threshold gives the same result (the selection below is exact; too few or too
+    // many candidates fall back to select_generic), so T may be approximate: float math
     const uint64_t E = 2ull * (uint64_t)k + 32;
-    const uint64_t T = (E >= (uint64_t)d) ? (1ull << 32) : ((E << 32) / (uint64_t)d);
+    const uint64_t T = (E >= (uint64_t)d) ? (1ull << 32)
+                                          : (uint64_t)(__fdividef((float)E, (float)d) * 4294967296.0f);
     const int64_t nq = (d + 3) >> 2;
     int m = 0;
     for (int64_t q0 = 0; q0 < nq; q0 += 32) {
@@ -417,7 +478,9 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
         itm.eid_out = hd.eids[r] + pos0;
         const int k = hd.fanout[r];
         const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
-        if (k <= kSelMaxK)
+        if (d <= 128)
+            select_small(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
+        else if (k <= kSelMaxK)
             select_fast(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi, cand);
         else
             select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
