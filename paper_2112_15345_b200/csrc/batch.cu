@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev 
 __global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 5 * h);
+    stamp(bd, 1 + 6 * h);
     phase_count(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
     if (h > 0) phase_relabel(g, bd->hop[blockIdx.y][h - 1], blockIdx.x, gridDim.x);
 }
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__
 __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 2 + 5 * h);
+    stamp(bd, 2 + 6 * h);
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, (bd->n_chunks + kGroupChunks - 1) / kGroupChunks);
 }
 
@@ -60,46 +60,47 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_select(const __grid_consta
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
-    stamp(bd, 3 + 5 * h);
+    stamp(bd, 3 + 6 * h);
     phase_select(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
 }
 
 __global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
+    stamp(bd, 4 + 6 * h);
     phase_copy(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
                                                             const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 4 + 5 * h);
+    stamp(bd, 5 + 6 * h);
     phase_bitcount(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(kChunkWords, 2) k_emit(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 5 + 5 * h);
+    stamp(bd, 6 + 6 * h);
     phase_emit(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_relabel(const __grid_constant__ GraphDev g,
                                                            const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 5 * bd->n_hops);
+    stamp(bd, 1 + 6 * bd->n_hops);
     phase_relabel(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd)
 {
-    stamp(bd, 2 + 5 * bd->n_hops);
+    stamp(bd, 2 + 6 * bd->n_hops);
     phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
 }
 
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk)
+                 const Fork &fk, bool serial)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
@@ -112,12 +113,18 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_scan<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         // selections and full-neighbourhood copies write disjoint slots: two graph branches
-        cudaEventRecord(fk.fork, s);
-        cudaStreamWaitEvent(fk.side, fk.fork, 0);
-        k_copy<<<dim3(per, B), kBatchThreads, 0, fk.side>>>(g, bd_dev, h);
-        cudaEventRecord(fk.join, fk.side);
-        k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        cudaStreamWaitEvent(s, fk.join, 0);
+        // (EG_TRACE=1 serialises them so that each gets its own phase stamp)
+        if (serial) {
+            k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+            k_copy<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        } else {
+            cudaEventRecord(fk.fork, s);
+            cudaStreamWaitEvent(fk.side, fk.fork, 0);
+            k_copy<<<dim3(per, B), kBatchThreads, 0, fk.side>>>(g, bd_dev, h);
+            cudaEventRecord(fk.join, fk.side);
+            k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+            cudaStreamWaitEvent(s, fk.join, 0);
+        }
         k_bitcount<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_emit<<<dim3(n_chunks, B), kChunkWords, 0, s>>>(g, bd_dev, h);
         nk += 6;

@@ -890,7 +890,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork, c->trace);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -1002,7 +1002,7 @@ void slot_finished(eg_ctx *c, Slot *sl)
         const uint64_t *st = reinterpret_cast<const uint64_t *>(sl->h_meta + kMetaStamps);
         std::vector<std::string> names = {"k.seed"};
         for (int h = 0; h < sl->plan->n_hops; ++h)
-            for (const char *x : {"count", "scan", "sample", "bitcount", "emit"})
+            for (const char *x : {"count", "scan", "select", "copy", "bitcount", "emit"})
                 names.push_back("k.h" + std::to_string(h) + "." + x);
         names.push_back("k.relabel");
         for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
