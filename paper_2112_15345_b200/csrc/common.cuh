@@ -15,6 +15,14 @@ constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
 constexpr int kScanBlocks = 64;           // virtual blocks per relation in the two-phase scan
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
+// Heavy items (d > kHeavyD, k <= kHeavyMaxK) are split into tasks of kHeavyChunk keys
+// sampled by different warps; their candidates meet in a per-item buffer.
+constexpr int kHeavyD = 2048;
+constexpr int kHeavyChunk = 1024;
+constexpr int kHeavyMaxK = 48;
+constexpr int kHeavyCap = 512;            // candidate slots per heavy item
+constexpr int kMaxHeavy = 256;            // heavy items per (batch, hop); overflow -> warp per item
+constexpr int kMaxHeavyTasks = kMaxHeavy * ((1 << 20) / kHeavyChunk + 1);
 
 // Error bits written by kernels into meta[kMetaErr].
 enum : int32_t { kErrSeedRange = 1, kErrSeedDup = 2, kErrCapacity = 4 };
@@ -47,7 +55,11 @@ struct FeatDev {
 constexpr int kMetaNodes = 0;
 constexpr int kMetaNnz = kMetaNodes + (EG_MAX_HOPS + 1) * EG_MAX_VT;
 constexpr int kMetaSel = kMetaNnz + EG_MAX_HOPS * EG_MAX_REL;   // selection-queue length per hop
-constexpr int kMetaErr = kMetaSel + EG_MAX_HOPS;
+constexpr int kMetaSelNext = kMetaSel + EG_MAX_HOPS;             // dynamic fetch counter per hop
+constexpr int kMetaHeavy = kMetaSelNext + EG_MAX_HOPS;           // heavy items per hop
+constexpr int kMetaHeavyQ = kMetaHeavy + EG_MAX_HOPS;            // heavy tasks per hop
+constexpr int kMetaHeavyNext = kMetaHeavyQ + EG_MAX_HOPS;        // dynamic fetch counter per hop
+constexpr int kMetaErr = kMetaHeavyNext + EG_MAX_HOPS;
 constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase timestamps (tracing)
 constexpr int kMaxStamps = 64;
 constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
@@ -72,6 +84,11 @@ struct HopDev {
     int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
     uint64_t *selq;                  // items that need a selection: (r << 32) | i
+    uint64_t *heavy_items;           // [kMaxHeavy] (r << 32) | i
+    uint32_t *heavy_cnt;             // [kMaxHeavy] candidates found
+    uint32_t *heavy_done;            // [kMaxHeavy] finished tasks
+    uint64_t *heavy_cand;            // [kMaxHeavy][kHeavyCap] (key << 32) | j
+    uint32_t *heavyq;                // tasks: (heavy item << 16) | chunk
     int32_t cap_nodes[EG_MAX_VT];    // capacity of nodes[u]
 };
 

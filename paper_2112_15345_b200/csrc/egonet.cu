@@ -79,6 +79,10 @@ struct Lane {
     std::vector<BatchState> st;
 };
 
+// per (batch, hop): heavy items, their counters, candidate buffers and chunk tasks
+constexpr size_t kHeavyBytes = sizeof(uint64_t) * kMaxHeavy + 2 * sizeof(uint32_t) * kMaxHeavy +
+                               sizeof(uint64_t) * kMaxHeavy * kHeavyCap + sizeof(uint32_t) * kMaxHeavyTasks;
+
 // A batch "plan": everything fixed by (hops, fanouts, seed capacity, features, bundle
 // size B): upper bounds, the memory layout of one batch (repeated B times), its slots.
 struct Slot;
@@ -95,7 +99,7 @@ struct Plan {
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_selq[EG_MAX_HOPS] = {};
+           o_selq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
     size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
@@ -788,6 +792,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         int64_t items = 0;
         for (int r = 0; r < R; ++r) items += p->capF[h][dst_vt[r]];
         p->o_selq[h] = take(sizeof(uint64_t) * items);
+        p->o_heavy[h] = take(kHeavyBytes);
     }
     if (features)
         for (int u = 0; u < V; ++u)
@@ -860,6 +865,12 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
                 x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
             }
             x.selq = (uint64_t *)(base + p->o_selq[h]);
+            char *hv = base + p->o_heavy[h];
+            x.heavy_items = (uint64_t *)hv;
+            x.heavy_cnt = (uint32_t *)(hv + sizeof(uint64_t) * kMaxHeavy);
+            x.heavy_done = x.heavy_cnt + kMaxHeavy;
+            x.heavy_cand = (uint64_t *)(hv + sizeof(uint64_t) * kMaxHeavy + 2 * sizeof(uint32_t) * kMaxHeavy);
+            x.heavyq = (uint32_t *)(x.heavy_cand + (size_t)kMaxHeavy * kHeavyCap);
             bd->hop[b][h] = x;
         }
         GatherDev &gd = gs.b[b];

@@ -132,6 +132,25 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
                 bip[i] = c;
                 sum += c;
             }
+            // heavy items (d > kHeavyD): split into tasks of kHeavyChunk keys for several warps
+            if (sel && k <= kHeavyMaxK && ideg[i] > kHeavyD) {
+                const int64_t d = ideg[i];
+                const uint32_t nch = (uint32_t)((d + kHeavyChunk - 1) / kHeavyChunk);
+                const uint32_t hs = atomicAdd((uint32_t *)(hd.meta + kMetaHeavy + hd.h), 1u);
+                if (hs < (uint32_t)kMaxHeavy) {
+                    const uint32_t t0 = atomicAdd((uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), nch);
+                    if (t0 + nch <= (uint32_t)kMaxHeavyTasks) {
+                        hd.heavy_items[hs] = ((uint64_t)r << 32) | (uint64_t)i;
+                        hd.heavy_cnt[hs] = 0;
+                        hd.heavy_done[hs] = 0;
+                        for (uint32_t c = 0; c < nch; ++c) hd.heavyq[t0 + c] = (hs << 16) | c;
+                        sel = false;
+                    } else {   // task list full: mark the reserved entries void, item goes to the normal queue
+                        for (uint32_t c = 0; c < nch && t0 + c < (uint32_t)kMaxHeavyTasks; ++c)
+                            hd.heavyq[t0 + c] = 0xFFFFFFFFu;
+                    }
+                }
+            }
             const uint32_t m = __ballot_sync(0xffffffffu, sel);
             if (m) {
                 uint32_t q = 0;
@@ -444,19 +463,184 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
     __syncwarp();
 }
 
-// Sampling of one hop, part 1: the selection items (d > k, queued by phase_count),
-// one warp per item.  cand: kSelCap slots of this warp in shared memory.
+// One chunk of a heavy item (d > kHeavyD): keys of offsets [c * kHeavyChunk, ...) below
+// the item's threshold go to the item's candidate buffer; the warp that finishes the
+// item's last chunk selects the k smallest composites and emits them in ascending j.
+__device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, uint32_t seed_lo, uint32_t seed_hi,
+                           uint64_t *cand)
+{
+    const int lane = lane_id();
+    const uint32_t hs = task >> 16, c = task & 0xFFFFu;
+    const uint64_t e = hd.heavy_items[hs];
+    const int r = (int)(e >> 32);
+    const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+    const RelDev &R = g.rel[r];
+    const int64_t ib = hd.ibase[r][i];
+    const int64_t d = hd.ideg[r][i];
+    const int64_t v = hd.nodes[R.dst_vt][i];
+    const int k = hd.fanout[r];
+    const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
+    const uint32_t v_lo = (uint32_t)v, v_hi = (uint32_t)((uint64_t)v >> 32);
+    const uint64_t E = 2ull * (uint64_t)k + 32;
+    const uint64_t T = (uint64_t)(__fdividef((float)E, (float)d) * 4294967296.0f);   // identical for every chunk
+    uint32_t *cnt = hd.heavy_cnt + hs;
+    uint64_t *buf = hd.heavy_cand + (int64_t)hs * kHeavyCap;
+    const int64_t q_lo = (int64_t)c * (kHeavyChunk / 4), q_hi = min((d + 3) >> 2, q_lo + kHeavyChunk / 4);
+    for (int64_t q0 = q_lo; q0 < q_hi; q0 += 32) {
+        const int64_t q = q0 + lane;
+        uint32_t w[4] = {0, 0, 0, 0};
+        uint32_t f = 0;
+        if (q < q_hi) {
+            keys4((uint32_t)q, v_lo, v_hi, hr, seed_lo, seed_hi, w);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) f |= (uint32_t)(4 * q + t < d && (uint64_t)w[t] < T) << t;
+        }
+        const int cf = __popc(f);
+        const int ex = warp_incl_scan(cf) - cf;
+        const int tot = __shfl_sync(0xffffffffu, ex + cf, 31);
+        if (tot) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(cnt, (uint32_t)tot);
+            base = __shfl_sync(0xffffffffu, base, 0) + ex;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (f >> t & 1) {
+                    if (base < (uint32_t)kHeavyCap) buf[base] = ((uint64_t)w[t] << 32) | (uint64_t)(4 * q + t);
+                    ++base;
+                }
+        }
+    }
+    __threadfence();
+    uint32_t done = 0;
+    const uint32_t nch = (uint32_t)((d + kHeavyChunk - 1) / kHeavyChunk);
+    if (lane == 0) done = atomicAdd(hd.heavy_done + hs, 1u);
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done != nch - 1) return;
+    // ---- last chunk: finalize the item
+    __threadfence();
+    const int32_t pos0 = hd.indptr[r][i];
+    const int p = (int)(ib >> 56);
+    const int64_t base0 = ib & ((1ll << 56) - 1);
+    Item itm;
+    itm.pos = hd.pos;
+    itm.bitmap = hd.bitmap;
+    itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
+    itm.soff = (uint32_t)g.off[R.src_vt];
+    itm.ebase = R.edge_base[p] + base0;
+    itm.ix = R.indices[p] + base0;
+    itm.src_out = hd.src[r] + pos0;
+    itm.eid_out = hd.eids[r] + pos0;
+    const int m = (int)*(volatile uint32_t *)cnt;
+    if (m < k || m > kHeavyCap) {   // astronomically rare: exact recomputation over all d keys
+        select_generic(hd, itm, d, k, v_lo, v_hi, hr, seed_lo, seed_hi);
+        return;
+    }
+    for (int slot = lane; slot < m; slot += 32) cand[slot] = __ldcg(buf + slot);
+    __syncwarp();
+    // selected flags of this lane's slots (slot = lane + 32 t): the k smallest composites
+    uint32_t selm = 0;
+    bool done_sel = false;
+    if (m <= 128) {
+        // radix select of the k-th smallest key over registers (as in select_small)
+        uint32_t key[4];
+        bool val[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int slot = lane + 32 * t;
+            val[t] = slot < m;
+            key[t] = val[t] ? (uint32_t)(cand[slot] >> 32) : 0u;
+        }
+        uint32_t P = 0;
+        int krem = k, s = 32;
+        while (s > 0) {
+            const int b = s - 1;
+            uint32_t c0 = 0, cm = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const bool match = val[t] && (s == 32 || (key[t] >> s) == (P >> s));
+                cm += match;
+                c0 += match && !((key[t] >> b) & 1u);
+            }
+            cm = __reduce_add_sync(0xffffffffu, cm);
+            if ((int)cm == krem) break;
+            c0 = __reduce_add_sync(0xffffffffu, c0);
+            if (krem > (int)c0) {
+                krem -= (int)c0;
+                P |= 1u << b;
+            }
+            s = b;
+        }
+        uint32_t neq = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t hi = s == 32 ? 0u : (key[t] >> s), ph = s == 32 ? 0u : (P >> s);
+            const bool lt = val[t] && hi < ph, eq = val[t] && hi == ph;
+            neq += eq;
+            if (lt || eq) selm |= 1u << t;
+        }
+        neq = __reduce_add_sync(0xffffffffu, neq);
+        done_sel = (int)neq == krem;   // else a key tie straddles the boundary: composite ranks below
+    }
+    if (!done_sel) {
+        selm = 0;
+        for (int t = 0; lane + 32 * t < m; ++t) {
+            const uint64_t mine = cand[lane + 32 * t];
+            int rank = 0;
+            for (int o = 0; o < m; ++o) rank += cand[o] < mine;   // composites are unique
+            if (rank < k) selm |= 1u << t;
+        }
+    }
+    // emit the k selected offsets in ascending j: rank among the selected by j
+    __syncwarp();
+    uint32_t *sel_j = reinterpret_cast<uint32_t *>(buf);   // the item's buffer is free now
+    const int cs = __popc(selm);
+    int w0 = warp_incl_scan(cs) - cs;
+    for (int t = 0; t < 16; ++t)
+        if (selm >> t & 1) sel_j[w0++] = (uint32_t)cand[lane + 32 * t];
+    __threadfence_block();
+    __syncwarp();
+    for (int t = 0; t < 16; ++t)
+        if (selm >> t & 1) {
+            const uint32_t j = (uint32_t)cand[lane + 32 * t];
+            int rank = 0;
+            for (int o = 0; o < k; ++o) rank += ((volatile uint32_t *)sel_j)[o] < j;
+            emit_edge(hd, itm, rank, (int64_t)j);
+        }
+    __syncwarp();
+}
+
+// Sampling of one hop, part 1: the selection items (d > k, queued by phase_count):
+// heavy items as chunk tasks first (largest work first), then one warp per item;
+// both fetched dynamically.  cand: kSelCap slots of this warp in shared memory.
 __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
 {
-    const int warps = blockDim.x >> 5;
-    const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
+    const int lane = lane_id();
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
     const int32_t *const pos = hd.pos;
     uint32_t *const bitmap = hd.bitmap;
     const uint64_t *const selq = hd.selq;
+    (void)bid;
+    (void)nb;
+    // ---- heavy chunk tasks
+    const uint32_t ntask = min(*(const volatile uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), (uint32_t)kMaxHeavyTasks);
+    uint32_t *hnext = (uint32_t *)(hd.meta + kMetaHeavyNext + hd.h);
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(hnext, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntask) break;
+        const uint32_t task = hd.heavyq[t];
+        if (task != 0xFFFFFFFFu) heavy_task(g, hd, task, seed_lo, seed_hi, cand);
+    }
     // ---- selections (d > k): warp per item
     const int64_t nsel = *(const volatile uint32_t *)(hd.meta + kMetaSel + hd.h);
-    for (int64_t w = gw; w < nsel; w += nw) {
+    uint32_t *snext = (uint32_t *)(hd.meta + kMetaSelNext + hd.h);
+    for (;;) {
+        uint32_t wi = 0;
+        if (lane == 0) wi = atomicAdd(snext, 1u);
+        wi = __shfl_sync(0xffffffffu, wi, 0);
+        if ((int64_t)wi >= nsel) break;
+        const int64_t w = wi;
         const uint64_t e = selq[w];
         const int r = (int)(e >> 32);
         const int64_t i = (int64_t)(e & 0xFFFFFFFFu);

@@ -347,3 +347,17 @@ def test_c2_bundles_of_4_on_2_lanes(c2):
             b.free()
     finally:
         ctx.set_pipeline(1, 1)
+
+
+def test_c3_heavy_items_split_and_not():
+    """Hubs (d > 2048) are split into chunk tasks over several warps when k <= 48 and take
+    the one-warp paths otherwise; both bit-exact (k = 48 / 49 / 1 / 5 on C3's hubs)."""
+    cfg = synth.config("C3")
+    g = synth.build_host_graph(cfg)
+    rows = {0: synth.host_features(cfg, 0)}
+    ctx = _ctx(g)
+    deg = np.diff(g.indptr[0])
+    hubs = np.argsort(deg)[-40:].astype(np.int64)          # the 40 largest in-degrees
+    for fo in ([[48]], [[49]], [[1], [2]], [[5], [48], [3]]):
+        run_and_compare(ctx, g, cfg, hubs, fo, 4242, rows)
+    ctx.close()
