@@ -264,15 +264,21 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from collections import deque
 
+    host_t = {"launch": 0.0, "retire": 0.0}
+
     def run(lo, hi, seeds, on_retire):
         """Launch batches lo..hi-1 in bundles, keeping `depth` launches in flight."""
         q = deque()
         for b0 in range(lo, hi, args.bundle):
+            t0 = time.perf_counter()
             q.append(launch(b0, min(hi, b0 + args.bundle), seeds))
+            host_t["launch"] += time.perf_counter() - t0
             if len(q) >= args.depth:
                 for bl in q.popleft():
+                    t0 = time.perf_counter()
                     on_retire(bl)
                     bl.free()
+                    host_t["retire"] += time.perf_counter() - t0
         while q:
             for bl in q.popleft():
                 on_retire(bl)
@@ -300,7 +306,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
         ev0.record(stream)
+        host_t["launch"] = host_t["retire"] = 0.0
         run(W, steps, seeds_dev, count)
+        host_us = {k: 1e6 * v / K for k, v in host_t.items()}
         edges, gbytes = acc["edges"], acc["gbytes"]
         ev1.record(stream)
         torch.cuda.synchronize(dev)
@@ -440,7 +448,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "sampled_edges_per_batch": edges / (world * K),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
-                "pipeline_depth": args.depth, "bundle": args.bundle, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+                "pipeline_depth": args.depth, "bundle": args.bundle, "host_us_per_batch": host_us, "host": {"cores": host_cores(), "cpu": cpu_model()}}
         emit(args, line)
     ctx.close()
     del shard
