@@ -257,10 +257,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                                  async_=True)
 
     def retire(bl):
-        bl.wait()
-        e = bl.nnz()
-        rows = [bl.n_inputs(u) for u in range(cfg.n_vt)]
-        return e, rows
+        return bl.stats()      # waits for the batch; one call
 
     from collections import deque
 

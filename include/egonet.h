@@ -156,6 +156,10 @@ EG_API eg_status eg_sample_blocks(eg_ctx *ctx, const int64_t *seeds, int64_t n_s
 #define EG_FEATURES 1   /* also gather the input vertices' feature rows (library-owned) */
 #define EG_ASYNC 2      /* return right after enqueueing; sizes are resolved by eg_blocks_wait */
 
+/* Seeds buffers passed to the sampling calls are read in place when they are device
+ * memory or pinned host memory (so they must stay unchanged until the batch is resolved)
+ * and copied when they are pageable host memory. */
+
 /* One whole mini-batch as ONE CUDA-graph launch: sampling + compaction of every hop
  * and, with EG_FEATURES, the feature gather of the input vertices into buffers the
  * blocks handle owns (eg_blocks_features).  Same semantics and errors as
@@ -185,6 +189,11 @@ EG_API eg_status eg_set_pipeline(eg_ctx *ctx, int32_t depth, int32_t bundle);
 EG_API eg_status eg_sample_bundle(eg_ctx *ctx, int32_t n_batches, const int64_t *const *seeds,
                                   const int64_t *n_seeds, int32_t n_hops, const int32_t *fanouts,
                                   const uint64_t *rng_seeds, int32_t flags, eg_blocks **out);
+
+/* Totals of a batch (waits if pending): sampled edges over all hops and relations, and
+ * the input vertices (src nodes of the last block) per type (n_inputs: host [n_vt]);
+ * either may be NULL. */
+EG_API eg_status eg_blocks_stats(const eg_blocks *blocks, int64_t *total_edges, int64_t *n_inputs);
 
 /* Wait for an EG_ASYNC batch; returns its status (EG_ERANGE / EG_EINVAL for bad seeds). */
 EG_API eg_status eg_blocks_wait(eg_blocks *blocks);

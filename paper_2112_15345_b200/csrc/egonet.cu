@@ -775,7 +775,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         return o;
     };
     p->o_meta = take(sizeof(int32_t) * kMetaSize);
-    p->o_dyn = take(sizeof(uint64_t) * 2);
+    p->o_dyn = take(sizeof(uint64_t) * 4);
     p->o_seeds = take(sizeof(int64_t) * n_cap);
     for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
     for (int h = 0; h < L; ++h)
@@ -896,7 +896,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     for (int b = 0; b < B; ++b) {
         char *base = p->batch_base(sl->mem, b);
-        cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + 2 * b, sizeof(uint64_t) * 2, cudaMemcpyHostToDevice, cs);
+        cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + 4 * b, sizeof(uint64_t) * 4, cudaMemcpyHostToDevice, cs);
         cudaMemsetAsync(base + p->o_meta, 0, sizeof(int32_t) * kMetaSize, cs);
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
@@ -948,7 +948,7 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
         return fail(c, EG_ENOMEM, std::string("batch slot cudaMalloc: ") + cudaGetErrorString(e));
     }
     EG_CUDA(c, cudaMallocHost(&sl->h_meta, sizeof(int32_t) * kMetaSize * p->B));
-    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 2 * p->B));
+    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 4 * p->B));
     EG_CUDA(c, cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming));
     EG_CUDA(c, cudaEventCreate(&sl->s0));
     EG_CUDA(c, cudaEventCreate(&sl->s1));
@@ -1093,11 +1093,25 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
     EG_CUDA(c, cudaStreamWaitEvent(ln.stream, ln.ready, 0));
     for (int b = 0; b < B; ++b) {
         const int64_t n = b < nb ? n_seeds[b] : 0;
-        if (n > 0)
-            EG_CUDA(c, cudaMemcpyAsync(p->batch_base(sl->mem, b) + p->o_seeds, seeds[b], sizeof(int64_t) * n,
-                                       cudaMemcpyDefault, ln.stream));
-        sl->h_dyn[2 * b] = b < nb ? rng_seeds[b] : 0;
-        sl->h_dyn[2 * b + 1] = (uint64_t)n;
+        uint64_t direct = 0;
+        if (n > 0) {
+            // device memory (or pinned host memory, read over PCIe): the seed split reads the
+            // caller's buffer in place; pageable host memory is staged into the slot
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, seeds[b]) == cudaSuccess &&
+                (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ||
+                 (at.type == cudaMemoryTypeHost && at.devicePointer)))
+                direct = (uint64_t)(uintptr_t)(at.type == cudaMemoryTypeHost ? at.devicePointer : seeds[b]);
+            else {
+                cudaGetLastError();
+                EG_CUDA(c, cudaMemcpyAsync(p->batch_base(sl->mem, b) + p->o_seeds, seeds[b], sizeof(int64_t) * n,
+                                           cudaMemcpyDefault, ln.stream));
+            }
+        }
+        sl->h_dyn[4 * b] = b < nb ? rng_seeds[b] : 0;
+        sl->h_dyn[4 * b + 1] = (uint64_t)n;
+        sl->h_dyn[4 * b + 2] = direct;
+        sl->h_dyn[4 * b + 3] = 0;
     }
     sl->timed = c->prof;
     sl->finished = false;
@@ -1157,6 +1171,23 @@ eg_status eg_sample_bundle(eg_ctx *c, int32_t n_batches, const int64_t *const *s
             return first;
         }
     }
+    return EG_OK;
+}
+
+eg_status eg_blocks_stats(const eg_blocks *cb, int64_t *total_edges, int64_t *n_inputs)
+{
+    if (!cb) return EG_EINVAL;
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    eg_status st = finish(b);
+    if (st) return st;
+    if (total_edges) {
+        int64_t e = 0;
+        for (int h = 0; h < b->n_hops; ++h)
+            for (int r = 0; r < b->n_rel; ++r) e += b->nnz[h][r];
+        *total_edges = e;
+    }
+    if (n_inputs)
+        for (int u = 0; u < b->n_vt; ++u) n_inputs[u] = b->n_nodes[b->n_hops][u];
     return EG_OK;
 }
 

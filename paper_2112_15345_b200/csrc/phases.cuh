@@ -23,8 +23,10 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 
 // Seeds (caller order, mixed types) -> F_0[u] (stable per type) + pos[] for the
 // dst-prefix relabel; flags out-of-range and duplicate seeds.  One block.
-__device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ seeds)
+__device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds)
 {
+    // the caller's buffer when it is device-accessible, else the slot's staged copy
+    const int64_t *__restrict__ seeds = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : slot_seeds;
     __shared__ int32_t wcnt[32][EG_MAX_VT];   // per warp, per type: count, then exclusive offset
     __shared__ int32_t base[EG_MAX_VT];
     // pointers hoisted into registers: HopDev lives in global memory and every store

@@ -29,6 +29,7 @@ ABI_SYMBOLS = [
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
+    "eg_blocks_stats",
 ]
 
 EG_FEATURES = 1
@@ -134,6 +135,7 @@ def lib(build_if_missing: bool = True):
         L.eg_block_view_get.argtypes = [vp, c.c_int32, P(BlockView)]
         L.eg_sample_minibatch.argtypes = [vp, vp, c.c_int64, c.c_int32, vp, c.c_uint64, c.c_int32, P(vp)]
         L.eg_blocks_wait.argtypes = [vp]
+        L.eg_blocks_stats.argtypes = [vp, P(c.c_int64), vp]
         L.eg_blocks_features.argtypes = [vp, c.c_int32, P(vp), P(c.c_int64), P(c.c_int64)]
         L.eg_blocks_n_hops.argtypes = [vp]
         L.eg_blocks_n_hops.restype = c.c_int32
@@ -273,6 +275,15 @@ class Blocks:
 
     def __len__(self):
         return self.n_hops
+
+    def stats(self):
+        """(total sampled edges, [input vertices per type]) in one call (waits if pending)."""
+        e = ctypes.c_int64()
+        n = np.zeros(EG_MAX_VT, np.int64)
+        rc = lib().eg_blocks_stats(self._h, ctypes.byref(e), n.ctypes.data)
+        if rc:
+            raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        return int(e.value), [int(x) for x in n[:len(self._ctx.vt_counts)]]
 
     def nnz(self, h=None) -> int:
         vs = self.views

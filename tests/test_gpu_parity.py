@@ -223,7 +223,8 @@ def test_c1_async_error_reported_at_wait(c1):
     from paper_2112_15345_b200 import EgError
     import torch
     cfg, g, rows, ctx = c1
-    b = ctx.sample_minibatch(torch.tensor([3, 99999], device="cuda:0"), cfg.fanouts, 1, async_=True)
+    bad = torch.tensor([3, 99999], device="cuda:0")
+    b = ctx.sample_minibatch(bad, cfg.fanouts, 1, async_=True)
     with pytest.raises(EgError) as e:
         b.wait()
     assert e.value.code == -2
@@ -326,18 +327,17 @@ def test_c2_bundles_of_4_on_2_lanes(c2):
             seeds[1] = seeds[1][:100] if rnd == 1 else seeds[1]
             seeds[2] = seeds[2][:0] if rnd == 2 else seeds[2]
             rs = [synth.rng_seed(cfg, i) for i in idx]
-            bls = ctx.sample_bundle([torch.from_numpy(s).cuda() for s in seeds], cfg.fanouts, rs, features=True,
-                                    async_=(rnd != 0))
+            dev = [torch.from_numpy(s).cuda() for s in seeds]   # read in place: keep alive until resolved
+            bls = ctx.sample_bundle(dev, cfg.fanouts, rs, features=True, async_=(rnd != 0))
             for s, r, b in zip(seeds, rs, bls):
                 res = oracle.sample(g, s, cfg.fanouts, r)
                 assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
                 assert_same_features(res, _features_of(b, cfg), cfg, rows)
                 b.free()
         # a partial bundle (3 of 4) and a bad batch inside an async bundle
-        bls = ctx.sample_bundle([torch.from_numpy(synth.batch_seeds(cfg, 90)).cuda(),
-                                 torch.tensor([1, 99999999], device="cuda:0"),
-                                 torch.from_numpy(synth.batch_seeds(cfg, 91)).cuda()], cfg.fanouts, [5, 6, 7],
-                                async_=True)
+        dev = [torch.from_numpy(synth.batch_seeds(cfg, 90)).cuda(), torch.tensor([1, 99999999], device="cuda:0"),
+               torch.from_numpy(synth.batch_seeds(cfg, 91)).cuda()]
+        bls = ctx.sample_bundle(dev, cfg.fanouts, [5, 6, 7], async_=True)
         from paper_2112_15345_b200 import EgError
         with pytest.raises(EgError):
             bls[1].wait()
