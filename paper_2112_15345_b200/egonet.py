@@ -239,10 +239,10 @@ class Blocks:
     use (waiting for an EG_ASYNC batch); per-hop tensors are zero-copy views of
     library memory built lazily."""
 
-    def __init__(self, ctx: "Context", handle: int):
+    def __init__(self, ctx: "Context", handle: int, n_hops: int | None = None):
         self._ctx = ctx
         self._h = handle
-        self.n_hops = lib().eg_blocks_n_hops(handle)
+        self.n_hops = lib().eg_blocks_n_hops(handle) if n_hops is None else n_hops
         self._views = None
         self._blocks = [None] * self.n_hops
 
@@ -474,7 +474,8 @@ class Context:
         self._check(lib().eg_sample_bundle(self._h, n, ctypes.cast(ptrs, ctypes.c_void_p), cnts.ctypes.data,
                                            fo.shape[0], fo.ctypes.data, rs.ctypes.data, flags,
                                            ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_bundle")
-        return [Blocks(self, outs[i]) for i in range(n)]
+        L = fo.shape[0]
+        return [Blocks(self, outs[i], L) for i in range(n)]
 
     def gather_features(self, blocks: Blocks, out=None, types=None):
         """Feature rows of the input vertices per type (None for types without
