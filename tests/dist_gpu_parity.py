@@ -57,6 +57,21 @@ def main():
             assert_same_features(res, outs, cfg, rows)
         bl.free()
         ok += 1
+    # pipelined, bundled launches (the bench's mode) read the same peer shards
+    ctx.set_pipeline(2, 4)
+    gis = [1000 + (b * world + rank) for b in range(8)]
+    dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).cuda() for gi in gis]
+    launches = [ctx.sample_bundle(dev[i:i + 4], cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis[i:i + 4]],
+                                  features=True, async_=True) for i in (0, 4)]
+    for li, bls in enumerate(launches):
+        for j, bl in enumerate(bls):
+            gi = gis[4 * li + j]
+            res = oracle.sample(g, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi))
+            assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, [bl.features(u) if u in cfg.feats else None for u in range(cfg.n_vt)], cfg,
+                                 rows)
+            bl.free()
+            ok += 1
     t = torch.tensor([ok], device="cuda")
     dist.all_reduce(t)
     if rank == 0:
