@@ -106,6 +106,10 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
     const int per = (kSMs * 8 + B - 1) / B;
     const int wide = kScanBlocks * g.n_rel;        // count / scan: one block per virtual block
     const int samp = (kSMs * 4 + B - 1) / B;
+    // bitmap chunks: at most about two waves of blocks in total; blocks loop over chunks
+    // (a 111M-vertex graph has 3.4k chunks: one block each would be 27k blocks per bundle)
+    const int chunk_blocks = n_chunks < (kSMs * 16 + B - 1) / B ? n_chunks : (kSMs * 16 + B - 1) / B;
+    const int emit_blocks = n_chunks < (kSMs * 4 + B - 1) / B ? n_chunks : (kSMs * 4 + B - 1) / B;
     int nk = 0;
     k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
     ++nk;
@@ -125,8 +129,8 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
-        k_bitcount<<<dim3(n_chunks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_emit<<<dim3(n_chunks, B), kChunkWords, 0, s>>>(g, bd_dev, h);
+        k_bitcount<<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        k_emit<<<dim3(emit_blocks, B), kChunkWords, 0, s>>>(g, bd_dev, h);
         nk += 6;
     }
     k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
