@@ -1,6 +1,6 @@
 // batch.cu -- the sampling + compaction of a bundle of mini-batches, one kernel per phase.
 //
-//   seed_split | for h: count(+relabel h-1) | scan | sample | bitcount | emit | ... | relabel | reset
+//   seed_split | for h: count(+relabel h-1) | scan | select+copy+tiny | bitcount | cscan | emit | ... | relabel | reset
 //
 // Every phase kernel runs with grid.y = the batch of the bundle (each batch has its own
 // HopDev / compaction state), so B mini-batches cost about what one does: at batch ~1k
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev 
 __global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 6 * h);
+    stamp(bd, 1 + 8 * h);
     phase_count(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
     if (h > 0) phase_relabel(g, bd->hop[blockIdx.y][h - 1], blockIdx.x, gridDim.x);
 }
@@ -52,64 +52,89 @@ __global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__
 __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 2 + 6 * h);
-    phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, (bd->n_chunks + kGroupChunks - 1) / kGroupChunks);
+    stamp(bd, 2 + 8 * h);
+    phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads, 3) k_select(const __grid_constant__ GraphDev g,
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
-    stamp(bd, 3 + 6 * h);
+    stamp(bd, 3 + 8 * h);
     phase_select(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
 }
 
 __global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 4 + 6 * h);
+    stamp(bd, 4 + 8 * h);
     phase_copy(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
+__global__ void __launch_bounds__(kBatchThreads) k_tiny(const __grid_constant__ GraphDev g,
+                                                        const BatchDev *__restrict__ bd, int h)
+{
+    stamp(bd, 5 + 8 * h);
+    phase_tiny(g, bd->hop[blockIdx.y][h]);
+}
+
+template <bool kSparse>
 __global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
                                                             const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 5 + 6 * h);
-    phase_bitcount(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+    stamp(bd, 6 + 8 * h);
+    if (kSparse)
+        phase_bitcount_sparse(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+    else
+        phase_bitcount_dense(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
-__global__ void __launch_bounds__(kChunkWords, 2) k_emit(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(1024) k_cscan(const __grid_constant__ GraphDev g,
+                                                 const BatchDev *__restrict__ bd, int h)
+{
+    stamp(bd, 7 + 8 * h);
+    phase_chunk_scan(g, bd->hop[blockIdx.y][h]);
+}
+
+template <bool kSparse>
+__global__ void __launch_bounds__(kBatchThreads) k_emit(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 6 + 6 * h);
-    phase_emit(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+    stamp(bd, 8 + 8 * h);
+    if (kSparse)
+        phase_emit_sparse(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+    else
+        phase_emit_dense(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_relabel(const __grid_constant__ GraphDev g,
                                                            const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 6 * bd->n_hops);
+    stamp(bd, 1 + 8 * bd->n_hops);
     phase_relabel(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd)
 {
-    stamp(bd, 2 + 6 * bd->n_hops);
+    stamp(bd, 2 + 8 * bd->n_hops);
     phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
 }
 
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial)
+                 const Fork &fk, bool serial, int compact)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
     const int wide = kScanBlocks * g.n_rel;        // count / scan: one block per virtual block
     const int samp = (kSMs * 4 + B - 1) / B;
-    // bitmap chunks: at most about two waves of blocks in total; blocks loop over chunks
-    // (a 111M-vertex graph has 3.4k chunks: one block each would be 27k blocks per bundle)
-    const int chunk_blocks = n_chunks < (kSMs * 16 + B - 1) / B ? n_chunks : (kSMs * 16 + B - 1) / B;
-    const int emit_blocks = n_chunks < (kSMs * 4 + B - 1) / B ? n_chunks : (kSMs * 4 + B - 1) / B;
+    // bitmap chunks: at most one resident wave in total (8 blocks of 256 threads per SM);
+    // blocks loop.  Dense variant: a block per chunk; sparse (a 111M-vertex graph has
+    // 3.4k chunks per batch): a warp per half chunk.
+    const bool sparse = compact == 2 || (compact == 0 && n_chunks > kSparseChunks);
+    const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
+    const int chunk_cap = (kSMs * 8 + B - 1) / B;
+    const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
     int nk = 0;
     k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
     ++nk;
@@ -121,17 +146,26 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
         if (serial) {
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             k_copy<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+            k_tiny<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         } else {
             cudaEventRecord(fk.fork, s);
             cudaStreamWaitEvent(fk.side, fk.fork, 0);
             k_copy<<<dim3(per, B), kBatchThreads, 0, fk.side>>>(g, bd_dev, h);
+            k_tiny<<<dim3(per, B), kBatchThreads, 0, fk.side>>>(g, bd_dev, h);
             cudaEventRecord(fk.join, fk.side);
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
-        k_bitcount<<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_emit<<<dim3(emit_blocks, B), kChunkWords, 0, s>>>(g, bd_dev, h);
-        nk += 6;
+        if (sparse)
+            k_bitcount<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        else
+            k_bitcount<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        k_cscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
+        if (sparse)
+            k_emit<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        else
+            k_emit<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        nk += 8;
     }
     k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
     k_reset<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);

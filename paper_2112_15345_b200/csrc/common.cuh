@@ -10,11 +10,12 @@ namespace eg {
 
 constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
-constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one CTA)
+constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one block)
 constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
 constexpr int kScanBlocks = 64;           // virtual blocks per relation in the two-phase scan
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
+constexpr int kTinyD = 32;                // selections with d <= this: 8 lanes per item
 // Heavy items (d > kHeavyD, k <= kHeavyMaxK) are split into tasks of kHeavyChunk keys
 // sampled by different warps; their candidates meet in a per-item buffer.
 constexpr int kHeavyD = 2048;
@@ -59,9 +60,11 @@ constexpr int kMetaSelNext = kMetaSel + EG_MAX_HOPS;             // dynamic fetc
 constexpr int kMetaHeavy = kMetaSelNext + EG_MAX_HOPS;           // heavy items per hop
 constexpr int kMetaHeavyQ = kMetaHeavy + EG_MAX_HOPS;            // heavy tasks per hop
 constexpr int kMetaHeavyNext = kMetaHeavyQ + EG_MAX_HOPS;        // dynamic fetch counter per hop
-constexpr int kMetaErr = kMetaHeavyNext + EG_MAX_HOPS;
+constexpr int kMetaTiny = kMetaHeavyNext + EG_MAX_HOPS;         // tiny selection items per hop
+constexpr int kMetaTinyNext = kMetaTiny + EG_MAX_HOPS;            // dynamic fetch counter per hop
+constexpr int kMetaErr = kMetaTinyNext + EG_MAX_HOPS;
 constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase timestamps (tracing)
-constexpr int kMaxStamps = 64;
+constexpr int kMaxStamps = 80;
 constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
 
 // Everything a hop's kernels touch.
@@ -78,12 +81,15 @@ struct HopDev {
     int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
     uint32_t *bitmap;                // this hop's marks: every sampled source (A)
     uint32_t *members;               // vertices already in the batch (M); new = A & ~M
-    int32_t *chunk_cnt;              // popcount per bitmap chunk
-    int32_t *chunk_pre;              // sums of groups of kGroupChunks chunks
+    uint32_t *summary;               // bit w of the summary = A word w may be nonzero
+    int32_t *chunk_cnt;              // new vertices per bitmap chunk
+    int32_t *seg_cnt;                // new vertices per slice (16 bitmap words)
+    int32_t *chunk_pre;              // new vertices in the chunks before, within the type
     int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
     int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
-    uint64_t *selq;                  // items that need a selection: (r << 32) | i
+    uint64_t *selq;                  // items that need a selection: (r << 32) | i; tiny ones from the top
+    int32_t selq_cap;                // slots of selq
     uint64_t *heavy_items;           // [kMaxHeavy] (r << 32) | i
     uint32_t *heavy_cnt;             // [kMaxHeavy] candidates found
     uint32_t *heavy_done;            // [kMaxHeavy] finished tasks

@@ -65,7 +65,9 @@ struct BatchState {
     int32_t *pos = nullptr;
     uint32_t *bitmap = nullptr;
     uint32_t *members = nullptr;
+    uint32_t *summary = nullptr;
     int32_t *chunk_cnt = nullptr;
+    int32_t *seg_cnt = nullptr;
     int32_t *chunk_pre = nullptr;
     int32_t *partial = nullptr;
 };
@@ -100,6 +102,7 @@ struct Plan {
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_selq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
+    int64_t selq_items[EG_MAX_HOPS] = {};
     size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
@@ -157,6 +160,7 @@ struct eg_ctx {
     cudaStream_t cap_stream = nullptr;
     Fork fork{};                          // capture side stream + events (graph branches)
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
+    int compact = 0;                      // EG_COMPACT at create: 0 by size, 1 dense, 2 sparse
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
@@ -333,7 +337,11 @@ eg_status alloc_state(eg_ctx *c, BatchState *st)
     EG_CUDA(c, cudaMemset(st->bitmap, 0, sizeof(uint32_t) * words));
     EG_CUDA(c, cudaMalloc(&st->members, sizeof(uint32_t) * words));
     EG_CUDA(c, cudaMemset(st->members, 0, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMalloc(&st->summary, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
+    EG_CUDA(c, cudaMemset(st->summary, 0, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
     EG_CUDA(c, cudaMalloc(&st->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
+    EG_CUDA(c, cudaMemset(st->chunk_cnt, 0, sizeof(int32_t) * std::max(1, c->n_chunks)));   // accumulated
+    EG_CUDA(c, cudaMalloc(&st->seg_cnt, sizeof(int32_t) * std::max(1, c->n_chunks) * (kChunkWords / 16)));
     EG_CUDA(c, cudaMalloc(&st->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
     EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
     return EG_OK;
@@ -508,6 +516,9 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
     {
         const char *tr = getenv("EG_TRACE");
         c->trace = tr && tr[0] == '1';
+        // EG_COMPACT=dense|sparse forces a compaction variant (tests); default by graph size
+        const char *cm = getenv("EG_COMPACT");
+        c->compact = !cm ? 0 : (cm[0] == 'd' ? 1 : (cm[0] == 's' ? 2 : 0));
     }
     if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->fork.side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -791,6 +802,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
     for (int h = 0; h < L; ++h) {
         int64_t items = 0;
         for (int r = 0; r < R; ++r) items += p->capF[h][dst_vt[r]];
+        p->selq_items[h] = items;
         p->o_selq[h] = take(sizeof(uint64_t) * items);
         p->o_heavy[h] = take(kHeavyBytes);
     }
@@ -845,7 +857,9 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.pos = st.pos;
         hd.bitmap = st.bitmap;
         hd.members = st.members;
+        hd.summary = st.summary;
         hd.chunk_cnt = st.chunk_cnt;
+        hd.seg_cnt = st.seg_cnt;
         hd.chunk_pre = st.chunk_pre;
         for (int u = 0; u < V; ++u) {
             hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
@@ -865,6 +879,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
                 x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
             }
             x.selq = (uint64_t *)(base + p->o_selq[h]);
+            x.selq_cap = (int32_t)p->selq_items[h];
             char *hv = base + p->o_heavy[h];
             x.heavy_items = (uint64_t *)hv;
             x.heavy_cnt = (uint32_t *)(hv + sizeof(uint64_t) * kMaxHeavy);
@@ -901,7 +916,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork, c->trace);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork, c->trace,
+                       c->compact);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -1009,11 +1025,11 @@ void slot_finished(eg_ctx *c, Slot *sl)
         c->prof_n[1] += 1;
     }
     if (c->trace) {
-        // in-kernel phase stamps of batch 0: seed, per hop count/scan/sample/bitcount/emit, relabel, reset
+        // in-kernel phase stamps of batch 0: seed, per hop count/scan/select/copy/tiny/bitcount/cscan/emit, relabel, reset
         const uint64_t *st = reinterpret_cast<const uint64_t *>(sl->h_meta + kMetaStamps);
         std::vector<std::string> names = {"k.seed"};
         for (int h = 0; h < sl->plan->n_hops; ++h)
-            for (const char *x : {"count", "scan", "select", "copy", "bitcount", "emit"})
+            for (const char *x : {"count", "scan", "select", "copy", "tiny", "bitcount", "cscan", "emit"})
                 names.push_back("k.h" + std::to_string(h) + "." + x);
         names.push_back("k.relabel");
         for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
@@ -1367,7 +1383,9 @@ eg_status eg_destroy(eg_ctx *c)
             cudaFree(bs.pos);
             cudaFree(bs.bitmap);
             cudaFree(bs.members);
+            cudaFree(bs.summary);
             cudaFree(bs.chunk_cnt);
+            cudaFree(bs.seg_cnt);
             cudaFree(bs.chunk_pre);
             cudaFree(bs.partial);
         }

@@ -97,8 +97,6 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
 {
     __shared__ int32_t sh[33];
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
-    if (bid == 0 && threadIdx.x < g.n_vt)   // S_h starts as F_h; emit adds the new ones
-        meta_nodes(hd.meta, hd.h + 1)[threadIdx.x] = nF[threadIdx.x];
     for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
         const int r = vb / kScanBlocks, b = vb % kScanBlocks;
         const RelDev &R = g.rel[r];
@@ -113,10 +111,12 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
         int32_t *const bip = hd.indptr[r];
         uint64_t *const selq = hd.selq;
         uint32_t *const selc = (uint32_t *)(hd.meta + kMetaSel + hd.h);
+        uint32_t *const tinyc = (uint32_t *)(hd.meta + kMetaTiny + hd.h);
         int32_t sum = 0;
         for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {   // block-uniform trip count
             const int64_t i = t0 + threadIdx.x;
             bool sel = false;
+            int64_t dd = 0;
             if (i < hi) {
                 int32_t c = 0;
                 if (k != 0) {
@@ -128,6 +128,7 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
                     const bool all = (k < 0 || d <= k);
                     c = (int32_t)(all ? d : k);
                     sel = !all;
+                    dd = d;
                     ibase[i] = ((int64_t)p << 56) | b0;
                     ideg[i] = (int32_t)d;
                 }
@@ -153,12 +154,20 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
                     }
                 }
             }
-            const uint32_t m = __ballot_sync(0xffffffffu, sel);
+            const bool tiny = sel && dd <= kTinyD;   // 8 lanes per item (phase_tiny)
+            const uint32_t m = __ballot_sync(0xffffffffu, sel && !tiny);
             if (m) {
                 uint32_t q = 0;
                 if (lane_id() == 0) q = atomicAdd(selc, (uint32_t)__popc(m));
                 q = __shfl_sync(0xffffffffu, q, 0);
-                if (sel) selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
+                if (sel && !tiny) selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
+            }
+            const uint32_t mt = __ballot_sync(0xffffffffu, tiny);
+            if (mt) {
+                uint32_t q = 0;
+                if (lane_id() == 0) q = atomicAdd(tinyc, (uint32_t)__popc(mt));
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (tiny) selq[hd.selq_cap - 1 - (q + __popc(mt & lanemask_lt()))] = ((uint64_t)r << 32) | (uint64_t)i;
             }
         }
         sum = block_sum(sum, sh);
@@ -166,13 +175,10 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
     }
 }
 
-// Exclusive scan of the counts in place -> block indptr; nnz(h, r).  Also clears the
-// chunk-group sums used by this hop's compaction.
-__device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_groups)
+// Exclusive scan of the counts in place -> block indptr; nnz(h, r).
+__device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
     __shared__ int32_t sh[33];
-    if (bid == 0)
-        for (int i = threadIdx.x; i < n_groups; i += blockDim.x) hd.chunk_pre[i] = 0;
     for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
         const int r = vb / kScanBlocks, b = vb % kScanBlocks;
         const int t = g.rel[r].dst_vt;
@@ -204,6 +210,7 @@ __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb,
 struct Item {
     const int32_t *pos;     // the batch's gid -> position map (read only here)
     uint32_t *bitmap;       // the batch's new-vertex bitmap
+    uint32_t *summary;      // and its summary (one bit per bitmap word)
     int64_t bit_base;       // boff[s(r)] - off[s(r)]: bitmap bit of gid = bit_base + gid
     uint32_t soff;          // off[s(r)]
     int64_t ebase;          // global CSC position of this dst's first edge
@@ -216,10 +223,15 @@ struct Item {
 // sampling).  Fire-and-forget RED.OR, no load: sources already in the batch are
 // cleared from the bitmap by phase_bitcount (one check per unique source instead of
 // a dependent pos[] load per sampled edge).
-__device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t gid, int64_t bit_base)
+//
+// The summary bit of the word is set too, so that the compaction visits only the words
+// that hold marks: at hop 2 of a 111M-vertex graph a batch marks ~1% of the words.
+__device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t *summary, uint32_t gid, int64_t bit_base)
 {
     const int64_t bit = bit_base + gid;
-    atomicOr(bitmap + (bit >> 5), 1u << (bit & 31));   // result unused: RED
+    const int64_t w = bit >> 5;
+    atomicOr(bitmap + w, 1u << (bit & 31));   // results unused: RED
+    atomicOr(summary + (w >> 5), 1u << (w & 31));
 }
 
 __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_t slot, int64_t j)
@@ -227,7 +239,7 @@ __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_
     const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
     it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
-    mark_src(it.bitmap, gid, it.bit_base);
+    mark_src(it.bitmap, it.summary, gid, it.bit_base);
 }
 
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
@@ -526,6 +538,7 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
     Item itm;
     itm.pos = hd.pos;
     itm.bitmap = hd.bitmap;
+    itm.summary = hd.summary;
     itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
     itm.soff = (uint32_t)g.off[R.src_vt];
     itm.ebase = R.edge_base[p] + base0;
@@ -656,6 +669,7 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
         Item itm;
         itm.pos = pos;
         itm.bitmap = bitmap;
+        itm.summary = hd.summary;
         itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
         itm.soff = (uint32_t)g.off[R.src_vt];
         itm.ebase = R.edge_base[p] + base;
@@ -673,6 +687,124 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
     }
 }
 
+// Selections of tiny items (k < d <= kTinyD): 8 lanes per item, 4 items per warp.  The
+// same register radix select as select_small, with the sums taken over the 8 lanes of
+// the item; all groups step together (finished groups idle).
+__device__ void phase_tiny(const GraphDev &g, const HopDev &hd)
+{
+    static_assert(kTinyD == 32, "8 lanes x 4 keys");
+    const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
+    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
+    const uint32_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
+    uint32_t *const tnext = (uint32_t *)(hd.meta + kMetaTinyNext + hd.h);
+    for (;;) {
+        uint32_t q0 = 0;
+        if (lane == 0) q0 = atomicAdd(tnext, 4u);
+        q0 = __shfl_sync(0xffffffffu, q0, 0);
+        if (q0 >= ntiny) break;
+        const uint32_t qi = q0 + gi;
+        const bool act = qi < ntiny;
+        Item itm;
+        int k = 0;
+        int32_t d = 0;
+        uint32_t w[4] = {0, 0, 0, 0}, vm = 0;
+        if (act) {
+            const uint64_t e = hd.selq[hd.selq_cap - 1 - qi];
+            const int r = (int)(e >> 32);
+            const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+            const RelDev &R = g.rel[r];
+            const int32_t pos0 = hd.indptr[r][i];
+            const int64_t ib = hd.ibase[r][i];
+            d = hd.ideg[r][i];
+            const int64_t v = hd.nodes[R.dst_vt][i];
+            const int p = (int)(ib >> 56);
+            const int64_t base = ib & ((1ll << 56) - 1);
+            itm.pos = hd.pos;
+            itm.bitmap = hd.bitmap;
+            itm.summary = hd.summary;
+            itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
+            itm.soff = (uint32_t)g.off[R.src_vt];
+            itm.ebase = R.edge_base[p] + base;
+            itm.ix = R.indices[p] + base;
+            itm.src_out = hd.src[r] + pos0;
+            itm.eid_out = hd.eids[r] + pos0;
+            k = hd.fanout[r];
+            if (4 * sl < d) {
+                keys4((uint32_t)sl, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), ((uint32_t)hd.h << 16) | (uint32_t)r,
+                      seed_lo, seed_hi, w);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) vm |= (uint32_t)(4 * sl + t < d) << t;
+            }
+        }
+        uint32_t P = 0;
+        int krem = k, s = 32;
+        bool done = !act;
+        while (__any_sync(0xffffffffu, !done)) {
+            const int b = s - 1;
+            uint32_t c0 = 0, cm = 0;
+            if (!done) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const bool match = (vm >> t & 1) && (s == 32 || (w[t] >> s) == (P >> s));
+                    cm += match;
+                    c0 += match && !((w[t] >> b) & 1u);
+                }
+            }
+            uint32_t pk = cm | (c0 << 16);   // both <= 32
+            pk += __shfl_xor_sync(0xffffffffu, pk, 1);
+            pk += __shfl_xor_sync(0xffffffffu, pk, 2);
+            pk += __shfl_xor_sync(0xffffffffu, pk, 4);
+            if (!done) {
+                cm = pk & 0xFFFFu;
+                c0 = pk >> 16;
+                if ((int)cm == krem) {
+                    done = true;
+                } else {
+                    if (krem > (int)c0) {
+                        krem -= (int)c0;
+                        P |= 1u << b;
+                    }
+                    s = b;
+                    done = (s == 0);
+                }
+            }
+        }
+        uint32_t ltm = 0, eqm = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t hi = s == 32 ? 0u : (w[t] >> s), ph = s == 32 ? 0u : (P >> s);
+            ltm |= (uint32_t)((vm >> t & 1) && hi < ph) << t;
+            eqm |= (uint32_t)((vm >> t & 1) && hi == ph) << t;
+        }
+        // exclusive scans over the 8 lanes of the item (ascending j)
+        auto group_excl = [&](int x) {
+            int y = x;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const int z = __shfl_up_sync(0xffffffffu, y, o, 8);
+                if (sl >= o) y += z;
+            }
+            return y - x;
+        };
+        const int ce = __popc(eqm);
+        int er = group_excl(ce);
+        uint32_t sel = ltm;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (eqm >> t & 1) {
+                if (er < krem) sel |= 1u << t;
+                ++er;
+            }
+        const int cs = __popc(sel);
+        int slot = group_excl(cs);
+        if (act) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (sel >> t & 1) emit_edge(hd, itm, slot++, 4 * sl + t);
+        }
+    }
+}
+
 // Sampling of one hop, part 2: the full-neighbourhood items (d <= k or k = -1) as
 // segmented copies, 32 items per warp, 4 independent load chains per lane.
 __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
@@ -681,6 +813,7 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     uint32_t *const bitmap = hd.bitmap;
+    uint32_t *const summary = hd.summary;
     // ---- full neighbourhoods: segmented copy over groups of 32 items
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
     int64_t cum[EG_MAX_REL + 1];
@@ -757,97 +890,284 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
                 if (dsrc[q]) {
                     *dsrc[q] = gid[q];
                     *deid[q] = eid[q];
-                    mark_src(bitmap, gid[q], bb[q]);
+                    mark_src(bitmap, summary, gid[q], bb[q]);
                 }
         }
     }
 }
 
 // ============================================================================ compaction
+//
+// Work unit: a slice of kLaneWords bitmap words per lane (half a summary word), a warp
+// per 32 slices (half a chunk).  A lane loads only the words whose summary bits are
+// set, four at a time, so a sparse slice (the common case at 10^8 vertices) costs one
+// round of loads and a dense one (10^6 vertices) at most four.
 
-// Popcount of each bitmap chunk (virtual block per chunk, one uint4 per thread) and
-// the sums of groups of kGroupChunks chunks.
-constexpr int kGroupChunks = 256;
+constexpr int kLaneWords = 16;
+constexpr int kSlices = kChunkWords / kLaneWords;     // slices per chunk (64)
+constexpr int kHalves = kSlices / 32;                 // warps per chunk (2)
+static_assert(kHalves == 2, "slice layout");
 
-__device__ void phase_bitcount(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+// Summary bits of slice (c, hc, lane): bit t = word t of the slice may hold marks.
+__device__ __forceinline__ uint32_t slice_bits(const uint32_t *summary, int64_t c, int hc, int lane)
 {
-    static_assert(kChunkWords == 4 * 256, "one uint4 per thread");
-    __shared__ int32_t sh[33];
-    for (int c = bid; c < n_chunks; c += nb) {
-        const int64_t wq = (int64_t)c * (kChunkWords / 4) + threadIdx.x;
-        uint4 *ap = reinterpret_cast<uint4 *>(hd.bitmap) + wq;
-        const uint4 a = __ldcg(ap);
-        int32_t v = 0;
-        if (a.x | a.y | a.z | a.w) {
-            const uint4 m = __ldcg(reinterpret_cast<const uint4 *>(hd.members) + wq);
-            v = __popc(a.x & ~m.x) + __popc(a.y & ~m.y) + __popc(a.z & ~m.z) + __popc(a.w & ~m.w);
-            if (v == 0) *ap = make_uint4(0, 0, 0, 0);   // only members marked: consumed here, emit skips
+    const int sl = hc * 32 + lane;
+    return (__ldcg(summary + c * 32 + (sl >> 1)) >> ((sl & 1) * kLaneWords)) & 0xFFFFu;
+}
+
+// New vertices (A & ~M) per slice and chunk.  Words whose marks are all members are
+// cleared here, so that emit finds only words with new vertices.  chunk_cnt[] is zero
+// on entry (phase_chunk_scan consumes and clears it).
+__device__ void phase_bitcount_sparse(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+{
+    const int lane = lane_id();
+    uint32_t *const bitmap = hd.bitmap;
+    const uint32_t *const members = hd.members;
+    const int64_t n_items = (int64_t)n_chunks * kHalves;
+    const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
+    int64_t it = (int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t bits_next = it < n_items ? slice_bits(hd.summary, it / kHalves, (int)(it % kHalves), lane) : 0u;
+    for (; it < n_items; it += stride) {
+        const int64_t c = it / kHalves;
+        const int hc = (int)(it % kHalves);
+        uint32_t bits = bits_next;
+        if (it + stride < n_items)   // prefetch the next slice's summary
+            bits_next = slice_bits(hd.summary, (it + stride) / kHalves, (int)((it + stride) % kHalves), lane);
+        const int64_t w0 = c * kChunkWords + (hc * 32 + lane) * kLaneWords;
+        int32_t cnt = 0;
+        while (bits) {
+            int t[4];
+            uint32_t a[4], m[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                t[q] = -1;
+                a[q] = m[q] = 0u;
+                if (bits) {
+                    t[q] = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    a[q] = __ldcg(bitmap + w0 + t[q]);
+                    m[q] = __ldcg(members + w0 + t[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t nw = a[q] & ~m[q];
+                cnt += __popc(nw);
+                if (a[q] && !nw) bitmap[w0 + t[q]] = 0u;   // only members marked: consumed here
+            }
         }
-        v = block_sum(v, sh);
-        if (threadIdx.x == 0) {
-            hd.chunk_cnt[c] = v;
-            if (v) atomicAdd(hd.chunk_pre + c / kGroupChunks, v);
+        hd.seg_cnt[c * kSlices + hc * 32 + lane] = cnt;
+        const int32_t total = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)cnt);
+        if (lane == 0 && total) atomicAdd(hd.chunk_cnt + c, total);
+    }
+}
+
+// Exclusive scan of the chunk counts within each vertex type (one 1024-thread block per
+// batch) -> chunk_pre[]; sets |S_h+1[u]| = |F_h[u]| + new[u] and clears chunk_cnt[].
+__device__ void phase_chunk_scan(const GraphDev &g, const HopDev &hd)
+{
+    __shared__ int32_t sh[33];
+    int32_t *const nn = meta_nodes(hd.meta, hd.h + 1);
+    const int32_t *const nF = meta_nodes(hd.meta, hd.h);
+    for (int u = 0; u < g.n_vt; ++u) {
+        const int lo = (int)(g.boff[u] / kChunkBits), hi = (int)(g.boff[u + 1] / kChunkBits);
+        const int per = (hi - lo + (int)blockDim.x - 1) / (int)blockDim.x;
+        const int a = min(hi, lo + (int)threadIdx.x * per), b = min(hi, a + per);
+        int32_t s = 0;
+        for (int c = a; c < b; ++c) s += __ldcg(hd.chunk_cnt + c);
+        int32_t tot;
+        int32_t run = block_excl_scan(s, sh, &tot);
+        for (int c = a; c < b; ++c) {
+            const int32_t v = __ldcg(hd.chunk_cnt + c);
+            hd.chunk_pre[c] = run;
+            hd.chunk_cnt[c] = 0;
+            run += v;
+        }
+        if (threadIdx.x == 0) nn[u] = nF[u] + tot;
+        __syncthreads();   // sh reuse by the next type
+    }
+}
+
+// New vertices of each chunk, in gid order: append to the node array of their type,
+// set pos[], fold them into the members, clear the marks and the summary.  A lane
+// emits its slice's new vertices in ascending gid from its prefix position.
+__device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+{
+    const int lane = lane_id();
+    uint32_t *const bitmap = hd.bitmap;
+    uint32_t *const members = hd.members;
+    int32_t *const pos = hd.pos;
+    const int64_t n_items = (int64_t)n_chunks * kHalves;
+    const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
+    for (int64_t it = (int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5); it < n_items; it += stride) {
+        const int64_t c = it / kHalves;
+        const int hc = (int)(it % kHalves);
+        const int sl = hc * 32 + lane;
+        uint32_t *const sp = hd.summary + c * 32 + (sl >> 1);
+        const uint32_t sw = __ldcg(sp);
+        uint32_t bits = (sw >> ((sl & 1) * kLaneWords)) & 0xFFFFu;
+        if (!__any_sync(0xffffffffu, bits != 0)) continue;
+        __syncwarp();
+        if ((sl & 1) == 0 && sw) *sp = 0u;   // both halves of the word are read (this warp)
+        const int32_t cnt = __ldcg(hd.seg_cnt + c * kSlices + sl);
+        int32_t ex = warp_incl_scan(cnt) - cnt;
+        if (hc) ex += (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)__ldcg(hd.seg_cnt + c * kSlices + lane));
+        if (!bits) continue;
+        const int64_t bit0 = c * kChunkBits;
+        int u = 0;
+        while (bit0 >= g.boff[u + 1]) ++u;
+        int32_t position = meta_nodes(hd.meta, hd.h)[u] + __ldcg(hd.chunk_pre + c) + ex;
+        const int32_t cap = hd.cap_nodes[u];
+        int64_t *const nodes = hd.nodes[u];
+        const int64_t w0 = c * kChunkWords + sl * kLaneWords;
+        const int64_t gid0 = g.off[u] - g.boff[u] + w0 * 32;   // gid of bit b of word w0 + t: gid0 + 32t + b
+        while (bits) {
+            int t[4];
+            uint32_t a[4], m[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                t[q] = -1;
+                a[q] = m[q] = 0u;
+                if (bits) {
+                    t[q] = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    a[q] = __ldcg(bitmap + w0 + t[q]);
+                    m[q] = __ldcg(members + w0 + t[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t word = a[q] & ~m[q];
+                if (a[q]) bitmap[w0 + t[q]] = 0u;
+                if (!word) continue;
+                members[w0 + t[q]] = m[q] | word;   // now members
+                const int64_t gb = gid0 + 32 * t[q];
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    if (position < cap) {
+                        nodes[position] = gb + b;
+                        pos[gb + b] = position;
+                    } else {
+                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                    }
+                    ++position;
+                }
+            }
         }
     }
 }
 
-// number of set bits in chunks [0, c): group sums + the chunks of c's group before it
-__device__ __forceinline__ int32_t bits_before(const HopDev &hd, int c, int32_t *sh)
+// ---- dense variant (graphs of <= kSparseChunks chunks, where a batch marks a large
+// fraction of the words): a block of 8 warps per chunk = 32 units of 32 words (one
+// summary word each); warp w takes units w, w+8, w+16, w+24, one word per lane, so
+// that the emission of a dense word (up to 32 new vertices) is spread over the lanes.
+constexpr int kSparseChunks = 512;
+constexpr int kUnitsPerWarp = kChunkWords / 32 / 8;   // 4 (blockDim.x == 256)
+constexpr int kPrefetch = 8;                          // chunks whose summary words one load fetches
+
+__device__ void phase_bitcount_dense(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
 {
-    const int gi = c / kGroupChunks;
-    int32_t s = 0;
-    for (int j = threadIdx.x; j < gi; j += blockDim.x) s += __ldcg(hd.chunk_pre + j);
-    for (int j = gi * kGroupChunks + threadIdx.x; j < c; j += blockDim.x) s += __ldcg(hd.chunk_cnt + j);
-    return block_sum(s, sh);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t *const bitmap = hd.bitmap;
+    const uint32_t *const members = hd.members;
+    // rounds of 8 chunks c0 + j nb: lane 4j + q prefetches summary word q of chunk j
+    for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
+        const int cp = c0 + (lane >> 2) * nb;
+        const uint32_t swall = cp < n_chunks ? __ldcg(hd.summary + (int64_t)cp * 32 + wid + 8 * (lane & 3)) : 0u;
+        for (int j = 0; j < kPrefetch; ++j) {
+            const int c = c0 + j * nb;
+            if (c >= n_chunks) break;
+            const int64_t u0 = (int64_t)c * 32 + wid;      // unit of q = 0; unit q = u0 + 8q
+            const uint32_t sw = __shfl_sync(0xffffffffu, swall, 4 * j + (lane & 3));   // lanes q < 4
+            if (!__ballot_sync(0xffffffffu, lane < kUnitsPerWarp && sw != 0)) {
+                if (lane < kUnitsPerWarp) hd.seg_cnt[u0 + 8 * lane] = 0;
+                continue;
+            }
+            uint32_t a[kUnitsPerWarp], m[kUnitsPerWarp];
+#pragma unroll
+            for (int q = 0; q < kUnitsPerWarp; ++q) {
+                const bool b = (__shfl_sync(0xffffffffu, sw, q) >> lane) & 1u;
+                const int64_t w = (u0 + 8 * q) * 32 + lane;
+                a[q] = b ? __ldcg(bitmap + w) : 0u;
+                m[q] = b ? __ldcg(members + w) : 0u;
+            }
+            int32_t cnt_mine = 0, total = 0;
+#pragma unroll
+            for (int q = 0; q < kUnitsPerWarp; ++q) {
+                const uint32_t nw = a[q] & ~m[q];
+                if (a[q] && !nw) bitmap[(u0 + 8 * q) * 32 + lane] = 0u;   // only members marked: consumed
+                const int32_t v = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)__popc(nw));
+                if (lane == q) cnt_mine = v;
+                total += v;
+            }
+            if (lane < kUnitsPerWarp) hd.seg_cnt[u0 + 8 * lane] = cnt_mine;
+            if (lane == 0 && total) atomicAdd(hd.chunk_cnt + c, total);
+        }
+    }
 }
 
-// New vertices of each chunk, in gid order: append to the node array of their type,
-// set pos[], fold them into the members, clear the marks.  Virtual block per chunk,
-// one word per thread (1024 threads).
-__device__ void phase_emit(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
+__device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
 {
-    __shared__ int32_t sh[33];   // blockDim.x == kChunkWords == 1024
-    for (int c = bid; c < n_chunks; c += nb) {
-        const int32_t mine = __ldcg(hd.chunk_cnt + c);
-        if (mine == 0) continue;   // block-uniform
-        const int64_t bit0 = (int64_t)c * kChunkBits;
-        int u = 0;
-        while (bit0 >= g.boff[u + 1]) ++u;
-        const int fc = (int)(g.boff[u] / kChunkBits);
-        const int32_t prior = bits_before(hd, c, sh) - bits_before(hd, fc, sh);
-        const int32_t nF = meta_nodes(hd.meta, hd.h)[u];
-        // one bitmap word per thread (blockDim.x == kChunkWords)
-        const int64_t wi = (int64_t)c * kChunkWords + threadIdx.x;
-        uint32_t *wp = hd.bitmap + wi;
-        uint32_t *mp = hd.members + wi;
-        const uint32_t x = __ldcg(wp);
-        const uint32_t mm = x ? __ldcg(mp) : 0u;
-        uint32_t word = x & ~mm;
-        const int32_t pc = __popc(word);
-        int32_t tot;
-        int32_t position = nF + prior + block_excl_scan(pc, sh, &tot);
-        if (pc) {
-            const int64_t gbase = (g.off[u] - g.boff[u]) + wi * 32;   // gid of bit 0 of word wi
-            int64_t *const nodes = hd.nodes[u];
-            int32_t *const pos = hd.pos;
-            int32_t *const meta = hd.meta;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t *const bitmap = hd.bitmap;
+    uint32_t *const members = hd.members;
+    int32_t *const pos = hd.pos;
+    for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
+        const int cp = c0 + (lane >> 2) * nb;
+        uint32_t *const spp = hd.summary + (int64_t)cp * 32 + wid + 8 * (lane & 3);
+        const uint32_t swall = cp < n_chunks ? __ldcg(spp) : 0u;
+        if (swall) *spp = 0u;   // this warp's units of the round's chunks are consumed below
+        for (int j = 0; j < kPrefetch; ++j) {
+            const int c = c0 + j * nb;
+            if (c >= n_chunks) break;
+            const int64_t u0 = (int64_t)c * 32 + wid;
+            const uint32_t sw = __shfl_sync(0xffffffffu, swall, 4 * j + (lane & 3));   // lanes q < 4
+            if (!__ballot_sync(0xffffffffu, lane < kUnitsPerWarp && sw != 0)) continue;
+            const int64_t bit0 = (int64_t)c * kChunkBits;
+            int u = 0;
+            while (bit0 >= g.boff[u + 1]) ++u;
+            const int32_t uc = __ldcg(hd.seg_cnt + (int64_t)c * 32 + lane);   // unit `lane` of the chunk
+            const int32_t uex = warp_incl_scan(uc) - uc;
+            const int32_t base = meta_nodes(hd.meta, hd.h)[u] + __ldcg(hd.chunk_pre + c);
             const int32_t cap = hd.cap_nodes[u];
-            *mp = mm | word;                                          // now members
-            while (word) {
-                const int b = __ffs(word) - 1;
-                word &= word - 1;
-                const int64_t gid = gbase + b;
-                if (position < cap) {
-                    nodes[position] = gid;
-                    pos[gid] = position;
-                } else {
-                    atomicOr(meta + kMetaErr, kErrCapacity);
+            int64_t *const nodes = hd.nodes[u];
+            const int64_t gid0 = g.off[u] - g.boff[u];   // gid of bitmap bit b = gid0 + b
+            uint32_t su[kUnitsPerWarp], a[kUnitsPerWarp], m[kUnitsPerWarp];
+#pragma unroll
+            for (int q = 0; q < kUnitsPerWarp; ++q) {
+                su[q] = __shfl_sync(0xffffffffu, sw, q);
+                const int64_t w = (u0 + 8 * q) * 32 + lane;
+                const bool b = (su[q] >> lane) & 1u;
+                a[q] = b ? __ldcg(bitmap + w) : 0u;
+                m[q] = b ? __ldcg(members + w) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < kUnitsPerWarp; ++q) {
+                const int unit = wid + 8 * q;
+                const int32_t ubase = __shfl_sync(0xffffffffu, uex, unit);
+                if (!su[q]) continue;   // warp-uniform
+                uint32_t word = a[q] & ~m[q];
+                const int32_t pc = __popc(word);
+                int32_t position = base + ubase + (warp_incl_scan(pc) - pc);
+                const int64_t w = (u0 + 8 * q) * 32 + lane;
+                if (a[q]) bitmap[w] = 0u;
+                if (!word) continue;
+                members[w] = m[q] | word;   // now members
+                const int64_t gb = gid0 + w * 32;
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    if (position < cap) {
+                        nodes[position] = gb + b;
+                        pos[gb + b] = position;
+                    } else {
+                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                    }
+                    ++position;
                 }
-                ++position;
             }
         }
-        if (x) *wp = 0u;                                              // marks consumed
-        if (threadIdx.x == 0) atomicAdd(meta_nodes(hd.meta, hd.h + 1) + u, mine);
     }
 }
 

@@ -263,6 +263,34 @@ def test_c2_pipeline_depth4_concurrent_lanes(c2):
         ctx.set_pipeline(1)
 
 
+# ----------------------------------------------------------------------------- compaction variants
+
+@pytest.mark.parametrize("mode", ["sparse", "dense"])
+def test_compaction_variant_forced(c1, c2, mode, monkeypatch):
+    """Both compaction variants (lane-per-word blocks for small graphs, lane-per-slice
+    warps for large ones; default chosen by graph size) give the oracle's blocks on C1
+    and C2, alone and in a bundle of 3 batches."""
+    import torch
+    monkeypatch.setenv("EG_COMPACT", mode)   # read at context creation
+    for cfg, g, rows, _ in (c1, c2):
+        ctx = _ctx(g)
+        for gi in (0, 1):
+            run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 100 + gi), cfg.fanouts, synth.rng_seed(cfg, 100 + gi),
+                            rows, check_invariants=(gi == 0))
+        ctx.set_pipeline(1, 4)
+        idx = [110, 111, 112]
+        seeds = [synth.batch_seeds(cfg, i) for i in idx]
+        rs = [synth.rng_seed(cfg, i) for i in idx]
+        dev = [torch.from_numpy(x).cuda() for x in seeds]
+        bls = ctx.sample_bundle(dev, cfg.fanouts, rs, features=True)
+        for x, r, b in zip(seeds, rs, bls):
+            res = oracle.sample(g, x, cfg.fanouts, r)
+            assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, _features_of(b, cfg), cfg, rows)
+            b.free()
+        ctx.close()
+
+
 # ----------------------------------------------------------------------------- C4 / C5 (full size)
 
 def test_c4_full_size_batches():
