@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ 
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 3) k_select(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, 4) k_select(const __grid_constant__ GraphDev g,
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
@@ -71,11 +71,11 @@ __global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant
     phase_copy(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_tiny(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, 4) k_tiny(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 5 + 8 * h);
-    phase_tiny(g, bd->hop[blockIdx.y][h]);
+    phase_tiny(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 template <bool kSparse>

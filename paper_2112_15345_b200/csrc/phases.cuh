@@ -635,7 +635,6 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
     uint32_t *const bitmap = hd.bitmap;
     const uint64_t *const selq = hd.selq;
     (void)bid;
-    (void)nb;
     // ---- heavy chunk tasks
     const uint32_t ntask = min(*(const volatile uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), (uint32_t)kMaxHeavyTasks);
     uint32_t *hnext = (uint32_t *)(hd.meta + kMetaHeavyNext + hd.h);
@@ -647,80 +646,42 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
         const uint32_t task = hd.heavyq[t];
         if (task != 0xFFFFFFFFu) heavy_task(g, hd, task, seed_lo, seed_hi, cand);
     }
-    // ---- selections (d > k): warp per item
-    const int64_t nsel = *(const volatile uint32_t *)(hd.meta + kMetaSel + hd.h);
+    // ---- selections (d > k): warp per item, fetched kGrab at a time (lane q < kGrab
+    // loads item q's data, so the fetch chain costs one round per kGrab items)
+    // (kGrab = 1 when there are few items per warp: load balance first)
+    const uint32_t nsel = *(const volatile uint32_t *)(hd.meta + kMetaSel + hd.h);
+    const int kGrab = nsel >= 16u * (uint32_t)nb * (blockDim.x >> 5) ? 4 : 1;
     uint32_t *snext = (uint32_t *)(hd.meta + kMetaSelNext + hd.h);
     for (;;) {
-        uint32_t wi = 0;
-        if (lane == 0) wi = atomicAdd(snext, 1u);
-        wi = __shfl_sync(0xffffffffu, wi, 0);
-        if ((int64_t)wi >= nsel) break;
-        const int64_t w = wi;
-        const uint64_t e = selq[w];
-        const int r = (int)(e >> 32);
-        const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
-        const RelDev &R = g.rel[r];
-        const int32_t pos0 = hd.indptr[r][i];
-        const int64_t ib = hd.ibase[r][i];
-        const int64_t d = hd.ideg[r][i];
-        const int64_t v = hd.nodes[R.dst_vt][i];
-        const int p = (int)(ib >> 56);
-        const int64_t base = ib & ((1ll << 56) - 1);
-        Item itm;
-        itm.pos = pos;
-        itm.bitmap = bitmap;
-        itm.summary = hd.summary;
-        itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
-        itm.soff = (uint32_t)g.off[R.src_vt];
-        itm.ebase = R.edge_base[p] + base;
-        itm.ix = R.indices[p] + base;
-        itm.src_out = hd.src[r] + pos0;
-        itm.eid_out = hd.eids[r] + pos0;
-        const int k = hd.fanout[r];
-        const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
-        if (d <= 128)
-            select_small(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
-        else if (k <= kSelMaxK)
-            select_fast(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi, cand);
-        else
-            select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
-    }
-}
-
-// Selections of tiny items (k < d <= kTinyD): 8 lanes per item, 4 items per warp.  The
-// same register radix select as select_small, with the sums taken over the 8 lanes of
-// the item; all groups step together (finished groups idle).
-__device__ void phase_tiny(const GraphDev &g, const HopDev &hd)
-{
-    static_assert(kTinyD == 32, "8 lanes x 4 keys");
-    const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
-    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const uint32_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
-    uint32_t *const tnext = (uint32_t *)(hd.meta + kMetaTinyNext + hd.h);
-    for (;;) {
-        uint32_t q0 = 0;
-        if (lane == 0) q0 = atomicAdd(tnext, 4u);
-        q0 = __shfl_sync(0xffffffffu, q0, 0);
-        if (q0 >= ntiny) break;
-        const uint32_t qi = q0 + gi;
-        const bool act = qi < ntiny;
-        Item itm;
-        int k = 0;
-        int32_t d = 0;
-        uint32_t w[4] = {0, 0, 0, 0}, vm = 0;
-        if (act) {
-            const uint64_t e = hd.selq[hd.selq_cap - 1 - qi];
-            const int r = (int)(e >> 32);
-            const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+        uint32_t w0 = 0;
+        if (lane == 0) w0 = atomicAdd(snext, (uint32_t)kGrab);
+        w0 = __shfl_sync(0xffffffffu, w0, 0);
+        if (w0 >= nsel) break;
+        uint32_t my_r = 0, my_i = 0;
+        int32_t my_pos0 = 0, my_d = 0;
+        int64_t my_ib = 0, my_v = 0;
+        if (lane < kGrab && w0 + lane < nsel) {
+            const uint64_t e = selq[w0 + lane];
+            my_r = (uint32_t)(e >> 32);
+            my_i = (uint32_t)e;
+            my_pos0 = hd.indptr[my_r][my_i];
+            my_ib = hd.ibase[my_r][my_i];
+            my_d = hd.ideg[my_r][my_i];
+            my_v = hd.nodes[g.rel[my_r].dst_vt][my_i];
+        }
+        const int cnt = (int)min((uint32_t)kGrab, nsel - w0);
+        for (int q = 0; q < cnt; ++q) {
+            const int r = (int)__shfl_sync(0xffffffffu, my_r, q);
+            const int32_t pos0 = __shfl_sync(0xffffffffu, my_pos0, q);
+            const int64_t ib = __shfl_sync(0xffffffffu, my_ib, q);
+            const int64_t d = __shfl_sync(0xffffffffu, my_d, q);
+            const int64_t v = __shfl_sync(0xffffffffu, my_v, q);
             const RelDev &R = g.rel[r];
-            const int32_t pos0 = hd.indptr[r][i];
-            const int64_t ib = hd.ibase[r][i];
-            d = hd.ideg[r][i];
-            const int64_t v = hd.nodes[R.dst_vt][i];
             const int p = (int)(ib >> 56);
             const int64_t base = ib & ((1ll << 56) - 1);
-            itm.pos = hd.pos;
-            itm.bitmap = hd.bitmap;
+            Item itm;
+            itm.pos = pos;
+            itm.bitmap = bitmap;
             itm.summary = hd.summary;
             itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
             itm.soff = (uint32_t)g.off[R.src_vt];
@@ -728,10 +689,86 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd)
             itm.ix = R.indices[p] + base;
             itm.src_out = hd.src[r] + pos0;
             itm.eid_out = hd.eids[r] + pos0;
+            const int k = hd.fanout[r];
+            const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
+            if (d <= 128)
+                select_small(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
+            else if (k <= kSelMaxK)
+                select_fast(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi, cand);
+            else
+                select_generic(hd, itm, d, k, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), hr, seed_lo, seed_hi);
+        }
+    }
+}
+
+// Selections of tiny items (k < d <= kTinyD): 8 lanes per item, 4 items per warp.  The
+// same register radix select as select_small, with the sums taken over the 8 lanes of
+// the item; all groups step together (finished groups idle).  Tiny items cost about
+// the same, so they are strided statically over the warps, and the queue entry and
+// item data of the next round are loaded while this round computes.
+struct TinyItem {
+    uint32_t r, i;
+    int32_t pos0, d;
+    int64_t ib, v;
+};
+
+__device__ __forceinline__ void tiny_load(const GraphDev &g, const HopDev &hd, uint64_t e, bool ok, TinyItem &t)
+{
+    t.r = (uint32_t)(e >> 32);
+    t.i = (uint32_t)e;
+    t.pos0 = 0;
+    t.d = 0;
+    t.ib = 0;
+    t.v = 0;
+    if (ok) {
+        t.pos0 = hd.indptr[t.r][t.i];
+        t.ib = hd.ibase[t.r][t.i];
+        t.d = hd.ideg[t.r][t.i];
+        t.v = hd.nodes[g.rel[t.r].dst_vt][t.i];
+    }
+}
+
+__device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
+{
+    static_assert(kTinyD == 32, "8 lanes x 4 keys");
+    const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
+    const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
+    const int64_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
+    const int64_t nw = (int64_t)nb * (blockDim.x >> 5);
+    const uint64_t *const selq_top = hd.selq + (hd.selq_cap - 1);   // item q at selq_top[-q]
+    int64_t q = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + gi;
+    if (q - gi >= ntiny) return;   // warp-uniform
+    TinyItem cur;
+    tiny_load(g, hd, q < ntiny ? selq_top[-q] : 0ull, q < ntiny, cur);
+    const int64_t step = nw * 4;
+    uint64_t e_next = q + step < ntiny ? selq_top[-(q + step)] : 0ull;
+    for (; q - gi < ntiny; q += step) {
+        const bool act = q < ntiny;
+        TinyItem nxt;
+        tiny_load(g, hd, e_next, q + step < ntiny, nxt);   // next round's data in flight
+        e_next = q + 2 * step < ntiny ? selq_top[-(q + 2 * step)] : 0ull;
+        Item itm;
+        int k = 0;
+        const int32_t d = cur.d;
+        uint32_t w[4] = {0, 0, 0, 0}, vm = 0;
+        if (act) {
+            const int r = (int)cur.r;
+            const RelDev &R = g.rel[r];
+            const int p = (int)(cur.ib >> 56);
+            const int64_t base = cur.ib & ((1ll << 56) - 1);
+            itm.pos = hd.pos;
+            itm.bitmap = hd.bitmap;
+            itm.summary = hd.summary;
+            itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
+            itm.soff = (uint32_t)g.off[R.src_vt];
+            itm.ebase = R.edge_base[p] + base;
+            itm.ix = R.indices[p] + base;
+            itm.src_out = hd.src[r] + cur.pos0;
+            itm.eid_out = hd.eids[r] + cur.pos0;
             k = hd.fanout[r];
             if (4 * sl < d) {
-                keys4((uint32_t)sl, (uint32_t)v, (uint32_t)((uint64_t)v >> 32), ((uint32_t)hd.h << 16) | (uint32_t)r,
-                      seed_lo, seed_hi, w);
+                keys4((uint32_t)sl, (uint32_t)cur.v, (uint32_t)((uint64_t)cur.v >> 32),
+                      ((uint32_t)hd.h << 16) | (uint32_t)r, seed_lo, seed_hi, w);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) vm |= (uint32_t)(4 * sl + t < d) << t;
             }
@@ -802,6 +839,7 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd)
             for (int t = 0; t < 4; ++t)
                 if (sel >> t & 1) emit_edge(hd, itm, slot++, 4 * sl + t);
         }
+        cur = nxt;
     }
 }
 
