@@ -121,24 +121,22 @@ __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__
     phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
 }
 
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial, int compact)
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
+                 const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
+                 const Fork &fk, bool serial)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
-    const int wide = kScanBlocks * g.n_rel;        // count / scan: one block per virtual block
     const int samp = (kSMs * 4 + B - 1) / B;
     // bitmap chunks: at most one resident wave in total (8 blocks of 256 threads per SM);
-    // blocks loop.  Dense variant: a block per chunk; sparse (a 111M-vertex graph has
-    // 3.4k chunks per batch): a warp per half chunk.
-    const bool sparse = compact == 2 || (compact == 0 && n_chunks > kSparseChunks);
-    const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
+    // blocks loop.  Dense variant: a block per chunk; sparse (per hop, chosen by the
+    // plan): a warp per half chunk.
     const int chunk_cap = (kSMs * 8 + B - 1) / B;
-    const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
     int nk = 0;
     k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
     ++nk;
     for (int h = 0; h < n_hops; ++h) {
+        const int wide = scan_blocks[h] * g.n_rel;   // count / scan: one block per virtual block
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_scan<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         // selections and full-neighbourhood copies write disjoint slots: two graph branches
@@ -156,6 +154,9 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_ch
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
+        const bool sparse = sparse_hop[h] != 0;
+        const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
+        const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
         if (sparse)
             k_bitcount<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         else

@@ -12,7 +12,8 @@ constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
 constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one block)
 constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
-constexpr int kScanBlocks = 64;           // virtual blocks per relation in the two-phase scan
+constexpr int kMinScanBlocks = 64;        // virtual blocks per relation in the two-phase scan: per hop,
+constexpr int kMaxScanBlocks = 1024;      // about one per 4096 frontier items, within these bounds
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
 constexpr int kTinyD = 32;                // selections with d <= this: 8 lanes per item
@@ -22,8 +23,9 @@ constexpr int kHeavyD = 2048;
 constexpr int kHeavyChunk = 1024;
 constexpr int kHeavyMaxK = 48;
 constexpr int kHeavyCap = 512;            // candidate slots per heavy item
-constexpr int kMaxHeavy = 256;            // heavy items per (batch, hop); overflow -> warp per item
-constexpr int kMaxHeavyTasks = kMaxHeavy * ((1 << 20) / kHeavyChunk + 1);
+constexpr int kMinHeavy = 256;            // heavy items per (batch, hop): at least this, more for large
+                                          // frontiers (HopDev::max_heavy); overflow -> warp per item
+constexpr int kHeavyTasksPerItem = (1 << 20) / kHeavyChunk + 1;   // d <= 2^20 (generator Dmax)
 
 // Error bits written by kernels into meta[kMetaErr].
 enum : int32_t { kErrSeedRange = 1, kErrSeedDup = 2, kErrCapacity = 4 };
@@ -77,7 +79,10 @@ struct HopDev {
     int64_t *eids[EG_MAX_REL];
     uint32_t *src[EG_MAX_REL];       // sampled src gids (scratch)
     int32_t *meta;                   // batch counters
-    int32_t *partial;                // scan scratch [EG_MAX_REL][kScanBlocks]
+    int32_t *partial;                // scan scratch [EG_MAX_REL][scan_blocks]
+    int32_t scan_blocks;             // virtual blocks per relation (count / scan)
+    int32_t max_heavy;               // heavy item slots
+    int32_t max_heavy_tasks;         // heavy task slots
     int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
     uint32_t *bitmap;                // this hop's marks: every sampled source (A)
     uint32_t *members;               // vertices already in the batch (M); new = A & ~M
@@ -90,10 +95,10 @@ struct HopDev {
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
     uint64_t *selq;                  // items that need a selection: (r << 32) | i; tiny ones from the top
     int32_t selq_cap;                // slots of selq
-    uint64_t *heavy_items;           // [kMaxHeavy] (r << 32) | i
-    uint32_t *heavy_cnt;             // [kMaxHeavy] candidates found
-    uint32_t *heavy_done;            // [kMaxHeavy] finished tasks
-    uint64_t *heavy_cand;            // [kMaxHeavy][kHeavyCap] (key << 32) | j
+    uint64_t *heavy_items;           // [max_heavy] (r << 32) | i
+    uint32_t *heavy_cnt;             // [max_heavy] candidates found
+    uint32_t *heavy_done;            // [max_heavy] finished tasks
+    uint64_t *heavy_cand;            // [max_heavy][kHeavyCap] (key << 32) | j
     uint32_t *heavyq;                // tasks: (heavy item << 16) | chunk
     int32_t cap_nodes[EG_MAX_VT];    // capacity of nodes[u]
 };

@@ -82,8 +82,11 @@ struct Lane {
 };
 
 // per (batch, hop): heavy items, their counters, candidate buffers and chunk tasks
-constexpr size_t kHeavyBytes = sizeof(uint64_t) * kMaxHeavy + 2 * sizeof(uint32_t) * kMaxHeavy +
-                               sizeof(uint64_t) * kMaxHeavy * kHeavyCap + sizeof(uint32_t) * kMaxHeavyTasks;
+size_t heavy_bytes(int64_t mh, int64_t mt)
+{
+    return sizeof(uint64_t) * mh + 2 * sizeof(uint32_t) * mh + sizeof(uint64_t) * mh * kHeavyCap +
+           sizeof(uint32_t) * mt;
+}
 
 // A batch "plan": everything fixed by (hops, fanouts, seed capacity, features, bundle
 // size B): upper bounds, the memory layout of one batch (repeated B times), its slots.
@@ -103,6 +106,8 @@ struct Plan {
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_selq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
     int64_t selq_items[EG_MAX_HOPS] = {};
+    int32_t scan_blocks[EG_MAX_HOPS] = {}, max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
+    int32_t sparse[EG_MAX_HOPS] = {};   // compaction variant per hop (1 = lane-per-slice)
     size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
@@ -160,7 +165,7 @@ struct eg_ctx {
     cudaStream_t cap_stream = nullptr;
     Fork fork{};                          // capture side stream + events (graph branches)
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
-    int compact = 0;                      // EG_COMPACT at create: 0 by size, 1 dense, 2 sparse
+    int compact = 0;                      // EG_COMPACT at create: 0 per hop, 1 dense, 2 sparse
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
@@ -343,7 +348,7 @@ eg_status alloc_state(eg_ctx *c, BatchState *st)
     EG_CUDA(c, cudaMemset(st->chunk_cnt, 0, sizeof(int32_t) * std::max(1, c->n_chunks)));   // accumulated
     EG_CUDA(c, cudaMalloc(&st->seg_cnt, sizeof(int32_t) * std::max(1, c->n_chunks) * (kChunkWords / 16)));
     EG_CUDA(c, cudaMalloc(&st->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kScanBlocks));
+    EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kMaxScanBlocks));
     return EG_OK;
 }
 
@@ -516,7 +521,7 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
     {
         const char *tr = getenv("EG_TRACE");
         c->trace = tr && tr[0] == '1';
-        // EG_COMPACT=dense|sparse forces a compaction variant (tests); default by graph size
+        // EG_COMPACT=dense|sparse forces a compaction variant (tests); default per hop (plan)
         const char *cm = getenv("EG_COMPACT");
         c->compact = !cm ? 0 : (cm[0] == 'd' ? 1 : (cm[0] == 's' ? 2 : 0));
     }
@@ -804,7 +809,22 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         for (int r = 0; r < R; ++r) items += p->capF[h][dst_vt[r]];
         p->selq_items[h] = items;
         p->o_selq[h] = take(sizeof(uint64_t) * items);
-        p->o_heavy[h] = take(kHeavyBytes);
+        // scan virtual blocks: ~one per 4096 items of the largest relation's frontier;
+        // heavy slots: one per 2048 frontier items beyond the first kMinHeavy
+        int64_t most = 0;
+        for (int r = 0; r < R; ++r) most = std::max<int64_t>(most, p->capF[h][dst_vt[r]]);
+        p->scan_blocks[h] = (int32_t)std::min<int64_t>(kMaxScanBlocks, std::max<int64_t>(kMinScanBlocks, (most + 4095) / 4096));
+        p->max_heavy[h] = (int32_t)std::min<int64_t>(65535, kMinHeavy + items / 2048);
+        p->max_heavy_tasks[h] = (int32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)p->max_heavy[h] * kHeavyTasksPerItem);
+        p->o_heavy[h] = take(heavy_bytes(p->max_heavy[h], p->max_heavy_tasks[h]));
+        // compaction variant: sparse (lane per 16-word slice) when the hop's edge bound is
+        // below one mark per bitmap word, else dense (lane per word); EG_COMPACT forces.
+        // (Measured: sparse wins at ~1 mark per 20 words -- C4 hop 2, bound ~6x actual --
+        // dense at 1.6 per word -- a 10^6-vertex frontier on C4 -- and on C2 / C3.)
+        int64_t edges = 0;
+        for (int r = 0; r < R; ++r) edges += p->capE[h][r];
+        const int64_t words = c->g.boff[V] / 32;
+        p->sparse[h] = c->compact == 2 ? 1 : c->compact == 1 ? 0 : (edges < words ? 1 : 0);
     }
     if (features)
         for (int u = 0; u < V; ++u)
@@ -882,10 +902,14 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             x.selq_cap = (int32_t)p->selq_items[h];
             char *hv = base + p->o_heavy[h];
             x.heavy_items = (uint64_t *)hv;
-            x.heavy_cnt = (uint32_t *)(hv + sizeof(uint64_t) * kMaxHeavy);
-            x.heavy_done = x.heavy_cnt + kMaxHeavy;
-            x.heavy_cand = (uint64_t *)(hv + sizeof(uint64_t) * kMaxHeavy + 2 * sizeof(uint32_t) * kMaxHeavy);
-            x.heavyq = (uint32_t *)(x.heavy_cand + (size_t)kMaxHeavy * kHeavyCap);
+            const int64_t mh = p->max_heavy[h];
+            x.max_heavy = p->max_heavy[h];
+            x.max_heavy_tasks = p->max_heavy_tasks[h];
+            x.scan_blocks = p->scan_blocks[h];
+            x.heavy_cnt = (uint32_t *)(hv + sizeof(uint64_t) * mh);
+            x.heavy_done = x.heavy_cnt + mh;
+            x.heavy_cand = (uint64_t *)(hv + sizeof(uint64_t) * mh + 2 * sizeof(uint32_t) * mh);
+            x.heavyq = (uint32_t *)(x.heavy_cand + (size_t)mh * kHeavyCap);
             bd->hop[b][h] = x;
         }
         GatherDev &gd = gs.b[b];
@@ -916,8 +940,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, c->n_chunks, B, cs, c->fork, c->trace,
-                       c->compact);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->scan_blocks, p->sparse, c->n_chunks, B, cs,
+                       c->fork, c->trace);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {

@@ -36,8 +36,9 @@ struct Fork {
 
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
 // returns the number of kernels.
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial, int compact);
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
+                 const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
+                 const Fork &fk, bool serial);
 
 // gather.cu
 void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);

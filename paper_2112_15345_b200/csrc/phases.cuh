@@ -90,20 +90,21 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
 
 // ============================================================================ count + scan
 
-// Virtual blocks (r, b), b < kScanBlocks: count c for the dst items of chunk b of
+// Virtual blocks (r, b), b < hd.scan_blocks: count c for the dst items of chunk b of
 // F_h[t(r)] into the block indptr slots, record (owner, CSC row start) and d for
 // the sampler, enqueue the items that need a selection; per-chunk sums -> partial.
 __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
     __shared__ int32_t sh[33];
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
-    for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
-        const int r = vb / kScanBlocks, b = vb % kScanBlocks;
+    const int SB = hd.scan_blocks;
+    for (int vb = bid; vb < SB * g.n_rel; vb += nb) {
+        const int r = vb / SB, b = vb % SB;
         const RelDev &R = g.rel[r];
         const int t = R.dst_vt;
         const int k = hd.fanout[r];
         const int64_t n = nF[t];
-        const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
+        const int64_t chunk = (n + SB - 1) / SB;
         const int64_t lo = b * chunk, hi = min(n, lo + chunk);
         const int64_t *const nodes = hd.nodes[t];
         int64_t *const ibase = hd.ibase[r];
@@ -140,16 +141,16 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
                 const int64_t d = ideg[i];
                 const uint32_t nch = (uint32_t)((d + kHeavyChunk - 1) / kHeavyChunk);
                 const uint32_t hs = atomicAdd((uint32_t *)(hd.meta + kMetaHeavy + hd.h), 1u);
-                if (hs < (uint32_t)kMaxHeavy) {
+                if (hs < (uint32_t)hd.max_heavy) {
                     const uint32_t t0 = atomicAdd((uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), nch);
-                    if (t0 + nch <= (uint32_t)kMaxHeavyTasks) {
+                    if (t0 + nch <= (uint32_t)hd.max_heavy_tasks) {
                         hd.heavy_items[hs] = ((uint64_t)r << 32) | (uint64_t)i;
                         hd.heavy_cnt[hs] = 0;
                         hd.heavy_done[hs] = 0;
                         for (uint32_t c = 0; c < nch; ++c) hd.heavyq[t0 + c] = (hs << 16) | c;
                         sel = false;
                     } else {   // task list full: mark the reserved entries void, item goes to the normal queue
-                        for (uint32_t c = 0; c < nch && t0 + c < (uint32_t)kMaxHeavyTasks; ++c)
+                        for (uint32_t c = 0; c < nch && t0 + c < (uint32_t)hd.max_heavy_tasks; ++c)
                             hd.heavyq[t0 + c] = 0xFFFFFFFFu;
                     }
                 }
@@ -171,7 +172,7 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
             }
         }
         sum = block_sum(sum, sh);
-        if (threadIdx.x == 0) hd.partial[r * kScanBlocks + b] = sum;
+        if (threadIdx.x == 0) hd.partial[r * SB + b] = sum;
     }
 }
 
@@ -179,14 +180,15 @@ __device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb
 __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
     __shared__ int32_t sh[33];
-    for (int vb = bid; vb < kScanBlocks * g.n_rel; vb += nb) {
-        const int r = vb / kScanBlocks, b = vb % kScanBlocks;
+    const int SB = hd.scan_blocks;
+    for (int vb = bid; vb < SB * g.n_rel; vb += nb) {
+        const int r = vb / SB, b = vb % SB;
         const int t = g.rel[r].dst_vt;
         const int64_t n = meta_nodes(hd.meta, hd.h)[t];
-        const int64_t chunk = (n + kScanBlocks - 1) / kScanBlocks;
+        const int64_t chunk = (n + SB - 1) / SB;
         const int64_t lo = b * chunk, hi = min(n, lo + chunk);
         int32_t s = 0;
-        const int32_t *const partial = hd.partial + r * kScanBlocks;
+        const int32_t *const partial = hd.partial + r * SB;
         for (int j = threadIdx.x; j < b; j += blockDim.x) s += partial[j];
         int32_t carry = block_sum(s, sh);
         int32_t *const ip = hd.indptr[r];
@@ -198,7 +200,7 @@ __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb)
             if (i < hi) ip[i] = carry + ex;
             carry += tot;
         }
-        if (b == kScanBlocks - 1 && threadIdx.x == 0) {
+        if (b == SB - 1 && threadIdx.x == 0) {
             ip[n] = carry;
             meta_nnz(hd.meta, hd.h)[r] = carry;
         }
@@ -636,7 +638,7 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
     const uint64_t *const selq = hd.selq;
     (void)bid;
     // ---- heavy chunk tasks
-    const uint32_t ntask = min(*(const volatile uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), (uint32_t)kMaxHeavyTasks);
+    const uint32_t ntask = min(*(const volatile uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), (uint32_t)hd.max_heavy_tasks);
     uint32_t *hnext = (uint32_t *)(hd.meta + kMetaHeavyNext + hd.h);
     for (;;) {
         uint32_t t = 0;
@@ -1096,11 +1098,10 @@ __device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, 
     }
 }
 
-// ---- dense variant (graphs of <= kSparseChunks chunks, where a batch marks a large
-// fraction of the words): a block of 8 warps per chunk = 32 units of 32 words (one
-// summary word each); warp w takes units w, w+8, w+16, w+24, one word per lane, so
-// that the emission of a dense word (up to 32 new vertices) is spread over the lanes.
-constexpr int kSparseChunks = 512;
+// ---- dense variant (hops that mark a large fraction of the words): a block of 8 warps
+// per chunk = 32 units of 32 words (one summary word each); warp w takes units w, w+8,
+// w+16, w+24, one word per lane, so that the emission of a dense word (up to 32 new
+// vertices) is spread over the lanes and the node-array stores of a warp are contiguous.
 constexpr int kUnitsPerWarp = kChunkWords / 32 / 8;   // 4 (blockDim.x == 256)
 constexpr int kPrefetch = 8;                          // chunks whose summary words one load fetches
 
@@ -1218,7 +1219,19 @@ __device__ void phase_relabel(const GraphDev &g, const HopDev &hd, int bid, int 
         const int64_t n = meta_nnz(hd.meta, hd.h)[r];
         const uint32_t *const src = hd.src[r];
         int32_t *const idx = hd.indices[r];
-        for (int64_t e = bid * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) idx[e] = __ldcg(pos + src[e]);
+        // four independent src -> pos[] chains per thread in flight
+        int64_t e = bid * (int64_t)blockDim.x + threadIdx.x;
+        for (; e + 3 * stride < n; e += 4 * stride) {
+            uint32_t sv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sv[q] = __ldcs(src + e + q * stride);
+            int32_t pv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pv[q] = __ldcg(pos + sv[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) idx[e + q * stride] = pv[q];
+        }
+        for (; e < n; e += stride) idx[e] = __ldcg(pos + src[e]);
     }
 }
 

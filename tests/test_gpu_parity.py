@@ -267,8 +267,8 @@ def test_c2_pipeline_depth4_concurrent_lanes(c2):
 
 @pytest.mark.parametrize("mode", ["sparse", "dense"])
 def test_compaction_variant_forced(c1, c2, mode, monkeypatch):
-    """Both compaction variants (lane-per-word blocks for small graphs, lane-per-slice
-    warps for large ones; default chosen by graph size) give the oracle's blocks on C1
+    """Both compaction variants (lane-per-word blocks for hops that mark many words,
+    lane-per-slice warps for sparse hops; chosen per hop by the plan) give the oracle's blocks on C1
     and C2, alone and in a bundle of 3 batches."""
     import torch
     monkeypatch.setenv("EG_COMPACT", mode)   # read at context creation
