@@ -13,3 +13,5 @@ for n in 1 2 4; do
 done
 CUDA_VISIBLE_DEVICES=0,1 timeout 1500 $R --nproc-per-node 2 --master-port 29621 tests/dist_gpu_parity.py --config C5 \
     --batches 1 > gpurun_out/dist_c5_n2.log 2>&1; echo dist_c5_n2=$?; tail -2 gpurun_out/dist_c5_n2.log
+timeout 600 $R --nproc-per-node 4 --master-port 29631 profiles/nvlink_sweep.py > gpurun_out/nvlink_sweep_n4.log 2>&1; echo nvlink_n4=$?
+grep '^{' gpurun_out/nvlink_sweep_n4.log | tail -1
