@@ -16,6 +16,9 @@ Parity status of each oracle function (pins are in ``tests/test_oracle_*.py``):
                     full neighbourhood, dst prefix, sorted new, round trip),
                     BFS closed form at fanout -1, worked example, uniformity
   og_gather         pinned: numpy.take on the same rows
+  og_lp_targets     pinned: negatives vs an independent pure-Python Philox and a
+                    chi-square over the dst range; seeds = brute-force set of the
+                    endpoints; every pair round-trips through the seeds
   exact sampled sets vs the paper: parity unpinned (the paper fixes only the
                     distribution; bit-exactness is relative to key32)
 """
@@ -69,6 +72,9 @@ def lib():
         L.og_n_nodes.restype = ctypes.c_int64
         L.og_nodes.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
         L.og_nodes.restype = P(ctypes.c_int64)
+        L.og_lp_targets.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p,
+                                    ctypes.c_void_p, P(ctypes.c_int64), ctypes.c_void_p]
         L.og_block.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_int64),
                                P(ctypes.c_int64), P(P(ctypes.c_int32)), P(P(ctypes.c_int32)),
                                P(P(ctypes.c_int64)), P(P(ctypes.c_int64))]
@@ -188,6 +194,43 @@ def sample(graph, seeds, fanouts, rng_seed: int) -> OracleResult:
         return out
     finally:
         L.og_free(res)
+
+
+@dataclass
+class LpTargets:
+    """Link-prediction targets of one mini-batch (og_lp_targets)."""
+    seeds: np.ndarray     # int64 distinct endpoints, ascending gid
+    neg_dst: np.ndarray   # int64 [n_pos * n_neg] corrupted dst gids
+    pos_src: np.ndarray   # int32 local ids (index among the seeds of the endpoint's type)
+    pos_dst: np.ndarray
+    neg_src: np.ndarray
+    neg_dst_local: np.ndarray
+
+
+def lp_targets(graph, src, dst, rel: int, n_neg: int, neg_seed: int) -> LpTargets:
+    g = _Graph(graph)
+    src = np.ascontiguousarray(src, dtype=np.int64)
+    dst = np.ascontiguousarray(dst, dtype=np.int64)
+    n = len(src)
+    assert len(dst) == n
+    neg = np.zeros(max(1, n * n_neg), np.int64)
+    seeds = np.zeros(max(1, n * (2 + n_neg)), np.int64)
+    pairs = np.zeros(max(1, 2 * n + 2 * n * n_neg), np.int32)
+    ns = ctypes.c_int64()
+    rc = lib().og_lp_targets(ctypes.addressof(g.c), src.ctypes.data, dst.ctypes.data, n, rel, n_neg,
+                             neg_seed & (2**64 - 1), neg.ctypes.data, seeds.ctypes.data, ctypes.byref(ns),
+                             pairs.ctypes.data)
+    if rc != OG_OK:
+        raise OracleError(rc)
+    m = n * n_neg
+    return LpTargets(seeds[:ns.value].copy(), neg[:m].copy(), pairs[:n].copy(), pairs[n:2 * n].copy(),
+                     pairs[2 * n:2 * n + m].copy(), pairs[2 * n + m:2 * n + 2 * m].copy())
+
+
+def sample_lp(graph, src, dst, rel: int, n_neg: int, neg_seed: int, fanouts, rng_seed: int):
+    """A link-prediction mini-batch: its targets, then og_sample from their seeds."""
+    t = lp_targets(graph, src, dst, rel, n_neg, neg_seed)
+    return sample(graph, t.seeds, fanouts, rng_seed), t
 
 
 def gather(result: OracleResult, vt_counts, u: int, rows: np.ndarray) -> np.ndarray:

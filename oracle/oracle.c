@@ -335,6 +335,94 @@ int og_gather(const int64_t *ids, int64_t n, int64_t off_u, int64_t n_u,
     return OG_OK;
 }
 
+/* ---------------------------------------------------------------- link prediction targets */
+
+/* The scheduler "determines target vertices or target edges in each mini-batch to
+ * support various learning tasks (e.g., node classification, link prediction)"
+ * (§4.2.1); link prediction trains on edges (§5).  SPEC's
+ * make_link_task: per positive edge, num_negatives corrupted pairs with the
+ * dst resampled uniformly from the dst vertex type's ID range; the seed vertex set is
+ * the union of all endpoints.  Readings (L1-L4):
+ *   L1 corrupted pair q of positive i keeps src_i; its dst is
+ *      off[t(r)] + floor(w * N_{t(r)} / 2^32),
+ *      w = Philox4x32-10(ctr = {i, q, 0, 0x4E454721 'NEG!'}, key = {lo32(neg_seed),
+ *      hi32(neg_seed)}).word[0];
+ *   L2 the seeds are the distinct endpoints in ascending gid (type-contiguous gids, so
+ *      (type, gid) order); sampling then starts from them exactly as og_sample does;
+ *   L3 every pair is returned as the local ids of its endpoints (index among the seeds
+ *      of the endpoint's type = its position in block 0's dst nodes);
+ *   L4 no seed edge is excluded from sampling (the paper states no exclusion).
+ * neg_dst: n_pos*n_neg gids; seeds: capacity n_pos*(2+n_neg); pairs: int32
+ * [pos_src n_pos][pos_dst n_pos][neg_src n_pos*n_neg][neg_dst n_pos*n_neg]. */
+int og_lp_targets(const og_graph *g, const int64_t *src, const int64_t *dst, int64_t n_pos, int32_t rel,
+                  int32_t n_neg, uint64_t neg_seed, int64_t *neg_dst, int64_t *seeds, int64_t *n_seeds,
+                  int32_t *pairs)
+{
+    if (rel < 0 || rel >= g->n_rel || n_pos < 0 || n_neg < 0 || n_pos >= ((int64_t)1 << 32)) return OG_EINVAL;
+    const int V = g->n_vt;
+    int64_t *off = xcalloc((size_t)V + 1, sizeof(int64_t));
+    for (int t = 0; t < V; ++t) off[t + 1] = off[t] + g->vt_count[t];
+    const int s = g->rel_src_vt[rel], t = g->rel_dst_vt[rel];
+    for (int64_t i = 0; i < n_pos; ++i)
+        if (src[i] < off[s] || src[i] >= off[s + 1] || dst[i] < off[t] || dst[i] >= off[t + 1]) {
+            free(off);
+            return OG_ERANGE;
+        }
+    /* L1: negatives */
+    const uint32_t key[2] = {(uint32_t)neg_seed, (uint32_t)(neg_seed >> 32)};
+    const uint64_t n_t = (uint64_t)g->vt_count[t];
+    for (int64_t i = 0; i < n_pos; ++i)
+        for (int32_t q = 0; q < n_neg; ++q) {
+            const uint32_t ctr[4] = {(uint32_t)i, (uint32_t)q, 0u, 0x4E454721u};
+            uint32_t w[4];
+            og_philox4x32_10(ctr, key, w);
+            neg_dst[i * n_neg + q] = off[t] + (int64_t)(((uint64_t)w[0] * n_t) >> 32);
+        }
+    /* L2: distinct endpoints, ascending */
+    const int64_t n_end = n_pos * (2 + (int64_t)n_neg);
+    int64_t *e = xcalloc((size_t)n_end + 1, sizeof(int64_t));
+    int64_t m = 0;
+    for (int64_t i = 0; i < n_pos; ++i) e[m++] = src[i];
+    for (int64_t i = 0; i < n_pos; ++i) e[m++] = dst[i];
+    for (int64_t i = 0; i < n_pos * n_neg; ++i) e[m++] = neg_dst[i];
+    qsort(e, (size_t)m, sizeof(int64_t), cmp_i64);
+    int64_t k = 0;
+    for (int64_t i = 0; i < m; ++i)
+        if (k == 0 || e[i] != seeds[k - 1]) seeds[k++] = e[i];
+    *n_seeds = k;
+    /* L3: local ids = index among the seeds of the endpoint's type */
+    int64_t *first = xcalloc((size_t)V + 1, sizeof(int64_t));   /* first seed index of type u */
+    for (int u = 0; u <= V; ++u) {
+        int64_t lo = 0, hi = k;                                    /* first seed >= off[u] */
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (seeds[mid] < off[u]) lo = mid + 1; else hi = mid;
+        }
+        first[u] = lo;
+    }
+    for (int64_t i = 0; i < m; ++i) {
+        const int64_t x = i < n_pos ? src[i] : i < 2 * n_pos ? dst[i - n_pos] : neg_dst[i - 2 * n_pos];
+        int64_t lo = 0, hi = k;                                    /* index of x in seeds */
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (seeds[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        int u = 0;
+        while (x >= off[u + 1]) ++u;
+        const int32_t local = (int32_t)(lo - first[u]);
+        if (i < 2 * n_pos) pairs[i] = local;                                   /* pos_src, pos_dst */
+        else {
+            const int64_t j = i - 2 * n_pos;                                  /* negative j */
+            pairs[2 * n_pos + j] = pairs[j / (n_neg ? n_neg : 1)];               /* neg_src = pos_src */
+            pairs[2 * n_pos + n_pos * n_neg + j] = local;                        /* neg_dst */
+        }
+    }
+    free(first);
+    free(e);
+    free(off);
+    return OG_OK;
+}
+
 /* ---------------------------------------------------------------- accessors */
 
 int64_t og_n_nodes(const og_result *res, int32_t level, int32_t u)

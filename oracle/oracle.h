@@ -35,6 +35,12 @@ int og_gather(const int64_t *ids, int64_t n, int64_t off_u, int64_t n_u,
               const void *rows, int64_t row_bytes, void *out);
 void og_free(og_result *res);
 
+/* Link-prediction targets (see oracle.c): negatives, the seed set (distinct endpoints,
+ * ascending) and every pair in local ids.  Sampling then runs og_sample on the seeds. */
+int og_lp_targets(const og_graph *g, const int64_t *src, const int64_t *dst, int64_t n_pos, int32_t rel,
+                  int32_t n_neg, uint64_t neg_seed, int64_t *neg_dst, int64_t *seeds, int64_t *n_seeds,
+                  int32_t *pairs);
+
 /* level 0 = seeds per type (F_0); level h+1 = S_h (src nodes of block h). */
 int64_t og_n_nodes(const og_result *res, int32_t level, int32_t u);
 const int64_t *og_nodes(const og_result *res, int32_t level, int32_t u);
