@@ -190,6 +190,41 @@ EG_API eg_status eg_sample_bundle(eg_ctx *ctx, int32_t n_batches, const int64_t 
                                   const int64_t *n_seeds, int32_t n_hops, const int32_t *fanouts,
                                   const uint64_t *rng_seeds, int32_t flags, eg_blocks **out);
 
+/* ---- Link-prediction mini-batches (DESIGN.md §3 readings L1-L4).
+ * The scheduler picks "target edges in each mini-batch" for link prediction (PAPER.md
+ * P:558-560 §4.2.1; trained on all edges, §5; fanout 25, 15).
+ * Batch b: positives (src[b][i], dst[b][i]), i < n_pos[b], gids of relation rel's
+ * src / dst vertex types (host or device int64 arrays, read in place when device-
+ * accessible, which then must stay valid until the batch resolves).  Per positive,
+ * n_neg corrupted pairs keep the src and draw the dst uniformly from t(rel)'s range:
+ *   dst' = off[t] + floor(w * N_t / 2^32),
+ *   w = Philox4x32-10(ctr = {i, q, 0, 0x4E454721}, key = {lo32(neg_seeds[b]), hi32(..)}).word[0]
+ * (SPEC S:401-404).  The seeds are the distinct endpoints in ascending gid; sampling
+ * then runs exactly as eg_sample_bundle from them (block 0's dst nodes).  Flags as
+ * eg_sample_bundle (EG_FEATURES, EG_ASYNC); one bundle = one CUDA-graph launch.
+ * Errors: EG_EINVAL (rel out of range, n_neg outside [0, EG_MAX_NEG], n_pos < 0 or >=
+ * 2^31, null arrays); EG_ERANGE (an endpoint outside its vertex type; reported when the
+ * batch resolves). */
+#define EG_MAX_NEG 64
+EG_API eg_status eg_sample_lp_bundle(eg_ctx *ctx, int32_t n_batches, const int64_t *const *src,
+                                     const int64_t *const *dst, const int64_t *n_pos, int32_t rel, int32_t n_neg,
+                                     const uint64_t *neg_seeds, int32_t n_hops, const int32_t *fanouts,
+                                     const uint64_t *rng_seeds, int32_t flags, eg_blocks **out);
+
+/* The pairs of a link-prediction batch (waits if pending), as device int32 arrays of
+ * local ids (index among the seeds of the endpoint's type = position in block 0's dst
+ * nodes of that type): pos_src / pos_dst [n_pos], neg_src / neg_dst [n_pos * n_neg]
+ * (negative q of positive i at i * n_neg + q), and the corrupted dst gids neg_dst_gid
+ * (device int64 [n_pos * n_neg]).  Valid until eg_blocks_free.  EG_EINVAL for a
+ * node-classification batch. */
+typedef struct {
+    int64_t n_pos;
+    int32_t n_neg, rel;
+    const int32_t *pos_src, *pos_dst, *neg_src, *neg_dst;
+    const int64_t *neg_dst_gid;
+} eg_lp_view;
+EG_API eg_status eg_lp_view_get(const eg_blocks *blocks, eg_lp_view *out);
+
 /* Totals of a batch (waits if pending): sampled edges over all hops and relations, and
  * the input vertices (src nodes of the last block) per type (n_inputs: host [n_vt]);
  * either may be NULL. */

@@ -30,8 +30,27 @@ __device__ __forceinline__ uint64_t globaltimer()
 // into batch b's counters (copied to the host with them).
 __device__ __forceinline__ void stamp(const BatchDev *bd, int k)
 {
-    if (bd->trace && blockIdx.x == 0 && threadIdx.x == 0 && k < kMaxStamps)
+    if (bd->trace && blockIdx.x == 0 && threadIdx.x == 0 && k >= 0 && k < kMaxStamps)
         reinterpret_cast<uint64_t *>(bd->hop[blockIdx.y][0].meta + kMetaStamps)[k] = globaltimer();
+}
+
+// Hop h of batch blockIdx.y; h = -1: the link-prediction seed compaction.
+__device__ __forceinline__ const HopDev &hop_of(const BatchDev *bd, int h)
+{
+    return h < 0 ? bd->lph[blockIdx.y] : bd->hop[blockIdx.y][h];
+}
+
+__global__ void __launch_bounds__(kBatchThreads) k_lp_mark(const __grid_constant__ GraphDev g,
+                                                           const BatchDev *__restrict__ bd)
+{
+    stamp(bd, 0);
+    phase_lp_mark(g, bd->lph[blockIdx.y], bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(kBatchThreads) k_lp_pairs(const __grid_constant__ GraphDev g,
+                                                            const BatchDev *__restrict__ bd)
+{
+    phase_lp_pairs(g, bd->lph[blockIdx.y], bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev g,
@@ -82,29 +101,29 @@ template <bool kSparse>
 __global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
                                                             const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 6 + 8 * h);
+    if (h >= 0) stamp(bd, 6 + 8 * h);
     if (kSparse)
-        phase_bitcount_sparse(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+        phase_bitcount_sparse(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
     else
-        phase_bitcount_dense(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+        phase_bitcount_dense(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(1024) k_cscan(const __grid_constant__ GraphDev g,
                                                  const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 7 + 8 * h);
-    phase_chunk_scan(g, bd->hop[blockIdx.y][h]);
+    if (h >= 0) stamp(bd, 7 + 8 * h);
+    phase_chunk_scan(g, hop_of(bd, h));
 }
 
 template <bool kSparse>
 __global__ void __launch_bounds__(kBatchThreads) k_emit(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 8 + 8 * h);
+    if (h >= 0) stamp(bd, 8 + 8 * h);
     if (kSparse)
-        phase_emit_sparse(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+        phase_emit_sparse(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
     else
-        phase_emit_dense(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, bd->n_chunks);
+        phase_emit_dense(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_relabel(const __grid_constant__ GraphDev g,
@@ -123,7 +142,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__
 
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
                  const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial)
+                 const Fork &fk, bool serial, int lp)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
@@ -133,8 +152,28 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
     // plan): a warp per half chunk.
     const int chunk_cap = (kSMs * 8 + B - 1) / B;
     int nk = 0;
-    k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
-    ++nk;
+    auto compaction = [&](int h, bool sparse) {
+        const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
+        const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
+        if (sparse)
+            k_bitcount<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        else
+            k_bitcount<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        k_cscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
+        if (sparse)
+            k_emit<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        else
+            k_emit<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+    };
+    if (lp >= 0) {   // link prediction: targets -> marks -> seed compaction -> pairs
+        k_lp_mark<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
+        compaction(-1, lp == 1);
+        k_lp_pairs<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
+        nk += 5;
+    } else {
+        k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
+        ++nk;
+    }
     for (int h = 0; h < n_hops; ++h) {
         const int wide = scan_blocks[h] * g.n_rel;   // count / scan: one block per virtual block
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
@@ -154,18 +193,7 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
-        const bool sparse = sparse_hop[h] != 0;
-        const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
-        const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
-        if (sparse)
-            k_bitcount<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        else
-            k_bitcount<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_cscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
-        if (sparse)
-            k_emit<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        else
-            k_emit<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        compaction(h, sparse_hop[h] != 0);
         nk += 8;
     }
     k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);

@@ -69,6 +69,22 @@ constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase times
 constexpr int kMaxStamps = 80;
 constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
 
+// Per-batch launch parameters copied H2D at the start of every launch (kDyn u64):
+//   [0] rng_seed  [1] n_seeds (node classification) / n_pos (link prediction)
+//   [2] seeds / positive src pointer when device-accessible, else 0 (staged copy)
+//   [3] positive dst pointer (LP)  [4] neg_seed (LP)  [5] relation (LP)
+constexpr int kDyn = 8;
+
+// Link-prediction targets of one batch (NEXT-3, DESIGN.md §3 L1-L4).
+struct LpDev {
+    int32_t n_neg;
+    int64_t cap_pos;              // pairs layout stride
+    const int64_t *src_stage;     // staged positives (pageable host input)
+    const int64_t *dst_stage;
+    int64_t *neg;                 // [cap_pos * n_neg] corrupted dst gids
+    int32_t *pairs;               // [pos_src cap][pos_dst cap][neg_src cap*n][neg_dst cap*n], local ids
+};
+
 // Everything a hop's kernels touch.
 struct HopDev {
     int32_t h;
@@ -105,6 +121,14 @@ struct HopDev {
 
 __device__ __forceinline__ int32_t *meta_nodes(int32_t *meta, int l) { return meta + kMetaNodes + l * EG_MAX_VT; }
 __device__ __forceinline__ int32_t *meta_nnz(int32_t *meta, int h) { return meta + kMetaNnz + h * EG_MAX_REL; }
+
+// |F_h[u]| before hop h's compaction; the link-prediction seed compaction runs as
+// "hop -1" over an empty frontier.
+__device__ const int32_t kNoNodes[EG_MAX_VT] = {0, 0, 0, 0, 0, 0, 0, 0};
+__device__ __forceinline__ const int32_t *nodes_before(const HopDev &hd)
+{
+    return hd.h < 0 ? kNoNodes : meta_nodes(hd.meta, hd.h);
+}
 
 // ------------------------------------------------------------------ ids / partition
 

@@ -108,6 +108,10 @@ struct Plan {
     int64_t selq_items[EG_MAX_HOPS] = {};
     int32_t scan_blocks[EG_MAX_HOPS] = {}, max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
     int32_t sparse[EG_MAX_HOPS] = {};   // compaction variant per hop (1 = lane-per-slice)
+    // link prediction (NEXT-3): n_cap = positives capacity; seeds <= n_cap * (2 + n_neg)
+    bool lp = false;
+    int32_t n_neg = 0, lp_sparse = 0;
+    size_t o_lp_src = 0, o_lp_dst = 0, o_lp_neg = 0, o_lp_pairs = 0;
     size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
     std::vector<Slot *> slots;
@@ -122,7 +126,7 @@ struct Slot {
     Plan *plan = nullptr;
     char *mem = nullptr;
     int32_t *h_meta = nullptr;   // pinned, B x kMetaSize
-    uint64_t *h_dyn = nullptr;   // pinned, B x {rng_seed, n_seeds}
+    uint64_t *h_dyn = nullptr;   // pinned, B x kDyn launch parameters (common.cuh)
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t done = nullptr, s0 = nullptr, s1 = nullptr, g0 = nullptr, g1 = nullptr;
     int refs = 0;                // live eg_blocks handles of the last launch
@@ -186,6 +190,12 @@ struct eg_blocks {
     int32_t *meta = nullptr;  // device
     int64_t n_nodes[EG_MAX_HOPS + 1][EG_MAX_VT] = {};
     int64_t nnz[EG_MAX_HOPS][EG_MAX_REL] = {};
+    // link prediction
+    bool lp = false;
+    int32_t lp_rel = 0, n_neg = 0;
+    int64_t n_pos = 0, cap_pos = 0;
+    int32_t *pairs = nullptr;
+    int64_t *neg = nullptr;
 };
 
 
@@ -749,13 +759,13 @@ eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
 namespace {
 
 eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, bool features, int32_t B,
-                   Plan **out)
+                   Plan **out, bool lp = false, int32_t n_neg = 0)
 {
     const GraphDev &g = c->g;
     const int V = g.n_vt, R = g.n_rel;
     for (Plan *p : c->plans)
-        if (p->n_hops == L && p->n_cap == n_cap && p->features == features && p->B == B &&
-            !memcmp(p->fanouts, fanouts, sizeof(int32_t) * L * R)) {
+        if (p->n_hops == L && p->n_cap == n_cap && p->features == features && p->B == B && p->lp == lp &&
+            p->n_neg == n_neg && !memcmp(p->fanouts, fanouts, sizeof(int32_t) * L * R)) {
             *out = p;
             return EG_OK;
         }
@@ -765,12 +775,15 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
     p->n_cap = n_cap;
     p->features = features;
     p->B = B;
+    p->lp = lp;
+    p->n_neg = n_neg;
+    const int64_t seed_cap = lp ? n_cap * (2 + (int64_t)n_neg) : n_cap;   // distinct endpoints (LP)
     int32_t src_vt[EG_MAX_REL], dst_vt[EG_MAX_REL];
     for (int r = 0; r < R; ++r) {
         src_vt[r] = g.rel[r].src_vt;
         dst_vt[r] = g.rel[r].dst_vt;
     }
-    compute_caps(V, c->vt_counts, R, src_vt, dst_vt, c->rel_edges_total, c->rel_max_degree, n_cap, L, fanouts,
+    compute_caps(V, c->vt_counts, R, src_vt, dst_vt, c->rel_edges_total, c->rel_max_degree, seed_cap, L, fanouts,
                  p->capF, p->capE);
     for (int h = 0; h <= L; ++h)
         for (int u = 0; u < V; ++u)
@@ -791,8 +804,15 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         return o;
     };
     p->o_meta = take(sizeof(int32_t) * kMetaSize);
-    p->o_dyn = take(sizeof(uint64_t) * 4);
-    p->o_seeds = take(sizeof(int64_t) * n_cap);
+    p->o_dyn = take(sizeof(uint64_t) * kDyn);
+    p->o_seeds = take(sizeof(int64_t) * (lp ? 1 : n_cap));
+    if (lp) {
+        p->o_lp_src = take(sizeof(int64_t) * n_cap);
+        p->o_lp_dst = take(sizeof(int64_t) * n_cap);
+        p->o_lp_neg = take(sizeof(int64_t) * n_cap * n_neg);
+        p->o_lp_pairs = take(sizeof(int32_t) * n_cap * (2 + 2 * (int64_t)n_neg));
+        p->lp_sparse = c->compact == 2 ? 1 : c->compact == 1 ? 0 : (seed_cap < c->g.boff[V] / 32 ? 1 : 0);
+    }
     for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
     for (int h = 0; h < L; ++h)
         for (int r = 0; r < R; ++r) {
@@ -865,6 +885,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     bd->n_chunks = c->n_chunks;
     bd->trace = c->trace ? 1 : 0;
     bd->B = B;
+    bd->lp = p->lp ? 1 : 0;
     GatherSet gs{};
     gs.nb = B;
     for (int b = 0; b < B; ++b) {
@@ -886,6 +907,18 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             hd.cap_nodes[u] = (int32_t)p->capF[L][u];
         }
         bd->seeds[b] = (const int64_t *)(base + p->o_seeds);
+        if (p->lp) {
+            HopDev x = hd;
+            x.h = -1;
+            bd->lph[b] = x;
+            LpDev &lp = bd->lpd[b];
+            lp.n_neg = p->n_neg;
+            lp.cap_pos = p->n_cap;
+            lp.src_stage = (const int64_t *)(base + p->o_lp_src);
+            lp.dst_stage = (const int64_t *)(base + p->o_lp_dst);
+            lp.neg = (int64_t *)(base + p->o_lp_neg);
+            lp.pairs = (int32_t *)(base + p->o_lp_pairs);
+        }
         for (int h = 0; h < L; ++h) {
             HopDev x = hd;
             x.h = h;
@@ -935,13 +968,13 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     for (int b = 0; b < B; ++b) {
         char *base = p->batch_base(sl->mem, b);
-        cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + 4 * b, sizeof(uint64_t) * 4, cudaMemcpyHostToDevice, cs);
+        cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + kDyn * b, sizeof(uint64_t) * kDyn, cudaMemcpyHostToDevice, cs);
         cudaMemsetAsync(base + p->o_meta, 0, sizeof(int32_t) * kMetaSize, cs);
     }
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
     nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->scan_blocks, p->sparse, c->n_chunks, B, cs,
-                       c->fork, c->trace);
+                       c->fork, c->trace, p->lp ? p->lp_sparse : -1);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -988,7 +1021,7 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
         return fail(c, EG_ENOMEM, std::string("batch slot cudaMalloc: ") + cudaGetErrorString(e));
     }
     EG_CUDA(c, cudaMallocHost(&sl->h_meta, sizeof(int32_t) * kMetaSize * p->B));
-    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * 4 * p->B));
+    EG_CUDA(c, cudaMallocHost(&sl->h_dyn, sizeof(uint64_t) * kDyn * p->B));
     EG_CUDA(c, cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming));
     EG_CUDA(c, cudaEventCreate(&sl->s0));
     EG_CUDA(c, cudaEventCreate(&sl->s1));
@@ -1085,7 +1118,9 @@ eg_status finish(eg_blocks *b)
     for (int h = 0; h < b->n_hops; ++h)
         for (int r = 0; r < b->n_rel; ++r) b->nnz[h][r] = m[kMetaNnz + h * EG_MAX_REL + r];
     const int32_t errbits = m[kMetaErr];
-    if (errbits & kErrSeedRange) return b->status = fail(c, EG_ERANGE, "seed gid outside [0, N_total)");
+    if (errbits & kErrSeedRange)
+        return b->status = fail(c, EG_ERANGE, b->lp ? "link-prediction endpoint outside its relation's vertex type"
+                                                    : "seed gid outside [0, N_total)");
     if (errbits & kErrSeedDup) return b->status = fail(c, EG_EINVAL, "duplicate seeds");
     if (errbits) {   // cannot happen with true upper bounds; the batch state is not trustworthy
         c->broken = true;
@@ -1101,10 +1136,32 @@ int64_t round_cap(int64_t n)
     return c;
 }
 
-// One launch for nb batches (nb <= the context's bundle size).
+// Link-prediction inputs of a bundle (NEXT-3).
+struct LpArgs {
+    const int64_t *const *src;
+    const int64_t *const *dst;
+    int32_t rel, n_neg;
+    const uint64_t *neg_seeds;
+};
+
+// A device pointer the kernels can read for host or device memory `p`, or 0 when `p`
+// is pageable host memory (then staged into the slot).
+uint64_t device_view(const void *p)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+        (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ||
+         (at.type == cudaMemoryTypeHost && at.devicePointer)))
+        return (uint64_t)(uintptr_t)(at.type == cudaMemoryTypeHost ? at.devicePointer : p);
+    cudaGetLastError();
+    return 0;
+}
+
+// One launch for nb batches (nb <= the context's bundle size).  n_seeds[b] = seeds of
+// batch b, or its positives for link prediction (lp != null: seeds unused).
 eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, const int64_t *n_seeds,
                          int32_t n_hops, const int32_t *fanouts, const uint64_t *rng_seeds, bool features,
-                         eg_blocks **out)
+                         eg_blocks **out, const LpArgs *lp = nullptr)
 {
     eg_status st = enter(c);
     if (st) return st;
@@ -1113,11 +1170,18 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
     if (nb < 1 || nb > kMaxBundle) return fail(c, EG_EINVAL, "bundle size out of [1, 16]");
     if (nb > c->bundle) return fail(c, EG_EINVAL, "bundle larger than eg_set_pipeline's bundle size");
     if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
-    if (!fanouts || !seeds || !n_seeds || !rng_seeds) return fail(c, EG_EINVAL, "null argument");
+    if (!fanouts || !n_seeds || !rng_seeds || (!lp && !seeds)) return fail(c, EG_EINVAL, "null argument");
+    if (lp) {
+        if (!lp->src || !lp->dst || !lp->neg_seeds) return fail(c, EG_EINVAL, "null argument");
+        if (lp->rel < 0 || lp->rel >= c->g.n_rel) return fail(c, EG_EINVAL, "relation out of range");
+        if (lp->n_neg < 0 || lp->n_neg > EG_MAX_NEG) return fail(c, EG_EINVAL, "n_neg out of [0, EG_MAX_NEG]");
+    }
     int64_t nmax = 0;
     for (int b = 0; b < nb; ++b) {
         out[b] = nullptr;
-        if (n_seeds[b] < 0 || (n_seeds[b] > 0 && !seeds[b])) return fail(c, EG_EINVAL, "bad seeds");
+        const bool bad = lp ? (n_seeds[b] > 0 && (!lp->src[b] || !lp->dst[b])) : (n_seeds[b] > 0 && !seeds[b]);
+        if (n_seeds[b] < 0 || bad) return fail(c, EG_EINVAL, lp ? "bad positives" : "bad seeds");
+        if (lp && n_seeds[b] >= ((int64_t)1 << 31)) return fail(c, EG_EINVAL, "more than 2^31 positives");
         nmax = std::max(nmax, n_seeds[b]);
     }
     for (int i = 0; i < n_hops * c->g.n_rel; ++i)
@@ -1125,33 +1189,37 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
     // a single batch uses a 1-batch plan; bundles use the context's bundle size
     const int32_t B = nb == 1 ? 1 : c->bundle;
     Plan *p = nullptr;
-    if ((st = get_plan(c, n_hops, fanouts, round_cap(nmax), features, B, &p))) return st;
+    if ((st = get_plan(c, n_hops, fanouts, round_cap(nmax), features, B, &p, lp != nullptr, lp ? lp->n_neg : 0)))
+        return st;
     Slot *sl = nullptr;
     if ((st = acquire_slot(c, p, &sl))) return st;
     Lane &ln = c->lanes[sl->lane];
-    EG_CUDA(c, cudaEventRecord(ln.ready, c->stream));          // seeds produced on the caller's stream
+    EG_CUDA(c, cudaEventRecord(ln.ready, c->stream));          // inputs produced on the caller's stream
     EG_CUDA(c, cudaStreamWaitEvent(ln.stream, ln.ready, 0));
     for (int b = 0; b < B; ++b) {
         const int64_t n = b < nb ? n_seeds[b] : 0;
-        uint64_t direct = 0;
-        if (n > 0) {
-            // device memory (or pinned host memory, read over PCIe): the seed split reads the
-            // caller's buffer in place; pageable host memory is staged into the slot
-            cudaPointerAttributes at;
-            if (cudaPointerGetAttributes(&at, seeds[b]) == cudaSuccess &&
-                (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ||
-                 (at.type == cudaMemoryTypeHost && at.devicePointer)))
-                direct = (uint64_t)(uintptr_t)(at.type == cudaMemoryTypeHost ? at.devicePointer : seeds[b]);
-            else {
-                cudaGetLastError();
-                EG_CUDA(c, cudaMemcpyAsync(p->batch_base(sl->mem, b) + p->o_seeds, seeds[b], sizeof(int64_t) * n,
-                                           cudaMemcpyDefault, ln.stream));
-            }
+        uint64_t *dyn = sl->h_dyn + (size_t)kDyn * b;
+        for (int k = 0; k < kDyn; ++k) dyn[k] = 0;
+        dyn[0] = b < nb ? rng_seeds[b] : 0;
+        dyn[1] = (uint64_t)n;
+        // device memory (or pinned host memory, read over PCIe): the kernels read the
+        // caller's buffer in place; pageable host memory is staged into the slot
+        char *base = p->batch_base(sl->mem, b);
+        auto place = [&](const int64_t *src, size_t off, uint64_t *slot) -> eg_status {
+            if (n <= 0) return EG_OK;
+            *slot = device_view(src);
+            if (!*slot)
+                EG_CUDA(c, cudaMemcpyAsync(base + off, src, sizeof(int64_t) * n, cudaMemcpyDefault, ln.stream));
+            return EG_OK;
+        };
+        if (!lp) {
+            if ((st = place(b < nb ? seeds[b] : nullptr, p->o_seeds, &dyn[2]))) return st;
+        } else {
+            if ((st = place(b < nb ? lp->src[b] : nullptr, p->o_lp_src, &dyn[2]))) return st;
+            if ((st = place(b < nb ? lp->dst[b] : nullptr, p->o_lp_dst, &dyn[3]))) return st;
+            dyn[4] = b < nb ? lp->neg_seeds[b] : 0;
+            dyn[5] = (uint64_t)lp->rel;
         }
-        sl->h_dyn[4 * b] = b < nb ? rng_seeds[b] : 0;
-        sl->h_dyn[4 * b + 1] = (uint64_t)n;
-        sl->h_dyn[4 * b + 2] = direct;
-        sl->h_dyn[4 * b + 3] = 0;
     }
     sl->timed = c->prof;
     sl->finished = false;
@@ -1169,6 +1237,15 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
         h->n_vt = c->g.n_vt;
         h->n_rel = c->g.n_rel;
         fill_views(p, p->batch_base(sl->mem, b), h);
+        if (lp) {
+            h->lp = true;
+            h->lp_rel = lp->rel;
+            h->n_neg = lp->n_neg;
+            h->n_pos = n_seeds[b];
+            h->cap_pos = p->n_cap;
+            h->pairs = (int32_t *)(p->batch_base(sl->mem, b) + p->o_lp_pairs);
+            h->neg = (int64_t *)(p->batch_base(sl->mem, b) + p->o_lp_neg);
+        }
         out[b] = h;
     }
     return EG_OK;
@@ -1211,6 +1288,51 @@ eg_status eg_sample_bundle(eg_ctx *c, int32_t n_batches, const int64_t *const *s
             return first;
         }
     }
+    return EG_OK;
+}
+
+eg_status eg_sample_lp_bundle(eg_ctx *c, int32_t n_batches, const int64_t *const *src, const int64_t *const *dst,
+                              const int64_t *n_pos, int32_t rel, int32_t n_neg, const uint64_t *neg_seeds,
+                              int32_t n_hops, const int32_t *fanouts, const uint64_t *rng_seeds, int32_t flags,
+                              eg_blocks **out)
+{
+    LpArgs lp{src, dst, rel, n_neg, neg_seeds};
+    eg_status st = enqueue_bundle(c, n_batches, nullptr, n_pos, n_hops, fanouts, rng_seeds,
+                                  (flags & EG_FEATURES) != 0, out, &lp);
+    if (st) return st;
+    if (!(flags & EG_ASYNC)) {
+        eg_status first = EG_OK;
+        for (int b = 0; b < n_batches; ++b) {
+            st = finish(out[b]);
+            if (st && !first) first = st;
+        }
+        if (first) {
+            for (int b = 0; b < n_batches; ++b) {
+                eg_blocks_free(out[b]);
+                out[b] = nullptr;
+            }
+            return first;
+        }
+    }
+    return EG_OK;
+}
+
+eg_status eg_lp_view_get(const eg_blocks *cb, eg_lp_view *out)
+{
+    if (!cb || !out) return EG_EINVAL;
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    if (!b->lp) return EG_EINVAL;
+    eg_status st = finish(b);
+    if (st) return st;
+    const int64_t cap = b->cap_pos, m = (int64_t)b->n_neg;
+    out->n_pos = b->n_pos;
+    out->n_neg = b->n_neg;
+    out->rel = b->lp_rel;
+    out->pos_src = b->pairs;
+    out->pos_dst = b->pairs + cap;
+    out->neg_src = b->pairs + 2 * cap;
+    out->neg_dst = b->pairs + 2 * cap + cap * m;
+    out->neg_dst_gid = b->neg;
     return EG_OK;
 }
 

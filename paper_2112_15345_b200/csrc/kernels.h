@@ -24,8 +24,11 @@ struct GatherSet {
 
 struct BatchDev {
     int32_t n_hops, n_chunks, trace, B;
+    int32_t lp;                            // link-prediction batches (seeds from targets)
     const int64_t *seeds[kMaxBundle];
     HopDev hop[kMaxBundle][EG_MAX_HOPS];
+    HopDev lph[kMaxBundle];                // LP seed compaction ("hop -1")
+    LpDev lpd[kMaxBundle];
 };
 
 // A side stream + two events to fork / join independent kernels inside a capture.
@@ -36,9 +39,10 @@ struct Fork {
 
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
 // returns the number of kernels.
+// lp >= 0: link-prediction batches, seed compaction variant lp (1 = sparse).
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
                  const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial);
+                 const Fork &fk, bool serial, int lp);
 
 // gather.cu
 void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);

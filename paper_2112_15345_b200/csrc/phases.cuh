@@ -1008,7 +1008,7 @@ __device__ void phase_chunk_scan(const GraphDev &g, const HopDev &hd)
 {
     __shared__ int32_t sh[33];
     int32_t *const nn = meta_nodes(hd.meta, hd.h + 1);
-    const int32_t *const nF = meta_nodes(hd.meta, hd.h);
+    const int32_t *const nF = nodes_before(hd);
     for (int u = 0; u < g.n_vt; ++u) {
         const int lo = (int)(g.boff[u] / kChunkBits), hi = (int)(g.boff[u + 1] / kChunkBits);
         const int per = (hi - lo + (int)blockDim.x - 1) / (int)blockDim.x;
@@ -1056,7 +1056,7 @@ __device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, 
         const int64_t bit0 = c * kChunkBits;
         int u = 0;
         while (bit0 >= g.boff[u + 1]) ++u;
-        int32_t position = meta_nodes(hd.meta, hd.h)[u] + __ldcg(hd.chunk_pre + c) + ex;
+        int32_t position = nodes_before(hd)[u] + __ldcg(hd.chunk_pre + c) + ex;
         const int32_t cap = hd.cap_nodes[u];
         int64_t *const nodes = hd.nodes[u];
         const int64_t w0 = c * kChunkWords + sl * kLaneWords;
@@ -1168,7 +1168,7 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
             while (bit0 >= g.boff[u + 1]) ++u;
             const int32_t uc = __ldcg(hd.seg_cnt + (int64_t)c * 32 + lane);   // unit `lane` of the chunk
             const int32_t uex = warp_incl_scan(uc) - uc;
-            const int32_t base = meta_nodes(hd.meta, hd.h)[u] + __ldcg(hd.chunk_pre + c);
+            const int32_t base = nodes_before(hd)[u] + __ldcg(hd.chunk_pre + c);
             const int32_t cap = hd.cap_nodes[u];
             int64_t *const nodes = hd.nodes[u];
             const int64_t gid0 = g.off[u] - g.boff[u];   // gid of bitmap bit b = gid0 + b
@@ -1206,6 +1206,69 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
                     ++position;
                 }
             }
+        }
+    }
+}
+
+// ============================================================================ link prediction
+
+// Link-prediction targets (NEXT-3, DESIGN.md §3 L1-L4): per positive (src_i, dst_i) of
+// relation r, n_neg corrupted dsts drawn uniformly from t(r)'s range; every endpoint is
+// marked in the bitmap so that the ordinary compaction (run as "hop -1" over an empty
+// frontier) yields the distinct endpoints in ascending gid as the seeds F_0.
+__device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
+{
+    const int64_t n = (int64_t)hd.dyn[1];
+    const int64_t *__restrict__ src = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : lp.src_stage;
+    const int64_t *__restrict__ dst = hd.dyn[3] ? (const int64_t *)hd.dyn[3] : lp.dst_stage;
+    const uint32_t k0 = (uint32_t)hd.dyn[4], k1 = (uint32_t)(hd.dyn[4] >> 32);
+    const int r = (int)hd.dyn[5];
+    const int sv = g.rel[r].src_vt, tv = g.rel[r].dst_vt;
+    const int64_t s_lo = g.off[sv], s_hi = g.off[sv + 1], t_lo = g.off[tv], t_hi = g.off[tv + 1];
+    const int64_t sb = g.boff[sv] - s_lo, tb = g.boff[tv] - t_lo;   // bitmap bit of gid = base + gid
+    const uint64_t n_t = (uint64_t)(t_hi - t_lo);
+    const int n_neg = lp.n_neg;
+    uint32_t *const bitmap = hd.bitmap;
+    uint32_t *const summary = hd.summary;
+    int64_t *const neg = lp.neg;
+    for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
+        const int64_t a = src[i], b = dst[i];
+        if (a < s_lo || a >= s_hi || b < t_lo || b >= t_hi) {
+            atomicOr(hd.meta + kMetaErr, kErrSeedRange);
+            continue;
+        }
+        mark_src(bitmap, summary, (uint32_t)a, sb);
+        mark_src(bitmap, summary, (uint32_t)b, tb);
+        for (int q = 0; q < n_neg; ++q) {
+            uint32_t c0 = (uint32_t)i, c1 = (uint32_t)q, c2 = 0u, c3 = 0x4E454721u;   // 'NEG!'
+            philox4x32_10(c0, c1, c2, c3, k0, k1);
+            const int64_t x = t_lo + (int64_t)(((uint64_t)c0 * n_t) >> 32);
+            neg[i * n_neg + q] = x;
+            mark_src(bitmap, summary, (uint32_t)x, tb);
+        }
+    }
+}
+
+// After the seed compaction: every pair in local ids (pos[] = index among the seeds of
+// the endpoint's type).
+__device__ void phase_lp_pairs(const GraphDev &, const HopDev &hd, const LpDev &lp, int bid, int nb)
+{
+    const int64_t n = (int64_t)hd.dyn[1];
+    const int64_t *__restrict__ src = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : lp.src_stage;
+    const int64_t *__restrict__ dst = hd.dyn[3] ? (const int64_t *)hd.dyn[3] : lp.dst_stage;
+    const int32_t *const pos = hd.pos;
+    const int n_neg = lp.n_neg;
+    const int64_t cap = lp.cap_pos;
+    int32_t *const pairs = lp.pairs;
+    const int64_t *const neg = lp.neg;
+    if (*(volatile int32_t *)(hd.meta + kMetaErr)) return;   // a range error: pos[] is not valid
+    for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
+        const int32_t ps = __ldcg(pos + src[i]);
+        pairs[i] = ps;
+        pairs[cap + i] = __ldcg(pos + dst[i]);
+        for (int q = 0; q < n_neg; ++q) {
+            pairs[2 * cap + i * n_neg + q] = ps;
+            pairs[2 * cap + cap * n_neg + i * n_neg + q] = __ldcg(pos + neg[i * n_neg + q]);
         }
     }
 }

@@ -29,7 +29,7 @@ ABI_SYMBOLS = [
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
-    "eg_blocks_stats",
+    "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get",
 ]
 
 EG_FEATURES = 1
@@ -101,6 +101,12 @@ class BlockView(ctypes.Structure):
                 ("eids", ctypes.c_void_p * EG_MAX_REL), ("nnz", ctypes.c_int64 * EG_MAX_REL)]
 
 
+class LpView(ctypes.Structure):
+    _fields_ = [("n_pos", ctypes.c_int64), ("n_neg", ctypes.c_int32), ("rel", ctypes.c_int32),
+                ("pos_src", ctypes.c_void_p), ("pos_dst", ctypes.c_void_p), ("neg_src", ctypes.c_void_p),
+                ("neg_dst", ctypes.c_void_p), ("neg_dst_gid", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -128,6 +134,9 @@ def lib(build_if_missing: bool = True):
         L.eg_attach_peer.argtypes = [vp, vp]
         L.eg_set_pipeline.argtypes = [vp, c.c_int32, c.c_int32]
         L.eg_sample_bundle.argtypes = [vp, c.c_int32, vp, vp, c.c_int32, vp, vp, c.c_int32, vp]
+        L.eg_sample_lp_bundle.argtypes = [vp, c.c_int32, vp, vp, vp, c.c_int32, c.c_int32, vp, c.c_int32, vp, vp,
+                                          c.c_int32, vp]
+        L.eg_lp_view_get.argtypes = [vp, P(LpView)]
         L.eg_trace_get.argtypes = [vp, c.c_int32, c.c_char_p, c.c_size_t, P(c.c_double), P(c.c_int64)]
         L.eg_trace_get.restype = c.c_int32
         L.eg_check_shard_metas.argtypes = [c.c_int32, vp, vp, vp, c.c_char_p, c.c_size_t]
@@ -293,6 +302,21 @@ class Blocks:
     def n_inputs(self, u) -> int:
         self.views
         return int(lib().eg_blocks_n_inputs(self._h, u))
+
+    def lp(self):
+        """Pairs of a link-prediction batch as zero-copy device tensors: pos_src,
+        pos_dst [n_pos], neg_src, neg_dst [n_pos * n_neg] (int32 local ids = positions
+        in block 0's dst nodes of the endpoint's type) and neg_dst_gid (int64)."""
+        v = LpView()
+        rc = lib().eg_lp_view_get(self._h, ctypes.byref(v))
+        if rc:
+            raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        n, m = int(v.n_pos), int(v.n_pos) * int(v.n_neg)
+        d = self._ctx.device
+        return {"n_pos": n, "n_neg": int(v.n_neg), "rel": int(v.rel),
+                "pos_src": _wrap(v.pos_src, n, "<i4", self, d), "pos_dst": _wrap(v.pos_dst, n, "<i4", self, d),
+                "neg_src": _wrap(v.neg_src, m, "<i4", self, d), "neg_dst": _wrap(v.neg_dst, m, "<i4", self, d),
+                "neg_dst_gid": _wrap(v.neg_dst_gid, m, "<i8", self, d)}
 
     def features(self, u):
         """Feature rows of the input vertices of type u gathered in the same graph
@@ -476,6 +500,45 @@ class Context:
                                            ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_bundle")
         L = fo.shape[0]
         return [Blocks(self, outs[i], L) for i in range(n)]
+
+    def sample_lp_bundle(self, src_list, dst_list, rel: int, n_neg: int, neg_seeds, fanouts, rng_seeds,
+                         features: bool = True, async_: bool = False):
+        """Link-prediction mini-batches (positives (src, dst) of relation rel + n_neg
+        corrupted dsts each) as ONE graph launch; one Blocks per batch, with .lp()."""
+        torch = _torch()
+        fo = np.ascontiguousarray(fanouts, np.int32)
+        n = len(src_list)
+        assert len(dst_list) == n
+        sp, dp = (ctypes.c_void_p * n)(), (ctypes.c_void_p * n)()
+        cnts = np.zeros(n, np.int64)
+        keep = []
+        for i, (a, b) in enumerate(zip(src_list, dst_list)):
+            for arr, tab in ((a, sp), (b, dp)):
+                if isinstance(arr, np.ndarray):
+                    arr = np.ascontiguousarray(arr, np.int64)
+                    keep.append(arr)
+                    tab[i] = arr.ctypes.data
+                    m = len(arr)
+                else:
+                    assert arr.dtype == torch.int64 and arr.is_contiguous()
+                    tab[i] = arr.data_ptr()
+                    m = arr.numel()
+                assert tab is sp or m == cnts[i], "src / dst lengths differ"
+                cnts[i] = m
+        ns = np.ascontiguousarray([int(x) & (2**64 - 1) for x in neg_seeds], np.uint64)
+        rs = np.ascontiguousarray([int(x) & (2**64 - 1) for x in rng_seeds], np.uint64)
+        outs = (ctypes.c_void_p * n)()
+        flags = (EG_FEATURES if features else 0) | (EG_ASYNC if async_ else 0)
+        self._check(lib().eg_sample_lp_bundle(self._h, n, ctypes.cast(sp, ctypes.c_void_p),
+                                              ctypes.cast(dp, ctypes.c_void_p), cnts.ctypes.data, rel, n_neg,
+                                              ns.ctypes.data, fo.shape[0], fo.ctypes.data, rs.ctypes.data, flags,
+                                              ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_lp_bundle")
+        return [Blocks(self, outs[i], fo.shape[0]) for i in range(n)]
+
+    def sample_lp(self, src, dst, rel: int, n_neg: int, neg_seed: int, fanouts, rng_seed: int,
+                  features: bool = True, async_: bool = False) -> Blocks:
+        """One link-prediction mini-batch (eg_sample_lp_bundle with one batch)."""
+        return self.sample_lp_bundle([src], [dst], rel, n_neg, [neg_seed], fanouts, [rng_seed], features, async_)[0]
 
     def gather_features(self, blocks: Blocks, out=None, types=None):
         """Feature rows of the input vertices per type (None for types without

@@ -335,6 +335,35 @@ def batch_seeds(cfg: Config, g: int, batch: int | None = None) -> np.ndarray:
     return (perm[k * B:(k + 1) * B] + int(cfg.offsets[cfg.seed_vt])).astype(np.int64)
 
 
+# link-prediction inputs (NEXT-3): the paper trains LP on all edges with
+# fanout 25, 15; a batch is a seeded uniform draw of existing edges.
+LP_TAG = 0x4C50   # 'LP'
+
+
+def lp_fanouts(cfg: Config) -> list:
+    return [[25] * cfg.n_rel, [15] * cfg.n_rel]
+
+
+def lp_rel(cfg: Config) -> int:
+    """The relation LP batches train on: the first one into the seed type."""
+    return next(r for r, x in enumerate(cfg.rels) if x[2] == cfg.seed_vt)
+
+
+def lp_positives(cfg: Config, graph, rel: int, g: int, n: int | None = None):
+    """Positive edges (src gid, dst gid) of global LP batch g: n uniformly drawn edge
+    positions of relation rel (with repetition), their dst from the CSC row and their
+    src from the generator's source formula (no host copy of the indices needed)."""
+    n = cfg.batch if n is None else n
+    ip = graph.indptr[rel]
+    E = int(ip[-1])
+    rng = np.random.default_rng([int(cfg.gen_seed & 0xFFFFFFFF), LP_TAG, rel, g])
+    e = rng.integers(0, E, n).astype(np.int64)
+    _, s, t, _ = cfg.rels[rel]
+    dst = np.searchsorted(ip, e, side="right") - 1 + int(cfg.offsets[t])
+    src = np.array([int(gen_indices(cfg, rel, int(x), int(x) + 1)[0]) for x in e], np.int64) + int(cfg.offsets[s])
+    return src, dst.astype(np.int64)
+
+
 def rng_seed(cfg: Config, g: int) -> int:
     return int(lib().sy_mix(cfg.base_rng ^ g))
 
