@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=256)
     ap.add_argument("--warmup", type=int, default=32)
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--task", default="nc", choices=["nc", "lp"],
+                    help="nc: node-classification batches (seed vertices, the headline); lp: link-prediction "
+                         "batches (NEXT-3: cfg.batch positive edges + 1 negative each, fanout [25, 15])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
     ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
@@ -73,7 +76,28 @@ def cpu_model():
     return "unknown"
 
 
-def workload(cfg, world):
+LP_NEG = 1   # negatives per positive edge in --task lp
+LP_NEG_KEY = 0x4E4547   # neg_seed(g) = rng_seed(g) ^ LP_NEG_KEY
+
+
+def task_fanouts(cfg, task):
+    import synth
+    return synth.lp_fanouts(cfg) if task == "lp" else cfg.fanouts
+
+
+def workload(cfg, world, task="nc"):
+    import synth
+    if task == "lp":
+        rel = synth.lp_rel(cfg)
+        return {"workload": f"{cfg.name} link prediction: {cfg.batch} positive edges of relation "
+                            f"{cfg.rels[rel][0]} + {LP_NEG} uniform negative each (seeds = distinct endpoints), "
+                            f"fanout [25, 15] (P:970-971); graph: {cfg.description}",
+                "task": "lp", "positives_per_rank": cfg.batch, "negatives_per_positive": LP_NEG,
+                "fanouts": synth.lp_fanouts(cfg), "n_vertices": int(cfg.vt_counts.sum()),
+                "n_edges": int(sum(r[3] for r in cfg.rels)), "ranks": world,
+                "partition": "per-type vertex range, floor(p*N_t/P)",
+                "l2": "inputs larger than L2 (feature store %.2f GB, random rows)" % (
+                    sum(cfg.row_bytes(u) * int(cfg.vt_counts[u]) for u in cfg.feats) / 1e9)}
     return {"workload": f"{cfg.name}: {cfg.description}", "batch_per_rank": cfg.batch, "fanouts": cfg.fanouts,
             "n_vertices": int(cfg.vt_counts.sum()), "n_edges": int(sum(r[3] for r in cfg.rels)),
             "ranks": world, "partition": "per-type vertex range, floor(p*N_t/P)",
@@ -138,7 +162,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- oracle timing
 
-def time_oracle(cfg, graph, host_rows, batches, budget_s, min_batches=1):
+def time_oracle(cfg, graph, host_rows, batches, budget_s, min_batches=1, task="nc"):
     """The oracle as it stands (single-threaded C), sample + gather per batch.
 
     host_rows None (C4 / C5: the feature store does not fit the host): the rows of the
@@ -153,10 +177,18 @@ def time_oracle(cfg, graph, host_rows, batches, budget_s, min_batches=1):
     gathered = 0
     spent = 0.0
     for g in batches:
-        seeds = synth.batch_seeds(cfg, g)
-        t0 = time.perf_counter()
-        res = oracle.sample(graph, seeds, cfg.fanouts, synth.rng_seed(cfg, g))
-        spent += time.perf_counter() - t0
+        if task == "lp":
+            rel = synth.lp_rel(cfg)
+            src, dst = synth.lp_positives(cfg, graph, rel, g)
+            t0 = time.perf_counter()
+            res, _ = oracle.sample_lp(graph, src, dst, rel, LP_NEG, synth.rng_seed(cfg, g) ^ LP_NEG_KEY,
+                                      synth.lp_fanouts(cfg), synth.rng_seed(cfg, g))
+            spent += time.perf_counter() - t0
+        else:
+            seeds = synth.batch_seeds(cfg, g)
+            t0 = time.perf_counter()
+            res = oracle.sample(graph, seeds, cfg.fanouts, synth.rng_seed(cfg, g))
+            spent += time.perf_counter() - t0
         n_edges += sum(len(b.eids) for hop in res.blocks for b in hop)
         for u in cfg.feats:
             if host_rows is not None:
@@ -184,12 +216,12 @@ def run_reference(args, cfg, rank, world):
     graph = synth.build_host_graph(cfg, materialize_indices=True)
     rows = {u: synth.host_features(cfg, u) for u in cfg.feats} if cfg.name in ("C1", "C2", "C3") else None
     for b in range(args.warmup):
-        time_oracle(cfg, graph, rows, [b * world], 0.0)
+        time_oracle(cfg, graph, rows, [b * world], 0.0, task=args.task)
     per_step = []
     edges = 0
     nbytes = 0
     for b in range(args.warmup, args.warmup + args.steps):
-        r = time_oracle(cfg, graph, rows, [b * world], 0.0)
+        r = time_oracle(cfg, graph, rows, [b * world], 0.0, task=args.task)
         per_step.append(r["seconds"])
         edges += r["edges"]
         nbytes += r["bytes"]
@@ -198,7 +230,7 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/bytes",
-            "data": "synthetic", "config": workload(cfg, 1),
+            "data": "synthetic", "config": workload(cfg, 1, args.task),
             "minibatches_per_s": args.steps / total, "gather_GBps": nbytes / total / 1e9,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{args.steps} full {cfg.name} batches (sample+compact+gather), one step "
@@ -261,19 +293,30 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_load = time.perf_counter() - t_load
     W, K = args.warmup, args.steps
     steps = W + K
-    seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
     rngs = [synth.rng_seed(cfg, b * world + rank) for b in range(steps)]
-    seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
-    fanouts = np.array(cfg.fanouts, np.int32)
+    fanouts = np.array(task_fanouts(cfg, args.task), np.int32)
+    lp = args.task == "lp"
+    if lp:   # link prediction: positives (src, dst) per batch; inputs[b] = (src, dst)
+        rel = synth.lp_rel(cfg)
+        seeds_host = [synth.lp_positives(cfg, graph, rel, b * world + rank) for b in range(steps)]
+        seeds_dev = [(torch.from_numpy(a).to(dev), torch.from_numpy(c).to(dev)) for a, c in seeds_host]
+        negs = [r ^ LP_NEG_KEY for r in rngs]
+    else:
+        seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
+        seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
     row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
     torch.cuda.synchronize(dev)
 
-    def launch(b0, b1, seeds):
+    def launch(b0, b1, seeds, features=True):
         # one CUDA-graph launch for batches b0..b1-1: sample + compact all hops + gather
         # features; no host sync
+        if lp:
+            return ctx.sample_lp_bundle([seeds[b][0] for b in range(b0, b1)], [seeds[b][1] for b in range(b0, b1)],
+                                        rel, LP_NEG, negs[b0:b1], fanouts, rngs[b0:b1], features=features,
+                                        async_=True)
         if b1 - b0 == 1 and args.bundle == 1:
-            return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=True, async_=True)]  # noqa
-        return ctx.sample_bundle([seeds[b] for b in range(b0, b1)], fanouts, rngs[b0:b1], features=True,
+            return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=features, async_=True)]  # noqa
+        return ctx.sample_bundle([seeds[b] for b in range(b0, b1)], fanouts, rngs[b0:b1], features=features,
                                  async_=True)
 
     def retire(bl):
@@ -351,10 +394,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     # e2e: host seeds in (pinned), features out to pinned host memory, through the C ABI
     e2e = None
     if not args.no_e2e:
-        pinned_seeds = [torch.from_numpy(s).pin_memory() for s in seeds_host]
+        if lp:
+            pinned_seeds = [(torch.from_numpy(a).pin_memory(), torch.from_numpy(c).pin_memory()) for a, c in seeds_host]
+        else:
+            pinned_seeds = [torch.from_numpy(s).pin_memory() for s in seeds_host]
         caps_nodes, _ = __import__("paper_2112_15345_b200").batch_caps(
             cfg.vt_counts, [r[1] for r in cfg.rels], [r[2] for r in cfg.rels], [r[3] for r in cfg.rels],
-            [cfg.dmax(r) for r in range(cfg.n_rel)], cfg.batch, fanouts)
+            [cfg.dmax(r) for r in range(cfg.n_rel)], cfg.batch * (2 + LP_NEG) if lp else cfg.batch, fanouts)
         host_outs = [None] * cfg.n_vt
         for u in cfg.feats:
             dim, dt = cfg.feats[u]
@@ -375,7 +421,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         def e2e_count(bl):
             e, nb = e2e_retire(bl)
             e2e_acc["edges"] += e
-            e2e_acc["h2d"] += cfg.batch * 8
+            e2e_acc["h2d"] += cfg.batch * (16 if lp else 8)
             e2e_acc["d2h"] += nb + 576
 
         with torch.cuda.stream(stream):
@@ -421,7 +467,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms}
     if world > 1:
         with torch.cuda.stream(stream):
-            bl = ctx.sample_minibatch(seeds_dev[0], fanouts, rngs[0], features=False)
+            bl = launch(0, 1, seeds_dev, features=False)[0]
             bl.wait()
             remote = 0
             rows_tot = 0
@@ -448,7 +494,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         full = cfg.name in ("C1", "C2", "C3")
         rows_h = {u: synth.host_features(cfg, u) for u in cfg.feats} if full else None
-        r = time_oracle(cfg, graph, rows_h, range(1000, 100000), args.cpu_seconds)
+        r = time_oracle(cfg, graph, rows_h, range(1000, 100000), args.cpu_seconds, task=args.task)
         cpu = {"value": r["edges"] / r["seconds"], "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{r['batches']} full {cfg.name} batches (sample+compact+gather) in "
                          f"{r['seconds']:.1f} s, single-threaded C oracle on {cpu_model()} "
@@ -461,7 +507,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "int32 ids / raw feature bytes (%s)" % ",".join(
                     sorted({"fp32" if cfg.feats[u][1] == 0 else "fp16" for u in cfg.feats})),
-                "data": "synthetic (seeded generator, synth/)", "config": workload(cfg, world),
+                "data": "synthetic (seeded generator, synth/)", "config": workload(cfg, world, args.task),
                 "minibatches_per_s": world * K / (ms / 1e3),
                 "gather_GBps": achieved if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),

@@ -58,6 +58,7 @@ def lib():
         L.sy_indptr.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_double, c.c_void_p]
         L.sy_indptr.restype = c.c_int
         L.sy_indices.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_void_p]
+        L.sy_indices_at.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_void_p, c.c_int64, c.c_void_p]
         L.sy_features.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
         L.sy_features_ids.argtypes = [c.c_uint64, c.c_int32, c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
         L.sy_select_train.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_uint64, c.c_void_p, c.c_int64]
@@ -360,7 +361,9 @@ def lp_positives(cfg: Config, graph, rel: int, g: int, n: int | None = None):
     e = rng.integers(0, E, n).astype(np.int64)
     _, s, t, _ = cfg.rels[rel]
     dst = np.searchsorted(ip, e, side="right") - 1 + int(cfg.offsets[t])
-    src = np.array([int(gen_indices(cfg, rel, int(x), int(x) + 1)[0]) for x in e], np.int64) + int(cfg.offsets[s])
+    tid = np.empty(n, np.int32)
+    lib().sy_indices_at(cfg.gen_seed, rel, int(cfg.vt_counts[s]), e.ctypes.data, n, tid.ctypes.data)
+    src = tid.astype(np.int64) + int(cfg.offsets[s])
     return src, dst.astype(np.int64)
 
 

@@ -103,6 +103,13 @@ void sy_indices(uint64_t G, int32_t r, int64_t n_src, int64_t e_lo, int64_t e_hi
 }
 
 /* feature rows [tid_lo, tid_hi) of vertex type u, dim columns, dtype 0=f32 1=f16 */
+/* src tids of the given CSC positions of relation r (link-prediction positives) */
+void sy_indices_at(uint64_t G, int32_t r, int64_t n_src, const int64_t *e, int64_t n, int32_t *out)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = sy_src_tid(G, r, e[i], n_src);
+}
+
 void sy_features(uint64_t G, int32_t u, int64_t tid_lo, int64_t tid_hi, int64_t dim,
                  int32_t dtype, void *out)
 {
