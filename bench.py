@@ -45,6 +45,9 @@ def parse():
                     help="nc: node-classification batches (seed vertices, the headline); lp: link-prediction "
                          "batches (NEXT-3: cfg.batch positive edges + 1 negative each, fanout [25, 15])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--features", default="device", choices=["device", "host"],
+                    help="feature rows in HBM (default) or in pinned host memory read zero-copy over PCIe "
+                         "(NEXT-4 ii: the paper's placement, lets C5 run on one GPU)")
     ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
     ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -286,7 +289,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                                    (world == 1 and not args.no_cpu_baseline))
     t_load = time.perf_counter()
     ctx = Context(rank, world, local_rank, stream)
-    shard = load_context(ctx, graph, world, rank, dev)
+    shard = load_context(ctx, graph, world, rank, dev, features=args.features if args.features != "device" else True)
     if world > 1:
         ctx.connect_peers()
     ctx.set_pipeline(args.depth, args.bundle)
@@ -344,12 +347,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                 on_retire(bl)
                 bl.free()
 
-    acc = {"edges": 0, "gbytes": 0}
+    acc = {"edges": 0, "gbytes": 0, "rbytes": 0}
 
     def count(bl):
         e, rows = retire(bl)
         acc["edges"] += e
         acc["gbytes"] += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
+        acc["rbytes"] += sum(rows[u] * row_bytes[u] for u in cfg.feats)
 
     with torch.cuda.stream(stream):
         run(0, W, seeds_dev, retire)
@@ -490,6 +494,29 @@ def run_ours(args, cfg, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": nv_bytes, "remote_row_fraction": frac_remote,
                          "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak}})
 
+    if args.features != "device":
+        # rows read zero-copy over PCIe: bound = the measured pinned host -> device copy bandwidth
+        src = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        dst = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            with torch.cuda.stream(stream):
+                dst.copy_(src, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            best = max(best, (1 << 30) / (a.elapsed_time(b) / 1e3) / 1e9)
+        del src, dst
+        pc_bytes = acc["rbytes"] / n_launch
+        pc_achieved = pc_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
+        roofline.update({"kernel": "gather_ldg_kernel", "bound": "pcie", "achieved": pc_achieved, "peak": best,
+                         "frac": pc_achieved / best if best else None,
+                         "peak_source": "measured here: pinned host -> device copy of 1 GiB (best of 5, CUDA events)",
+                         "per_unit": "row_bytes per input row read zero-copy from pinned host memory",
+                         "algorithmic_bytes_per_launch": pc_bytes, "traffic": None,
+                         "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak}})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         full = cfg.name in ("C1", "C2", "C3")
@@ -507,7 +534,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "int32 ids / raw feature bytes (%s)" % ",".join(
                     sorted({"fp32" if cfg.feats[u][1] == 0 else "fp16" for u in cfg.feats})),
-                "data": "synthetic (seeded generator, synth/)", "config": workload(cfg, world, args.task),
+                "data": "synthetic (seeded generator, synth/)", "config": dict(workload(cfg, world, args.task), features_in=(
+                    "pinned host memory (zero-copy over PCIe)" if args.features == "host" else "HBM")),
                 "minibatches_per_s": world * K / (ms / 1e3),
                 "gather_GBps": achieved if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),

@@ -80,9 +80,14 @@ typedef struct {
     int64_t edge_base;       /* global CSC position of local edge 0 (edge ids = base + local pos) */
 } eg_relation;
 
-/* One vertex type's feature shard on this rank (borrowed, device memory). */
+/* One vertex type's feature shard on this rank (borrowed).  rows may be device memory
+ * or, at world 1, pinned / registered host memory (cudaHostAlloc, cudaHostRegister):
+ * the gather kernel then reads the rows zero-copy over PCIe -- the paper's placement of
+ * graph data in CPU memory (SURVEY §8f NEXT-4 ii), which lets a
+ * feature store larger than HBM (C5: 187 GB) serve one GPU.  Pageable host memory, or
+ * host memory at world > 1, is EG_EINVAL. */
 typedef struct {
-    const void *rows;        /* device, n_local_rows x row_bytes, row-major; NULL: no features */
+    const void *rows;        /* n_local_rows x row_bytes, row-major; NULL: no features */
     int64_t row_bytes;       /* multiple of 16 (or 0 when rows == NULL) */
 } eg_features;
 

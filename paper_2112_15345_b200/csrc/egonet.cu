@@ -150,6 +150,7 @@ struct eg_ctx {
     // own shard (for export)
     eg_relation own_rel[EG_MAX_REL] = {};
     eg_features own_feat[EG_MAX_VT] = {};
+    bool host_feat[EG_MAX_VT] = {};                  // feature rows in pinned host memory (PCIe)
     // pipeline: `depth` lanes, each carrying bundles of up to `bundle` batches
     std::vector<Lane> lanes;
     int next_lane = 0;
@@ -624,7 +625,27 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
             return fail(c, EG_EINVAL, "row_bytes must be a positive multiple of 16");
         if (!F.rows && F.row_bytes > 0 && n_rows > 0)
             return fail(c, EG_EINVAL, "feature rows missing for a non-empty local range");
-        c->f.rows[t][c->rank] = (const uint8_t *)F.rows;
+        const void *rows_dev = F.rows;
+        c->host_feat[t] = false;
+        if (F.rows) {
+            // device memory, or pinned / registered host memory read zero-copy over PCIe by
+            // the gather kernel (the paper's placement of graph data in CPU memory)
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, F.rows) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, EG_EINVAL, "feature rows: not device, pinned or registered host memory");
+            }
+            if (at.type == cudaMemoryTypeHost) {
+                if (!at.devicePointer) return fail(c, EG_EINVAL, "feature rows: host memory not mapped for the device");
+                if (c->world > 1)
+                    return fail(c, EG_EINVAL, "host-memory feature rows are supported at world 1 only");
+                rows_dev = at.devicePointer;
+                c->host_feat[t] = true;
+            } else if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) {
+                return fail(c, EG_EINVAL, "feature rows: pageable host memory (pin or register it)");
+            }
+        }
+        c->f.rows[t][c->rank] = (const uint8_t *)rows_dev;
         c->f.row_bytes[t] = F.row_bytes;
         c->own_feat[t] = F;
     }

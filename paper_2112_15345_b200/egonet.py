@@ -380,7 +380,8 @@ class Context:
 
     def load_partition(self, vt_counts, rels, feats, bounds=None):
         """rels: list of dicts {src_vt, dst_vt, indptr (cuda int64), indices (cuda int32), edge_base};
-        feats: list (per type) of cuda tensors [n_local_rows, ...] or None."""
+        feats: list (per type) of cuda tensors [n_local_rows, ...], pinned CPU tensors
+        (world 1: gathered zero-copy over PCIe) or None."""
         vtc = np.ascontiguousarray(vt_counts, np.int64)
         self.vt_counts = vtc
         R = len(rels)
@@ -399,7 +400,9 @@ class Context:
                 farr[u] = Features(None, 0)
                 self.row_bytes.append(0)
             else:
-                assert t.is_cuda and t.is_contiguous()
+                # cuda tensors, or CPU tensors (pinned: read zero-copy over PCIe at world 1; the
+                # library rejects pageable memory with EG_EINVAL)
+                assert t.is_contiguous()
                 rb = t.stride(0) * t.element_size() if t.dim() > 1 else t.element_size()
                 farr[u] = Features(t.data_ptr() if t.numel() else None, rb)
                 self.row_bytes.append(rb)

@@ -32,7 +32,24 @@ def feature_shard(cfg: Config, u: int, lo: int, hi: int, device):
     return t
 
 
-def device_shard(graph: HostGraph, world: int, rank: int, device, features: bool = True):
+def host_feature_shard(cfg: Config, u: int, lo: int, hi: int):
+    """The same rows in pinned host memory (NEXT-4 ii: features in CPU memory, read
+    zero-copy by the gather kernel over PCIe)."""
+    from . import lib
+    torch = _torch()
+    dim, dt = cfg.feats[u]
+    tdt = torch.float32 if dt == 0 else torch.float16
+    t = torch.empty((hi - lo, dim), dtype=tdt, pin_memory=True)
+    step = 1 << 22   # rows per generator call (OpenMP inside)
+    base = t.data_ptr()
+    rb = t.element_size() * dim
+    for a in range(lo, hi, step):
+        b = min(hi, a + step)
+        lib().sy_features(cfg.gen_seed, u, a, b, dim, dt, ctypes.c_void_p(base + (a - lo) * rb))
+    return t
+
+
+def device_shard(graph: HostGraph, world: int, rank: int, device, features=True):
     """Returns dict(vt_counts, bounds, rels=[{src_vt,dst_vt,indptr,indices,edge_base}], feats=[tensor|None])."""
     torch = _torch()
     cfg = graph.cfg
@@ -56,7 +73,9 @@ def device_shard(graph: HostGraph, world: int, rank: int, device, features: bool
                          "edge_base": rs.e_lo})
     feats = []
     for u in range(cfg.n_vt):
-        if features and u in cfg.feats:
+        if features == "host" and u in cfg.feats:
+            feats.append(host_feature_shard(cfg, u, int(bounds[u][rank]), int(bounds[u][rank + 1])))
+        elif features and u in cfg.feats:
             feats.append(feature_shard(cfg, u, int(bounds[u][rank]), int(bounds[u][rank + 1]), device))
         else:
             feats.append(None)
@@ -64,8 +83,9 @@ def device_shard(graph: HostGraph, world: int, rank: int, device, features: bool
     return {"vt_counts": cfg.vt_counts, "bounds": bounds, "rels": out_rels, "feats": feats}
 
 
-def load_context(ctx, graph: HostGraph, world: int, rank: int, device, features: bool = True):
-    """device_shard + Context.load_partition; returns the shard dict (keep it alive)."""
+def load_context(ctx, graph: HostGraph, world: int, rank: int, device, features=True):
+    """device_shard + Context.load_partition; returns the shard dict (keep it alive).
+    features: True (rows on the GPU), False (none) or "host" (pinned host memory)."""
     sh = device_shard(graph, world, rank, device, features)
     ctx.load_partition(sh["vt_counts"], sh["rels"], sh["feats"], bounds=sh["bounds"])
     return sh
