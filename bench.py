@@ -45,6 +45,9 @@ def parse():
                     help="nc: node-classification batches (seed vertices, the headline); lp: link-prediction "
                          "batches (NEXT-3: cfg.batch positive edges + 1 negative each, fanout [25, 15])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--confine", action="store_true",
+                    help="seed confinement (NEXT-2, P:428-431): each rank draws its seeds from the train ids "
+                         "of its own vertex range (use with the planted-community configs C2L / C4L)")
     ap.add_argument("--features", default="device", choices=["device", "host"],
                     help="feature rows in HBM (default) or in pinned host memory read zero-copy over PCIe "
                          "(NEXT-4 ii: the paper's placement, lets C5 run on one GPU)")
@@ -305,7 +308,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         seeds_dev = [(torch.from_numpy(a).to(dev), torch.from_numpy(c).to(dev)) for a, c in seeds_host]
         negs = [r ^ LP_NEG_KEY for r in rngs]
     else:
-        seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
+        if args.confine:
+            seeds_host = [synth.batch_seeds_confined(cfg, b, rank, world) for b in range(steps)]
+        else:
+            seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
         seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
     row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
     torch.cuda.synchronize(dev)
@@ -347,11 +353,12 @@ def run_ours(args, cfg, rank, world, local_rank):
                 on_retire(bl)
                 bl.free()
 
-    acc = {"edges": 0, "gbytes": 0, "rbytes": 0}
+    acc = {"edges": 0, "gbytes": 0, "rbytes": 0, "inputs": 0}
 
     def count(bl):
         e, rows = retire(bl)
         acc["edges"] += e
+        acc["inputs"] += sum(rows)
         acc["gbytes"] += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
         acc["rbytes"] += sum(rows[u] * row_bytes[u] for u in cfg.feats)
 
@@ -534,11 +541,14 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "int32 ids / raw feature bytes (%s)" % ",".join(
                     sorted({"fp32" if cfg.feats[u][1] == 0 else "fp16" for u in cfg.feats})),
-                "data": "synthetic (seeded generator, synth/)", "config": dict(workload(cfg, world, args.task), features_in=(
+                "data": "synthetic (seeded generator, synth/)", "config": dict(workload(cfg, world, args.task), seeds=(
+                    "confined to the rank's vertex range (second-level partition, P:428-431)" if args.confine
+                    else "global epoch permutation, batch g = b*P + p"), features_in=(
                     "pinned host memory (zero-copy over PCIe)" if args.features == "host" else "HBM")),
                 "minibatches_per_s": world * K / (ms / 1e3),
                 "gather_GBps": achieved if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),
+                "input_vertices_per_batch_rank0": acc["inputs"] / K,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
                 "pipeline_depth": args.depth, "bundle": args.bundle, "host_us_per_batch": host_us, "host": {"cores": host_cores(), "cpu": cpu_model()}}

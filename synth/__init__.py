@@ -59,6 +59,10 @@ def lib():
         L.sy_indptr.restype = c.c_int
         L.sy_indices.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_void_p]
         L.sy_indices_at.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_void_p, c.c_int64, c.c_void_p]
+        L.sy_indices_loc.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_void_p, c.c_int64, c.c_int64,
+                                     c.c_uint32, c.c_int32, c.c_void_p]
+        L.sy_indices_at_loc.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_void_p, c.c_void_p,
+                                        c.c_int64, c.c_uint32, c.c_int32, c.c_void_p]
         L.sy_features.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
         L.sy_features_ids.argtypes = [c.c_uint64, c.c_int32, c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p]
         L.sy_select_train.argtypes = [c.c_uint64, c.c_int32, c.c_int64, c.c_uint64, c.c_void_p, c.c_int64]
@@ -107,6 +111,12 @@ class Config:
     base_rng: int = 0xD15_7D61_0002
     min_gpus: int = 1
     description: str = ""
+    locality: float = 0.0   # planted communities (NEXT-2): P(src from the dst's community)
+    n_comm: int = 8         # contiguous communities per vertex type
+
+    @property
+    def q_thr(self) -> int:
+        return int(min(2**32 - 1, round(self.locality * 2**32)))
 
     @property
     def n_vt(self):
@@ -183,7 +193,21 @@ def _c5():
                               "fanout [25,15], batch 1024, 768-d fp16 on paper vertices")
 
 
-CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5}
+def _planted(base, q=0.9):
+    """NEXT-2: the same shape with planted communities (8 contiguous blocks per type,
+    sources from the dst's block with probability q), for the locality-aware partition
+    (P:421-437): per-GPU ranges aligned with the blocks at P = 1, 2, 4, 8."""
+    def make():
+        c = base()
+        c.name = c.name + "L"
+        c.locality = q
+        c.description = c.description + f"; planted communities (8 per type, p_local={q})"
+        return c
+    return make
+
+
+CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5,
+           "C1L": _planted(_c1), "C2L": _planted(_c2), "C4L": _planted(_c4)}
 
 
 def config(name: str) -> Config:
@@ -206,7 +230,7 @@ class HostGraph:
     def indices_slice(self, r, e_lo, e_hi):
         if self.indices and self.indices[r] is not None:
             return self.indices[r][e_lo:e_hi]
-        return gen_indices(self.cfg, r, e_lo, e_hi)
+        return gen_indices(self.cfg, r, e_lo, e_hi, self.indptr[r])
 
 
 def gen_indptr(cfg: Config, r: int) -> np.ndarray:
@@ -219,16 +243,22 @@ def gen_indptr(cfg: Config, r: int) -> np.ndarray:
     return ip
 
 
-def gen_indices(cfg: Config, r: int, e_lo: int, e_hi: int) -> np.ndarray:
+def gen_indices(cfg: Config, r: int, e_lo: int, e_hi: int, indptr=None) -> np.ndarray:
     _, s, t, ne = cfg.rels[r]
     out = np.empty(max(0, e_hi - e_lo), dtype=np.int32)
-    lib().sy_indices(cfg.gen_seed, r, int(cfg.vt_counts[s]), e_lo, e_hi, out.ctypes.data)
+    if cfg.locality > 0:   # planted communities: the source depends on the dst's community
+        ip = np.ascontiguousarray(gen_indptr(cfg, r) if indptr is None else indptr, np.int64)
+        lib().sy_indices_loc(cfg.gen_seed, r, int(cfg.vt_counts[s]), int(cfg.vt_counts[t]), ip.ctypes.data,
+                             e_lo, e_hi, cfg.q_thr, cfg.n_comm, out.ctypes.data)
+    else:
+        lib().sy_indices(cfg.gen_seed, r, int(cfg.vt_counts[s]), e_lo, e_hi, out.ctypes.data)
     return out
 
 
 def build_host_graph(cfg: Config, materialize_indices: bool = True) -> HostGraph:
     indptr = [gen_indptr(cfg, r) for r in range(cfg.n_rel)]
-    indices = [gen_indices(cfg, r, 0, int(indptr[r][-1])) if materialize_indices else None
+    materialize_indices = materialize_indices or cfg.locality > 0   # (no device generator for these)
+    indices = [gen_indices(cfg, r, 0, int(indptr[r][-1]), indptr[r]) if materialize_indices else None
                for r in range(cfg.n_rel)]
     return HostGraph(cfg, cfg.vt_counts, np.array([s for _, s, _, _ in cfg.rels], np.int32),
                      np.array([t for _, _, t, _ in cfg.rels], np.int32), indptr, indices)
@@ -362,9 +392,36 @@ def lp_positives(cfg: Config, graph, rel: int, g: int, n: int | None = None):
     _, s, t, _ = cfg.rels[rel]
     dst = np.searchsorted(ip, e, side="right") - 1 + int(cfg.offsets[t])
     tid = np.empty(n, np.int32)
-    lib().sy_indices_at(cfg.gen_seed, rel, int(cfg.vt_counts[s]), e.ctypes.data, n, tid.ctypes.data)
+    if cfg.locality > 0:
+        dt = np.ascontiguousarray(dst - int(cfg.offsets[t]), np.int64)
+        lib().sy_indices_at_loc(cfg.gen_seed, rel, int(cfg.vt_counts[s]), int(cfg.vt_counts[t]), e.ctypes.data,
+                                dt.ctypes.data, n, cfg.q_thr, cfg.n_comm, tid.ctypes.data)
+    else:
+        lib().sy_indices_at(cfg.gen_seed, rel, int(cfg.vt_counts[s]), e.ctypes.data, n, tid.ctypes.data)
     src = tid.astype(np.int64) + int(cfg.offsets[s])
     return src, dst.astype(np.int64)
+
+
+def batch_seeds_confined(cfg: Config, b: int, rank: int, world: int, batch: int | None = None) -> np.ndarray:
+    """Seed confinement (NEXT-2: "split the training set accordingly ... a
+    trainer samples target vertices ... from the local second-level partition"): rank p's
+    b-th batch is slice b of a seeded epoch permutation of the train ids inside p's own
+    vertex range [floor(p*N/P), floor((p+1)*N/P)) of the seed type."""
+    B = cfg.batch if batch is None else batch
+    n = int(cfg.vt_counts[cfg.seed_vt])
+    lo, hi = (rank * n) // world, ((rank + 1) * n) // world
+    ids = train_ids(cfg)
+    ids = ids[(ids >= lo) & (ids < hi)]
+    per_epoch = max(1, len(ids) // B)
+    epoch, k = divmod(b, per_epoch)
+    pk = (cfg.name, "confined", rank, world, epoch)
+    if pk not in _perm_cache:
+        keys = np.empty(len(ids), dtype=np.uint64)
+        lib().sy_perm_keys(cfg.gen_seed, epoch, ids.ctypes.data, len(ids), keys.ctypes.data)
+        _perm_cache.clear()
+        _perm_cache[pk] = ids[np.argsort(keys, kind="stable")]
+    perm = _perm_cache[pk]
+    return (perm[k * B:(k + 1) * B] + int(cfg.offsets[cfg.seed_vt])).astype(np.int64)
 
 
 def rng_seed(cfg: Config, g: int) -> int:

@@ -15,6 +15,9 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -103,6 +106,41 @@ void sy_indices(uint64_t G, int32_t r, int64_t n_src, int64_t e_lo, int64_t e_hi
 }
 
 /* feature rows [tid_lo, tid_hi) of vertex type u, dim columns, dtype 0=f32 1=f16 */
+/* planted-community src tids of CSC positions [e_lo, e_hi) of relation r; indptr is the
+ * relation's global CSC row pointer (n_dst + 1) */
+void sy_indices_loc(uint64_t G, int32_t r, int64_t n_src, int64_t n_dst, const int64_t *indptr, int64_t e_lo,
+                    int64_t e_hi, uint32_t q_thr, int32_t n_comm, int32_t *out)
+{
+    if (e_hi <= e_lo) return;
+#pragma omp parallel
+    {
+        int nt = 1, id = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads();
+        id = omp_get_thread_num();
+#endif
+        int64_t n = e_hi - e_lo, a = e_lo + n * id / nt, b = e_lo + n * (id + 1) / nt;
+        int64_t lo = 0, hi = n_dst;                /* dst of edge a: last x with indptr[x] <= a */
+        while (lo < hi) {
+            int64_t mid = (lo + hi + 1) / 2;
+            if (indptr[mid] <= a) lo = mid; else hi = mid - 1;
+        }
+        int64_t x = lo;
+        for (int64_t e = a; e < b; ++e) {
+            while (x < n_dst && indptr[x + 1] <= e) ++x;
+            out[e - e_lo] = sy_src_tid_loc(G, r, e, n_src, x, n_dst, q_thr, n_comm);
+        }
+    }
+}
+
+/* planted-community src tids of given CSC positions with their dst tids (LP positives) */
+void sy_indices_at_loc(uint64_t G, int32_t r, int64_t n_src, int64_t n_dst, const int64_t *e, const int64_t *dst,
+                       int64_t n, uint32_t q_thr, int32_t n_comm, int32_t *out)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = sy_src_tid_loc(G, r, e[i], n_src, dst[i], n_dst, q_thr, n_comm);
+}
+
 /* src tids of the given CSC positions of relation r (link-prediction positives) */
 void sy_indices_at(uint64_t G, int32_t r, int64_t n_src, const int64_t *e, int64_t n, int32_t *out)
 {

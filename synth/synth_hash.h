@@ -50,6 +50,23 @@ SY_FN int32_t sy_src_tid(uint64_t G, int32_t r, int64_t e, int64_t n_src)
     return (int32_t)((w * (uint64_t)n_src) >> 32);
 }
 
+/* Planted communities: each vertex type is split into n_comm
+ * contiguous blocks; the source of an edge whose dst lies in block c is drawn from the
+ * src type's block c with probability q_thr / 2^32, else uniformly (the same hash word
+ * as sy_src_tid for the uniform draw, the low word for the coin). */
+SY_FN int32_t sy_src_tid_loc(uint64_t G, int32_t r, int64_t e, int64_t n_src, int64_t dst_tid, int64_t n_dst,
+                             uint32_t q_thr, int32_t n_comm)
+{
+    uint64_t h = sy_hash(G, SY_TAG_SRC + (uint64_t)r, (uint64_t)e, 0);
+    uint64_t w = h >> 32;
+    if ((uint32_t)h < q_thr && n_dst > 0) {
+        int64_t c = dst_tid * n_comm / n_dst;
+        int64_t lo = c * n_src / n_comm, hi = (c + 1) * n_src / n_comm;
+        if (hi > lo) return (int32_t)(lo + (int64_t)((w * (uint64_t)(hi - lo)) >> 32));
+    }
+    return (int32_t)((w * (uint64_t)n_src) >> 32);
+}
+
 /* feature element c of row (u, tid): dtype 0 = fp32 bits in [1,2), 1 = fp16 bits in [1,2).
  * One 64-bit hash yields two 32-bit words (columns 2m and 2m+1). */
 SY_FN uint32_t sy_feat_word(uint64_t G, int32_t u, int64_t tid, int64_t c)

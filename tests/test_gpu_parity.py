@@ -291,6 +291,23 @@ def test_compaction_variant_forced(c1, c2, mode, monkeypatch):
         ctx.close()
 
 
+# ----------------------------------------------------------------------------- planted communities (NEXT-2)
+
+def test_c1l_planted_world2_confined_seeds():
+    """C1L (planted communities) at world 2 with each rank's seeds confined to its own
+    range: every batch bit-exact (the locality-aware partition changes inputs, not the
+    method)."""
+    cfg = synth.config("C1L")
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    ctxs = _world(g, 2)
+    for p in range(2):
+        for b in range(3):
+            seeds = synth.batch_seeds_confined(cfg, b, p, 2)
+            run_and_compare(ctxs[p], g, cfg, seeds, cfg.fanouts, synth.rng_seed(cfg, 2 * b + p), rows,
+                            check_invariants=(b == 0))
+
+
 # ----------------------------------------------------------------------------- C4 / C5 (full size)
 
 def test_c4_full_size_batches():

@@ -76,3 +76,47 @@ def test_seeds():
     assert not np.intersect1d(s0, s1).size        # one epoch = disjoint batches
     assert np.all((s0 >= cfg.offsets[0]) & (s0 < cfg.offsets[1]))
     assert synth.rng_seed(cfg, 0) != synth.rng_seed(cfg, 1)
+
+
+# ----------------------------------------------------------------------------- planted communities (NEXT-2)
+
+def test_planted_generator_locality_and_identity():
+    """C1L: the fraction of edges whose src lies in the dst's community is q + (1-q)/8
+    (a uniform draw lands in the right block 1/8 of the time); q = 0 reproduces the
+    uniform generator byte for byte; LP positives of a planted graph are real edges."""
+    import dataclasses
+    cfg = synth.config("C1L")
+    g = synth.build_host_graph(cfg)
+    for r, (_, s, t, _) in enumerate(cfg.rels):
+        ip, ix = g.indptr[r], g.indices[r]
+        n_s, n_t = int(cfg.vt_counts[s]), int(cfg.vt_counts[t])
+        dst = np.repeat(np.arange(n_t), np.diff(ip))
+        same = (dst * cfg.n_comm // n_t) == np.searchsorted(
+            [(c * n_s) // cfg.n_comm for c in range(1, cfg.n_comm + 1)], ix, side="right")
+        want = cfg.locality + (1 - cfg.locality) / cfg.n_comm
+        assert abs(same.mean() - want) < 0.01, (r, same.mean(), want)
+    base = synth.config("C1")
+    zero = dataclasses.replace(base, locality=1e-15)          # q_thr == 0: only the uniform branch
+    assert zero.q_thr == 0
+    gz = synth.build_host_graph(zero)
+    gb = synth.build_host_graph(base)
+    for r in range(base.n_rel):
+        assert np.array_equal(gz.indices[r], gb.indices[r])
+    rel = synth.lp_rel(cfg)
+    src, dst = synth.lp_positives(cfg, g, rel, 0, 200)
+    off_s, off_t = int(cfg.offsets[cfg.rels[rel][1]]), int(cfg.offsets[cfg.rels[rel][2]])
+    ip = g.indptr[rel]
+    for a, b in zip(src, dst):
+        x = b - off_t
+        assert (g.indices[rel][ip[x]:ip[x + 1]] + off_s == a).any()
+
+
+def test_confined_seeds_stay_in_the_rank_range():
+    cfg = synth.config("C2L")
+    n = int(cfg.vt_counts[cfg.seed_vt])
+    for world in (2, 4):
+        for p in range(world):
+            lo, hi = (p * n) // world, ((p + 1) * n) // world
+            s = synth.batch_seeds_confined(cfg, 3, p, world) - int(cfg.offsets[cfg.seed_vt])
+            assert len(s) == cfg.batch and len(set(s.tolist())) == len(s)
+            assert s.min() >= lo and s.max() < hi
