@@ -16,6 +16,8 @@ Parity status of each oracle function (pins are in ``tests/test_oracle_*.py``):
                     full neighbourhood, dst prefix, sorted new, round trip),
                     BFS closed form at fanout -1, worked example, uniformity
   og_gather         pinned: numpy.take on the same rows
+  sage_mean_layer   pinned: dense-matrix form (D^-1 A X W^T via numpy matmul), closed
+                    forms (constant inputs, isolated dsts), neighbour-order invariance
   og_lp_targets     pinned: negatives vs an independent pure-Python Philox and a
                     chi-square over the dst range; seeds = brute-force set of the
                     endpoints; every pair round-trips through the seeds
@@ -251,3 +253,33 @@ def gather_ids(ids, vt_counts, u: int, rows: np.ndarray) -> np.ndarray:
     if rc != OG_OK:
         raise OracleError(rc)
     return out
+
+
+# ----------------------------------------------------------------------------- consumer step (NEXT-4 i)
+
+def sage_mean_layer(indptr, indices, x_src, x_dst, w):
+    """GraphSAGE-mean layer over one block relation, pre-activation, in fp64 -- the
+    paper's message passing h_v' = g(h_v, (+)_{u in N(v)} f(h_u, ...)) (P:244-246, Eq. 1)
+    with f = identity, (+) = mean over the block's sampled in-edges of v (an edge sampled
+    twice counts twice; no in-edge -> 0), g(a, b) = W_self a + W_neigh b (GraphSAGE,
+    P:964; DESIGN.md §3 reading C1).  x_src [n_src, F] (rows = the block's src nodes),
+    x_dst [n_dst, F] or None (no self term), w [H, 2F] = [W_self | W_neigh] (or [H, F]
+    = W_neigh without a self term).  Returns z [n_dst, H] float64.  Plain loop over the
+    dst vertices in the definition's order."""
+    indptr = np.asarray(indptr, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    xs = np.asarray(x_src, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    n_dst, F = len(indptr) - 1, xs.shape[1]
+    self_term = x_dst is not None
+    w_self, w_neigh = (w[:, :F], w[:, F:]) if self_term else (None, w)
+    z = np.zeros((n_dst, w.shape[0]), dtype=np.float64)
+    xd = np.asarray(x_dst, dtype=np.float64) if self_term else None
+    for v in range(n_dst):
+        nb = indices[indptr[v]:indptr[v + 1]]
+        m = xs[nb].mean(axis=0) if len(nb) else np.zeros(F)
+        z[v] = w_neigh @ m
+        if self_term:
+            z[v] += w_self @ xd[v]
+    return z
+
