@@ -230,6 +230,28 @@ typedef struct {
 } eg_lp_view;
 EG_API eg_status eg_lp_view_get(const eg_blocks *blocks, eg_lp_view *out);
 
+/* ---- Consumer step (SURVEY §8f NEXT-4 i; DESIGN.md §3 readings C1-C2): one GraphSAGE-
+ * mean layer over relation `rel` of block `hop`, pre-activation (Eq. 1, P:244-246,
+ * GraphSAGE P:964):  out[v] (+)= W_self x_dst[v] + W_neigh mean_{sampled in-edges u->v} x_src[u]
+ * (mean over the block's sampled edges of v, multiplicity counted; 0 without any).
+ *   x_src   device rows of the block's src nodes of type s(rel) (local id = row), x_dtype
+ *           0 fp32 / 1 fp16 / 2 bf16, row stride ld_src elements (rows 16-B aligned);
+ *           for the input layer these are exactly eg_blocks_features(s(rel)).
+ *   x_dst   device rows of the dst nodes of type t(rel) (same dtype, stride ld_dst), or
+ *           NULL: no self term (K = F; RGCN-style per-relation terms with EG_ACCUMULATE).
+ *   w       device bf16 [H][K] row-major, K = 2F ([W_self | W_neigh]) or F.
+ *   out     device fp32 [n_dst][ld_out], n_dst = |dst nodes of type t(rel)| of the block;
+ *           flags & EG_ACCUMULATE adds to it.
+ * Runs on the context's stream after the batch resolves; the operands are rounded to
+ * bf16 for the tensor cores, accumulation is fp32.  Errors: EG_EINVAL (hop / rel out of
+ * range, F outside [1, 256], H not a multiple of 16 in [16, 256], unaligned rows,
+ * shared-memory budget (128 + H) * K_padded * 2 B > 200 KB). */
+#define EG_ACCUMULATE 1
+EG_API eg_status eg_sage_mean_layer(eg_ctx *ctx, const eg_blocks *blocks, int32_t hop, int32_t rel,
+                                    const void *x_src, int32_t x_dtype, int64_t ld_src, const void *x_dst,
+                                    int64_t ld_dst, int32_t F, const void *w, int32_t H, float *out,
+                                    int64_t ld_out, int32_t flags);
+
 /* Totals of a batch (waits if pending): sampled edges over all hops and relations, and
  * the input vertices (src nodes of the last block) per type (n_inputs: host [n_vt]);
  * either may be NULL. */

@@ -1357,6 +1357,52 @@ eg_status eg_lp_view_get(const eg_blocks *cb, eg_lp_view *out)
     return EG_OK;
 }
 
+eg_status eg_sage_mean_layer(eg_ctx *c, const eg_blocks *cb, int32_t hop, int32_t rel, const void *x_src,
+                             int32_t x_dtype, int64_t ld_src, const void *x_dst, int64_t ld_dst, int32_t F,
+                             const void *w, int32_t H, float *out, int64_t ld_out, int32_t flags)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!cb) return fail(c, EG_EINVAL, "blocks is null");
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    if ((st = finish(b))) return st;
+    if (hop < 0 || hop >= b->n_hops || rel < 0 || rel >= b->n_rel) return fail(c, EG_EINVAL, "hop / rel out of range");
+    if (F < 1 || F > 256) return fail(c, EG_EINVAL, "F must be in [1, 256]");
+    if (H < 16 || H > 256 || H % 16) return fail(c, EG_EINVAL, "H must be a multiple of 16 in [16, 256]");
+    if (x_dtype < 0 || x_dtype > 2) return fail(c, EG_EINVAL, "x_dtype must be 0 (f32), 1 (f16) or 2 (bf16)");
+    if (!x_src || !w || !out) return fail(c, EG_EINVAL, "null operand");
+    const int esz = x_dtype == 0 ? 4 : 2;
+    auto aligned = [&](const void *p, int64_t ld) {
+        return ((uintptr_t)p % 16) == 0 && (ld * esz) % 16 == 0 && ld >= F;
+    };
+    if (!aligned(x_src, ld_src) || (x_dst && !aligned(x_dst, ld_dst)))
+        return fail(c, EG_EINVAL, "input rows must be 16-byte aligned with ld >= F");
+    if (((uintptr_t)out % 16) || ld_out % 4 || ld_out < H) return fail(c, EG_EINVAL, "out rows must be 16-byte aligned");
+    if (sage_smem_bytes(F, H, x_dst != nullptr) > 200 * 1024)
+        return fail(c, EG_EINVAL, "shared-memory budget exceeded: (128 + H) * padded K * 2 > 200 KB");
+    const int t = c->g.rel[rel].dst_vt;
+    SageArgs a{};
+    a.indptr = b->indptr[hop][rel];
+    a.indices = b->indices[hop][rel];
+    a.x_src = x_src;
+    a.x_dst = x_dst;
+    a.ld_src = ld_src;
+    a.ld_dst = ld_dst;
+    a.w = w;
+    a.out = out;
+    a.ld_out = ld_out;
+    a.n_dst = (int32_t)b->n_nodes[hop][t];
+    a.F = F;
+    a.H = H;
+    a.accumulate = (flags & EG_ACCUMULATE) ? 1 : 0;
+    uint32_t cols = 32;
+    while ((int)cols < H) cols <<= 1;
+    a.tmem_cols = cols;
+    EG_CUDA(c, launch_sage(a, x_dtype, c->stream));
+    ++c->launches;
+    return EG_OK;
+}
+
 eg_status eg_blocks_stats(const eg_blocks *cb, int64_t *total_edges, int64_t *n_inputs)
 {
     if (!cb) return EG_EINVAL;

@@ -47,6 +47,22 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
 // gather.cu
 void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);
 
+// sage.cu: one GraphSAGE-mean layer over a block relation on the tensor cores (NEXT-4 i).
+struct SageArgs {
+    const int32_t *indptr;      // block CSC over the dst vertices (n_dst + 1)
+    const int32_t *indices;     // local src ids
+    const void *x_src;          // [n_src][ld_src] input rows of the relation's src nodes
+    const void *x_dst;          // [n_dst][ld_dst] input rows of the dst nodes, or null (no self term)
+    int64_t ld_src, ld_dst;     // row strides in elements
+    const void *w;              // bf16 [H][K], K = (x_dst ? 2F : F): [W_self | W_neigh]
+    float *out;                 // [n_dst][ld_out] fp32
+    int64_t ld_out;
+    int32_t n_dst, F, H, accumulate;
+    uint32_t tmem_cols;         // power of two >= max(32, H)
+};
+cudaError_t launch_sage(const SageArgs &a, int x_dtype, cudaStream_t s);   // x_dtype 0 f32, 1 f16, 2 bf16
+size_t sage_smem_bytes(int F, int H, bool self_term);
+
 // store.cu
 void launch_max_degree(const int64_t *indptr, int64_t n, unsigned long long *out, cudaStream_t s);
 

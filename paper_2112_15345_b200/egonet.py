@@ -29,7 +29,7 @@ ABI_SYMBOLS = [
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
-    "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get",
+    "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer",
 ]
 
 EG_FEATURES = 1
@@ -137,6 +137,8 @@ def lib(build_if_missing: bool = True):
         L.eg_sample_lp_bundle.argtypes = [vp, c.c_int32, vp, vp, vp, c.c_int32, c.c_int32, vp, c.c_int32, vp, vp,
                                           c.c_int32, vp]
         L.eg_lp_view_get.argtypes = [vp, P(LpView)]
+        L.eg_sage_mean_layer.argtypes = [vp, vp, c.c_int32, c.c_int32, vp, c.c_int32, c.c_int64, vp, c.c_int64,
+                                         c.c_int32, vp, c.c_int32, vp, c.c_int64, c.c_int32]
         L.eg_trace_get.argtypes = [vp, c.c_int32, c.c_char_p, c.c_size_t, P(c.c_double), P(c.c_int64)]
         L.eg_trace_get.restype = c.c_int32
         L.eg_check_shard_metas.argtypes = [c.c_int32, vp, vp, vp, c.c_char_p, c.c_size_t]
@@ -542,6 +544,30 @@ class Context:
                   features: bool = True, async_: bool = False) -> Blocks:
         """One link-prediction mini-batch (eg_sample_lp_bundle with one batch)."""
         return self.sample_lp_bundle([src], [dst], rel, n_neg, [neg_seed], fanouts, [rng_seed], features, async_)[0]
+
+    def sage_mean_layer(self, blocks: Blocks, hop: int, rel: int, x_src, w, x_dst=None, out=None,
+                        accumulate: bool = False):
+        """The consumer step (NEXT-4 i): one GraphSAGE-mean layer over relation rel of block
+        hop on the tensor cores -- out = W_self x_dst + W_neigh mean(x_src over sampled
+        in-edges), pre-activation, fp32 [n_dst, H].  x_src / x_dst: cuda fp32 / fp16 /
+        bf16 [rows, F]; w: cuda bf16 [H, 2F] ([W_self | W_neigh]) or [H, F] without x_dst."""
+        torch = _torch()
+        dt = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}[x_src.dtype]
+        F = x_src.shape[1]
+        assert w.dtype == torch.bfloat16 and w.is_contiguous()
+        H = w.shape[0]
+        ok = 0 <= hop < blocks.n_hops and 0 <= rel < len(self.rel_dst)   # else the library reports EG_EINVAL
+        n_dst = blocks[hop].n_dst[self.rel_dst[rel]] if ok else 0
+        if out is None:
+            out = (torch.zeros if accumulate else torch.empty)((n_dst, H), dtype=torch.float32, device=self.device)
+        if x_dst is not None:
+            assert x_dst.dtype == x_src.dtype and x_dst.shape[1] == F
+        self._check(lib().eg_sage_mean_layer(self._h, blocks.handle, hop, rel, x_src.data_ptr(), dt, x_src.stride(0),
+                                             x_dst.data_ptr() if x_dst is not None else None,
+                                             x_dst.stride(0) if x_dst is not None else 0, F, w.data_ptr(), H,
+                                             out.data_ptr(), out.stride(0), 1 if accumulate else 0),
+                    "eg_sage_mean_layer")
+        return out
 
     def gather_features(self, blocks: Blocks, out=None, types=None):
         """Feature rows of the input vertices per type (None for types without
