@@ -5,16 +5,16 @@
 //
 // as ONE fused kernel on the 5th-generation tensor cores: z = [X_dst | M] [W_self | W_neigh]^T
 // where the mean-aggregated rows M are never written to HBM.  Persistent CTAs (one per SM,
-// 4 warps):
+// 16 warps):
 //   * W (H x K, bf16, K-major) is staged once per CTA into shared memory in the canonical
 //     128-byte-swizzled K-major layout the MMA reads;
-//   * per tile of 128 dst rows the 4 warps build the A operand in the same layout: the
+//   * per tile of 128 dst rows the 16 warps build the A operand in the same layout: the
 //     self rows (converted to bf16) and the neighbour means (one warp-wide coalesced row
 //     read per sampled edge, fp32 accumulation, then bf16);
 //   * one thread issues K/16 tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = H) into a
 //     TMEM accumulator and commits them to an mbarrier;
-//   * the epilogue reads the accumulator back with tcgen05.ld (warp w owns TMEM lanes
-//     32w .. 32w+31 = tile rows) and stores fp32 rows.
+//   * the epilogue reads the accumulator back with tcgen05.ld (warp w reads TMEM lanes
+//     32 (w % 4) .. +31 = tile rows, a quarter of the columns) and stores fp32 rows.
 // The layer is bound by the neighbour-row reads (HBM); the MMAs take ~10 % of a tile.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -129,11 +129,17 @@ __device__ __forceinline__ void store_bf16(uint8_t *base, int rows, int row, int
 }
 
 constexpr int kTileM = 128;
+// warps per CTA (A-operand builders; TMEM lane group = warp % 4): as many as the
+// registers allow -- the A build is a latency-bound gather (ncu: 16 warps, 25 %
+// occupancy, stalls on the row loads)
+template <int CPL> __host__ __device__ constexpr int warps_for() { return CPL <= 4 ? 32 : 16; }
 
 // CPL = Fp / 32 columns per lane (Fp = F rounded up to 64).
 template <typename T, int CPL>
-__global__ void __launch_bounds__(128, 1) sage_kernel(const __grid_constant__ SageArgs a)
+__global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __grid_constant__ SageArgs a)
 {
+    constexpr int kWarps = warps_for<CPL>();
+    constexpr int kRowsPerWarp = kTileM / kWarps;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     constexpr int Fp = CPL * 32;
@@ -155,14 +161,22 @@ __global__ void __launch_bounds__(128, 1) sage_kernel(const __grid_constant__ Sa
     // W -> sB: padded column kp of part p maps to W column p * F + (kp - p * Fp)
     const int K = parts * a.F;
     const __nv_bfloat16 *wt = static_cast<const __nv_bfloat16 *>(a.w);
+    const bool wvec = (a.F % 8) == 0 && ((uintptr_t)a.w % 16) == 0;   // 16-B chunks of W rows
     for (int i = threadIdx.x; i < a.H * (Kp / 8); i += blockDim.x) {
         const int n = i / (Kp / 8), kp = (i % (Kp / 8)) * 8;
         const int p = kp / Fp, c = kp - p * Fp;
-        float v[8];
+        uint8_t *dst = sB + sw128_off(a.H, n, kp);
+        if (wvec) {   // bf16 bits copied as they are
+            const uint4 v = c < a.F ? __ldg(reinterpret_cast<const uint4 *>(wt + (int64_t)n * K + p * a.F + c))
+                                    : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4 *>(dst) = v;
+        } else {
+            float v[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            v[e] = c + e < a.F ? __bfloat162float(wt[(int64_t)n * K + p * a.F + c + e]) : 0.f;
-        store_bf16<8>(sB, a.H, n, kp, v);
+            for (int e = 0; e < 8; ++e)
+                v[e] = c + e < a.F ? __bfloat162float(wt[(int64_t)n * K + p * a.F + c + e]) : 0.f;
+            store_bf16<8>(sB, a.H, n, kp, v);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -175,45 +189,68 @@ __global__ void __launch_bounds__(128, 1) sage_kernel(const __grid_constant__ Sa
 
     for (int tile = blockIdx.x; tile * kTileM < a.n_dst; tile += gridDim.x) {
         const int row0 = tile * kTileM;
-        // ---- A operand: warp w builds rows 32w .. 32w+31, lanes over columns
-        for (int rr = 0; rr < 32; ++rr) {
-            const int r = warp * 32 + rr;
-            const int v = row0 + r;
-            const int c = lane * CPL;
-            float acc[CPL];
-#pragma unroll
-            for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
+        // ---- A operand: warp w builds rows w + kWarps q, two rows at a time with
+        // independent accumulators; the rows' CSC bounds are loaded up front (lane q)
+        const int c = lane * CPL;
+        int jq0 = 0, jq1 = 0;
+        if (lane < kRowsPerWarp) {
+            const int v = row0 + warp + kWarps * lane;
             if (v < a.n_dst) {
-                if (xd) {
-                    float sv[CPL];
-                    load_cols<T, CPL>(xd + (int64_t)v * a.ld_dst, c, a.F, sv);
-                    store_bf16<CPL>(sA, kTileM, r, c, sv);
-                }
-                const int j0 = __ldg(a.indptr + v), j1 = __ldg(a.indptr + v + 1);
-                int j = j0;
-                for (; j + 4 <= j1; j += 4) {   // four independent row reads in flight
-                    float t[4][CPL];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        load_cols<T, CPL>(xs + (int64_t)__ldg(a.indices + j + q) * a.ld_src, c, a.F, t[q]);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-#pragma unroll
-                        for (int e = 0; e < CPL; ++e) acc[e] += t[q][e];
-                }
-                for (; j < j1; ++j) {
-                    float t[CPL];
-                    load_cols<T, CPL>(xs + (int64_t)__ldg(a.indices + j) * a.ld_src, c, a.F, t);
-#pragma unroll
-                    for (int e = 0; e < CPL; ++e) acc[e] += t[e];
-                }
-                const float inv = j1 > j0 ? 1.f / (float)(j1 - j0) : 0.f;
-#pragma unroll
-                for (int e = 0; e < CPL; ++e) acc[e] *= inv;
-            } else if (xd) {
-                store_bf16<CPL>(sA, kTileM, r, c, acc);   // tail rows: zeros
+                jq0 = __ldg(a.indptr + v);
+                jq1 = __ldg(a.indptr + v + 1);
             }
-            store_bf16<CPL>(sA, kTileM, r, (parts - 1) * Fp + c, acc);
+        }
+#pragma unroll 1
+        for (int rp = 0; rp < kRowsPerWarp; rp += 2) {
+            const int r0 = warp + kWarps * rp, r1 = r0 + kWarps;
+            const int v0 = row0 + r0, v1 = row0 + r1;
+            const int a0 = __shfl_sync(0xffffffffu, jq0, rp), a1 = __shfl_sync(0xffffffffu, jq1, rp);
+            const int b0 = __shfl_sync(0xffffffffu, jq0, rp + 1), b1 = __shfl_sync(0xffffffffu, jq1, rp + 1);
+            float acc0[CPL], acc1[CPL];
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc0[e] = acc1[e] = 0.f;
+            if (xd) {
+                float s0[CPL], s1[CPL];
+                if (v0 < a.n_dst) load_cols<T, CPL>(xd + (int64_t)v0 * a.ld_dst, c, a.F, s0);
+                else
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) s0[e] = 0.f;
+                if (v1 < a.n_dst) load_cols<T, CPL>(xd + (int64_t)v1 * a.ld_dst, c, a.F, s1);
+                else
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) s1[e] = 0.f;
+                store_bf16<CPL>(sA, kTileM, r0, c, s0);
+                store_bf16<CPL>(sA, kTileM, r1, c, s1);
+            }
+            // two edges of each row per step: four independent row reads in flight
+            for (int ja = a0, jb = b0; ja < a1 || jb < b1; ja += 2, jb += 2) {
+                int ix[4];
+                ix[0] = ja < a1 ? __ldg(a.indices + ja) : -1;
+                ix[1] = ja + 1 < a1 ? __ldg(a.indices + ja + 1) : -1;
+                ix[2] = jb < b1 ? __ldg(a.indices + jb) : -1;
+                ix[3] = jb + 1 < b1 ? __ldg(a.indices + jb + 1) : -1;
+                float t[4][CPL];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (ix[q] >= 0) load_cols<T, CPL>(xs + (int64_t)ix[q] * a.ld_src, c, a.F, t[q]);
+                    else
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) t[q][e] = 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    acc0[e] += t[0][e] + t[1][e];
+                    acc1[e] += t[2][e] + t[3][e];
+                }
+            }
+            const float i0 = a1 > a0 ? 1.f / (float)(a1 - a0) : 0.f, i1 = b1 > b0 ? 1.f / (float)(b1 - b0) : 0.f;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) {
+                acc0[e] *= i0;
+                acc1[e] *= i1;
+            }
+            store_bf16<CPL>(sA, kTileM, r0, (parts - 1) * Fp + c, acc0);
+            store_bf16<CPL>(sA, kTileM, r1, (parts - 1) * Fp + c, acc1);
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -240,15 +277,17 @@ __global__ void __launch_bounds__(128, 1) sage_kernel(const __grid_constant__ Sa
         mbar_wait_parity(mbar, phase);
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // ---- epilogue: TMEM lanes 32w + lane = tile rows, 8 fp32 columns per load
-        const int row = row0 + warp * 32 + lane;
+        // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) + lane (= tile rows), columns
+        // 8 (w / 4) + 2 kWarps j, 8 fp32 per load
+        const int lg = warp & 3;
+        const int row = row0 + lg * 32 + lane;
         float *orow = a.out + (int64_t)row * a.ld_out;
-        for (int col = 0; col < a.H; col += 8) {
+        for (int col = (warp >> 2) * 8; col < a.H; col += 2 * kWarps) {
             uint32_t r[8];
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)col));
+                : "r"(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)col));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (row < a.n_dst) {
                 float4 x0 = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
@@ -284,7 +323,7 @@ cudaError_t launch_typed(const SageArgs &a, cudaStream_t s)
     if (e != cudaSuccess) return e;
     const int tiles = (a.n_dst + kTileM - 1) / kTileM;
     if (tiles == 0) return cudaSuccess;
-    sage_kernel<T, CPL><<<tiles < kSMs ? tiles : kSMs, 128, smem, s>>>(a);
+    sage_kernel<T, CPL><<<tiles < kSMs ? tiles : kSMs, warps_for<CPL>() * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
