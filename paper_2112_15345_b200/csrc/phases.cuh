@@ -74,9 +74,12 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
             const int32_t p = wcnt[w][vt] + rank;
             if (p < hd.cap_nodes[vt]) {
                 hd.nodes[vt][p] = gid;
-                if (atomicCAS(pos + gid, -1, p) != -1) atomicOr(meta + kMetaErr, kErrSeedDup);
+                pos[gid] = p;
+                // duplicate seed: its member bit is already set (pos[] is only ever read for
+                // members of the current batch, so it needs no reset between batches)
                 const int64_t bit = g.boff[vt] + (gid - g.off[vt]);
-                atomicOr(hd.members + (bit >> 5), 1u << (bit & 31));
+                const uint32_t mb = 1u << (bit & 31);
+                if (atomicOr(hd.members + (bit >> 5), mb) & mb) atomicOr(meta + kMetaErr, kErrSeedDup);
             } else {
                 atomicOr(meta + kMetaErr, kErrCapacity);
             }
@@ -1298,25 +1301,23 @@ __device__ void phase_relabel(const GraphDev &g, const HopDev &hd, int bid, int 
     }
 }
 
-// End of batch: pos[] back to -1 for every vertex of the batch.
+// End of batch: clear the member bitmap.  Every bit set in it belongs to this batch, so the
+// whole word of each vertex is zeroed with a plain store (idempotent across the vertices
+// sharing it); pos[] keeps stale values, which are never read (only members are looked up).
 __device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, int bid, int nb)
 {
     const int32_t *n = meta_nodes(hd.meta, level);
     int64_t cum[EG_MAX_VT + 1];
     cum[0] = 0;
     for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
-    int32_t *const pos = hd.pos;
     uint32_t *const members = hd.members;
     for (int u = 0; u < g.n_vt; ++u) {
         const int64_t *const nodes = hd.nodes[u];
         const int64_t n = cum[u + 1] - cum[u];
+        const int64_t lo = g.off[u], hi = g.off[u + 1], b0 = g.boff[u];
         for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
             const int64_t gid = nodes[i];
-            if (gid >= g.off[u] && gid < g.off[u + 1]) {
-                pos[gid] = -1;
-                const int64_t bit = g.boff[u] + (gid - g.off[u]);
-                atomicAnd(members + (bit >> 5), ~(1u << (bit & 31)));
-            }
+            if (gid >= lo && gid < hi) members[(b0 + (gid - lo)) >> 5] = 0u;
         }
     }
 }

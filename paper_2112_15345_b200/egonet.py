@@ -114,12 +114,14 @@ def lib(build_if_missing: bool = True):
     """Load libegonet.so (building it with nvcc if it is missing or stale)."""
     global _lib
     if _lib is None:
-        if build_if_missing:
+        alt = os.environ.get("EG_LIB")   # A/B experiments: another build of the same library
+        if build_if_missing and not alt:
             from . import build as _b
             _b.build()
-        if not os.path.exists(_SO):
-            raise RuntimeError(f"{_SO} missing: run paper_2112_15345_b200/build.py (no CPU fallback exists)")
-        L = ctypes.CDLL(_SO)
+        so = alt or _SO
+        if not os.path.exists(so):
+            raise RuntimeError(f"{so} missing: run paper_2112_15345_b200/build.py (no CPU fallback exists)")
+        L = ctypes.CDLL(so)
         c = ctypes
         P = c.POINTER
         vp = c.c_void_p
