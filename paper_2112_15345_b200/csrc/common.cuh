@@ -103,6 +103,7 @@ struct HopDev {
     uint32_t *bitmap;                // this hop's marks: every sampled source (A)
     uint32_t *members;               // vertices already in the batch (M); new = A & ~M
     uint32_t *summary;               // bit w of the summary = A word w may be nonzero
+    uint32_t *summary_mark;          // = summary on sparse hops; null on dense hops (no summary)
     int32_t *chunk_cnt;              // new vertices per bitmap chunk
     int32_t *seg_cnt;                // new vertices per slice (16 bitmap words)
     int32_t *chunk_pre;              // new vertices in the chunks before, within the type

@@ -931,6 +931,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         if (p->lp) {
             HopDev x = hd;
             x.h = -1;
+            x.summary_mark = p->lp_sparse ? x.summary : nullptr;
             bd->lph[b] = x;
             LpDev &lp = bd->lpd[b];
             lp.n_neg = p->n_neg;
@@ -952,6 +953,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
                 x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
                 x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
             }
+            x.summary_mark = p->sparse[h] ? x.summary : nullptr;
             x.selq = (uint64_t *)(base + p->o_selq[h]);
             x.selq_cap = (int32_t)p->selq_items[h];
             char *hv = base + p->o_heavy[h];

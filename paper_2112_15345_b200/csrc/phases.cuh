@@ -236,7 +236,7 @@ __device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t *summary, ui
     const int64_t bit = bit_base + gid;
     const int64_t w = bit >> 5;
     atomicOr(bitmap + w, 1u << (bit & 31));   // results unused: RED
-    atomicOr(summary + (w >> 5), 1u << (w & 31));
+    if (summary) atomicOr(summary + (w >> 5), 1u << (w & 31));   // sparse hops only
 }
 
 __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_t slot, int64_t j)
@@ -543,7 +543,7 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
     Item itm;
     itm.pos = hd.pos;
     itm.bitmap = hd.bitmap;
-    itm.summary = hd.summary;
+    itm.summary = hd.summary_mark;
     itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
     itm.soff = (uint32_t)g.off[R.src_vt];
     itm.ebase = R.edge_base[p] + base0;
@@ -687,7 +687,7 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
             Item itm;
             itm.pos = pos;
             itm.bitmap = bitmap;
-            itm.summary = hd.summary;
+            itm.summary = hd.summary_mark;
             itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
             itm.soff = (uint32_t)g.off[R.src_vt];
             itm.ebase = R.edge_base[p] + base;
@@ -763,7 +763,7 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
             const int64_t base = cur.ib & ((1ll << 56) - 1);
             itm.pos = hd.pos;
             itm.bitmap = hd.bitmap;
-            itm.summary = hd.summary;
+            itm.summary = hd.summary_mark;
             itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
             itm.soff = (uint32_t)g.off[R.src_vt];
             itm.ebase = R.edge_base[p] + base;
@@ -856,7 +856,7 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const summary = hd.summary;
+    uint32_t *const summary = hd.summary_mark;
     // ---- full neighbourhoods: segmented copy over groups of 32 items
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
     int64_t cum[EG_MAX_REL + 1];
@@ -1101,8 +1101,9 @@ __device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, 
     }
 }
 
-// ---- dense variant (hops that mark a large fraction of the words): a block of 8 warps
-// per chunk = 32 units of 32 words (one summary word each); warp w takes units w, w+8,
+// ---- dense variant (hops that mark a large fraction of the words; they keep no summary,
+// every word is visited): a block of 8 warps per chunk = 32 units of 32 words; warp w
+// takes units w, w+8,
 // w+16, w+24, one word per lane, so that the emission of a dense word (up to 32 new
 // vertices) is spread over the lanes and the node-array stores of a warp are contiguous.
 constexpr int kUnitsPerWarp = kChunkWords / 32 / 8;   // 4 (blockDim.x == 256)
@@ -1116,7 +1117,7 @@ __device__ void phase_bitcount_dense(const GraphDev &, const HopDev &hd, int bid
     // rounds of 8 chunks c0 + j nb: lane 4j + q prefetches summary word q of chunk j
     for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
         const int cp = c0 + (lane >> 2) * nb;
-        const uint32_t swall = cp < n_chunks ? __ldcg(hd.summary + (int64_t)cp * 32 + wid + 8 * (lane & 3)) : 0u;
+        const uint32_t swall = cp < n_chunks ? 0xFFFFFFFFu : 0u;   // dense hops keep no summary: every word
         for (int j = 0; j < kPrefetch; ++j) {
             const int c = c0 + j * nb;
             if (c >= n_chunks) break;
@@ -1157,9 +1158,7 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
     int32_t *const pos = hd.pos;
     for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
         const int cp = c0 + (lane >> 2) * nb;
-        uint32_t *const spp = hd.summary + (int64_t)cp * 32 + wid + 8 * (lane & 3);
-        const uint32_t swall = cp < n_chunks ? __ldcg(spp) : 0u;
-        if (swall) *spp = 0u;   // this warp's units of the round's chunks are consumed below
+        const uint32_t swall = cp < n_chunks ? 0xFFFFFFFFu : 0u;   // dense hops keep no summary: every word
         for (int j = 0; j < kPrefetch; ++j) {
             const int c = c0 + j * nb;
             if (c >= n_chunks) break;
@@ -1232,7 +1231,7 @@ __device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &
     const uint64_t n_t = (uint64_t)(t_hi - t_lo);
     const int n_neg = lp.n_neg;
     uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const summary = hd.summary;
+    uint32_t *const summary = hd.summary_mark;
     int64_t *const neg = lp.neg;
     for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
         const int64_t a = src[i], b = dst[i];
