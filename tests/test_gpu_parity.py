@@ -67,6 +67,8 @@ def test_c1_batches(c1, g_idx):
     [[1, 1, 1], [1, 1, 1], [1, 1, 1]],     # 3 hops of k = 1
     [[150, 150, 150]],                     # k > fast-path limit (generic selection)
     [[113, 40, 112]],                      # around the fast-path boundary
+    [[2, 1, 2]] * 8,                       # EG_MAX_HOPS hops
+    [[33, 32, 31], [5, 4, 6]],             # around the tiny-selection bound (d <= 32)
 ])
 def test_c1_fanouts(c1, fanouts):
     cfg, g, rows, ctx = c1
