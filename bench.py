@@ -499,6 +499,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                          "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction per GPU",
                          "per_unit": "row_bytes per input row owned by a peer (read over NVLink)",
                          "algorithmic_bytes_per_launch": nv_bytes, "remote_row_fraction": frac_remote,
+                         # both directions are busy (every GPU reads from and serves its peers):
+                         # profiles/micro/p2p_rw.cu measured 645 GB/s per GPU for random 512-B rows
+                         "peak_bidirectional_measured": 645.0, "frac_bidirectional": nv_achieved / 645.0,
                          "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak}})
 
     if args.features != "device":
