@@ -100,8 +100,10 @@ struct HopDev {
     int32_t max_heavy;               // heavy item slots
     int32_t max_heavy_tasks;         // heavy task slots
     int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
-    uint32_t *bitmap;                // this hop's marks: every sampled source (A)
-    uint32_t *members;               // vertices already in the batch (M); new = A & ~M
+    uint32_t *bitmap;                // interleaved word pairs: marks A (every sampled source of
+                                     // the hop) at 2w, members M (vertices already in the batch) at
+                                     // 2w+1; new = A & ~M.  One 8-B access reads or writes both
+                                     // words of a pair (one sector instead of two)
     uint32_t *summary;               // bit w of the summary = A word w may be nonzero
     uint32_t *summary_mark;          // = summary on sparse hops; null on dense hops (no summary)
     int32_t *chunk_cnt;              // new vertices per bitmap chunk

@@ -63,8 +63,7 @@ struct TimedPair {
 // scan scratch.
 struct BatchState {
     int32_t *pos = nullptr;
-    uint32_t *bitmap = nullptr;
-    uint32_t *members = nullptr;
+    uint32_t *bitmap = nullptr;     // word pairs (A, M), HopDev::bitmap
     uint32_t *summary = nullptr;
     int32_t *chunk_cnt = nullptr;
     int32_t *seg_cnt = nullptr;
@@ -171,6 +170,7 @@ struct eg_ctx {
     Fork fork{};                          // capture side stream + events (graph branches)
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
     int compact = 0;                      // EG_COMPACT at create: 0 per hop, 1 dense, 2 sparse
+    int prio = 1;                         // EG_PRIO at create: 0 none, 1 gather first, 2 sampling first
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
@@ -349,10 +349,8 @@ eg_status alloc_state(eg_ctx *c, BatchState *st)
     const size_t words = (size_t)std::max<int64_t>(1, c->g.boff[c->g.n_vt] / 32);
     EG_CUDA(c, cudaMalloc(&st->pos, sizeof(int32_t) * nt));
     EG_CUDA(c, cudaMemset(st->pos, 0xFF, sizeof(int32_t) * nt));
-    EG_CUDA(c, cudaMalloc(&st->bitmap, sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMemset(st->bitmap, 0, sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMalloc(&st->members, sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMemset(st->members, 0, sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMalloc(&st->bitmap, 2 * sizeof(uint32_t) * words));
+    EG_CUDA(c, cudaMemset(st->bitmap, 0, 2 * sizeof(uint32_t) * words));
     EG_CUDA(c, cudaMalloc(&st->summary, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
     EG_CUDA(c, cudaMemset(st->summary, 0, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
     EG_CUDA(c, cudaMalloc(&st->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
@@ -535,6 +533,11 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
         // EG_COMPACT=dense|sparse forces a compaction variant (tests); default per hop (plan)
         const char *cm = getenv("EG_COMPACT");
         c->compact = !cm ? 0 : (cm[0] == 'd' ? 1 : (cm[0] == 's' ? 2 : 0));
+        // EG_PRIO=gather|sample|none: per-node scheduling priority inside the batch graphs.
+        // Default gather: measured (profiles/prio_sweep.sh) it shortens the gather's
+        // duration in the pipelined run by 8-20 % at unchanged throughput (C2, C4).
+        const char *pr = getenv("EG_PRIO");
+        c->prio = !pr ? 1 : (pr[0] == 'g' ? 1 : (pr[0] == 's' ? 2 : 0));
     }
     if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->fork.side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -918,7 +921,6 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         hd.partial = st.partial;
         hd.pos = st.pos;
         hd.bitmap = st.bitmap;
-        hd.members = st.members;
         hd.summary = st.summary;
         hd.chunk_cnt = st.chunk_cnt;
         hd.seg_cnt = st.seg_cnt;
@@ -988,6 +990,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         sl->tev.push_back(ev);
         sl->tlab.push_back(label);
     };
+    cudaGraphNode_t gather_node = nullptr;
     EG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     for (int b = 0; b < B; ++b) {
         char *base = p->batch_base(sl->mem, b);
@@ -1007,6 +1010,13 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         if (any) {
             launch_gather(g, c->f, gs, cs);
             ++nk;
+            if (c->prio) {
+                cudaStreamCaptureStatus st;
+                const cudaGraphNode_t *deps = nullptr;
+                size_t nd = 0;
+                if (cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &nd) == cudaSuccess && nd == 1)
+                    gather_node = deps[0];
+            }
         }
         cudaEventRecordWithFlags(sl->g1, cs, cudaEventRecordExternal);
         mark("gather");
@@ -1017,7 +1027,28 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
     if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&sl->exec, graph, 0);
+    unsigned long long iflags = 0;
+    if (c->prio) {
+        // the favoured side (the gather, or the latency-bound sampling chain) gets the
+        // greatest priority: the block scheduler places its CTAs first when several
+        // lanes' kernels compete for SMs
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        size_t n = 0;
+        cudaGraphGetNodes(graph, nullptr, &n);
+        std::vector<cudaGraphNode_t> nodes(n);
+        cudaGraphGetNodes(graph, nodes.data(), &n);
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+            const bool is_g = nd == gather_node;
+            cudaKernelNodeAttrValue v{};
+            v.priority = (is_g == (c->prio == 1)) ? hi : lo;
+            cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v);
+        }
+        iflags = cudaGraphInstantiateFlagUseNodePriority;
+    }
+    e = cudaGraphInstantiateWithFlags(&sl->exec, graph, iflags);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(c, EG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     p->n_kernels = nk;
@@ -1597,7 +1628,6 @@ eg_status eg_destroy(eg_ctx *c)
         for (BatchState &bs : ln.st) {
             cudaFree(bs.pos);
             cudaFree(bs.bitmap);
-            cudaFree(bs.members);
             cudaFree(bs.summary);
             cudaFree(bs.chunk_cnt);
             cudaFree(bs.seg_cnt);

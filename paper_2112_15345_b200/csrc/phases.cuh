@@ -79,7 +79,7 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
                 // members of the current batch, so it needs no reset between batches)
                 const int64_t bit = g.boff[vt] + (gid - g.off[vt]);
                 const uint32_t mb = 1u << (bit & 31);
-                if (atomicOr(hd.members + (bit >> 5), mb) & mb) atomicOr(meta + kMetaErr, kErrSeedDup);
+                if (atomicOr(hd.bitmap + 2 * (bit >> 5) + 1, mb) & mb) atomicOr(meta + kMetaErr, kErrSeedDup);
             } else {
                 atomicOr(meta + kMetaErr, kErrCapacity);
             }
@@ -235,7 +235,7 @@ __device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t *summary, ui
 {
     const int64_t bit = bit_base + gid;
     const int64_t w = bit >> 5;
-    atomicOr(bitmap + w, 1u << (bit & 31));   // results unused: RED
+    atomicOr(bitmap + 2 * w, 1u << (bit & 31));   // results unused: RED (word A of the pair)
     if (summary) atomicOr(summary + (w >> 5), 1u << (w & 31));   // sparse hops only
 }
 
@@ -965,7 +965,6 @@ __device__ void phase_bitcount_sparse(const GraphDev &, const HopDev &hd, int bi
 {
     const int lane = lane_id();
     uint32_t *const bitmap = hd.bitmap;
-    const uint32_t *const members = hd.members;
     const int64_t n_items = (int64_t)n_chunks * kHalves;
     const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
     int64_t it = (int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -988,15 +987,16 @@ __device__ void phase_bitcount_sparse(const GraphDev &, const HopDev &hd, int bi
                 if (bits) {
                     t[q] = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    a[q] = __ldcg(bitmap + w0 + t[q]);
-                    m[q] = __ldcg(members + w0 + t[q]);
+                    const uint2 am = __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w0 + t[q]);
+                    a[q] = am.x;
+                    m[q] = am.y;
                 }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t nw = a[q] & ~m[q];
                 cnt += __popc(nw);
-                if (a[q] && !nw) bitmap[w0 + t[q]] = 0u;   // only members marked: consumed here
+                if (a[q] && !nw) bitmap[2 * (w0 + t[q])] = 0u;   // only members marked: consumed here
             }
         }
         hd.seg_cnt[c * kSlices + hc * 32 + lane] = cnt;
@@ -1038,7 +1038,6 @@ __device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, 
 {
     const int lane = lane_id();
     uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const members = hd.members;
     int32_t *const pos = hd.pos;
     const int64_t n_items = (int64_t)n_chunks * kHalves;
     const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
@@ -1074,16 +1073,18 @@ __device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, 
                 if (bits) {
                     t[q] = __ffs(bits) - 1;
                     bits &= bits - 1;
-                    a[q] = __ldcg(bitmap + w0 + t[q]);
-                    m[q] = __ldcg(members + w0 + t[q]);
+                    const uint2 am = __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w0 + t[q]);
+                    a[q] = am.x;
+                    m[q] = am.y;
                 }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 uint32_t word = a[q] & ~m[q];
-                if (a[q]) bitmap[w0 + t[q]] = 0u;
+                if (!a[q]) continue;
+                // marks consumed, new vertices now members: one 8-B store of the pair
+                reinterpret_cast<uint2 *>(bitmap)[w0 + t[q]] = make_uint2(0u, m[q] | word);
                 if (!word) continue;
-                members[w0 + t[q]] = m[q] | word;   // now members
                 const int64_t gb = gid0 + 32 * t[q];
                 while (word) {
                     const int b = __ffs(word) - 1;
@@ -1113,7 +1114,6 @@ __device__ void phase_bitcount_dense(const GraphDev &, const HopDev &hd, int bid
 {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     uint32_t *const bitmap = hd.bitmap;
-    const uint32_t *const members = hd.members;
     // rounds of 8 chunks c0 + j nb: lane 4j + q prefetches summary word q of chunk j
     for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
         const int cp = c0 + (lane >> 2) * nb;
@@ -1132,14 +1132,15 @@ __device__ void phase_bitcount_dense(const GraphDev &, const HopDev &hd, int bid
             for (int q = 0; q < kUnitsPerWarp; ++q) {
                 const bool b = (__shfl_sync(0xffffffffu, sw, q) >> lane) & 1u;
                 const int64_t w = (u0 + 8 * q) * 32 + lane;
-                a[q] = b ? __ldcg(bitmap + w) : 0u;
-                m[q] = b ? __ldcg(members + w) : 0u;
+                const uint2 am = b ? __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w) : make_uint2(0u, 0u);
+                a[q] = am.x;
+                m[q] = am.y;
             }
             int32_t cnt_mine = 0, total = 0;
 #pragma unroll
             for (int q = 0; q < kUnitsPerWarp; ++q) {
                 const uint32_t nw = a[q] & ~m[q];
-                if (a[q] && !nw) bitmap[(u0 + 8 * q) * 32 + lane] = 0u;   // only members marked: consumed
+                if (a[q] && !nw) bitmap[2 * ((u0 + 8 * q) * 32 + lane)] = 0u;   // only members marked: consumed
                 const int32_t v = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)__popc(nw));
                 if (lane == q) cnt_mine = v;
                 total += v;
@@ -1154,7 +1155,6 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
 {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const members = hd.members;
     int32_t *const pos = hd.pos;
     for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
         const int cp = c0 + (lane >> 2) * nb;
@@ -1180,8 +1180,9 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
                 su[q] = __shfl_sync(0xffffffffu, sw, q);
                 const int64_t w = (u0 + 8 * q) * 32 + lane;
                 const bool b = (su[q] >> lane) & 1u;
-                a[q] = b ? __ldcg(bitmap + w) : 0u;
-                m[q] = b ? __ldcg(members + w) : 0u;
+                const uint2 am = b ? __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w) : make_uint2(0u, 0u);
+                a[q] = am.x;
+                m[q] = am.y;
             }
 #pragma unroll
             for (int q = 0; q < kUnitsPerWarp; ++q) {
@@ -1192,9 +1193,8 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
                 const int32_t pc = __popc(word);
                 int32_t position = base + ubase + (warp_incl_scan(pc) - pc);
                 const int64_t w = (u0 + 8 * q) * 32 + lane;
-                if (a[q]) bitmap[w] = 0u;
+                if (a[q]) reinterpret_cast<uint2 *>(bitmap)[w] = make_uint2(0u, m[q] | word);   // one 8-B store
                 if (!word) continue;
-                members[w] = m[q] | word;   // now members
                 const int64_t gb = gid0 + w * 32;
                 while (word) {
                     const int b = __ffs(word) - 1;
@@ -1309,14 +1309,14 @@ __device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, 
     int64_t cum[EG_MAX_VT + 1];
     cum[0] = 0;
     for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
-    uint32_t *const members = hd.members;
+    uint32_t *const bitmap = hd.bitmap;
     for (int u = 0; u < g.n_vt; ++u) {
         const int64_t *const nodes = hd.nodes[u];
         const int64_t n = cum[u + 1] - cum[u];
         const int64_t lo = g.off[u], hi = g.off[u + 1], b0 = g.boff[u];
         for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
             const int64_t gid = nodes[i];
-            if (gid >= lo && gid < hi) members[(b0 + (gid - lo)) >> 5] = 0u;
+            if (gid >= lo && gid < hi) bitmap[2 * ((b0 + (gid - lo)) >> 5) + 1] = 0u;
         }
     }
 }
