@@ -51,13 +51,20 @@ def parse():
     ap.add_argument("--features", default="device", choices=["device", "host"],
                     help="feature rows in HBM (default) or in pinned host memory read zero-copy over PCIe "
                          "(NEXT-4 ii: the paper's placement, lets C5 run on one GPU)")
+    ap.add_argument("--replicate", default="auto",
+                    help="replicated feature partition policy (P:468-473) for small vertex types: auto (N > 1: "
+                         "every type whose full table is <= 64 MiB gets a local copy on each GPU), none, or a "
+                         "comma list of type indices")
     ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
     ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.replicate not in ("auto", "none"):
+        a.replicate = [int(x) for x in a.replicate.split(",") if x != ""]
+    return a
 
 
 def dist_env():
@@ -292,7 +299,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                                    (world == 1 and not args.no_cpu_baseline))
     t_load = time.perf_counter()
     ctx = Context(rank, world, local_rank, stream)
-    shard = load_context(ctx, graph, world, rank, dev, features=args.features if args.features != "device" else True)
+    shard = load_context(ctx, graph, world, rank, dev, features=args.features if args.features != "device" else True,
+                         replicate=args.replicate if args.features == "device" else "none")
+    replicas = sorted(shard["replicas"])
     if world > 1:
         ctx.connect_peers()
     ctx.set_pipeline(args.depth, args.bundle)
@@ -486,7 +495,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             for u in cfg.feats:
                 ids = bl[bl.n_hops - 1].src_nodes[u] - int(cfg.offsets[u])
                 lo, hi = int(bounds[u][rank]), int(bounds[u][rank + 1])
-                n_remote = int(((ids < lo) | (ids >= hi)).sum().item())
+                n_remote = 0 if u in replicas else int(((ids < lo) | (ids >= hi)).sum().item())
                 remote += n_remote * row_bytes[u]
                 rows_tot += ids.numel() * row_bytes[u]
             bl.free()
@@ -547,7 +556,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "data": "synthetic (seeded generator, synth/)", "config": dict(workload(cfg, world, args.task), seeds=(
                     "confined to the rank's vertex range (second-level partition, P:428-431)" if args.confine
                     else "global epoch permutation, batch g = b*P + p"), features_in=(
-                    "pinned host memory (zero-copy over PCIe)" if args.features == "host" else "HBM")),
+                    "pinned host memory (zero-copy over PCIe)" if args.features == "host" else "HBM"),
+                    feature_replicas=[cfg.vtypes[u][0] for u in replicas]),
                 "minibatches_per_s": world * K / (ms / 1e3),
                 "gather_GBps": achieved if gather_ms > 0 else None,
                 "sampled_edges_per_batch": edges / (world * K),

@@ -146,6 +146,20 @@ EG_API eg_status eg_import_shards(eg_ctx *ctx, const void *blobs, size_t stride)
  * one GPU). */
 EG_API eg_status eg_attach_peer(eg_ctx *ctx, const eg_ctx *peer);
 
+/* Replicated partition policy for one vertex type's features ("Each ID
+ * space is also associated with a partition policy that maps vertex/edge data to
+ * physical machines"; here a policy may map a small type to every GPU).  rows: the
+ * type's FULL table, n_rows == N_vt rows of the row_bytes given at load, row-major by
+ * type-local id, in device memory of this context's GPU; BORROWED until eg_destroy.
+ * The gather then reads that type's rows from the local replica instead of the
+ * owners' shards (no NVLink traffic for it); results are byte-identical either way,
+ * since the replica must equal the sharded rows (not checked).  rows == NULL restores
+ * the sharded policy.  Per rank, not collective; call after eg_load_partition and
+ * before the first sampling call (the batch graphs capture the policy): EG_ESTATE
+ * otherwise.  EG_EINVAL: vt out of range, a type without features, n_rows != N_vt,
+ * rows not device memory of this GPU. */
+EG_API eg_status eg_set_feature_replica(eg_ctx *ctx, int32_t vt, const void *rows, int64_t n_rows);
+
 /* Sample L = n_hops blocks from `seeds` (gids, unique, any vertex types, caller
  * order; host or device pointer; n_seeds may be 0).  fanouts: host [n_hops][n_rel],
  * row 0 = hop at the seeds; -1 = all in-neighbours, 0 = none, k > 0 = at most k,

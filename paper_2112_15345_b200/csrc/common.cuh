@@ -50,7 +50,9 @@ struct GraphDev {
 struct FeatDev {
     const uint8_t *rows[EG_MAX_VT][EG_MAX_RANKS];
     int64_t row_bytes[EG_MAX_VT];
+    const uint8_t *replica[EG_MAX_VT];   // full local table of a replicated type (tid-indexed), or null
 };
+
 
 // Device counters of one batch (int32 slots in one small array).
 //   nodes(l, u): |level l of type u|, l = 0 seeds, l = h+1 src nodes of block h
@@ -140,6 +142,15 @@ __device__ __forceinline__ int owner_of(const GraphDev &g, int t, int64_t tid)
     int p = 0;
     while (p < g.world - 1 && tid >= g.bounds[t][p + 1]) ++p;
     return p;
+}
+
+// Source row of (type u, type-local id tid): the local replica of a replicated type,
+// else the owner's shard (local HBM, or a peer's over NVLink).
+__device__ __forceinline__ const uint8_t *feature_row(const GraphDev &g, const FeatDev &f, int u, int64_t tid)
+{
+    if (f.replica[u]) return f.replica[u] + tid * f.row_bytes[u];
+    const int p = owner_of(g, u, tid);
+    return f.rows[u][p] + (tid - g.bounds[u][p]) * f.row_bytes[u];
 }
 
 // ------------------------------------------------------------------ warp / block scans

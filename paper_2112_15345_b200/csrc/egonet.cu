@@ -778,6 +778,29 @@ eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
     return EG_OK;
 }
 
+eg_status eg_set_feature_replica(eg_ctx *c, int32_t vt, const void *rows, int64_t n_rows)
+{
+    eg_status st = enter(c);
+    if (st) return st;
+    if (!c->loaded) return fail(c, EG_ESTATE, "eg_set_feature_replica before eg_load_partition");
+    if (!c->plans.empty()) return fail(c, EG_ESTATE, "eg_set_feature_replica after the first sampling call");
+    if (vt < 0 || vt >= c->g.n_vt) return fail(c, EG_EINVAL, "vertex type out of range");
+    if (!rows) {
+        c->f.replica[vt] = nullptr;
+        return EG_OK;
+    }
+    if (!c->f.row_bytes[vt]) return fail(c, EG_EINVAL, "vertex type has no features");
+    if (n_rows != c->vt_counts[vt]) return fail(c, EG_EINVAL, "replica must hold all N_t rows of the type");
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, rows) != cudaSuccess || at.type != cudaMemoryTypeDevice ||
+        at.device != c->device) {
+        cudaGetLastError();
+        return fail(c, EG_EINVAL, "replica rows must be device memory of this context's GPU");
+    }
+    c->f.replica[vt] = (const uint8_t *)rows;
+    return EG_OK;
+}
+
 }  // extern "C"
 
 namespace {

@@ -67,8 +67,7 @@ __global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__
         const uint8_t *srow = nullptr;
         if (lane < nrows) {
             const int64_t tid = __ldg(gd.nodes[u] + row0 + lane) - g.off[u];
-            const int p = owner_of(g, u, tid);
-            srow = f.rows[u][p] + (tid - g.bounds[u][p]) * rb;
+            srow = feature_row(g, f, u, tid);
         }
         uint8_t *dbase = gd.out[u] + row0 * rb;
         const bool wide = U >= 32;
@@ -229,8 +228,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             uint8_t *dst = stage_mem + s * kStageBytes;
             for (int rr = lane; rr < nrows; rr += 32) {
                 const int64_t tid = __ldg(gs.b[b].nodes[u] + row0 + rr) - g.off[u];
-                const int p = owner_of(g, u, tid);
-                bulk_g2s(dst + rr * rb, f.rows[u][p] + (tid - g.bounds[u][p]) * rb, (uint32_t)rb, &full[s]);
+                bulk_g2s(dst + rr * rb, feature_row(g, f, u, tid), (uint32_t)rb, &full[s]);
             }
         }
     } else if (lane == 0) {

@@ -29,7 +29,7 @@ ABI_SYMBOLS = [
     "eg_blocks_free", "eg_destroy", "eg_last_error", "eg_set_profiling", "eg_get_profile", "eg_kernel_launches",
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
-    "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer",
+    "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer", "eg_set_feature_replica",
 ]
 
 EG_FEATURES = 1
@@ -134,6 +134,7 @@ def lib(build_if_missing: bool = True):
         L.eg_export_shard.argtypes = [vp, vp, P(c.c_size_t)]
         L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
         L.eg_attach_peer.argtypes = [vp, vp]
+        L.eg_set_feature_replica.argtypes = [vp, c.c_int32, vp, c.c_int64]
         L.eg_set_pipeline.argtypes = [vp, c.c_int32, c.c_int32]
         L.eg_sample_bundle.argtypes = [vp, c.c_int32, vp, vp, c.c_int32, vp, vp, c.c_int32, vp]
         L.eg_sample_lp_bundle.argtypes = [vp, c.c_int32, vp, vp, vp, c.c_int32, c.c_int32, vp, c.c_int32, vp, vp,
@@ -435,6 +436,18 @@ class Context:
     def attach_peer(self, peer: "Context"):
         """Single-process peer mapping (another rank's context in this process)."""
         self._check(lib().eg_attach_peer(self._h, peer._h), "eg_attach_peer")
+
+    def set_feature_replica(self, vt: int, rows):
+        """Replicated partition policy for type vt's features: `rows` is the type's full
+        table on this GPU (cuda tensor [N_vt, ...]); None restores the sharded policy.
+        Call before the first sampling call."""
+        if rows is None:
+            self._check(lib().eg_set_feature_replica(self._h, vt, None, 0), "eg_set_feature_replica")
+            return
+        assert rows.is_contiguous()   # device memory of this GPU: checked by the library (EG_EINVAL)
+        self._check(lib().eg_set_feature_replica(self._h, vt, ctypes.c_void_p(rows.data_ptr()), rows.shape[0]),
+                    "eg_set_feature_replica")
+        self._keep.append(rows)
 
     def import_shards(self, blobs):
         stride = len(blobs[0])

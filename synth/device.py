@@ -83,9 +83,40 @@ def device_shard(graph: HostGraph, world: int, rank: int, device, features=True)
     return {"vt_counts": cfg.vt_counts, "bounds": bounds, "rels": out_rels, "feats": feats}
 
 
-def load_context(ctx, graph: HostGraph, world: int, rank: int, device, features=True):
+REPLICA_BUDGET = 64 << 20   # bytes: "auto" replicates feature types whose full table is this small
+
+
+def replica_types(cfg: Config, world: int, spec="auto", budget: int = REPLICA_BUDGET):
+    """Vertex types whose features follow the replicated partition policy.
+    spec: "auto" (world > 1: every type whose full table is <= budget bytes), "none", or an
+    iterable of type indices."""
+    if spec is None or spec == "none":
+        return []
+    if spec == "auto":
+        if world <= 1:
+            return []
+        out = []
+        for u, (dim, dt) in cfg.feats.items():
+            rb = dim * (4 if dt == 0 else 2)
+            if int(cfg.vt_counts[u]) * rb <= budget:
+                out.append(u)
+        return sorted(out)
+    return sorted(int(u) for u in spec)
+
+
+def load_context(ctx, graph: HostGraph, world: int, rank: int, device, features=True, replicate="none"):
     """device_shard + Context.load_partition; returns the shard dict (keep it alive).
-    features: True (rows on the GPU), False (none) or "host" (pinned host memory)."""
+    features: True (rows on the GPU), False (none) or "host" (pinned host memory).
+    replicate: see replica_types; each replicated type's full table is generated on this
+    GPU (same formula as the shards) and handed to Context.set_feature_replica."""
     sh = device_shard(graph, world, rank, device, features)
     ctx.load_partition(sh["vt_counts"], sh["rels"], sh["feats"], bounds=sh["bounds"])
+    cfg = graph.cfg
+    sh["replicas"] = {}
+    if features is True:
+        for u in replica_types(cfg, world, replicate):
+            t = feature_shard(cfg, u, 0, int(cfg.vt_counts[u]), device)
+            _torch().cuda.synchronize(device)
+            ctx.set_feature_replica(u, t)
+            sh["replicas"][u] = t
     return sh

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batches", type=int, default=4)
+    ap.add_argument("--replicate", default="auto", help="replicated feature types: auto | none")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -38,7 +39,7 @@ def main():
     cfg = synth.config(args.config)
     g = synth.build_host_graph(cfg)
     ctx = Context(rank, world, local)
-    shard = load_context(ctx, g, world, rank, f"cuda:{local}")
+    shard = load_context(ctx, g, world, rank, f"cuda:{local}", replicate=args.replicate)
     ctx.connect_peers()
     small = cfg.name in ("C1", "C2", "C3")
     rows = {u: (synth.host_features(cfg, u) if small else synth.LazyRows(cfg, u)) for u in cfg.feats}

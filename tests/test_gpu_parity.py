@@ -16,18 +16,18 @@ from gpu_util import assert_same_batch, assert_same_features, run_and_compare
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(graph, world=1, rank=0, features=True):
+def _ctx(graph, world=1, rank=0, features=True, replicate="none"):
     from paper_2112_15345_b200 import Context
     from synth.device import load_context
     ctx = Context(rank, world, 0)
-    shard = load_context(ctx, graph, world, rank, "cuda:0", features=features)
+    shard = load_context(ctx, graph, world, rank, "cuda:0", features=features, replicate=replicate)
     ctx._shard = shard
     return ctx
 
 
-def _world(graph, world, features=True):
+def _world(graph, world, features=True, replicate="none"):
     """All ranks of a world in this process on one GPU, mapped to each other."""
-    ctxs = [_ctx(graph, world, p, features) for p in range(world)]
+    ctxs = [_ctx(graph, world, p, features, replicate) for p in range(world)]
     for a in ctxs:
         for b in ctxs:
             if a is not b:
@@ -158,6 +158,55 @@ def test_c2_world4_invariance(c2):
     for p in (0, 3):
         run_and_compare(ctxs[p], g, cfg, synth.batch_seeds(cfg, 20 + p), cfg.fanouts, synth.rng_seed(cfg, 20 + p),
                         rows)
+
+
+# ----------------------------------------------------------------------------- replicated feature types
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c2_replicated_small_types(c2, world):
+    """Replicated partition policy for the small types (institution, field):
+    same bytes as the sharded policy, standalone gather and the graph path."""
+    import torch
+    from synth.device import replica_types
+    cfg, g, rows, _ = c2
+    assert replica_types(cfg, world) == [2, 3]
+    ctxs = _world(g, world, replicate="auto")
+    for p in (0, world - 1):
+        gi = 40 + p
+        seeds, rs = synth.batch_seeds(cfg, gi), synth.rng_seed(cfg, gi)
+        run_and_compare(ctxs[p], g, cfg, seeds, cfg.fanouts, rs, rows)
+        res = oracle.sample(g, seeds, cfg.fanouts, rs)
+        b = ctxs[p].sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+        assert_same_features(res, _features_of(b, cfg), cfg, rows)
+        b.free()
+
+
+def test_replica_is_what_the_gather_reads(c1):
+    """Negative control: a replica whose bytes differ from the shards shows up in the
+    output for that type only (so the policy is really applied), and the API errors."""
+    import torch
+    from paper_2112_15345_b200 import EgError
+    cfg, g, rows, _ = c1
+    ctxs = _world(g, 2)
+    n0 = int(cfg.vt_counts[0])
+    fake = torch.full((n0, cfg.feats[0][0]), 7.0, dtype=torch.float32, device="cuda:0")
+    with pytest.raises(EgError):
+        ctxs[0].set_feature_replica(0, fake[:-1])                    # not all N_t rows
+    with pytest.raises(EgError):
+        ctxs[0].set_feature_replica(0, fake.cpu())                   # not device memory
+    with pytest.raises(EgError):
+        ctxs[0].set_feature_replica(5, fake)                         # type out of range
+    ctxs[0].set_feature_replica(0, fake)
+    seeds, rs = synth.batch_seeds(cfg, 3), synth.rng_seed(cfg, 3)
+    res = oracle.sample(g, seeds, cfg.fanouts, rs)
+    b = ctxs[0].sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+    f = _features_of(b, cfg)
+    assert torch.all(f[0] == 7.0) and f[0].shape[0] == len(res.input_nodes(0))
+    want1 = oracle.gather(res, cfg.vt_counts, 1, rows[1])
+    assert f[1].cpu().numpy().tobytes() == want1.tobytes()
+    b.free()
+    with pytest.raises(EgError):
+        ctxs[0].set_feature_replica(0, None)                         # after the first sampling call
 
 
 # ----------------------------------------------------------------------------- C3 (3 hops, hub of degree 618k)
