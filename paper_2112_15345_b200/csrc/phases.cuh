@@ -247,6 +247,40 @@ __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_
     mark_src(it.bitmap, it.summary, gid, it.bit_base);
 }
 
+// Up to four selected edges of one lane: the source-id loads are issued together before
+// any store (the stores could alias them as far as the compiler knows, so the per-edge
+// form serialised load -> store chains; measured, ncu: the emission was the top stall
+// of the tiny-item kernel).  Edge t (bit t of sel) has offset j[t] and output slot
+// slot[t].
+__device__ __forceinline__ void emit_edges4(const Item &it, uint32_t sel, const int64_t j[4], const int32_t slot[4])
+{
+    uint32_t ix[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) ix[t] = (sel >> t & 1) ? __ldg(it.ix + j[t]) : 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (sel >> t & 1) {
+            const uint32_t gid = it.soff + ix[t];
+            it.src_out[slot[t]] = gid;
+            it.eid_out[slot[t]] = it.ebase + j[t];
+            mark_src(it.bitmap, it.summary, gid, it.bit_base);
+        }
+}
+
+// Consecutive offsets j0 .. j0+3 (bits of sel), emitted in ascending order from `slot`.
+__device__ __forceinline__ void emit_run4(const Item &it, uint32_t sel, int32_t slot, int64_t j0)
+{
+    int64_t j[4];
+    int32_t s[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        j[t] = j0 + t;
+        s[t] = slot;
+        slot += (sel >> t) & 1;
+    }
+    emit_edges4(it, sel, j, s);
+}
+
 // Four keys key32(seed, h, r, v, 4q .. 4q+3) from one Philox call.
 __device__ __forceinline__ void keys4(uint32_t q, uint32_t v_lo, uint32_t v_hi, uint32_t hr, uint32_t k0,
                                       uint32_t k1, uint32_t w[4])
@@ -366,10 +400,7 @@ __device__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k,
             ++er;
         }
     const int cs = __popc(sel);
-    int slot = warp_incl_scan(cs) - cs;
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-        if (sel >> t & 1) emit_edge(hd, it, slot++, 4 * lane + t);
+    emit_run4(it, sel, warp_incl_scan(cs) - cs, 4 * lane);
 }
 
 // Fast selection for k <= kSelMaxK: one pass over the d keys keeps the candidates
@@ -449,6 +480,9 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
         // selected: key below P on the decided bits, or matching them and among the first
         // krem such candidates in slot (= ascending j) order
         int eq_seen = 0;
+        uint32_t selm = 0;
+        int64_t jj[4];
+        int32_t ss[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = lane_id() + 32 * i;
@@ -459,9 +493,12 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
             const bool sel = lt || (eq && eq_seen + __popc(beq & lanemask_lt()) < krem);
             eq_seen += __popc(beq);
             const uint32_t bs = __ballot_sync(0xffffffffu, sel);
-            if (sel) emit_edge(hd, it, out + __popc(bs & lanemask_lt()), (int64_t)(uint32_t)cand[c]);
+            selm |= (uint32_t)sel << i;
+            jj[i] = sel ? (int64_t)(uint32_t)cand[c] : 0;
+            ss[i] = out + __popc(bs & lanemask_lt());
             out += __popc(bs);
         }
+        emit_edges4(it, selm, jj, ss);
         __syncwarp();
         return;
     }
@@ -838,12 +875,8 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
                 ++er;
             }
         const int cs = __popc(sel);
-        int slot = group_excl(cs);
-        if (act) {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (sel >> t & 1) emit_edge(hd, itm, slot++, 4 * sl + t);
-        }
+        const int slot = group_excl(cs);
+        if (act) emit_run4(itm, sel, slot, 4 * sl);
         cur = nxt;
     }
 }
