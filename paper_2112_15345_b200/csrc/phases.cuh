@@ -290,6 +290,42 @@ __device__ __forceinline__ void keys4(uint32_t q, uint32_t v_lo, uint32_t v_hi, 
     w[0] = c0; w[1] = c1; w[2] = c2; w[3] = c3;
 }
 
+// Radix select, two bits per step.  With bits [s, 32) of the threshold key decided (P),
+// a key "matches" when its bits [s, 32) equal P's; radix2_count packs, for this thread's
+// keys, the number that match (bits 0-7) and how many of those have digit
+// (key >> (s-2)) & 3 equal to 0, 1, 2 (bits 8-15, 16-23, 24-31); sums of these over the
+// item (<= 128 keys) do not overflow a field.  radix2_decide takes the summed counts and
+// either finishes (every matching key is selected: cm == krem) or fixes the next digit.
+__device__ __forceinline__ uint32_t radix2_count(uint32_t w, bool valid, uint32_t P, int s)
+{
+    const bool match = valid && (s == 32 || (w >> s) == (P >> s));
+    const uint32_t dg = (w >> (s - 2)) & 3u;
+    return match ? 1u + (dg < 3 ? (1u << (8 + 8 * dg)) : 0u) : 0u;
+}
+
+__device__ __forceinline__ bool radix2_decide(uint32_t x, int &krem, uint32_t &P, int &s)
+{
+    const int cm = (int)(x & 0xFFu);
+    if (cm == krem) return true;
+    const int n0 = (int)((x >> 8) & 0xFFu), n1 = (int)((x >> 16) & 0xFFu), n2 = (int)(x >> 24);
+    uint32_t dg;
+    if (krem <= n0) {
+        dg = 0;
+    } else if (krem <= n0 + n1) {
+        dg = 1;
+        krem -= n0;
+    } else if (krem <= n0 + n1 + n2) {
+        dg = 2;
+        krem -= n0 + n1;
+    } else {
+        dg = 3;
+        krem -= n0 + n1 + n2;
+    }
+    s -= 2;
+    P |= dg << s;
+    return s == 0;
+}
+
 // Generic exact selection for any k < d: binary search of the k-th smallest key
 // value T (33 counting passes over the d keys), then one ascending-j emission
 // pass taking key < T and the first (k - #{key < T}) offsets with key == T.
@@ -365,23 +401,11 @@ __device__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k,
     }
     uint32_t P = 0;
     int krem = k, s = 32;
-    while (s > 0) {
-        const int b = s - 1;
-        uint32_t c0 = 0, cm = 0;
+    while (true) {
+        uint32_t x = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const bool match = (vm >> t & 1) && (s == 32 || (w[t] >> s) == (P >> s));
-            cm += match;
-            c0 += match && !((w[t] >> b) & 1u);
-        }
-        cm = __reduce_add_sync(0xffffffffu, cm);
-        if ((int)cm == krem) break;
-        c0 = __reduce_add_sync(0xffffffffu, c0);
-        if (krem > (int)c0) {
-            krem -= (int)c0;
-            P |= 1u << b;
-        }
-        s = b;
+        for (int t = 0; t < 4; ++t) x += radix2_count(w[t], vm >> t & 1, P, s);
+        if (radix2_decide(__reduce_add_sync(0xffffffffu, x), krem, P, s)) break;
     }
     uint32_t ltm = 0, eqm = 0;
 #pragma unroll
@@ -446,7 +470,7 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
     int32_t out = 0;
     if (m <= 128) {
         // radix select of the k-th smallest key among the m candidates, held 4 per lane
-        // (slot c = lane + 32 i); two warp reductions per bit, early exit once every
+        // (slot c = lane + 32 i); one warp reduction per two bits, early exit once every
         // candidate that still matches the decided bits is selected.
         uint32_t key[4];
         bool val[4];
@@ -459,23 +483,11 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
         uint32_t P = 0;          // decided high bits of the threshold key
         int krem = k;            // selections still to make among keys matching P
         int s = 32;              // bits [s, 32) are decided
-        while (s > 0) {
-            const int b = s - 1;
-            uint32_t c0 = 0, cm = 0;
+        while (true) {   // two bits per step; early exit once every matching key is selected
+            uint32_t x = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const bool match = val[i] && (s == 32 || (key[i] >> s) == (P >> s));
-                cm += match;
-                c0 += match && !((key[i] >> b) & 1u);
-            }
-            cm = __reduce_add_sync(0xffffffffu, cm);
-            if ((int)cm == krem) break;                 // all matching keys are selected
-            c0 = __reduce_add_sync(0xffffffffu, c0);
-            if (krem > (int)c0) {
-                krem -= (int)c0;
-                P |= 1u << b;
-            }
-            s = b;
+            for (int i = 0; i < 4; ++i) x += radix2_count(key[i], val[i], P, s);
+            if (radix2_decide(__reduce_add_sync(0xffffffffu, x), krem, P, s)) break;
         }
         // selected: key below P on the decided bits, or matching them and among the first
         // krem such candidates in slot (= ascending j) order
@@ -609,23 +621,11 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
         }
         uint32_t P = 0;
         int krem = k, s = 32;
-        while (s > 0) {
-            const int b = s - 1;
-            uint32_t c0 = 0, cm = 0;
+        while (true) {
+            uint32_t x = 0;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const bool match = val[t] && (s == 32 || (key[t] >> s) == (P >> s));
-                cm += match;
-                c0 += match && !((key[t] >> b) & 1u);
-            }
-            cm = __reduce_add_sync(0xffffffffu, cm);
-            if ((int)cm == krem) break;
-            c0 = __reduce_add_sync(0xffffffffu, c0);
-            if (krem > (int)c0) {
-                krem -= (int)c0;
-                P |= 1u << b;
-            }
-            s = b;
+            for (int t = 0; t < 4; ++t) x += radix2_count(key[t], val[t], P, s);
+            if (radix2_decide(__reduce_add_sync(0xffffffffu, x), krem, P, s)) break;
         }
         uint32_t neq = 0;
 #pragma unroll
@@ -818,35 +818,16 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
         uint32_t P = 0;
         int krem = k, s = 32;
         bool done = !act;
-        while (__any_sync(0xffffffffu, !done)) {
-            const int b = s - 1;
-            uint32_t c0 = 0, cm = 0;
+        while (__any_sync(0xffffffffu, !done)) {   // two bits per step
+            uint32_t pk = 0;
             if (!done) {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const bool match = (vm >> t & 1) && (s == 32 || (w[t] >> s) == (P >> s));
-                    cm += match;
-                    c0 += match && !((w[t] >> b) & 1u);
-                }
+                for (int t = 0; t < 4; ++t) pk += radix2_count(w[t], vm >> t & 1, P, s);
             }
-            uint32_t pk = cm | (c0 << 16);   // both <= 32
             pk += __shfl_xor_sync(0xffffffffu, pk, 1);
             pk += __shfl_xor_sync(0xffffffffu, pk, 2);
             pk += __shfl_xor_sync(0xffffffffu, pk, 4);
-            if (!done) {
-                cm = pk & 0xFFFFu;
-                c0 = pk >> 16;
-                if ((int)cm == krem) {
-                    done = true;
-                } else {
-                    if (krem > (int)c0) {
-                        krem -= (int)c0;
-                        P |= 1u << b;
-                    }
-                    s = b;
-                    done = (s == 0);
-                }
-            }
+            if (!done) done = radix2_decide(pk, krem, P, s);
         }
         uint32_t ltm = 0, eqm = 0;
 #pragma unroll
