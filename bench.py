@@ -485,6 +485,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id); one launch gathers "
                             "the rows of a bundle of %d mini-batches" % args.bundle,
                 "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms}
+    frac_remote = None
     if world > 1:
         with torch.cuda.stream(stream):
             bl = launch(0, 1, seeds_dev, features=False)[0]
@@ -500,6 +501,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 rows_tot += ids.numel() * row_bytes[u]
             bl.free()
         frac_remote = remote / max(1, rows_tot)
+    if frac_remote:   # some rows cross NVLink: that is the bound (else all rows are local: HBM)
         nv_bytes = (gbytes / n_launch) / 2 * frac_remote   # row bytes read over NVLink per launch
         nv_peak = 770.0
         nv_achieved = nv_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0

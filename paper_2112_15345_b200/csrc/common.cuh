@@ -16,7 +16,7 @@ constexpr int kMinScanBlocks = 64;        // virtual blocks per relation in the 
 constexpr int kMaxScanBlocks = 1024;      // about one per 4096 frontier items, within these bounds
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
-constexpr int kTinyD = 32;                // selections with d <= this: 8 lanes per item
+constexpr int kTinyD = 64;                // selections with d <= this: 8 lanes per item (phase_tiny)
 // Heavy items (d > kHeavyD, k <= kHeavyMaxK) are split into tasks of kHeavyChunk keys
 // sampled by different warps; their candidates meet in a per-item buffer.
 constexpr int kHeavyD = 2048;

@@ -743,11 +743,14 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
     }
 }
 
-// Selections of tiny items (k < d <= kTinyD): 8 lanes per item, 4 items per warp.  The
-// same register radix select as select_small, with the sums taken over the 8 lanes of
-// the item; all groups step together (finished groups idle).  Tiny items cost about
-// the same, so they are strided statically over the warps, and the queue entry and
-// item data of the next round are loaded while this round computes.
+// Selections of tiny items (k < d <= kTinyD = 64): 8 lanes per item, 4 items per warp;
+// lane sl of an item holds the keys of offsets 4 sl .. 4 sl + 3 (one Philox call) and,
+// when d > 32, of 32 + 4 sl .. 32 + 4 sl + 3 (a second call).  The same register radix
+// select as select_small, with the sums taken over the 8 lanes of the item; all groups
+// step together (finished groups idle).  Tiny items cost about the same, so they are
+// strided statically over the warps, and the queue entry and item data of the next round
+// are loaded while this round computes.  (Measured: items with 32 < d <= 64 took a whole
+// warp each in select_small, with 3/4 of its 128 key slots empty.)
 struct TinyItem {
     uint32_t r, i;
     int32_t pos0, d;
@@ -772,7 +775,7 @@ __device__ __forceinline__ void tiny_load(const GraphDev &g, const HopDev &hd, u
 
 __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
-    static_assert(kTinyD == 32, "8 lanes x 4 keys");
+    static_assert(kTinyD == 64, "8 lanes x (4 + 4) keys");
     const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
     const int64_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
@@ -784,6 +787,17 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
     tiny_load(g, hd, q < ntiny ? selq_top[-q] : 0ull, q < ntiny, cur);
     const int64_t step = nw * 4;
     uint64_t e_next = q + step < ntiny ? selq_top[-(q + step)] : 0ull;
+    // exclusive scan / total over the 8 lanes of the item
+    auto group_excl = [&](int x, int &tot) {
+        int y = x;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int z = __shfl_up_sync(0xffffffffu, y, o, 8);
+            if (sl >= o) y += z;
+        }
+        tot = __shfl_sync(0xffffffffu, y, 7, 8);
+        return y - x;
+    };
     for (; q - gi < ntiny; q += step) {
         const bool act = q < ntiny;
         TinyItem nxt;
@@ -792,7 +806,7 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
         Item itm;
         int k = 0;
         const int32_t d = cur.d;
-        uint32_t w[4] = {0, 0, 0, 0}, vm = 0;
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vm = 0;   // bit t < 4: j = 4 sl + t; t >= 4: j = 32 + 4 sl + t - 4
         if (act) {
             const int r = (int)cur.r;
             const RelDev &R = g.rel[r];
@@ -808,13 +822,20 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
             itm.src_out = hd.src[r] + cur.pos0;
             itm.eid_out = hd.eids[r] + cur.pos0;
             k = hd.fanout[r];
+            const uint32_t vlo = (uint32_t)cur.v, vhi = (uint32_t)((uint64_t)cur.v >> 32);
+            const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
             if (4 * sl < d) {
-                keys4((uint32_t)sl, (uint32_t)cur.v, (uint32_t)((uint64_t)cur.v >> 32),
-                      ((uint32_t)hd.h << 16) | (uint32_t)r, seed_lo, seed_hi, w);
+                keys4((uint32_t)sl, vlo, vhi, hr, seed_lo, seed_hi, w);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) vm |= (uint32_t)(4 * sl + t < d) << t;
             }
+            if (32 + 4 * sl < d) {
+                keys4((uint32_t)(8 + sl), vlo, vhi, hr, seed_lo, seed_hi, w + 4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) vm |= (uint32_t)(32 + 4 * sl + t < d) << (4 + t);
+            }
         }
+        const bool upper = __any_sync(0xffffffffu, (vm >> 4) != 0);   // warp-uniform: any d > 32
         uint32_t P = 0;
         int krem = k, s = 32;
         bool done = !act;
@@ -823,6 +844,10 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
             if (!done) {
 #pragma unroll
                 for (int t = 0; t < 4; ++t) pk += radix2_count(w[t], vm >> t & 1, P, s);
+                if (upper) {
+#pragma unroll
+                    for (int t = 4; t < 8; ++t) pk += radix2_count(w[t], vm >> t & 1, P, s);
+                }
             }
             pk += __shfl_xor_sync(0xffffffffu, pk, 1);
             pk += __shfl_xor_sync(0xffffffffu, pk, 2);
@@ -831,33 +856,34 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
         }
         uint32_t ltm = 0, eqm = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < 8; ++t) {
             const uint32_t hi = s == 32 ? 0u : (w[t] >> s), ph = s == 32 ? 0u : (P >> s);
             ltm |= (uint32_t)((vm >> t & 1) && hi < ph) << t;
             eqm |= (uint32_t)((vm >> t & 1) && hi == ph) << t;
         }
-        // exclusive scans over the 8 lanes of the item (ascending j)
-        auto group_excl = [&](int x) {
-            int y = x;
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
-                const int z = __shfl_up_sync(0xffffffffu, y, o, 8);
-                if (sl >= o) y += z;
-            }
-            return y - x;
-        };
-        const int ce = __popc(eqm);
-        int er = group_excl(ce);
+        // ascending j: the lower halves of the item's 8 lanes (j < 32), then the upper halves
+        int te0, te1, tc0, tc1;
+        int er0 = group_excl(__popc(eqm & 0xFu), te0);
+        int er1 = te0 + group_excl(__popc(eqm >> 4), te1);
         uint32_t sel = ltm;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             if (eqm >> t & 1) {
-                if (er < krem) sel |= 1u << t;
-                ++er;
+                if (er0 < krem) sel |= 1u << t;
+                ++er0;
             }
-        const int cs = __popc(sel);
-        const int slot = group_excl(cs);
-        if (act) emit_run4(itm, sel, slot, 4 * sl);
+#pragma unroll
+        for (int t = 4; t < 8; ++t)
+            if (eqm >> t & 1) {
+                if (er1 < krem) sel |= 1u << t;
+                ++er1;
+            }
+        const int slot0 = group_excl(__popc(sel & 0xFu), tc0);
+        const int slot1 = tc0 + group_excl(__popc(sel >> 4), tc1);
+        if (act) {
+            emit_run4(itm, sel & 0xFu, slot0, 4 * sl);
+            if (sel >> 4) emit_run4(itm, sel >> 4, slot1, 32 + 4 * sl);
+        }
         cur = nxt;
     }
 }

@@ -68,7 +68,8 @@ def test_c1_batches(c1, g_idx):
     [[150, 150, 150]],                     # k > fast-path limit (generic selection)
     [[113, 40, 112]],                      # around the fast-path boundary
     [[2, 1, 2]] * 8,                       # EG_MAX_HOPS hops
-    [[33, 32, 31], [5, 4, 6]],             # around the tiny-selection bound (d <= 32)
+    [[33, 32, 31], [5, 4, 6]],             # around the lower half of a tiny item (d <= 32)
+    [[65, 64, 63], [40, 33, 20]],          # around the tiny-selection bound (d <= 64)
 ])
 def test_c1_fanouts(c1, fanouts):
     cfg, g, rows, ctx = c1
