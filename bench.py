@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
     ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--diag-no-gather", action="store_true",
+                    help="DIAGNOSTIC ONLY (not a bench line): sampling + compaction without the gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
@@ -349,7 +351,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         q = deque()
         for b0 in range(lo, hi, args.bundle):
             t0 = time.perf_counter()
-            q.append(launch(b0, min(hi, b0 + args.bundle), seeds))
+            q.append(launch(b0, min(hi, b0 + args.bundle), seeds, features=not args.diag_no_gather))
             host_t["launch"] += time.perf_counter() - t0
             if len(q) >= args.depth:
                 for bl in q.popleft():

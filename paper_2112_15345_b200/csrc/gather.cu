@@ -267,6 +267,8 @@ void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cud
         if (!blocks) {
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_ldg_kernel, 256, 0);
+            const char *e = getenv("EG_GATHER_CTAS");   // CTAs per SM (A/B runs); default: max resident
+            if (e && atoi(e) > 0 && atoi(e) < per_sm) per_sm = atoi(e);
             blocks = kSMs * (per_sm > 0 ? per_sm : 4);
         }
         gather_ldg_kernel<<<blocks, 256, 0, s>>>(g, f, gd);
