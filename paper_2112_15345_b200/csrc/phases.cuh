@@ -292,22 +292,22 @@ __device__ __forceinline__ void keys4(uint32_t q, uint32_t v_lo, uint32_t v_hi, 
 
 // Radix select, two bits per step.  With bits [s, 32) of the threshold key decided (P),
 // a key "matches" when its bits [s, 32) equal P's; radix2_count packs, for this thread's
-// keys, the number that match (bits 0-7) and how many of those have digit
-// (key >> (s-2)) & 3 equal to 0, 1, 2 (bits 8-15, 16-23, 24-31); sums of these over the
-// item (<= 128 keys) do not overflow a field.  radix2_decide takes the summed counts and
-// either finishes (every matching key is selected: cm == krem) or fixes the next digit.
+// keys, how many matching keys have digit (key >> (s-2)) & 3 equal to 0, 1, 2, 3 (bits
+// 0-7, 8-15, 16-23, 24-31); sums of these over the item (<= 128 keys) do not overflow a
+// field.  radix2_decide takes the summed counts and either finishes (every matching key
+// is selected: their number == krem) or fixes the next digit.
 __device__ __forceinline__ uint32_t radix2_count(uint32_t w, bool valid, uint32_t P, int s)
 {
-    const bool match = valid && (s == 32 || (w >> s) == (P >> s));
-    const uint32_t dg = (w >> (s - 2)) & 3u;
-    return match ? 1u + (dg < 3 ? (1u << (8 + 8 * dg)) : 0u) : 0u;
+    // (w ^ P) >> s with the shift clamped at 32 (s == 32: nothing decided, all match)
+    const bool match = valid && __funnelshift_rc(w ^ P, 0u, (uint32_t)s) == 0u;
+    return match ? 1u << (((w >> (s - 2)) & 3u) << 3) : 0u;
 }
 
 __device__ __forceinline__ bool radix2_decide(uint32_t x, int &krem, uint32_t &P, int &s)
 {
-    const int cm = (int)(x & 0xFFu);
+    const int n0 = (int)(x & 0xFFu), n1 = (int)((x >> 8) & 0xFFu), n2 = (int)((x >> 16) & 0xFFu);
+    const int cm = n0 + n1 + n2 + (int)(x >> 24);
     if (cm == krem) return true;
-    const int n0 = (int)((x >> 8) & 0xFFu), n1 = (int)((x >> 16) & 0xFFu), n2 = (int)(x >> 24);
     uint32_t dg;
     if (krem <= n0) {
         dg = 0;
