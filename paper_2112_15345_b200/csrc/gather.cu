@@ -34,6 +34,10 @@ namespace eg {
 // flight per lane before their stores.  Consecutive lanes touch consecutive 16-B units
 // of a row, so every row read and the output write are coalesced.
 constexpr int kBatch = 8;
+#ifndef EG_GATHER_MIN_BLOCKS
+#define EG_GATHER_MIN_BLOCKS 1
+#endif
+constexpr int kGatherMinBlocks = EG_GATHER_MIN_BLOCKS;   // CTAs per SM the register budget must allow
 
 __device__ __forceinline__ int32_t seg_rows(const GatherSet &gs, int b, int u)
 {
@@ -41,7 +45,7 @@ __device__ __forceinline__ int32_t seg_rows(const GatherSet &gs, int b, int u)
     return gd.out[u] ? gd.meta[kMetaNodes + gd.level * EG_MAX_VT + u] : 0;
 }
 
-__global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(256, kGatherMinBlocks) gather_ldg_kernel(const __grid_constant__ GraphDev g,
                                                          const __grid_constant__ FeatDev f,
                                                          const __grid_constant__ GatherSet gs)
 {
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__
         const int items = wide ? nrows * cpr : (nrows + rpi - 1) / rpi;
         for (int k0 = 0; k0 < items; k0 += kBatch) {
             int4 v[kBatch];
-            uint8_t *dst[kBatch];
+            uint32_t off[kBatch];   // output byte offset from dbase (< 32 rows x row_bytes), ~0u: none
 #pragma unroll
             for (int q = 0; q < kBatch; ++q) {
                 const int k = k0 + q;
@@ -91,15 +95,15 @@ __global__ void __launch_bounds__(256) gather_ldg_kernel(const __grid_constant__
                 }
                 const bool ok = k < items && row < nrows && unit < U && (wide || lane < rpi * U);
                 const uint8_t *sp = (const uint8_t *)__shfl_sync(0xffffffffu, (unsigned long long)srow, row & 31);
-                dst[q] = nullptr;
+                off[q] = ~0u;
                 if (ok) {
                     v[q] = ld_nc_v4(sp + 16 * unit);
-                    dst[q] = dbase + row * rb + 16 * unit;
+                    off[q] = (uint32_t)(row * rb + 16 * unit);
                 }
             }
 #pragma unroll
             for (int q = 0; q < kBatch; ++q)
-                if (dst[q]) st_v4(dst[q], v[q]);
+                if (off[q] != ~0u) st_v4(dbase + off[q], v[q]);
         }
     }
 }
