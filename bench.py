@@ -274,12 +274,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg_name):
+def load_traffic(cfg_name, kernel):
+    """ncu DRAM bytes per launch of `kernel` on this config (profiles/gather_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "gather_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(cfg_name)
+        e = d.get(cfg_name, {}).get(kernel)
+        return e
     except Exception:
         return None
 
@@ -479,14 +481,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])      # sampling + compaction nodes
     n_launch = max(1, prof["n_gather"])                             # one gather launch per bundle
     achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
-    tr = load_traffic(cfg.name)
-    roofline = {"kernel": "gather_ldg_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    gk = {"tma": "gather_tma_kernel", "ldg": "gather_ldg_kernel"}.get(ctx.gather_path(), "none")
+    tr = load_traffic(cfg.name, gk)
+    roofline = {"kernel": gk, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                 "algorithmic_bytes_per_launch": gbytes / n_launch,
                 "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id); one launch gathers "
                             "the rows of a bundle of %d mini-batches" % args.bundle,
                 "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms}
+    if tr and tr.get("ncu_duration_us"):
+        # the same kernel timed alone (ncu, serialised launch of one bundle): its own speed,
+        # without the other lanes' sampling kernels sharing the SMs and HBM
+        a1 = (gbytes / n_launch) / (tr["ncu_duration_us"] / 1e6) / 1e9
+        roofline["alone_ncu"] = {"achieved": a1, "frac": a1 / peak, "duration_us": tr["ncu_duration_us"]}
     frac_remote = None
     if world > 1:
         with torch.cuda.stream(stream):
@@ -507,7 +515,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         nv_bytes = (gbytes / n_launch) / 2 * frac_remote   # row bytes read over NVLink per launch
         nv_peak = 770.0
         nv_achieved = nv_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
-        roofline.update({"kernel": "gather_ldg_kernel", "bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak,
+        roofline.update({"kernel": gk, "bound": "nvlink", "achieved": nv_achieved, "peak": nv_peak,
                          "frac": nv_achieved / nv_peak,
                          "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction per GPU",
                          "per_unit": "row_bytes per input row owned by a peer (read over NVLink)",
@@ -533,7 +541,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         del src, dst
         pc_bytes = acc["rbytes"] / n_launch
         pc_achieved = pc_bytes / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
-        roofline.update({"kernel": "gather_ldg_kernel", "bound": "pcie", "achieved": pc_achieved, "peak": best,
+        roofline.update({"kernel": gk, "bound": "pcie", "achieved": pc_achieved, "peak": best,
                          "frac": pc_achieved / best if best else None,
                          "peak_source": "measured here: pinned host -> device copy of 1 GiB (best of 5, CUDA events)",
                          "per_unit": "row_bytes per input row read zero-copy from pinned host memory",

@@ -160,6 +160,14 @@ EG_API eg_status eg_attach_peer(eg_ctx *ctx, const eg_ctx *peer);
  * rows not device memory of this GPU. */
 EG_API eg_status eg_set_feature_replica(eg_ctx *ctx, int32_t vt, const void *rows, int64_t n_rows);
 
+/* Which feature-gather kernel the last enqueued gather used (instrumentation): 0 =
+ * gather_tma_kernel (TMA: cp.async.bulk.tensor tile::gather4, four rows per operation,
+ * for types whose full table is local with rows <= 1 KB and a multiple of 32 B; per-row
+ * bulk copies otherwise), 1 = gather_ldg_kernel (16-B vector loads; used when a requested
+ * type's rows live in peer shards), -1 = none yet.  EG_GATHER=tma|ldg|auto overrides
+ * the choice (default auto: TMA when every requested type has a gather4 map). */
+EG_API int32_t eg_gather_path(const eg_ctx *ctx);
+
 /* Sample L = n_hops blocks from `seeds` (gids, unique, any vertex types, caller
  * order; host or device pointer; n_seeds may be 0).  fanouts: host [n_hops][n_rel],
  * row 0 = hop at the seeds; -1 = all in-neighbours, 0 = none, k > 0 = at most k,

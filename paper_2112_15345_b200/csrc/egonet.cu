@@ -150,6 +150,8 @@ struct eg_ctx {
     eg_relation own_rel[EG_MAX_REL] = {};
     eg_features own_feat[EG_MAX_VT] = {};
     bool host_feat[EG_MAX_VT] = {};                  // feature rows in pinned host memory (PCIe)
+    GatherMaps gmaps{};                              // gather4 tensor maps of the local tables
+    int32_t gather_path = -1;                        // kernel of the last gather enqueued (eg_gather_path)
     // pipeline: `depth` lanes, each carrying bundles of up to `bundle` batches
     std::vector<Lane> lanes;
     int next_lane = 0;
@@ -464,6 +466,58 @@ eg_status finalize_peers(eg_ctx *c)
 
 // =============================================================================== ABI
 
+namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled()
+{
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// gather4 tensor maps for the types whose full table is local (world 1, or a replica):
+// [N_t][row_bytes / 4] u32, box {row_bytes / 4, 1}.  Rows must be <= 1 KB (box <= 256
+// elements) and a multiple of 32 B (4-row groups land 128-B aligned in shared memory).
+// A type without a map is gathered by the other paths (same bytes).
+void build_gather_maps(eg_ctx *c)
+{
+    EncodeTiledFn fn = encode_tiled();
+    for (int u = 0; u < EG_MAX_VT; ++u) c->gmaps.ok[u] = 0;
+    if (!fn) return;
+    for (int u = 0; u < c->g.n_vt; ++u) {
+        const int64_t rb = c->f.row_bytes[u];
+        const void *base = c->f.replica[u];
+        if (!base && c->world == 1 && !c->host_feat[u]) base = c->f.rows[u][c->rank];
+        const int64_t n = c->vt_counts[u];
+        if (!base || rb <= 0 || rb > 1024 || rb % 32 || n < 1 || n > INT32_MAX || ((uintptr_t)base & 15)) continue;
+        cuuint64_t dims[2] = {(cuuint64_t)(rb / 4), (cuuint64_t)n};
+        cuuint64_t strides[1] = {(cuuint64_t)rb};
+        cuuint32_t box[2] = {(cuuint32_t)(rb / 4), 1u};
+        cuuint32_t es[2] = {1u, 1u};
+        if (fn(&c->gmaps.map[u], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            c->gmaps.ok[u] = 1;
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char *eg_version(void) { return kVersion; }
@@ -661,6 +715,7 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     if ((st = ensure_lanes(c, 1, 1))) return st;
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
+    build_gather_maps(c);
     {
         ShardBlob self_meta;
         fill_meta(c, &self_meta);
@@ -778,6 +833,8 @@ eg_status eg_attach_peer(eg_ctx *c, const eg_ctx *peer)
     return EG_OK;
 }
 
+int32_t eg_gather_path(const eg_ctx *c) { return c ? c->gather_path : -1; }
+
 eg_status eg_set_feature_replica(eg_ctx *c, int32_t vt, const void *rows, int64_t n_rows)
 {
     eg_status st = enter(c);
@@ -787,6 +844,7 @@ eg_status eg_set_feature_replica(eg_ctx *c, int32_t vt, const void *rows, int64_
     if (vt < 0 || vt >= c->g.n_vt) return fail(c, EG_EINVAL, "vertex type out of range");
     if (!rows) {
         c->f.replica[vt] = nullptr;
+        build_gather_maps(c);
         return EG_OK;
     }
     if (!c->f.row_bytes[vt]) return fail(c, EG_EINVAL, "vertex type has no features");
@@ -798,6 +856,7 @@ eg_status eg_set_feature_replica(eg_ctx *c, int32_t vt, const void *rows, int64_
         return fail(c, EG_EINVAL, "replica rows must be device memory of this context's GPU");
     }
     c->f.replica[vt] = (const uint8_t *)rows;
+    build_gather_maps(c);
     return EG_OK;
 }
 
@@ -1031,7 +1090,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         for (int u = 0; u < V; ++u) any |= p->o_feat[u] != 0;
         cudaEventRecordWithFlags(sl->g0, cs, cudaEventRecordExternal);
         if (any) {
-            launch_gather(g, c->f, gs, cs);
+            c->gather_path = launch_gather(g, c->f, gs, c->gmaps, cs);
             ++nk;
             if (c->prio) {
                 cudaStreamCaptureStatus st;
@@ -1578,7 +1637,7 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
     if (!any) return EG_OK;
     TimedPair tp;
     record_start(c, &tp, 1);
-    launch_gather(c->g, c->f, gs, c->stream);
+    c->gather_path = launch_gather(c->g, c->f, gs, c->gmaps, c->stream);
     c->launches += 1;
     EG_CUDA(c, cudaGetLastError());
     record_end(c, &tp);

@@ -132,17 +132,30 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Bounded: a transfer that never completes (a bad tensor map, a faulting address) traps
+// after ~2 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+    uint64_t t0 = 0;
+    for (uint32_t it = 0;; ++it) {
+        uint32_t done;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if ((it & 1023) == 1023) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (!t0) t0 = t;
+            else if (t - t0 > 2000000000ull) __trap();
+        }
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
@@ -161,16 +174,30 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// Four rows (type-local indices r0..r3 of the map's table) of a 2-D tensor map into
+// shared memory, row after row: one TMA operation (tile::gather4, sm_100).
+__device__ __forceinline__ void gather4_g2s(void *dst, const CUtensorMap *map, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Tiles of consecutive rows of one (batch, type) segment; segments in (batch, type) order.
 struct TileCursor {
     int sg = 0;
     int64_t lo = 0, hi = 0;
 };
 
+// (a multiple of 4 when >= 4, so that the gather4 groups of a tile fit in its stage)
 __device__ __forceinline__ int32_t rows_per_tile(const FeatDev &f, int u)
 {
     const int64_t rb = f.row_bytes[u];
-    return rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
+    const int32_t r = rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
+    return r >= 4 ? (r & ~3) : (r > 0 ? r : 1);
 }
 
 __device__ __forceinline__ int64_t seg_tiles(const GatherSet &gs, const FeatDev &f, int V, int sg)
@@ -198,7 +225,8 @@ __device__ __forceinline__ void tile_of(const GatherSet &gs, const FeatDev &f, i
 
 __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant__ GraphDev g,
                                                            const __grid_constant__ FeatDev f,
-                                                           const __grid_constant__ GatherSet gs)
+                                                           const __grid_constant__ GatherSet gs,
+                                                           const __grid_constant__ GatherMaps m)
 {
     extern __shared__ __align__(128) uint8_t stage_mem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -218,25 +246,64 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
     TileCursor cur;
     cur.hi = seg_tiles(gs, f, V, 0);
     if (warp == 0) {
-        // producer: ids -> bulk loads of rows into the stage
-        for (int64_t j = 0; j < n_my; ++j) {
-            const int s = (int)(j % kStages);
-            mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));
+        // producer: ids -> TMA loads of rows into the stage.  The ids of tile j + 1 are
+        // loaded before waiting for tile j's stage (one id-load latency per tile was the
+        // producer's bound).  A lane holds 4 ids of a tile: rows 4 lane .. 4 lane + 3 (one
+        // gather4 group; rows_per_tile <= 128) or rows lane + 32 q (per-row copies).
+        struct Pre {
             int b, u;
             int64_t row0;
             int32_t nrows;
-            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, b, u, row0, nrows);
+            int64_t id[4];
+        };
+        auto prefetch = [&](int64_t j, Pre &p) {
+            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, p.b, p.u, p.row0, p.nrows);
+            const int64_t *ids = gs.b[p.b].nodes[p.u] + p.row0;
+            const bool grp = m.ok[p.u] != 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rr = grp ? min(4 * lane + q, p.nrows - 1) : lane + 32 * q;
+                const bool ok = grp ? 4 * lane < p.nrows : rr < p.nrows;
+                p.id[q] = ok ? __ldg(ids + rr) : 0;
+            }
+        };
+        Pre nx;
+        if (n_my > 0) prefetch(0, nx);
+        for (int64_t j = 0; j < n_my; ++j) {
+            const Pre cu = nx;
+            if (j + 1 < n_my) prefetch(j + 1, nx);
+            const int s = (int)(j % kStages);
+            mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));
+            const int u = cu.u;
+            const int32_t nrows = cu.nrows;
             const int64_t rb = f.row_bytes[u];
-            if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nrows * rb));
-            __syncwarp();
             uint8_t *dst = stage_mem + s * kStageBytes;
-            for (int rr = lane; rr < nrows; rr += 32) {
-                const int64_t tid = __ldg(gs.b[b].nodes[u] + row0 + rr) - g.off[u];
-                bulk_g2s(dst + rr * rb, feature_row(g, f, u, tid), (uint32_t)rb, &full[s]);
+            if (m.ok[u]) {
+                // groups of 4 rows, one gather4 each (a ragged last group repeats its last
+                // row: 4 rows always land, inside the stage since nrows <= rows_per_tile,
+                // a multiple of 4)
+                const int ng = (nrows + 3) >> 2;
+                if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(ng * 4 * rb));
+                __syncwarp();
+                if (lane < ng) {
+                    const int32_t o = (int32_t)g.off[u];
+                    gather4_g2s(dst + (int64_t)4 * lane * rb, &m.map[u], (int32_t)cu.id[0] - o,
+                                (int32_t)cu.id[1] - o, (int32_t)cu.id[2] - o, (int32_t)cu.id[3] - o, &full[s]);
+                }
+            } else {
+                if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nrows * rb));
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int rr = lane + 32 * q;
+                    if (rr < nrows)
+                        bulk_g2s(dst + rr * rb, feature_row(g, f, u, cu.id[q] - g.off[u]), (uint32_t)rb, &full[s]);
+                }
             }
         }
     } else if (lane == 0) {
-        // consumer: one bulk store of the staged rows (contiguous in the output)
+        // consumer: one bulk store of the staged rows (contiguous in the output); a stage
+        // is released once the NEXT store is issued and this one has been read
         for (int64_t j = 0; j < n_my; ++j) {
             const int s = (int)(j % kStages);
             mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
@@ -247,8 +314,10 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             const int64_t rb = f.row_bytes[u];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bulk_s2g(gs.b[b].out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            mbar_arrive(&empty[s]);
+            if (j > 0) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                mbar_arrive(&empty[(int)((j - 1) % kStages)]);
+            }
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
@@ -259,14 +328,22 @@ static int gather_mode()
     static int mode = -1;
     if (mode < 0) {
         const char *e = getenv("EG_GATHER");
-        mode = (e && !strcmp(e, "tma")) ? 0 : 1;   // default: LDG (measured faster)
+        mode = !e ? 2 : (!strcmp(e, "tma") ? 0 : (!strcmp(e, "ldg") ? 1 : 2));
     }
     return mode;
 }
 
-void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cudaStream_t s)
+int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, const GatherMaps &m, cudaStream_t s)
 {
-    if (gather_mode() == 1) {
+    int mode = gather_mode();
+    if (mode == 2) {
+        bool all = true;
+        for (int b = 0; b < gd.nb; ++b)
+            for (int u = 0; u < g.n_vt; ++u)
+                if (gd.b[b].out[u] && !m.ok[u]) all = false;
+        mode = all ? 0 : 1;
+    }
+    if (mode == 1) {
         static int blocks = 0;
         if (!blocks) {
             int per_sm = 0;
@@ -276,7 +353,7 @@ void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cud
             blocks = kSMs * (per_sm > 0 ? per_sm : 4);
         }
         gather_ldg_kernel<<<blocks, 256, 0, s>>>(g, f, gd);
-        return;
+        return 1;
     }
     static bool attr = false;
     const int smem = kStages * kStageBytes;
@@ -284,7 +361,13 @@ void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cud
         cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    gather_tma_kernel<<<kSMs * 2, 64, smem, s>>>(g, f, gd);
+    static int per_sm = 0;
+    if (!per_sm) {
+        const char *e = getenv("EG_TMA_CTAS");   // CTAs per SM (A/B runs); default 2
+        per_sm = (e && atoi(e) > 0 && atoi(e) <= 3) ? atoi(e) : 2;
+    }
+    gather_tma_kernel<<<kSMs * per_sm, 64, smem, s>>>(g, f, gd, m);
+    return 0;
 }
 
 }  // namespace eg

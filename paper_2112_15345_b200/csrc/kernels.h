@@ -1,5 +1,7 @@
 // kernels.h -- host launchers of the egonet kernels (internal).
 #pragma once
+#include <cuda.h>   // CUtensorMap (the maps are encoded through the runtime's driver entry point)
+
 #include "common.cuh"
 
 namespace eg {
@@ -44,8 +46,18 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
                  const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
                  const Fork &fk, bool serial, int lp);
 
+// TMA tensor maps of the feature tables the gather reads with cp.async.bulk.tensor
+// tile::gather4 (four rows per TMA operation): per vertex type one 2-D map over its full
+// local table ([n_rows][row_bytes / 4] u32, box {row_bytes / 4, 1}).  ok[u] == 0: the
+// type's rows are read otherwise (owner shards at world > 1, rows > 1 KB, host memory).
+struct __align__(64) GatherMaps {
+    CUtensorMap map[EG_MAX_VT];
+    int32_t ok[EG_MAX_VT];
+};
+
 // gather.cu
-void launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cudaStream_t s);
+// returns the kernel used: 0 gather_tma_kernel (gather4 / bulk copies), 1 gather_ldg_kernel
+int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, const GatherMaps &m, cudaStream_t s);
 
 // sage.cu: one GraphSAGE-mean layer over a block relation on the tensor cores (NEXT-4 i).
 struct SageArgs {

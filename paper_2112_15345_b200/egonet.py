@@ -30,6 +30,7 @@ ABI_SYMBOLS = [
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
     "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer", "eg_set_feature_replica",
+    "eg_gather_path",
 ]
 
 EG_FEATURES = 1
@@ -135,6 +136,8 @@ def lib(build_if_missing: bool = True):
         L.eg_import_shards.argtypes = [vp, vp, c.c_size_t]
         L.eg_attach_peer.argtypes = [vp, vp]
         L.eg_set_feature_replica.argtypes = [vp, c.c_int32, vp, c.c_int64]
+        L.eg_gather_path.argtypes = [vp]
+        L.eg_gather_path.restype = c.c_int32
         L.eg_set_pipeline.argtypes = [vp, c.c_int32, c.c_int32]
         L.eg_sample_bundle.argtypes = [vp, c.c_int32, vp, vp, c.c_int32, vp, vp, c.c_int32, vp]
         L.eg_sample_lp_bundle.argtypes = [vp, c.c_int32, vp, vp, vp, c.c_int32, c.c_int32, vp, c.c_int32, vp, vp,
@@ -436,6 +439,10 @@ class Context:
     def attach_peer(self, peer: "Context"):
         """Single-process peer mapping (another rank's context in this process)."""
         self._check(lib().eg_attach_peer(self._h, peer._h), "eg_attach_peer")
+
+    def gather_path(self) -> str:
+        """Kernel of the last enqueued feature gather: "tma" (gather4), "ldg" or "none"."""
+        return {0: "tma", 1: "ldg"}.get(int(lib().eg_gather_path(self._h)), "none")
 
     def set_feature_replica(self, vt: int, rows):
         """Replicated partition policy for type vt's features: `rows` is the type's full
