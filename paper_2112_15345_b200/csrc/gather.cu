@@ -7,18 +7,19 @@
 // rows_u[tid(src_nodes_{L-1}[u][i])], verbatim bytes (input order,
 // duplicates allowed).
 //
-// Two implementations of the same copy (EG_GATHER=tma|ldg):
-//  * gather_ldg_kernel (default): warp per group of 32 rows, 16-B vector loads, 8
-//    independent 16-B loads per lane in flight (measured on B200, C2: 5.08 TB/s of
-//    algorithmic bytes with bundles of 16 mini-batches vs 3.40 TB/s for the TMA form).
-//  * gather_tma_kernel: rows are staged through shared memory by the
-//    Tensor Memory Accelerator -- one cp.async.bulk per row into a stage, one bulk
-//    store per stage (the output of a tile of consecutive rows is contiguous) --
-//    with a producer warp (ids + bulk loads) and a consumer warp (bulk stores)
-//    around a ring of mbarrier-guarded stages.  Few instructions per byte and up to
-//    kStages * kStageBytes in flight per SM.  The per-row cp.async.bulk compiles to a
-//    serialised ELECT / R2UR / UBLKCP loop (one TMA op per 512-B row), which is why it
-//    loses to plain vector loads for rows this small.
+// Two implementations of the same copy (EG_GATHER=tma|ldg|auto):
+//  * gather_tma_kernel (default): rows are staged through shared memory by the Tensor
+//    Memory Accelerator -- one cp.async.bulk.tensor tile::gather4 per four rows of a
+//    type whose table is local (a 2-D tensor map per type), else one cp.async.bulk per
+//    row (e.g. rows in peer shards, over NVLink) -- and leave by one bulk store per stage
+//    (the output of a tile of consecutive rows is contiguous).  A producer warp (ids of
+//    the next tile prefetched) and a consumer thread around a ring of mbarrier-guarded
+//    stages; 64 threads per CTA, so the sampling kernels of the other pipeline lanes
+//    keep running beside it (measured: the path is faster although this gather alone is
+//    slightly slower than the LDG one).
+//  * gather_ldg_kernel: warp per group of 32 rows, 16-B vector loads, 8 independent
+//    16-B loads per lane in flight; used at world 1 when a type has no gather4 map
+//    (local per-row bulk copies are issue-bound: one UBLKCP per row).
 #include <cstdlib>
 #include <cstring>
 
@@ -337,11 +338,15 @@ int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cons
 {
     int mode = gather_mode();
     if (mode == 2) {
-        bool all = true;
+        // TMA unless a requested type would be read from LOCAL memory by per-row bulk copies
+        // (world 1 without a gather4 map: issue-bound, measured C3 12.7k vs 13.5k with LDG).
+        // Peer rows (world > 1) are NVLink-bound either way, and the TMA kernel leaves the
+        // SMs to the sampling kernels (measured N = 2: C2 +7 %, C3 +3 %, C4 +8 %, C5 +5 %).
+        bool ldg = false;
         for (int b = 0; b < gd.nb; ++b)
             for (int u = 0; u < g.n_vt; ++u)
-                if (gd.b[b].out[u] && !m.ok[u]) all = false;
-        mode = all ? 0 : 1;
+                if (gd.b[b].out[u] && !m.ok[u] && g.world == 1) ldg = true;
+        mode = ldg ? 1 : 0;
     }
     if (mode == 1) {
         static int blocks = 0;
