@@ -492,7 +492,7 @@ EncodeTiledFn encode_tiled()
 
 // gather4 tensor maps for the types whose full table is local (world 1, or a replica):
 // [N_t][row_bytes / 4] u32, box {row_bytes / 4, 1}.  Rows must be <= 1 KB (box <= 256
-// elements) and a multiple of 32 B (4-row groups land 128-B aligned in shared memory).
+// elements); the kernel places each 4-row group at a 128-B aligned stage offset.
 // A type without a map is gathered by the other paths (same bytes).
 void build_gather_maps(eg_ctx *c)
 {
@@ -504,7 +504,7 @@ void build_gather_maps(eg_ctx *c)
         const void *base = c->f.replica[u];
         if (!base && c->world == 1 && !c->host_feat[u]) base = c->f.rows[u][c->rank];
         const int64_t n = c->vt_counts[u];
-        if (!base || rb <= 0 || rb > 1024 || rb % 32 || n < 1 || n > INT32_MAX || ((uintptr_t)base & 15)) continue;
+        if (!base || rb <= 0 || rb > 1024 || rb % 16 || n < 1 || n > INT32_MAX || ((uintptr_t)base & 15)) continue;
         cuuint64_t dims[2] = {(cuuint64_t)(rb / 4), (cuuint64_t)n};
         cuuint64_t strides[1] = {(cuuint64_t)rb};
         cuuint32_t box[2] = {(cuuint32_t)(rb / 4), 1u};

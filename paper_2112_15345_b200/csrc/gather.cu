@@ -193,33 +193,42 @@ struct TileCursor {
     int64_t lo = 0, hi = 0;
 };
 
-// (a multiple of 4 when >= 4, so that the gather4 groups of a tile fit in its stage)
-__device__ __forceinline__ int32_t rows_per_tile(const FeatDev &f, int u)
+// Stage stride of a gather4 group of type u: 4 rows, rounded up to 128 B (the TMA writes
+// each group to a 128-B aligned shared address; rows of 400 B leave 64 B of padding).
+__device__ __forceinline__ int64_t group_stride(const FeatDev &f, int u)
 {
-    const int64_t rb = f.row_bytes[u];
-    const int32_t r = rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
-    return r >= 4 ? (r & ~3) : (r > 0 ? r : 1);
+    return (4 * f.row_bytes[u] + 127) & ~(int64_t)127;
 }
 
-__device__ __forceinline__ int64_t seg_tiles(const GatherSet &gs, const FeatDev &f, int V, int sg)
+// Rows per tile: gather4 types fill the stage with whole groups (a multiple of 4 rows);
+// per-row types with whole rows.
+__device__ __forceinline__ int32_t rows_per_tile(const FeatDev &f, const GatherMaps &m, int u)
+{
+    const int64_t rb = f.row_bytes[u];
+    if (m.ok[u]) return (int32_t)min((int64_t)kMaxRowsPerTile, 4 * ((int64_t)kStageBytes / group_stride(f, u)));
+    const int32_t r = rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
+    return r > 0 ? r : 1;
+}
+
+__device__ __forceinline__ int64_t seg_tiles(const GatherSet &gs, const FeatDev &f, const GatherMaps &m, int V, int sg)
 {
     const int32_t n = seg_rows(gs, sg / V, sg % V);
-    const int32_t rpt = rows_per_tile(f, sg % V);
+    const int32_t rpt = rows_per_tile(f, m, sg % V);
     return (n + rpt - 1) / rpt;
 }
 
 // tiles are visited in increasing order by each block: advance the cursor
-__device__ __forceinline__ void tile_of(const GatherSet &gs, const FeatDev &f, int V, TileCursor &cur, int64_t t,
+__device__ __forceinline__ void tile_of(const GatherSet &gs, const FeatDev &f, const GatherMaps &m, int V, TileCursor &cur, int64_t t,
                                         int &b, int &u, int64_t &row0, int32_t &nrows)
 {
     while (t >= cur.hi) {
         ++cur.sg;
         cur.lo = cur.hi;
-        cur.hi += seg_tiles(gs, f, V, cur.sg);
+        cur.hi += seg_tiles(gs, f, m, V, cur.sg);
     }
     b = cur.sg / V;
     u = cur.sg % V;
-    const int32_t rpt = rows_per_tile(f, u);
+    const int32_t rpt = rows_per_tile(f, m, u);
     row0 = (t - cur.lo) * rpt;
     nrows = (int32_t)min((int64_t)rpt, (int64_t)seg_rows(gs, b, u) - row0);
 }
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int V = g.n_vt, S = gs.nb * V;
     int64_t total = 0;
-    for (int sg = 0; sg < S; ++sg) total += seg_tiles(gs, f, V, sg);
+    for (int sg = 0; sg < S; ++sg) total += seg_tiles(gs, f, m, V, sg);
     const int64_t n_my = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
     }
     __syncthreads();
     TileCursor cur;
-    cur.hi = seg_tiles(gs, f, V, 0);
+    cur.hi = seg_tiles(gs, f, m, V, 0);
     if (warp == 0) {
         // producer: ids -> TMA loads of rows into the stage.  The ids of tile j + 1 are
         // loaded before waiting for tile j's stage (one id-load latency per tile was the
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             int64_t id[4];
         };
         auto prefetch = [&](int64_t j, Pre &p) {
-            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, p.b, p.u, p.row0, p.nrows);
+            tile_of(gs, f, m, V, cur, blockIdx.x + j * gridDim.x, p.b, p.u, p.row0, p.nrows);
             const int64_t *ids = gs.b[p.b].nodes[p.u] + p.row0;
             const bool grp = m.ok[p.u] != 0;
 #pragma unroll
@@ -280,15 +289,15 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             const int64_t rb = f.row_bytes[u];
             uint8_t *dst = stage_mem + s * kStageBytes;
             if (m.ok[u]) {
-                // groups of 4 rows, one gather4 each (a ragged last group repeats its last
-                // row: 4 rows always land, inside the stage since nrows <= rows_per_tile,
-                // a multiple of 4)
+                // groups of 4 rows, one gather4 each, at 128-B aligned group strides (a
+                // ragged last group repeats its last row: 4 rows always land, inside the
+                // stage since rows_per_tile counts whole groups)
                 const int ng = (nrows + 3) >> 2;
                 if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(ng * 4 * rb));
                 __syncwarp();
                 if (lane < ng) {
                     const int32_t o = (int32_t)g.off[u];
-                    gather4_g2s(dst + (int64_t)4 * lane * rb, &m.map[u], (int32_t)cu.id[0] - o,
+                    gather4_g2s(dst + lane * group_stride(f, u), &m.map[u], (int32_t)cu.id[0] - o,
                                 (int32_t)cu.id[1] - o, (int32_t)cu.id[2] - o, (int32_t)cu.id[3] - o, &full[s]);
                 }
             } else {
@@ -311,10 +320,17 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             int b, u;
             int64_t row0;
             int32_t nrows;
-            tile_of(gs, f, V, cur, blockIdx.x + j * gridDim.x, b, u, row0, nrows);
+            tile_of(gs, f, m, V, cur, blockIdx.x + j * gridDim.x, b, u, row0, nrows);
             const int64_t rb = f.row_bytes[u];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_s2g(gs.b[b].out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
+            const int64_t gsz = group_stride(f, u);
+            if (!m.ok[u] || gsz == 4 * rb) {   // rows contiguous in the stage: one store
+                bulk_s2g(gs.b[b].out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
+            } else {                             // padded groups: one store per group
+                for (int q = 0; 4 * q < nrows; ++q)
+                    bulk_s2g(gs.b[b].out[u] + (row0 + 4 * q) * rb, stage_mem + s * kStageBytes + q * gsz,
+                             (uint32_t)(min(4, nrows - 4 * q) * rb));
+            }
             if (j > 0) {
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 mbar_arrive(&empty[(int)((j - 1) % kStages)]);
