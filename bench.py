@@ -483,6 +483,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     gk = {"tma": "gather_tma_kernel", "ldg": "gather_ldg_kernel"}.get(ctx.gather_path(), "none")
     tr = load_traffic(cfg.name, gk)
+    if tr and not (args.task == "nc" and world == 1 and args.bundle == tr.get("bundle") and args.features == "device"):
+        tr = None   # the ncu capture was taken on node batches at N = 1 with this bundle size
     roofline = {"kernel": gk, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
