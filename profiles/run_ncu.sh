@@ -15,7 +15,7 @@ case "$1" in
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_list.log 2>&1 ;;
   gather)
-    ncu --set full --clock-control none --import-source on -k regex:"gather_ldg" -s 2 -c 1 \
+    ncu --set full --clock-control none --import-source on -k regex:"gather_(tma|ldg)" -s 2 -c 1 \
         -o gpurun_out/prof_gather $B > gpurun_out/ncu_gather.log 2>&1 ;;
   hop)
     ncu --set full --clock-control none --import-source on -k regex:"k_select|k_tiny|k_copy|k_emit|k_count" \
