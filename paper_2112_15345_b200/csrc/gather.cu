@@ -111,8 +111,14 @@ __global__ void __launch_bounds__(256, kGatherMinBlocks) gather_ldg_kernel(const
 
 // ----------------------------------------------------------------------------- TMA path
 
-constexpr int kStages = 4;
-constexpr int kStageBytes = 16384;
+#ifndef EG_TMA_STAGES
+#define EG_TMA_STAGES 4
+#endif
+#ifndef EG_TMA_STAGE_BYTES
+#define EG_TMA_STAGE_BYTES 16384
+#endif
+constexpr int kStages = EG_TMA_STAGES;           // ring depth per CTA
+constexpr int kStageBytes = EG_TMA_STAGE_BYTES;  // bytes per stage
 constexpr int kMaxRowsPerTile = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
