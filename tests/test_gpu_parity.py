@@ -210,6 +210,27 @@ def test_replica_is_what_the_gather_reads(c1):
         ctxs[0].set_feature_replica(0, None)                         # after the first sampling call
 
 
+def test_gather_kernel_choice(c1, c2):
+    """The default gather is the TMA kernel (tile::gather4) wherever every requested type
+    has a local table with a gather4 map, and at world > 1 (peer rows by bulk copies);
+    its output was compared with the oracle by the tests above / below."""
+    import torch
+    for cfg, g, rows, ctx in (c1, c2):
+        seeds, rs = synth.batch_seeds(cfg, 5), synth.rng_seed(cfg, 5)
+        b = ctx.sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+        res = oracle.sample(g, seeds, cfg.fanouts, rs)
+        assert_same_features(res, _features_of(b, cfg), cfg, rows)
+        b.free()
+        assert ctx.gather_path() == "tma", cfg.name
+    cfg, g, rows, _ = c2
+    ctxs = _world(g, 2)
+    seeds, rs = synth.batch_seeds(cfg, 6), synth.rng_seed(cfg, 6)
+    b = ctxs[1].sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+    assert_same_features(oracle.sample(g, seeds, cfg.fanouts, rs), _features_of(b, cfg), cfg, rows)
+    b.free()
+    assert ctxs[1].gather_path() == "tma"
+
+
 # ----------------------------------------------------------------------------- C3 (3 hops, hub of degree 618k)
 
 def test_c3_full_batch():
