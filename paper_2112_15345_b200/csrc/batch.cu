@@ -75,7 +75,10 @@ __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ 
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 4) k_select(const __grid_constant__ GraphDev g,
+#ifndef EG_SELECT_MIN_BLOCKS
+#define EG_SELECT_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kBatchThreads, EG_SELECT_MIN_BLOCKS) k_select(const __grid_constant__ GraphDev g,
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
@@ -115,8 +118,11 @@ __global__ void __launch_bounds__(1024) k_cscan(const __grid_constant__ GraphDev
     phase_chunk_scan(g, hop_of(bd, h));
 }
 
+#ifndef EG_EMIT_MIN_BLOCKS
+#define EG_EMIT_MIN_BLOCKS 1
+#endif
 template <bool kSparse>
-__global__ void __launch_bounds__(kBatchThreads) k_emit(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, EG_EMIT_MIN_BLOCKS) k_emit(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
     if (h >= 0) stamp(bd, 8 + 8 * h);
