@@ -1,6 +1,6 @@
 // batch.cu -- the sampling + compaction of a bundle of mini-batches, one kernel per phase.
 //
-//   seed_split | for h: count(+relabel h-1) | scan | select+copy+tiny | bitcount | cscan | emit | ... | relabel | reset
+//   seed_split | for h: count(+relabel h-1) | scan | select+copy+tiny | bitcount | cscan | emit | ... | relabel+reset
 //
 // Every phase kernel runs with grid.y = the batch of the bundle (each batch has its own
 // HopDev / compaction state), so B mini-batches cost about what one does: at batch ~1k
@@ -146,6 +146,16 @@ __global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__
     phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
 }
 
+// The last hop's relabel and the batch reset in one kernel: independent work (relabel
+// reads pos[], reset clears member words), one kernel boundary less per batch.
+__global__ void __launch_bounds__(kBatchThreads) k_finish(const __grid_constant__ GraphDev g,
+                                                          const BatchDev *__restrict__ bd, int h)
+{
+    stamp(bd, 1 + 8 * bd->n_hops);
+    phase_relabel(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
+    phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
+}
+
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
                  const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
                  const Fork &fk, bool serial, int lp)
@@ -202,9 +212,13 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
         compaction(h, sparse_hop[h] != 0);
         nk += 8;
     }
-    k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
-    k_reset<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
-    return nk + 2;
+    if (serial) {   // EG_TRACE: separate stamps
+        k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
+        k_reset<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
+        return nk + 2;
+    }
+    k_finish<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
+    return nk + 1;
 }
 
 }  // namespace eg
