@@ -446,7 +446,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             e, nb = e2e_retire(bl)
             e2e_acc["edges"] += e
             e2e_acc["h2d"] += cfg.batch * (16 if lp else 8)
-            e2e_acc["d2h"] += nb + 576
+            e2e_acc["d2h"] += nb + 1440   # + the per-batch counters (kMetaSize = 360 int32, csrc/common.cuh)
 
         with torch.cuda.stream(stream):
             run(0, min(W, 3), pinned_seeds, e2e_retire)
