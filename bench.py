@@ -55,8 +55,11 @@ def parse():
                     help="replicated feature partition policy (P:468-473) for small vertex types: auto (N > 1: "
                          "every type whose full table is <= 64 MiB gets a local copy on each GPU), none, or a "
                          "comma list of type indices")
-    ap.add_argument("--depth", type=int, default=4, help="launches in flight per GPU (pipeline lanes)")
-    ap.add_argument("--bundle", type=int, default=8, help="mini-batches per launch (bundled kernels)")
+    ap.add_argument("--depth", type=int, default=None,
+                    help="launches in flight per GPU (pipeline lanes); default 3 (4 for C5)")
+    ap.add_argument("--bundle", type=int, default=None,
+                    help="mini-batches per launch (bundled kernels); default 16 (8 for C5, whose per-batch "
+                         "state is ~1 GB: 48 states + a 98 GB shard would not fit 180 GB at N = 2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--diag-no-gather", action="store_true",
                     help="DIAGNOSTIC ONLY (not a bench line): sampling + compaction without the gather")
@@ -64,6 +67,13 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     a = ap.parse_args()
+    # pipeline shape (profiles/r01/diag/lanes_matrix2.txt): 3 lanes x bundles of
+    # 16 measured best with the TMA gather; C5 keeps 4 x 8 for memory
+    big = a.config.startswith("C5")
+    if a.depth is None:
+        a.depth = 4 if big else 3
+    if a.bundle is None:
+        a.bundle = 8 if big else 16
     if a.replicate not in ("auto", "none"):
         a.replicate = [int(x) for x in a.replicate.split(",") if x != ""]
     return a
@@ -274,14 +284,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg_name, kernel):
+def load_traffic(cfg_name, kernel, bundle):
     """ncu DRAM bytes per launch of `kernel` on this config (profiles/gather_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "gather_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(cfg_name, {}).get(kernel)
-        return e
+        c = d.get(cfg_name, {})
+        return c.get("%s@b%d" % (kernel, bundle)) or c.get(kernel)
     except Exception:
         return None
 
@@ -482,7 +492,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     n_launch = max(1, prof["n_gather"])                             # one gather launch per bundle
     achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     gk = {"tma": "gather_tma_kernel", "ldg": "gather_ldg_kernel"}.get(ctx.gather_path(), "none")
-    tr = load_traffic(cfg.name, gk)
+    tr = load_traffic(cfg.name, gk, args.bundle)
     if tr and not (args.task == "nc" and world == 1 and args.bundle == tr.get("bundle") and args.features == "device"):
         tr = None   # the ncu capture was taken on node batches at N = 1 with this bundle size
     roofline = {"kernel": gk, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

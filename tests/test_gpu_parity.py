@@ -343,25 +343,28 @@ def test_c2_pipeline_depth4_concurrent_lanes(c2):
 # ----------------------------------------------------------------------------- the bench's launch configuration
 
 @pytest.mark.parametrize("name", ["C2", "C4"])
-def test_bench_launch_configuration(name):
-    """Exactly what bench.py times: depth 4 lanes x bundles of 8, async, 4 launches in
-    flight; batches g = 0..31 as the bench draws them (rank 0 of world 1), each checked
-    against the oracle (C2: all 32 with features; C4: one batch per bundle, blocks +
-    features via the generator formula)."""
+@pytest.mark.parametrize("depth,bundle", [(4, 8), (3, 16)])
+def test_bench_launch_configuration(name, depth, bundle):
+    """Exactly what bench.py times: `depth` lanes x bundles of `bundle`, async, `depth`
+    launches in flight; batches g = 0..depth*bundle-1 as the bench draws them (rank 0 of
+    world 1), each checked against the oracle (C2: all with features; C4: one batch per
+    bundle, blocks + features via the generator formula)."""
     import torch
     cfg = synth.config(name)
     g = synth.build_host_graph(cfg, materialize_indices=True)
     rows = ({u: synth.host_features(cfg, u) for u in cfg.feats} if name == "C2"
             else {0: synth.LazyRows(cfg, 0)})
     ctx = _ctx(g)
-    ctx.set_pipeline(4, 8)
-    seeds = [torch.from_numpy(synth.batch_seeds(cfg, b)).cuda() for b in range(32)]
-    rngs = [synth.rng_seed(cfg, b) for b in range(32)]
-    launches = [ctx.sample_bundle(seeds[b0:b0 + 8], cfg.fanouts, rngs[b0:b0 + 8], features=True, async_=True)
-                for b0 in range(0, 32, 8)]                      # four launches in flight on four lanes
+    ctx.set_pipeline(depth, bundle)
+    n = depth * bundle
+    seeds = [torch.from_numpy(synth.batch_seeds(cfg, b)).cuda() for b in range(n)]
+    rngs = [synth.rng_seed(cfg, b) for b in range(n)]
+    launches = [ctx.sample_bundle(seeds[b0:b0 + bundle], cfg.fanouts, rngs[b0:b0 + bundle], features=True,
+                                  async_=True)
+                for b0 in range(0, n, bundle)]                  # `depth` launches in flight on `depth` lanes
     for k, bls in enumerate(launches):
         for j, b in enumerate(bls):
-            gi = 8 * k + j
+            gi = bundle * k + j
             if name == "C2" or j == k:
                 res = oracle.sample(g, synth.batch_seeds(cfg, gi), cfg.fanouts, rngs[gi])
                 assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
