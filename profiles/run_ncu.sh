@@ -8,7 +8,7 @@
 #   gather  --set full of one gather launch
 #   hop     --set full of the hop-1 sampling / compaction kernels of one bundle
 set -e
-B="python bench.py --steps 16 --warmup 16 --no-e2e --no-cpu-baseline"
+B="python bench.py --steps 32 --warmup 32 --no-e2e --no-cpu-baseline"
 case "$1" in
   list)
     $B > gpurun_out/plain.log 2>&1
