@@ -641,9 +641,14 @@ class Context:
         return int(lib().eg_kernel_launches(self._h))
 
     def close(self):
+        """Destroy the library context, then drop the buffers it borrowed (the shard
+        tensors kept alive for it), so that their device memory is released now rather
+        than whenever this object is collected."""
         if self._h:
             lib().eg_destroy(self._h)
             self._h = None
+        self._keep = []
+        self.__dict__.pop("_shard", None)
 
     def __del__(self):
         try:

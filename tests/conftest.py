@@ -26,3 +26,22 @@ def c1_graph():
 def c2_graph():
     import synth
     return synth.build_host_graph(synth.config("C2"))
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """After each GPU test: collect reference cycles (contexts <-> blocks) and return the
+    freed device memory, so that full-size shards (C4: 36 GB, C5) of earlier tests do not
+    accumulate on the 180 GB device."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+    gc.collect()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    except Exception:
+        pass

@@ -371,6 +371,7 @@ def test_bench_launch_configuration(name, depth, bundle):
                 assert_same_features(res, _features_of(b, cfg), cfg, rows)
             b.free()
     ctx.close()
+    del launches, ctx
 
 
 # ----------------------------------------------------------------------------- compaction variants
