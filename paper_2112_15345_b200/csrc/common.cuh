@@ -12,8 +12,19 @@ constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
 constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one block)
 constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
-constexpr int kMinScanBlocks = 64;        // virtual blocks per relation in the two-phase scan: per hop,
-constexpr int kMaxScanBlocks = 1024;      // about one per 4096 frontier items, within these bounds
+// Virtual blocks per relation in the two-phase count / scan: per hop, one per
+// kScanItemsPerBlock frontier-capacity items, within [kMinScanBlocks, kMaxScanBlocks].
+// (Measured, profiles/r01/diag/scan_blocks_ab*.txt: a floor of 64 left most threads of
+// the hop-0 blocks idle -- 1024 seeds over 64 blocks per relation -- and 8 is C2 +8 %.)
+#ifndef EG_MIN_SCAN_BLOCKS
+#define EG_MIN_SCAN_BLOCKS 8
+#endif
+constexpr int kMinScanBlocks = EG_MIN_SCAN_BLOCKS;
+#ifndef EG_SCAN_ITEMS_PER_BLOCK
+#define EG_SCAN_ITEMS_PER_BLOCK 4096
+#endif
+constexpr int64_t kScanItemsPerBlock = EG_SCAN_ITEMS_PER_BLOCK;
+constexpr int kMaxScanBlocks = 1024;
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
 constexpr int kTinyD = 64;                // selections with d <= this: 8 lanes per item (phase_tiny)

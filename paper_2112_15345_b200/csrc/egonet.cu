@@ -939,7 +939,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         // heavy slots: one per 2048 frontier items beyond the first kMinHeavy
         int64_t most = 0;
         for (int r = 0; r < R; ++r) most = std::max<int64_t>(most, p->capF[h][dst_vt[r]]);
-        p->scan_blocks[h] = (int32_t)std::min<int64_t>(kMaxScanBlocks, std::max<int64_t>(kMinScanBlocks, (most + 4095) / 4096));
+        p->scan_blocks[h] = (int32_t)std::min<int64_t>(kMaxScanBlocks, std::max<int64_t>(kMinScanBlocks, (most + kScanItemsPerBlock - 1) / kScanItemsPerBlock));
         p->max_heavy[h] = (int32_t)std::min<int64_t>(65535, kMinHeavy + items / 2048);
         p->max_heavy_tasks[h] = (int32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)p->max_heavy[h] * kHeavyTasksPerItem);
         p->o_heavy[h] = take(heavy_bytes(p->max_heavy[h], p->max_heavy_tasks[h]));
