@@ -67,11 +67,11 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     a = ap.parse_args()
-    # pipeline shape (profiles/r01/diag/lanes_matrix2.txt): 3 lanes x bundles of
-    # 16 measured best with the TMA gather; C5 keeps 4 x 8 for memory
+    # pipeline shape (profiles/r01/shape/): 4 lanes x bundles of 16 measured best
+    # once the count/scan block floor made sampling cheaper; C5 keeps 4 x 8 for memory
     big = a.config.startswith("C5")
     if a.depth is None:
-        a.depth = 4 if big else 3
+        a.depth = 4
     if a.bundle is None:
         a.bundle = 8 if big else 16
     if a.replicate not in ("auto", "none"):
