@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batches", type=int, default=4)
     ap.add_argument("--replicate", default="auto", help="replicated feature types: auto | none")
+    ap.add_argument("--depth", type=int, default=2, help="pipelined check: launches in flight")
+    ap.add_argument("--bundle", type=int, default=4, help="pipelined check: mini-batches per launch")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -59,14 +61,15 @@ def main():
         bl.free()
         ok += 1
     # pipelined, bundled launches (the bench's mode) read the same peer shards
-    ctx.set_pipeline(2, 4)
-    gis = [1000 + (b * world + rank) for b in range(8)]
+    D, B = args.depth, args.bundle
+    ctx.set_pipeline(D, B)
+    gis = [1000 + (b * world + rank) for b in range(D * B)]
     dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).cuda() for gi in gis]
-    launches = [ctx.sample_bundle(dev[i:i + 4], cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis[i:i + 4]],
-                                  features=True, async_=True) for i in (0, 4)]
+    launches = [ctx.sample_bundle(dev[i:i + B], cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis[i:i + B]],
+                                  features=True, async_=True) for i in range(0, D * B, B)]
     for li, bls in enumerate(launches):
         for j, bl in enumerate(bls):
-            gi = gis[4 * li + j]
+            gi = gis[B * li + j]
             res = oracle.sample(g, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi))
             assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
             assert_same_features(res, [bl.features(u) if u in cfg.feats else None for u in range(cfg.n_vt)], cfg,
