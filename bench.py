@@ -1,16 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the mini-batch ego-network generator (seeds -> blocks + features).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-A step = one pass of the whole hot path over one mini-batch: sample every hop
-(sampling + compaction kernels) and gather the input vertices' feature rows.
+Workload (N=1 default): C4, the ogbn-papers100M-shaped graph (111M vertices, 1.6B
+edges, 128-d fp16) -- the largest BASELINE config that fits one B200 (C5 needs two).
+
+A step = one launch of the whole hot path over a bundle of `--bundle` (16)
+mini-batches per rank: sample every hop (sampling + compaction kernels) and gather
+the input vertices' feature rows, as one CUDA graph; `--depth` (4) launches are in
+flight per GPU.  So `--steps 20` times 320 mini-batches per rank, and every timed
+launch carries a full bundle (steady state: the warm-up captures every lane's graph).
 Inputs (graph shard, feature shard, the seeds of every step) are resident in HBM
 before the timed region.  Each rank samples its own batches (global batch
 g = b * N + rank); the graph and features are range-sharded over the N GPUs and
 peer shards are read over NVLink.  Timing: W untimed warm-up steps, then K steps
 bracketed by barrier + synchronize, CUDA events on the context's stream, max over
 ranks.  Rank 0 prints one JSON line.
+
+The oracle leg (rank 0 at N=1, skipped with --no-cpu-baseline) re-runs the first
+timed mini-batches through the same bundled launch after the timed region and
+compares them element by element with oracle/ (parity_checked), then times the
+oracle on a bounded sample (cpu_baseline).
 
 --impl reference times the CPU oracle (oracle/, plain single-threaded C) on the
 host, on the same workload and metric (rank 0 only; other ranks exit 0).
@@ -38,9 +49,9 @@ UNIT = "sampled edges/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=256)
-    ap.add_argument("--warmup", type=int, default=32)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--steps", type=int, default=32, help="timed launches (each: --bundle mini-batches per rank)")
+    ap.add_argument("--warmup", type=int, default=8, help="untimed launches before the timed region")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--task", default="nc", choices=["nc", "lp"],
                     help="nc: node-classification batches (seed vertices, the headline); lp: link-prediction "
                          "batches (NEXT-3: cfg.batch positive edges + 1 negative each, fanout [25, 15])")
@@ -56,7 +67,7 @@ def parse():
                          "every type whose full table is <= 64 MiB gets a local copy on each GPU), none, or a "
                          "comma list of type indices")
     ap.add_argument("--depth", type=int, default=None,
-                    help="launches in flight per GPU (pipeline lanes); default 3 (4 for C5)")
+                    help="launches in flight per GPU (pipeline lanes); default 4")
     ap.add_argument("--bundle", type=int, default=None,
                     help="mini-batches per launch (bundled kernels); default 16 (8 for C5, whose per-batch "
                          "state is ~1 GB: 48 states + a 98 GB shard would not fit 180 GB at N = 2)")
@@ -65,6 +76,9 @@ def parse():
                     help="DIAGNOSTIC ONLY (not a bench line): sampling + compaction without the gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
+    ap.add_argument("--parity", type=int, default=None,
+                    help="timed mini-batches re-run and compared with the oracle after the timed region "
+                         "(default 8 for C4/C5, 16 otherwise; 0 = none)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     a = ap.parse_args()
     # pipeline shape (profiles/r01/shape/): 4 lanes x bundles of 16 measured best
@@ -133,20 +147,60 @@ def workload(cfg, world, task="nc"):
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region.
+
+    NVML polled every 5 ms from a thread (the timed region of a default run is tens of
+    ms, too short for nvidia-smi's loop); nvidia-smi -lms 50 when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, index):
+    def __init__(self, index, pci_bus_id=None):
         self.index = index
+        self.pci = pci_bus_id
         self.proc = None
         self.lines = []
+        self.samples = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop_ev = threading.Event()
+        self.nvml = None
 
     def start(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (nv, h)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        try:
+                            rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        except Exception:
+                            rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                          "-i", str(self.index), "-lms", "50"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -158,9 +212,17 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.t.join(timeout=1)
+            if not self.samples:
+                return None
+            reasons = sorted({n for _, rs in self.samples for n, b in self.BITS.items() if rs & b})
+            return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(self.samples), "source": "NVML, 5 ms polling"}
         if not self.proc:
             return None
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -182,7 +244,8 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 50"}
 
 
 # ----------------------------------------------------------------------------- oracle timing
@@ -235,18 +298,23 @@ def time_oracle(cfg, graph, host_rows, batches, budget_s, min_batches=1, task="n
 
 
 def run_reference(args, cfg, rank, world):
+    """The reference arm (this tier: the oracle as it stands, on the host cores): the
+    same workload, metric and step as our arm -- a step = the `--bundle` mini-batches one
+    launch of ours carries (rank 0's batches g = b*N), sampled, compacted and gathered by
+    the single-threaded C oracle."""
     if rank != 0:
         return
     import synth
+    B = args.bundle
     graph = synth.build_host_graph(cfg, materialize_indices=True)
     rows = {u: synth.host_features(cfg, u) for u in cfg.feats} if cfg.name in ("C1", "C2", "C3") else None
     for b in range(args.warmup):
-        time_oracle(cfg, graph, rows, [b * world], 0.0, task=args.task)
+        time_oracle(cfg, graph, rows, [(b * B + i) * world for i in range(B)], float("inf"), task=args.task)
     per_step = []
     edges = 0
     nbytes = 0
     for b in range(args.warmup, args.warmup + args.steps):
-        r = time_oracle(cfg, graph, rows, [b * world], 0.0, task=args.task)
+        r = time_oracle(cfg, graph, rows, [(b * B + i) * world for i in range(B)], float("inf"), task=args.task)
         per_step.append(r["seconds"])
         edges += r["edges"]
         nbytes += r["bytes"]
@@ -255,11 +323,12 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/bytes",
-            "data": "synthetic", "config": workload(cfg, 1, args.task),
-            "minibatches_per_s": args.steps / total, "gather_GBps": nbytes / total / 1e9,
+            "data": "synthetic", "config": dict(workload(cfg, world, args.task),
+                                               step_unit=f"a bundle of {B} mini-batches (rank 0's)"),
+            "minibatches_per_s": args.steps * B / total, "gather_GBps": nbytes / total / 1e9,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} full {cfg.name} batches (sample+compact+gather), one step "
-                                       f"= one batch, single-threaded C oracle on {cpu_model()}"},
+                             "sample": f"{args.steps} steps x {B} full {cfg.name} batches (sample+compact+gather), "
+                                       f"single-threaded C oracle on {cpu_model()}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(args, line)
 
@@ -284,16 +353,71 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# Version tag of the gather kernel the committed ncu traffic figures were captured on
+# (profiles/gather_traffic.json entries carry it; a changed kernel invalidates them).
+TRAFFIC_CODE = "r02"
+
+
 def load_traffic(cfg_name, kernel, bundle):
-    """ncu DRAM bytes per launch of `kernel` on this config (profiles/gather_traffic.json)."""
+    """ncu DRAM bytes (per mini-batch) and duration (per launch) of `kernel` on this
+    config at this bundle size (profiles/gather_traffic.json, from one --set full capture)."""
     p = os.path.join(ROOT, "profiles", "gather_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        c = d.get(cfg_name, {})
-        return c.get("%s@b%d" % (kernel, bundle)) or c.get(kernel)
+        return d.get(cfg_name, {}).get("%s@b%d" % (kernel, bundle))
     except Exception:
         return None
+
+
+def parity_check(cfg, graph, task, batches, outs, seeds_host, rngs, negs, rel):
+    """Oracle leg: the CUDA path's outputs of `batches` (host copies taken from the same
+    bundled launch configuration the bench times) vs oracle/, element by element:
+    every node list, block CSC (indptr, relabelled src ids, eids) and gathered feature
+    byte.  Raises on the first difference; returns the number of batches compared."""
+    import oracle
+    import synth
+    rows_full = cfg.name in ("C1", "C2", "C3")
+    for g, out in zip(batches, outs):
+        if task == "lp":
+            src, dst = seeds_host[g]
+            res, _ = oracle.sample_lp(graph, src, dst, rel, LP_NEG, negs[g], synth.lp_fanouts(cfg), rngs[g])
+        else:
+            res = oracle.sample(graph, seeds_host[g], cfg.fanouts, rngs[g])
+        for l, lv in enumerate(out["levels"]):
+            for u in range(cfg.n_vt):
+                if not np.array_equal(lv[u], res.levels[l][u]):
+                    raise AssertionError(f"parity: batch {g} level {l} type {u} differs")
+        for h, hop in enumerate(out["blocks"]):
+            for r in range(cfg.n_rel):
+                o = res.blocks[h][r]
+                for key, want in (("indptr", o.indptr), ("indices", o.indices), ("eids", o.eids)):
+                    if not np.array_equal(hop[r][key], want):
+                        raise AssertionError(f"parity: batch {g} hop {h} relation {r} {key} differs")
+        for u in cfg.feats:
+            ids = res.input_nodes(u)
+            if rows_full:
+                want = oracle.gather(res, cfg.vt_counts, u, synth.host_features(cfg, u))
+            else:   # the store does not fit host RAM: the rows of this batch's inputs only
+                off_u = int(cfg.offsets[u])
+                rows = synth.host_features_ids(cfg, u, ids - off_u)
+                want = oracle.gather_ids(off_u + np.arange(len(ids), dtype=np.int64), cfg.vt_counts, u, rows)
+            if out["feats"][u].tobytes() != want.tobytes():
+                raise AssertionError(f"parity: batch {g} feature bytes of type {u} differ")
+    return len(outs)
+
+
+def host_copy(bl, cfg):
+    """A batch's outputs as numpy (levels, per-hop CSCs, feature bytes)."""
+    levels = [[bl[0].dst_nodes[u].cpu().numpy() for u in range(cfg.n_vt)]]
+    blocks = []
+    for h in range(bl.n_hops):
+        b = bl[h]
+        levels.append([b.src_nodes[u].cpu().numpy() for u in range(cfg.n_vt)])
+        blocks.append([{"indptr": b.indptr[r].cpu().numpy(), "indices": b.indices[r].cpu().numpy(),
+                        "eids": b.eids[r].cpu().numpy()} for r in range(cfg.n_rel)])
+    feats = {u: bl.features(u).cpu().numpy() for u in cfg.feats}
+    return {"levels": levels, "blocks": blocks, "feats": feats}
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -308,9 +432,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)
-    # host src ids: for the oracle (cpu_baseline, C4: 6.5 GB) and small configs; C5 generates on the device
-    graph = synth.build_host_graph(cfg, materialize_indices=cfg.name in ("C1", "C2", "C3") or
-                                   (world == 1 and not args.no_cpu_baseline))
+    B = args.bundle
+    W, K = args.warmup, args.steps            # launches (steps); each carries B mini-batches per rank
+    n_b = (W + K) * B                          # mini-batches per rank
+    oracle_leg = rank == 0 and world == 1 and not args.no_cpu_baseline
+    # host src ids: for the oracle leg (C4: 6.5 GB) and small configs; C5 generates on the device
+    graph = synth.build_host_graph(cfg, materialize_indices=cfg.name in ("C1", "C2", "C3") or oracle_leg)
     t_load = time.perf_counter()
     ctx = Context(rank, world, local_rank, stream)
     shard = load_context(ctx, graph, world, rank, dev, features=args.features if args.features != "device" else True,
@@ -318,23 +445,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     replicas = sorted(shard["replicas"])
     if world > 1:
         ctx.connect_peers()
-    ctx.set_pipeline(args.depth, args.bundle)
+    ctx.set_pipeline(args.depth, B)
     t_load = time.perf_counter() - t_load
-    W, K = args.warmup, args.steps
-    steps = W + K
-    rngs = [synth.rng_seed(cfg, b * world + rank) for b in range(steps)]
+    rngs = [synth.rng_seed(cfg, b * world + rank) for b in range(n_b)]
     fanouts = np.array(task_fanouts(cfg, args.task), np.int32)
     lp = args.task == "lp"
+    rel, negs = None, None
     if lp:   # link prediction: positives (src, dst) per batch; inputs[b] = (src, dst)
         rel = synth.lp_rel(cfg)
-        seeds_host = [synth.lp_positives(cfg, graph, rel, b * world + rank) for b in range(steps)]
+        seeds_host = [synth.lp_positives(cfg, graph, rel, b * world + rank) for b in range(n_b)]
         seeds_dev = [(torch.from_numpy(a).to(dev), torch.from_numpy(c).to(dev)) for a, c in seeds_host]
         negs = [r ^ LP_NEG_KEY for r in rngs]
     else:
         if args.confine:
-            seeds_host = [synth.batch_seeds_confined(cfg, b, rank, world) for b in range(steps)]
+            seeds_host = [synth.batch_seeds_confined(cfg, b, rank, world) for b in range(n_b)]
         else:
-            seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(steps)]
+            seeds_host = [synth.batch_seeds(cfg, b * world + rank) for b in range(n_b)]
         seeds_dev = [torch.from_numpy(s).to(dev) for s in seeds_host]
     row_bytes = [cfg.row_bytes(u) for u in range(cfg.n_vt)]
     torch.cuda.synchronize(dev)
@@ -346,7 +472,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             return ctx.sample_lp_bundle([seeds[b][0] for b in range(b0, b1)], [seeds[b][1] for b in range(b0, b1)],
                                         rel, LP_NEG, negs[b0:b1], fanouts, rngs[b0:b1], features=features,
                                         async_=True)
-        if b1 - b0 == 1 and args.bundle == 1:
+        if b1 - b0 == 1 and B == 1:
             return [ctx.sample_minibatch(seeds[b0], fanouts, rngs[b0], features=features, async_=True)]  # noqa
         return ctx.sample_bundle([seeds[b] for b in range(b0, b1)], fanouts, rngs[b0:b1], features=features,
                                  async_=True)
@@ -359,11 +485,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     host_t = {"launch": 0.0, "retire": 0.0}
 
     def run(lo, hi, seeds, on_retire):
-        """Launch batches lo..hi-1 in bundles, keeping `depth` launches in flight."""
+        """Launches lo..hi-1 (launch l = batches l*B .. l*B+B-1), `depth` in flight."""
         q = deque()
-        for b0 in range(lo, hi, args.bundle):
+        for l in range(lo, hi):
             t0 = time.perf_counter()
-            q.append(launch(b0, min(hi, b0 + args.bundle), seeds, features=not args.diag_no_gather))
+            q.append(launch(l * B, (l + 1) * B, seeds, features=not args.diag_no_gather))
             host_t["launch"] += time.perf_counter() - t0
             if len(q) >= args.depth:
                 for bl in q.popleft():
@@ -385,6 +511,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         acc["gbytes"] += sum(rows[u] * (2 * row_bytes[u] + 8) for u in cfg.feats)
         acc["rbytes"] += sum(rows[u] * row_bytes[u] for u in cfg.feats)
 
+    pci = None
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        pci = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+    except Exception:
+        pass
     with torch.cuda.stream(stream):
         run(0, W, seeds_dev, retire)
         torch.cuda.synchronize(dev)
@@ -392,7 +524,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             torch.distributed.barrier()
         ctx.profile()                                   # drain
         ctx.set_profiling(True)
-        clocks = ClockSampler(local_rank)
+        clocks = ClockSampler(local_rank, pci)
         clocks.start()
         launches0 = ctx.kernel_launches()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -401,8 +533,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             torch.distributed.barrier()
         ev0.record(stream)
         host_t["launch"] = host_t["retire"] = 0.0
-        run(W, steps, seeds_dev, count)
-        host_us = {k: 1e6 * v / K for k, v in host_t.items()}
+        run(W, W + K, seeds_dev, count)
+        host_us = {k: 1e6 * v / (K * B) for k, v in host_t.items()}
         edges, gbytes = acc["edges"], acc["gbytes"]
         ev1.record(stream)
         torch.cuda.synchronize(dev)
@@ -424,6 +556,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         ms = float(mx[0])
         edges = float(totals[1])
     value = edges / (ms / 1e3)
+    n_timed = world * K * B                           # mini-batches, all ranks
 
     # e2e: host seeds in (pinned), features out to pinned host memory, through the C ABI
     e2e = None
@@ -459,14 +592,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             e2e_acc["d2h"] += nb + 1440   # + the per-batch counters (kMetaSize = 360 int32, csrc/common.cuh)
 
         with torch.cuda.stream(stream):
-            run(0, min(W, 3), pinned_seeds, e2e_retire)
+            run(0, min(W, 2), pinned_seeds, e2e_retire)
             torch.cuda.synchronize(dev)
             if world > 1:
                 torch.distributed.barrier()
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-            run(W, steps, pinned_seeds, e2e_count)
+            run(W, W + K, pinned_seeds, e2e_count)
             t1.record(stream)
             torch.cuda.synchronize(dev)
             ems = t0.elapsed_time(t1)
@@ -480,8 +613,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             ems, e_edges = float(m[0]), float(t[1])
         e2e = {"value": e_edges / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
                "d2h_bytes_per_step": d2h // K,
-               "note": "seeds from pinned host memory in (H2D inside eg_sample_minibatch), gathered feature rows "
-                       "out to pinned host memory (D2H), per-batch counters read back; blocks stay device-resident"}
+               "note": "per step (one launch of %d mini-batches): seeds from pinned host memory in (read in place "
+                       "by the seed split over PCIe), gathered feature rows out to pinned host memory (D2H), "
+                       "per-batch counters read back; blocks stay device-resident" % B}
 
     # roofline of the gather kernel (events inside the library's graph, on its stream,
     # timed region).  P = 1: HBM-bound (read row + write row + read id).  P > 1: rows owned
@@ -489,24 +623,29 @@ def run_ours(args, cfg, rank, world, local_rank):
     peak, peak_src = load_peaks()
     gather_ms = prof["gather_ms"] / max(1, prof["n_gather"])      # gather kernel node
     sample_ms = prof["sample_ms"] / max(1, prof["n_sample"])      # sampling + compaction nodes
-    n_launch = max(1, prof["n_gather"])                             # one gather launch per bundle
+    n_launch = max(1, prof["n_gather"])                             # one gather launch per step
     achieved = (gbytes / n_launch) / (gather_ms / 1e3) / 1e9 if gather_ms > 0 else 0.0
     gk = {"tma": "gather_tma_kernel", "ldg": "gather_ldg_kernel"}.get(ctx.gather_path(), "none")
-    tr = load_traffic(cfg.name, gk, args.bundle)
-    if tr and not (args.task == "nc" and world == 1 and args.bundle == tr.get("bundle") and args.features == "device"):
-        tr = None   # the ncu capture was taken on node batches at N = 1 with this bundle size
+    tr = load_traffic(cfg.name, gk, B)
+    if tr and not (args.task == "nc" and world == 1 and B == tr.get("bundle") and args.features == "device"
+                   and tr.get("code") == TRAFFIC_CODE):
+        tr = None   # the ncu capture must be of this kernel, bundle size, task and code version
+    alg_per_batch = gbytes / max(1, K * B)
     roofline = {"kernel": gk, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "traffic": (tr["dram_bytes_per_batch"] * B) if tr else None,
                 "algorithmic_bytes_per_launch": gbytes / n_launch,
                 "per_unit": "2*row_bytes + 8 B per input row (read row, write row, read id); one launch gathers "
-                            "the rows of a bundle of %d mini-batches" % args.bundle,
-                "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms}
-    if tr and tr.get("ncu_duration_us"):
-        # the same kernel timed alone (ncu, serialised launch of one bundle): its own speed,
-        # without the other lanes' sampling kernels sharing the SMs and HBM
-        a1 = (gbytes / n_launch) / (tr["ncu_duration_us"] / 1e6) / 1e9
-        roofline["alone_ncu"] = {"achieved": a1, "frac": a1 / peak, "duration_us": tr["ncu_duration_us"]}
+                            "the rows of a bundle of %d mini-batches" % B,
+                "gather_ms_per_launch": gather_ms, "sample_chain_ms_per_launch": sample_ms,
+                "launches_timed": n_launch}
+    if tr:
+        # the same kernel in one ncu --set full capture (serialised, one launch of B batches):
+        # its DRAM bytes (traffic, per batch x B) and its duration alone
+        a1 = alg_per_batch * B / (tr["ncu_duration_us_per_launch"] / 1e6) / 1e9
+        roofline["traffic_source"] = tr.get("source")
+        roofline["traffic_over_algorithmic"] = tr["dram_bytes_per_batch"] / alg_per_batch
+        roofline["alone_ncu"] = {"achieved": a1, "frac": a1 / peak, "duration_us": tr["ncu_duration_us_per_launch"]}
     frac_remote = None
     if world > 1:
         with torch.cuda.stream(stream):
@@ -561,10 +700,21 @@ def run_ours(args, cfg, rank, world, local_rank):
                          "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak}})
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    parity = None
+    if oracle_leg:
+        # parity: the first timed mini-batches again, through the same bundled launch
+        npar = min(B, args.parity if args.parity is not None else B)
+        if npar > 0:
+            g0 = W * B
+            with torch.cuda.stream(stream):
+                bls = launch(g0, g0 + npar, seeds_dev)
+                outs = [host_copy(bl, cfg) for bl in bls]
+                for bl in bls:
+                    bl.free()
+            parity = parity_check(cfg, graph, args.task, range(g0, g0 + npar), outs, seeds_host, rngs, negs, rel)
         full = cfg.name in ("C1", "C2", "C3")
         rows_h = {u: synth.host_features(cfg, u) for u in cfg.feats} if full else None
-        r = time_oracle(cfg, graph, rows_h, range(1000, 100000), args.cpu_seconds, task=args.task)
+        r = time_oracle(cfg, graph, rows_h, range(100000, 200000), args.cpu_seconds, task=args.task)
         cpu = {"value": r["edges"] / r["seconds"], "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{r['batches']} full {cfg.name} batches (sample+compact+gather) in "
                          f"{r['seconds']:.1f} s, single-threaded C oracle on {cpu_model()} "
@@ -581,14 +731,21 @@ def run_ours(args, cfg, rank, world, local_rank):
                     "confined to the rank's vertex range (second-level partition, P:428-431)" if args.confine
                     else "global epoch permutation, batch g = b*P + p"), features_in=(
                     "pinned host memory (zero-copy over PCIe)" if args.features == "host" else "HBM"),
-                    feature_replicas=[cfg.vtypes[u][0] for u in replicas]),
-                "minibatches_per_s": world * K / (ms / 1e3),
+                    feature_replicas=[cfg.vtypes[u][0] for u in replicas],
+                    step_unit=f"one launch (CUDA graph) of a bundle of {B} mini-batches per rank; {args.depth} "
+                              f"launches in flight per GPU"),
+                "minibatches_per_s": n_timed / (ms / 1e3),
                 "gather_GBps": achieved if gather_ms > 0 else None,
-                "sampled_edges_per_batch": edges / (world * K),
-                "input_vertices_per_batch_rank0": acc["inputs"] / K,
+                "sampled_edges_per_batch": edges / n_timed,
+                "input_vertices_per_batch_rank0": acc["inputs"] / (K * B),
+                "parity_checked": parity,
+                "parity_note": ("the first %d timed mini-batches of rank 0, re-run through the same bundled launch "
+                                "after the timed region, equal the oracle's element by element (node lists, block "
+                                "CSCs, eids, feature bytes)" % parity) if parity else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
-                "pipeline_depth": args.depth, "bundle": args.bundle, "host_us_per_batch": host_us, "host": {"cores": host_cores(), "cpu": cpu_model()}}
+                "pipeline_depth": args.depth, "bundle": B, "host_us_per_batch": host_us,
+                "host": {"cores": host_cores(), "cpu": cpu_model()}}
         emit(args, line)
     ctx.close()
     del shard

@@ -124,6 +124,8 @@ EG_API eg_status eg_set_stream(eg_ctx *ctx, void *stream);
  * bounds[t][world]=N_t, or NULL for the fixed policy bounds[t][p] = floor(p*N_t/world);
  * rels: host [n_rel]; feats: host [n_vt].  The buffers are BORROWED (not copied).
  * Validates shapes and ranges of the metadata; device contents are trusted.
+ * EG_EINVAL also when a relation's largest local in-degree exceeds 2^26 (the
+ * sampler splits hub rows into at most 2^16 tasks of 1024 keys).
  * Allocates the per-context compaction state (4 B per global vertex + a bitmap). */
 EG_API eg_status eg_load_partition(eg_ctx *ctx, int32_t n_vt, const int64_t *vt_counts, const int64_t *bounds,
                             int32_t n_rel, const eg_relation *rels, const eg_features *feats);
@@ -160,13 +162,15 @@ EG_API eg_status eg_attach_peer(eg_ctx *ctx, const eg_ctx *peer);
  * rows not device memory of this GPU. */
 EG_API eg_status eg_set_feature_replica(eg_ctx *ctx, int32_t vt, const void *rows, int64_t n_rows);
 
-/* Which feature-gather kernel the last enqueued gather used (instrumentation): 0 =
+/* Which feature-gather kernel the last enqueued gather used (instrumentation; the
+ * kernel captured into the launched batch graph, or of the last eg_gather_features): 0 =
  * gather_tma_kernel (TMA: cp.async.bulk.tensor tile::gather4, four rows per operation,
  * for types whose full table is local with rows <= 1 KB and a multiple of 32 B; per-row
  * bulk copies otherwise, e.g. rows in peer shards read over NVLink), 1 = gather_ldg_kernel
  * (16-B vector loads), -1 = none yet.  Default (EG_GATHER=auto): TMA, except at world 1
  * when a requested type has no gather4 map (local per-row bulk copies are issue-bound);
- * EG_GATHER=tma|ldg forces one. */
+ * EG_GATHER=tma|ldg forces one.  Rows wider than one 16 KB TMA stage always take the
+ * LDG kernel. */
 EG_API int32_t eg_gather_path(const eg_ctx *ctx);
 
 /* Sample L = n_hops blocks from `seeds` (gids, unique, any vertex types, caller
@@ -308,8 +312,10 @@ EG_API eg_status eg_gather_features(eg_ctx *ctx, const eg_blocks *blocks, void *
 /* Release a blocks handle (stream-ordered on the context's stream). */
 EG_API eg_status eg_blocks_free(eg_blocks *blocks);
 
-/* Destroy the context (closes peer mappings, frees its state; the borrowed
- * shard buffers are untouched). */
+/* Destroy the context: waits for every launch still in flight, closes the peer
+ * mappings, frees its state; the borrowed shard buffers are untouched.  Handles the
+ * caller has not freed are orphaned: their device views become invalid, every call on
+ * them returns EG_ESTATE, and eg_blocks_free only releases the handle. */
 EG_API eg_status eg_destroy(eg_ctx *ctx);
 
 /* Message of the last error on this context (thread-unsafe, never NULL). */

@@ -37,6 +37,9 @@ constexpr int kHeavyCap = 512;            // candidate slots per heavy item
 constexpr int kMinHeavy = 256;            // heavy items per (batch, hop): at least this, more for large
                                           // frontiers (HopDev::max_heavy); overflow -> warp per item
 constexpr int kHeavyTasksPerItem = (1 << 20) / kHeavyChunk + 1;   // d <= 2^20 (generator Dmax)
+// Largest in-degree a relation may have (eg_load_partition rejects more): heavy tasks are
+// encoded as (item << 16) | chunk, chunk < 2^16 chunks of kHeavyChunk keys.
+constexpr int64_t kMaxInDegree = (int64_t)kHeavyChunk << 16;
 
 // Error bits written by kernels into meta[kMetaErr].
 enum : int32_t { kErrSeedRange = 1, kErrSeedDup = 2, kErrCapacity = 4 };

@@ -7,7 +7,7 @@
 //     count -> scan                             block indptr (min(d,k) per dst)
 //     sample                                    warp per (dst, relation), key32
 //     mark -> bitcount -> emit -> relabel       frontier + compaction
-//   reset                                       pos[] back to -1
+//   finish                                      last relabel + member bits cleared
 //   one D2H of the batch counters (+ error bits)
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -131,6 +132,7 @@ struct Slot {
     int refs = 0;                // live eg_blocks handles of the last launch
     bool used = false, timed = false, finished = false;
     int lane = 0;
+    int32_t gather_path = -1;    // kernel the captured gather node uses (eg_gather_path)
     std::vector<cudaEvent_t> tev;        // EG_TRACE: one event after each stage of the graph
     std::vector<std::string> tlab;
 };
@@ -173,9 +175,11 @@ struct eg_ctx {
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
     int compact = 0;                      // EG_COMPACT at create: 0 per hop, 1 dense, 2 sparse
     int prio = 1;                         // EG_PRIO at create: 0 none, 1 gather first, 2 sampling first
+    int gather_mode = 2;                  // EG_GATHER at create: 0 tma, 1 ldg, 2 auto (gather.cu)
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
+    std::set<eg_blocks *> live;           // handles not yet freed (orphaned by eg_destroy)
 };
 
 struct eg_blocks {
@@ -592,6 +596,8 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
         // duration in the pipelined run by 8-20 % at unchanged throughput (C2, C4).
         const char *pr = getenv("EG_PRIO");
         c->prio = !pr ? 1 : (pr[0] == 'g' ? 1 : (pr[0] == 's' ? 2 : 0));
+        const char *ga = getenv("EG_GATHER");
+        c->gather_mode = !ga ? 2 : (!strcmp(ga, "tma") ? 0 : (!strcmp(ga, "ldg") ? 1 : 2));
     }
     if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->fork.side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -710,7 +716,14 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
     EG_CUDA(c, cudaMemcpyAsync(h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, c->stream));
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     EG_CUDA(c, cudaFree(d_max));
-    for (int r = 0; r < n_rel; ++r) c->rel_max_degree[r] = (int64_t)h_max[r];
+    for (int r = 0; r < n_rel; ++r) {
+        c->rel_max_degree[r] = (int64_t)h_max[r];
+        // heavy items are split into tasks (item << 16 | chunk of kHeavyChunk keys) and
+        // degrees are int32 in the batch: in-degrees above kMaxInDegree would wrap
+        if (c->rel_max_degree[r] > kMaxInDegree)
+            return fail(c, EG_EINVAL, "relation " + std::to_string(r) + ": in-degree " +
+                                          std::to_string(c->rel_max_degree[r]) + " exceeds 2^26");
+    }
 
     if ((st = ensure_lanes(c, 1, 1))) return st;
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1090,7 +1103,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         for (int u = 0; u < V; ++u) any |= p->o_feat[u] != 0;
         cudaEventRecordWithFlags(sl->g0, cs, cudaEventRecordExternal);
         if (any) {
-            c->gather_path = launch_gather(g, c->f, gs, c->gmaps, cs);
+            sl->gather_path = launch_gather(g, c->f, gs, c->gmaps, cs, c->gather_mode);
+            c->gather_path = sl->gather_path;
             ++nk;
             if (c->prio) {
                 cudaStreamCaptureStatus st;
@@ -1260,6 +1274,7 @@ eg_status finish(eg_blocks *b)
 {
     if (b->ready) return b->status;
     eg_ctx *c = b->ctx;
+    if (!c) return EG_ESTATE;   // orphaned by eg_destroy
     Slot *sl = b->slot;
     cudaError_t e = cudaEventSynchronize(sl->done);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, sl->done, 0);
@@ -1377,6 +1392,7 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
     }
     sl->timed = c->prof;
     sl->finished = false;
+    if (p->features) c->gather_path = sl->gather_path;
     EG_CUDA(c, cudaGraphLaunch(sl->exec, ln.stream));
     EG_CUDA(c, cudaEventRecord(sl->done, ln.stream));
     sl->used = true;
@@ -1400,6 +1416,7 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
             h->pairs = (int32_t *)(p->batch_base(sl->mem, b) + p->o_lp_pairs);
             h->neg = (int64_t *)(p->batch_base(sl->mem, b) + p->o_lp_neg);
         }
+        c->live.insert(h);
         out[b] = h;
     }
     return EG_OK;
@@ -1556,6 +1573,7 @@ eg_status eg_blocks_stats(const eg_blocks *cb, int64_t *total_edges, int64_t *n_
 eg_status eg_blocks_wait(eg_blocks *b)
 {
     if (!b) return EG_EINVAL;
+    if (!b->ctx) return EG_ESTATE;
     cudaSetDevice(b->ctx->device);
     return finish(b);
 }
@@ -1637,7 +1655,7 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
     if (!any) return EG_OK;
     TimedPair tp;
     record_start(c, &tp, 1);
-    c->gather_path = launch_gather(c->g, c->f, gs, c->gmaps, c->stream);
+    c->gather_path = launch_gather(c->g, c->f, gs, c->gmaps, c->stream, c->gather_mode);
     c->launches += 1;
     EG_CUDA(c, cudaGetLastError());
     record_end(c, &tp);
@@ -1656,7 +1674,10 @@ eg_status eg_gather_features(eg_ctx *c, const eg_blocks *cb, void *const *out)
 eg_status eg_blocks_free(eg_blocks *b)
 {
     if (!b) return EG_OK;
-    if (b->slot && b->slot->refs > 0) b->slot->refs -= 1;   // reuse waits for the slot's last run
+    if (b->ctx) {   // else orphaned: its context (and slot) are gone, only the handle remains
+        b->ctx->live.erase(b);
+        if (b->slot && b->slot->refs > 0) b->slot->refs -= 1;   // reuse waits for the slot's last run
+    }
     delete b;
     return EG_OK;
 }
@@ -1715,8 +1736,22 @@ eg_status eg_destroy(eg_ctx *c)
 {
     if (!c) return EG_OK;
     cudaSetDevice(c->device);
+    // every launch still in flight (async batches never resolved) reads slot memory and
+    // the peer mappings: wait for all lanes before anything is released
     cudaStreamSynchronize(c->stream);
+    for (Lane &ln : c->lanes)
+        if (ln.stream) cudaStreamSynchronize(ln.stream);
+    cudaDeviceSynchronize();
     drain_timing(c);
+    // handles the caller has not freed: orphan them, so that a later eg_blocks_free only
+    // deletes the handle and every other call on it returns EG_ESTATE
+    for (eg_blocks *b : c->live) {
+        b->ctx = nullptr;
+        b->slot = nullptr;
+        b->ready = true;
+        b->status = EG_ESTATE;
+    }
+    c->live.clear();
     destroy_plans(c);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->fork.side) cudaStreamDestroy(c->fork.side);

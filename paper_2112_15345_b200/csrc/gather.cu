@@ -368,19 +368,15 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
     }
 }
 
-static int gather_mode()
+int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, const GatherMaps &m, cudaStream_t s,
+                  int mode)
 {
-    static int mode = -1;
-    if (mode < 0) {
-        const char *e = getenv("EG_GATHER");
-        mode = !e ? 2 : (!strcmp(e, "tma") ? 0 : (!strcmp(e, "ldg") ? 1 : 2));
-    }
-    return mode;
-}
-
-int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, const GatherMaps &m, cudaStream_t s)
-{
-    int mode = gather_mode();
+    // The TMA kernel stages whole rows (per-row copies) or 4-row groups (gather4) in one
+    // stage of kStageBytes: a requested type with wider rows goes to the LDG kernel, which
+    // copies rows of any width in 16-B units (whatever EG_GATHER says).
+    for (int b = 0; b < gd.nb; ++b)
+        for (int u = 0; u < g.n_vt; ++u)
+            if (gd.b[b].out[u] && f.row_bytes[u] > kStageBytes) mode = 1;
     if (mode == 2) {
         // TMA unless a requested type would be read from LOCAL memory by per-row bulk copies
         // (world 1 without a gather4 map: issue-bound, measured C3 12.7k vs 13.5k with LDG).

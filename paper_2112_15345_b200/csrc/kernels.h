@@ -56,8 +56,10 @@ struct __align__(64) GatherMaps {
 };
 
 // gather.cu
-// returns the kernel used: 0 gather_tma_kernel (gather4 / bulk copies), 1 gather_ldg_kernel
-int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, const GatherMaps &m, cudaStream_t s);
+// mode: 0 TMA, 1 LDG, 2 automatic (EG_GATHER=tma|ldg|auto, read at eg_create).
+// Returns the kernel used: 0 gather_tma_kernel (gather4 / bulk copies), 1 gather_ldg_kernel
+int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, const GatherMaps &m, cudaStream_t s,
+                  int mode);
 
 // sage.cu: one GraphSAGE-mean layer over a block relation on the tensor cores (NEXT-4 i).
 struct SageArgs {

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 import numpy as np
 
@@ -256,17 +257,23 @@ class Blocks:
     use (waiting for an EG_ASYNC batch); per-hop tensors are zero-copy views of
     library memory built lazily."""
 
-    def __init__(self, ctx: "Context", handle: int, n_hops: int | None = None):
+    def __init__(self, ctx: "Context", handle: int, n_hops: int | None = None, inputs=None):
         self._ctx = ctx
         self._h = handle
         self.n_hops = lib().eg_blocks_n_hops(handle) if n_hops is None else n_hops
         self._views = None
         self._blocks = [None] * self.n_hops
+        # The launch reads device / pinned seed (and positive-edge) buffers IN PLACE on the
+        # library's lane stream, which torch's caching allocator does not know about: the
+        # caller's tensors of the whole launch are held here until it has completed.
+        self._inputs = inputs
+        ctx._live.add(self)
 
     def wait(self):
         rc = lib().eg_blocks_wait(self._h)
         if rc:
             raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        self._inputs = None   # the launch has completed: its inputs are no longer read
         return self
 
     @property
@@ -300,6 +307,7 @@ class Blocks:
         rc = lib().eg_blocks_stats(self._h, ctypes.byref(e), n.ctypes.data)
         if rc:
             raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        self._inputs = None
         return int(e.value), [int(x) for x in n[:len(self._ctx.vt_counts)]]
 
     def nnz(self, h=None) -> int:
@@ -349,10 +357,16 @@ class Blocks:
 
     def free(self):
         """Release the batch's slot now (tensors obtained from this handle must no
-        longer be used).  Otherwise it is released when the handle is garbage."""
+        longer be used).  Otherwise it is released when the handle is garbage.  A handle
+        that still holds the caller's input tensors of an unfinished launch waits for the
+        launch first, so that those buffers are not recycled while it reads them."""
         if self._h:
+            if self._inputs is not None:
+                lib().eg_blocks_wait(self._h)   # errors are reported by the calls that read results
+                self._inputs = None
             lib().eg_blocks_free(self._h)
             self._h = None
+            self._ctx._live.discard(self)
 
     def __del__(self):
         try:
@@ -374,6 +388,7 @@ class Context:
             raise EgError(rc, "eg_create (needs an sm_100 GPU; there is no CPU fallback)")
         self._h = h
         self._keep = []
+        self._live = weakref.WeakSet()   # Blocks handles not yet freed (close() frees them)
         self.rel_dst = []
         self.vt_counts = None
         self.row_bytes = []
@@ -483,7 +498,7 @@ class Context:
         h = ctypes.c_void_p()
         self._check(lib().eg_sample_blocks(self._h, ptr if n else None, n, fo.shape[0], fo.ctypes.data,
                                            rng_seed & (2**64 - 1), ctypes.byref(h)), "eg_sample_blocks")
-        return Blocks(self, h.value)
+        return Blocks(self, h.value)   # synchronous: the inputs have been read
 
     def sample_minibatch(self, seeds, fanouts, rng_seed: int, features: bool = True, async_: bool = False) -> Blocks:
         """One CUDA-graph launch: sample + compact every hop (+ gather features into
@@ -501,7 +516,7 @@ class Context:
         h = ctypes.c_void_p()
         self._check(lib().eg_sample_minibatch(self._h, ptr if n else None, n, fo.shape[0], fo.ctypes.data,
                                               rng_seed & (2**64 - 1), flags, ctypes.byref(h)), "eg_sample_minibatch")
-        return Blocks(self, h.value)
+        return Blocks(self, h.value, inputs=[seeds] if async_ else None)
 
     def sample_bundle(self, seeds_list, fanouts, rng_seeds, features: bool = True, async_: bool = False):
         """Several mini-batches as ONE graph launch (bundle); returns one Blocks per batch."""
@@ -518,6 +533,7 @@ class Context:
                 ptrs[i], cnts[i] = s.ctypes.data, len(s)
             else:
                 assert s.dtype == torch.int64 and s.is_contiguous()
+                keep.append(s)
                 ptrs[i], cnts[i] = s.data_ptr(), s.numel()
         rs = np.ascontiguousarray([int(x) & (2**64 - 1) for x in rng_seeds], np.uint64)
         outs = (ctypes.c_void_p * n)()
@@ -526,7 +542,8 @@ class Context:
                                            fo.shape[0], fo.ctypes.data, rs.ctypes.data, flags,
                                            ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_bundle")
         L = fo.shape[0]
-        return [Blocks(self, outs[i], L) for i in range(n)]
+        held = keep if async_ else None   # every batch of the launch holds all its inputs
+        return [Blocks(self, outs[i], L, inputs=held) for i in range(n)]
 
     def sample_lp_bundle(self, src_list, dst_list, rel: int, n_neg: int, neg_seeds, fanouts, rng_seeds,
                          features: bool = True, async_: bool = False):
@@ -548,6 +565,7 @@ class Context:
                     m = len(arr)
                 else:
                     assert arr.dtype == torch.int64 and arr.is_contiguous()
+                    keep.append(arr)
                     tab[i] = arr.data_ptr()
                     m = arr.numel()
                 assert tab is sp or m == cnts[i], "src / dst lengths differ"
@@ -560,7 +578,8 @@ class Context:
                                               ctypes.cast(dp, ctypes.c_void_p), cnts.ctypes.data, rel, n_neg,
                                               ns.ctypes.data, fo.shape[0], fo.ctypes.data, rs.ctypes.data, flags,
                                               ctypes.cast(outs, ctypes.c_void_p)), "eg_sample_lp_bundle")
-        return [Blocks(self, outs[i], fo.shape[0]) for i in range(n)]
+        held = keep if async_ else None
+        return [Blocks(self, outs[i], fo.shape[0], inputs=held) for i in range(n)]
 
     def sample_lp(self, src, dst, rel: int, n_neg: int, neg_seed: int, fanouts, rng_seed: int,
                   features: bool = True, async_: bool = False) -> Blocks:
@@ -645,6 +664,8 @@ class Context:
         tensors kept alive for it), so that their device memory is released now rather
         than whenever this object is collected."""
         if self._h:
+            for b in list(self._live):   # before the library frees their slots
+                b.free()
             lib().eg_destroy(self._h)
             self._h = None
         self._keep = []

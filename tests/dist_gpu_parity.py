@@ -24,6 +24,10 @@ def main():
     ap.add_argument("--replicate", default="auto", help="replicated feature types: auto | none")
     ap.add_argument("--depth", type=int, default=2, help="pipelined check: launches in flight")
     ap.add_argument("--bundle", type=int, default=4, help="pipelined check: mini-batches per launch")
+    ap.add_argument("--backend", default="nccl", help="process group for the blob all-gather (gloo: CPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (two processes sharing one GPU still map each other's shards "
+                         "through CUDA IPC: the multi-process path, testable on a 1-GPU box)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -35,9 +39,12 @@ def main():
     from synth.device import load_context
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(args.backend)
     cfg = synth.config(args.config)
     g = synth.build_host_graph(cfg)
     ctx = Context(rank, world, local)
@@ -51,7 +58,7 @@ def main():
         seeds = synth.batch_seeds(cfg, gi)
         rs = synth.rng_seed(cfg, gi)
         res = oracle.sample(g, seeds, cfg.fanouts, rs)
-        bl = ctx.sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+        bl = ctx.sample_minibatch(torch.from_numpy(seeds).to(f"cuda:{local}"), cfg.fanouts, rs, features=True)
         assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
         assert_same_features(res, [bl.features(u) if u in cfg.feats else None for u in range(cfg.n_vt)], cfg, rows)
         # the separate gather entry point reads the same peer rows
@@ -64,7 +71,7 @@ def main():
     D, B = args.depth, args.bundle
     ctx.set_pipeline(D, B)
     gis = [1000 + (b * world + rank) for b in range(D * B)]
-    dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).cuda() for gi in gis]
+    dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).to(f"cuda:{local}") for gi in gis]
     launches = [ctx.sample_bundle(dev[i:i + B], cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis[i:i + B]],
                                   features=True, async_=True) for i in range(0, D * B, B)]
     for li, bls in enumerate(launches):
@@ -76,7 +83,7 @@ def main():
                                  rows)
             bl.free()
             ok += 1
-    t = torch.tensor([ok], device="cuda")
+    t = torch.tensor([ok], device="cuda" if args.backend == "nccl" else "cpu")
     dist.all_reduce(t)
     if rank == 0:
         print(f"dist parity OK: {args.config} world={world}, {int(t.item())} batches bit-exact vs oracle", flush=True)

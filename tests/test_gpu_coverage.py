@@ -1,0 +1,208 @@
+"""GPU parity cases added in round 2 (VERDICT r01 "what's missing" 1, 3, 4, 7):
+
+* feature rows of 1536 B (C5's 768-d fp16) on both gather kernels: the LDG kernel (world
+  1, no gather4 map for rows > 1 KB) and the TMA kernel's per-row bulk copies (emulated
+  world 2, peer rows), and rows wider than one 16 KB TMA stage (the LDG fallback);
+* the multi-process peer path: two processes on ONE GPU map each other's shards through
+  CUDA IPC (eg_export_shard / eg_import_shards) over a gloo process group;
+* emulated world 8 on C2 and C4 (one GPU, eg_attach_peer), node batches + a bundle;
+* the in-degree limit of eg_load_partition.
+
+Every comparison is element by element against oracle/ on the same seeded inputs.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_same_batch, assert_same_features, run_and_compare
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ctx(graph, world=1, rank=0, features=True):
+    from paper_2112_15345_b200 import Context
+    from synth.device import load_context
+    ctx = Context(rank, world, 0)
+    ctx._shard = load_context(ctx, graph, world, rank, "cuda:0", features=features)
+    return ctx
+
+
+def _world(graph, world):
+    ctxs = [_ctx(graph, world, p) for p in range(world)]
+    for a in ctxs:
+        for b in ctxs:
+            if a is not b:
+                a.attach_peer(b)
+    return ctxs
+
+
+def _features_of(b, cfg):
+    return [b.features(u) if u in cfg.feats else None for u in range(cfg.n_vt)]
+
+
+def _wide(dim, dtype):
+    """C1's graph with `dim`-element rows on both vertex types."""
+    cfg = synth.config("C1")
+    cfg.feats = {0: (dim, dtype), 1: (dim, dtype)}
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    return cfg, g, rows
+
+
+def _check_world(cfg, g, rows, ctxs, batches):
+    import torch
+    for p, ctx in enumerate(ctxs):
+        for b in batches:
+            gi = b * len(ctxs) + p
+            seeds, rs = synth.batch_seeds(cfg, gi), synth.rng_seed(cfg, gi)
+            res = oracle.sample(g, seeds, cfg.fanouts, rs)
+            bl = ctx.sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+            assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, _features_of(bl, cfg), cfg, rows)
+            bl.free()
+            outs = ctx.gather_features(run_and_compare(ctx, g, cfg, seeds, cfg.fanouts, rs)[1])
+            assert_same_features(res, outs, cfg, rows)
+
+
+# ----------------------------------------------------------------------------- 1536-B rows
+
+def test_rows_1536b_world1_ldg():
+    """768-d fp16 rows (C5's paper features) at world 1: no gather4 map (rows > 1 KB), so
+    the LDG kernel copies them; bytes equal the oracle's gather."""
+    cfg, g, rows = _wide(768, synth.F16)
+    ctx = _ctx(g)
+    _check_world(cfg, g, rows, [ctx], range(3))
+    assert ctx.gather_path() == "ldg"
+    ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["tma", "auto"])
+def test_rows_1536b_world2_bulk_copies(mode, monkeypatch):
+    """The same rows at emulated world 2: the TMA kernel's per-row cp.async.bulk copies
+    (peer rows; EG_GATHER read at context creation), bytes equal the oracle's gather."""
+    monkeypatch.setenv("EG_GATHER", mode)
+    cfg, g, rows = _wide(768, synth.F16)
+    ctxs = _world(g, 2)
+    _check_world(cfg, g, rows, ctxs, range(2))
+    assert all(c.gather_path() == "tma" for c in ctxs)
+    for c in ctxs:
+        c.close()
+
+
+def test_rows_wider_than_a_tma_stage(monkeypatch):
+    """20 KB rows (5120 fp32) at world 2 with EG_GATHER=tma: wider than one 16 KB stage,
+    so the library takes the LDG kernel (the per-row TMA path would overrun
+    the stage); bytes equal the oracle's gather."""
+    monkeypatch.setenv("EG_GATHER", "tma")
+    cfg, g, rows = _wide(5120, synth.F32)
+    ctxs = _world(g, 2)
+    _check_world(cfg, g, rows, ctxs, range(1))
+    assert all(c.gather_path() == "ldg" for c in ctxs)
+    for c in ctxs:
+        c.close()
+
+
+# ----------------------------------------------------------------------------- two processes, one GPU
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_two_processes_ipc_one_gpu(name):
+    """The real multi-process peer path on a 1-GPU box: torchrun starts 2 ranks on cuda:0;
+    each exports its shard (CUDA IPC handles), the blobs are all-gathered over gloo, each
+    rank imports the other's shard and samples its own global batches g = b*2 + rank --
+    node batches (+ the standalone gather) and a pipelined bundle (2 lanes x 4) -- and
+    compares every batch with the oracle (tests/dist_gpu_parity.py)."""
+    port = 29600 + (os.getpid() % 200)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "dist_gpu_parity.py"),
+           "--config", name, "--batches", "2", "--depth", "2", "--bundle", "4", "--backend", "gloo",
+           "--same-device", "--replicate", "none"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"dist parity OK: {name} world=2, {2 * (2 + 8)} batches" in r.stdout, r.stdout[-2000:]
+
+
+# ----------------------------------------------------------------------------- emulated world 8
+
+def test_c2_emulated_world8():
+    """C2 range-sharded over 8 emulated ranks on one GPU: every rank's node batches and a
+    bundle read 7/8 of their CSC rows and feature rows from peer shards."""
+    import torch
+    cfg = synth.config("C2")
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    ctxs = _world(g, 8)
+    _check_world(cfg, g, rows, ctxs[:1] + ctxs[7:], range(1))
+    ctx = ctxs[5]
+    ctx.set_pipeline(2, 4)
+    gis = [200 + 8 * i + 5 for i in range(8)]
+    dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).cuda() for gi in gis]
+    launches = [ctx.sample_bundle(dev[i:i + 4], cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis[i:i + 4]],
+                                  features=True, async_=True) for i in (0, 4)]
+    for li, bls in enumerate(launches):
+        for j, bl in enumerate(bls):
+            gi = gis[4 * li + j]
+            res = oracle.sample(g, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi))
+            assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, _features_of(bl, cfg), cfg, rows)
+            bl.free()
+    for c in ctxs:
+        c.close()
+
+
+def test_c4_emulated_world8():
+    """C4 (111M vertices, 1.6B edges; its 8 shards total 36 GB) over 8 emulated ranks on
+    one GPU, as the 8-GPU bench shards it: a node batch on ranks 0 and 7 and a bundle of 4
+    on rank 3; blocks bit-exact vs the oracle, feature bytes vs the generator formula."""
+    import torch
+    cfg = synth.config("C4")
+    g = synth.build_host_graph(cfg, materialize_indices=True)
+    rows = {0: synth.LazyRows(cfg, 0)}
+    ctxs = _world(g, 8)
+    for p in (0, 7):
+        gi = p
+        seeds, rs = synth.batch_seeds(cfg, gi), synth.rng_seed(cfg, gi)
+        res = oracle.sample(g, seeds, cfg.fanouts, rs)
+        bl = ctxs[p].sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+        assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+        assert_same_features(res, _features_of(bl, cfg), cfg, rows)
+        bl.free()
+    ctx = ctxs[3]
+    ctx.set_pipeline(1, 4)
+    gis = [8 * i + 3 for i in range(1, 5)]
+    dev = [torch.from_numpy(synth.batch_seeds(cfg, gi)).cuda() for gi in gis]
+    bls = ctx.sample_bundle(dev, cfg.fanouts, [synth.rng_seed(cfg, gi) for gi in gis], features=True)
+    for gi, bl in zip(gis, bls):
+        res = oracle.sample(g, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi))
+        assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+        assert_same_features(res, _features_of(bl, cfg), cfg, rows)
+        bl.free()
+    for c in ctxs:
+        c.close()
+
+
+# ----------------------------------------------------------------------------- limits
+
+def test_in_degree_limit_rejected():
+    """eg_load_partition rejects a relation whose largest in-degree exceeds 2^26 (the
+    sampler's hub-task encoding) with EG_EINVAL, and accepts exactly 2^26."""
+    import torch
+    from paper_2112_15345_b200 import Context, EgError
+    for d, ok in ((1 << 26, True), ((1 << 26) + 1, False)):
+        ctx = Context(0, 1, 0)
+        ip = torch.tensor([0, d, d], dtype=torch.int64, device="cuda:0")
+        ix = torch.zeros(d, dtype=torch.int32, device="cuda:0")
+        rels = [{"src_vt": 0, "dst_vt": 0, "indptr": ip, "indices": ix, "edge_base": 0}]
+        if ok:
+            ctx.load_partition(np.array([2], np.int64), rels, [None])
+        else:
+            with pytest.raises(EgError) as e:
+                ctx.load_partition(np.array([2], np.int64), rels, [None])
+            assert e.value.code == -1 and "2^26" in str(e.value)
+        ctx.close()
+        del ix, ip
