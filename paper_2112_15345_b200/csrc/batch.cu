@@ -1,6 +1,7 @@
 // batch.cu -- the sampling + compaction of a bundle of mini-batches, one kernel per phase.
 //
-//   seed_split | for h: count(+relabel h-1) | scan | select+copy+tiny | bitcount | cscan | emit | ... | relabel+reset
+//   seed split | kscan scatter compact (level 0) |
+//   for h: count | scan | select + copy + tiny | kscan scatter compact (level h+1)
 //
 // Every phase kernel runs with grid.y = the batch of the bundle (each batch has its own
 // HopDev / compaction state), so B mini-batches cost about what one does: at batch ~1k
@@ -13,6 +14,7 @@
 // higher occupancy (130 vs 183 us per batch), so the per-phase form is the one kept.
 #include "kernels.h"
 #include "phases.cuh"
+#include "compact.cuh"
 
 namespace eg {
 
@@ -34,44 +36,37 @@ __device__ __forceinline__ void stamp(const BatchDev *bd, int k)
         reinterpret_cast<uint64_t *>(bd->hop[blockIdx.y][0].meta + kMetaStamps)[k] = globaltimer();
 }
 
-// Hop h of batch blockIdx.y; h = -1: the link-prediction seed compaction.
+// Hop h of batch blockIdx.y; h = -1: the seeds' level (the seed split / link-prediction targets).
 __device__ __forceinline__ const HopDev &hop_of(const BatchDev *bd, int h)
 {
-    return h < 0 ? bd->lph[blockIdx.y] : bd->hop[blockIdx.y][h];
+    return h < 0 ? bd->seedh[blockIdx.y] : bd->hop[blockIdx.y][h];
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_lp_mark(const __grid_constant__ GraphDev g,
                                                            const BatchDev *__restrict__ bd)
 {
     stamp(bd, 0);
-    phase_lp_mark(g, bd->lph[blockIdx.y], bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
-}
-
-__global__ void __launch_bounds__(kBatchThreads) k_lp_pairs(const __grid_constant__ GraphDev g,
-                                                            const BatchDev *__restrict__ bd)
-{
-    phase_lp_pairs(g, bd->lph[blockIdx.y], bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
+    phase_lp_mark(g, bd->seedh[blockIdx.y], bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd)
 {
     stamp(bd, 0);
-    phase_seed_split(g, bd->hop[blockIdx.y][0], bd->seeds[blockIdx.y]);
+    phase_seed_split(g, bd->seedh[blockIdx.y], bd->seeds[blockIdx.y]);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 8 * h);
+    stamp(bd, 4 + 8 * h);
     phase_count(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
-    if (h > 0) phase_relabel(g, bd->hop[blockIdx.y][h - 1], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 2 + 8 * h);
+    stamp(bd, 5 + 8 * h);
     phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
@@ -82,114 +77,67 @@ __global__ void __launch_bounds__(kBatchThreads, EG_SELECT_MIN_BLOCKS) k_select(
                                                              const BatchDev *__restrict__ bd, int h)
 {
     __shared__ uint64_t s_cand[kBatchWarps][kSelCap];
-    stamp(bd, 3 + 8 * h);
+    stamp(bd, 6 + 8 * h);
     phase_select(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
 }
 
 __global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 4 + 8 * h);
+    stamp(bd, 7 + 8 * h);
     phase_copy(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(kBatchThreads, 4) k_tiny(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 5 + 8 * h);
+    stamp(bd, 8 + 8 * h);
     phase_tiny(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
 }
 
-template <bool kSparse>
-__global__ void __launch_bounds__(kBatchThreads) k_bitcount(const __grid_constant__ GraphDev g,
-                                                            const BatchDev *__restrict__ bd, int h)
+// Compaction of level h + 1 (the keys produced by hop h; h = -1: the seeds' level).
+__global__ void __launch_bounds__(1024) k_kscan(const __grid_constant__ GraphDev g, const BatchDev *__restrict__ bd,
+                                                int h)
 {
-    if (h >= 0) stamp(bd, 6 + 8 * h);
-    if (kSparse)
-        phase_bitcount_sparse(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
-    else
-        phase_bitcount_dense(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
+    stamp(bd, 1 + 8 * (h + 1));
+    phase_kscan(g, hop_of(bd, h));
 }
 
-__global__ void __launch_bounds__(1024) k_cscan(const __grid_constant__ GraphDev g,
-                                                 const BatchDev *__restrict__ bd, int h)
-{
-    if (h >= 0) stamp(bd, 7 + 8 * h);
-    phase_chunk_scan(g, hop_of(bd, h));
-}
-
-#ifndef EG_EMIT_MIN_BLOCKS
-#define EG_EMIT_MIN_BLOCKS 1
-#endif
-template <bool kSparse>
-__global__ void __launch_bounds__(kBatchThreads, EG_EMIT_MIN_BLOCKS) k_emit(const __grid_constant__ GraphDev g,
-                                                        const BatchDev *__restrict__ bd, int h)
-{
-    if (h >= 0) stamp(bd, 8 + 8 * h);
-    if (kSparse)
-        phase_emit_sparse(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
-    else
-        phase_emit_dense(g, hop_of(bd, h), blockIdx.x, gridDim.x, bd->n_chunks);
-}
-
-__global__ void __launch_bounds__(kBatchThreads) k_relabel(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads) k_scatter(const __grid_constant__ GraphDev g,
                                                            const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 1 + 8 * bd->n_hops);
-    phase_relabel(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
+    stamp(bd, 2 + 8 * (h + 1));
+    phase_scatter(g, hop_of(bd, h), bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_reset(const __grid_constant__ GraphDev g,
-                                                         const BatchDev *__restrict__ bd)
+__global__ void __launch_bounds__(kBatchThreads) k_compact(const __grid_constant__ GraphDev g,
+                                                           const BatchDev *__restrict__ bd, int h)
 {
-    stamp(bd, 2 + 8 * bd->n_hops);
-    phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
+    __shared__ CompactSmem sm[kBatchWarps];
+    stamp(bd, 3 + 8 * (h + 1));
+    phase_compact(g, hop_of(bd, h), bd->lpd[blockIdx.y], sm);
 }
 
-// The last hop's relabel and the batch reset in one kernel: independent work (relabel
-// reads pos[], reset clears member words), one kernel boundary less per batch.
-__global__ void __launch_bounds__(kBatchThreads) k_finish(const __grid_constant__ GraphDev g,
-                                                          const BatchDev *__restrict__ bd, int h)
-{
-    stamp(bd, 1 + 8 * bd->n_hops);
-    phase_relabel(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
-    phase_reset(g, bd->hop[blockIdx.y][bd->n_hops - 1], bd->n_hops, blockIdx.x, gridDim.x);
-}
-
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
-                 const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial, int lp)
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks, int B,
+                 cudaStream_t s, const Fork &fk, bool serial, bool lp)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
     const int samp = (kSMs * 4 + B - 1) / B;
-    // bitmap chunks: at most one resident wave in total (8 blocks of 256 threads per SM);
-    // blocks loop.  Dense variant: a block per chunk; sparse (per hop, chosen by the
-    // plan): a warp per half chunk.
-    const int chunk_cap = (kSMs * 8 + B - 1) / B;
     int nk = 0;
-    auto compaction = [&](int h, bool sparse) {
-        const int chunk_need = sparse ? (2 * n_chunks + kBatchWarps - 1) / kBatchWarps : n_chunks;
-        const int chunk_blocks = chunk_need < chunk_cap ? chunk_need : chunk_cap;
-        if (sparse)
-            k_bitcount<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        else
-            k_bitcount<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_cscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
-        if (sparse)
-            k_emit<true><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        else
-            k_emit<false><<<dim3(chunk_blocks, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+    auto compaction = [&](int h) {   // level h + 1
+        k_kscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
+        k_scatter<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        k_compact<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        nk += 3;
     };
-    if (lp >= 0) {   // link prediction: targets -> marks -> seed compaction -> pairs
+    if (lp) {   // link prediction: targets -> endpoint keys -> seeds + pairs
         k_lp_mark<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
-        compaction(-1, lp == 1);
-        k_lp_pairs<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
-        nk += 5;
     } else {
         k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
-        ++nk;
     }
+    ++nk;
+    compaction(-1);
     for (int h = 0; h < n_hops; ++h) {
         const int wide = scan_blocks[h] * g.n_rel;   // count / scan: one block per virtual block
         k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
@@ -209,16 +157,10 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
-        compaction(h, sparse_hop[h] != 0);
-        nk += 8;
+        nk += 5;
+        compaction(h);
     }
-    if (serial) {   // EG_TRACE: separate stamps
-        k_relabel<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
-        k_reset<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
-        return nk + 2;
-    }
-    k_finish<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, n_hops - 1);
-    return nk + 1;
+    return nk;
 }
 
 }  // namespace eg

@@ -10,8 +10,13 @@ namespace eg {
 
 constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
-constexpr int kChunkWords = 1024;         // bitmap words per compaction chunk (one block)
-constexpr int64_t kChunkBits = (int64_t)kChunkWords * 32;
+// Compaction buckets (compact.cuh): each vertex type's id range is cut into fine buckets of
+// 2^bshift consecutive gids, bshift in [kMinBucketShift, kMaxBucketShift] chosen at load so
+// that a graph has at most ~2^16 buckets (C4: 2^11 gids, 54k buckets).  A bucket's bitmap is
+// 2^bshift / 32 words, at most 16 per lane of a warp.
+constexpr int kMinBucketShift = 10;
+constexpr int kMaxBucketShift = 14;
+constexpr int64_t kMaxBuckets = (int64_t)1 << 17;
 // Virtual blocks per relation in the two-phase count / scan: per hop, one per
 // kScanItemsPerBlock frontier-capacity items, within [kMinScanBlocks, kMaxScanBlocks].
 // (Measured, profiles/r01/diag/scan_blocks_ab*.txt: a floor of 64 left most threads of
@@ -57,7 +62,10 @@ struct GraphDev {
     int32_t n_vt, n_rel, world, rank;
     int64_t off[EG_MAX_VT + 1];                       // gid = off[t] + tid
     int64_t bounds[EG_MAX_VT][EG_MAX_RANKS + 1];      // owned tid ranges per rank
-    int64_t boff[EG_MAX_VT + 1];                      // bitmap bit offset per type (chunk aligned)
+    int64_t bbase[EG_MAX_VT + 1];                     // first compaction bucket of each type
+    int32_t bshift;                                   // log2 of the gids per bucket
+    int32_t nb;                                       // buckets in total (= bbase[n_vt])
+    int32_t compact_bitmap;                           // EG_COMPACT=bitmap: every bucket a task, bitmap path
     RelDev rel[EG_MAX_REL];
 };
 
@@ -80,7 +88,9 @@ constexpr int kMetaHeavyQ = kMetaHeavy + EG_MAX_HOPS;            // heavy tasks 
 constexpr int kMetaHeavyNext = kMetaHeavyQ + EG_MAX_HOPS;        // dynamic fetch counter per hop
 constexpr int kMetaTiny = kMetaHeavyNext + EG_MAX_HOPS;         // tiny selection items per hop
 constexpr int kMetaTinyNext = kMetaTiny + EG_MAX_HOPS;            // dynamic fetch counter per hop
-constexpr int kMetaErr = kMetaTinyNext + EG_MAX_HOPS;
+constexpr int kMetaTasks = kMetaTinyNext + EG_MAX_HOPS;           // compaction tasks per level (0..L)
+constexpr int kMetaTicket = kMetaTasks + EG_MAX_HOPS + 1;         // compaction task tickets per level
+constexpr int kMetaErr = kMetaTicket + EG_MAX_HOPS + 1;
 constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase timestamps (tracing)
 constexpr int kMaxStamps = 80;
 constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
@@ -101,6 +111,26 @@ struct LpDev {
     int32_t *pairs;               // [pos_src cap][pos_dst cap][neg_src cap*n][neg_dst cap*n], local ids
 };
 
+// Compaction modes (compact.cuh): the keys of a level are
+//   kModeHop    the sampled sources of hop h (level h+1): new ones are appended, every edge relabelled;
+//   kModeSeeds  the seeds (level 0, node classification): positions given by the seed split;
+//   kModeLp     the link-prediction endpoints (level 0): distinct ones become the seeds, pairs relabelled.
+enum : int32_t { kModeHop = 0, kModeSeeds = 1, kModeLp = 2 };
+
+// Batch-local compaction state (one per batch; sized by the batch's caps, not by the graph).
+struct CompactDev {
+    uint32_t *kcnt;                  // [nb] keys per bucket (counted by the marking kernels,
+                                     // counted back to 0 by the scatter)
+    uint32_t *mcnt;                  // [nb] members per bucket for the next level (zeroed by kscan)
+    uint32_t *kofs, *mofs;           // [nb + 1] exclusive prefixes of kcnt / mcnt
+    uint32_t *tstart;                // [nb + 1] first bucket of each compaction task
+    unsigned long long *lb;          // [nb] decoupled look-back words of the tasks
+    uint32_t *keys, *kidx;           // [cap_keys] keys (gids) in bucket order + payload
+    uint32_t *mg[2];                 // members (gids of the batch so far) sorted by gid, ping-pong by level
+    int32_t *mp[2];                  // their positions in their type's node array
+    int32_t cap_keys;
+};
+
 // Everything a hop's kernels touch.
 struct HopDev {
     int32_t h;
@@ -115,16 +145,9 @@ struct HopDev {
     int32_t scan_blocks;             // virtual blocks per relation (count / scan)
     int32_t max_heavy;               // heavy item slots
     int32_t max_heavy_tasks;         // heavy task slots
-    int32_t *pos;                    // gid -> position in its type's node array, -1 if absent
-    uint32_t *bitmap;                // interleaved word pairs: marks A (every sampled source of
-                                     // the hop) at 2w, members M (vertices already in the batch) at
-                                     // 2w+1; new = A & ~M.  One 8-B access reads or writes both
-                                     // words of a pair (one sector instead of two)
-    uint32_t *summary;               // bit w of the summary = A word w may be nonzero
-    uint32_t *summary_mark;          // = summary on sparse hops; null on dense hops (no summary)
-    int32_t *chunk_cnt;              // new vertices per bitmap chunk
-    int32_t *seg_cnt;                // new vertices per slice (16 bitmap words)
-    int32_t *chunk_pre;              // new vertices in the chunks before, within the type
+    CompactDev cd;                   // the batch's compaction state
+    int32_t mode;                    // compaction mode of the level this hop produces (kMode*)
+    int32_t last;                    // 1: the last level (no member list for a next level)
     int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
     int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
@@ -139,6 +162,12 @@ struct HopDev {
 };
 
 __device__ __forceinline__ int32_t *meta_nodes(int32_t *meta, int l) { return meta + kMetaNodes + l * EG_MAX_VT; }
+
+// Compaction bucket of gid (vertex type u): buckets are type-aligned, 2^bshift gids each.
+__device__ __forceinline__ int64_t bucket_of(const GraphDev &g, int u, int64_t gid)
+{
+    return g.bbase[u] + ((gid - g.off[u]) >> g.bshift);
+}
 __device__ __forceinline__ int32_t *meta_nnz(int32_t *meta, int h) { return meta + kMetaNnz + h * EG_MAX_REL; }
 
 // |F_h[u]| before hop h's compaction; the link-prediction seed compaction runs as

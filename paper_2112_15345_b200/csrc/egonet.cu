@@ -60,25 +60,12 @@ struct TimedPair {
 
 }  // namespace
 
-// Compaction state of one batch in flight: gid -> position map, new-vertex bitmap,
-// scan scratch.
-struct BatchState {
-    int32_t *pos = nullptr;
-    uint32_t *bitmap = nullptr;     // word pairs (A, M), HopDev::bitmap
-    uint32_t *summary = nullptr;
-    int32_t *chunk_cnt = nullptr;
-    int32_t *seg_cnt = nullptr;
-    int32_t *chunk_pre = nullptr;
-    int32_t *partial = nullptr;
-};
-
-// A lane: one stream + the states of the `bundle` batches one launch carries.  Launches
-// on different lanes are independent and run concurrently (the asynchronous mini-batch
-// pipeline); launches on one lane are ordered.
+// A lane: one stream.  Launches on different lanes are independent and run concurrently
+// (the asynchronous mini-batch pipeline); launches on one lane are ordered.  Every
+// batch's state (incl. its compaction state) lives in its slot: batch-sized, not graph-sized.
 struct Lane {
     cudaStream_t stream = nullptr;
     cudaEvent_t ready = nullptr;     // caller stream -> lane ordering
-    std::vector<BatchState> st;
 };
 
 // per (batch, hop): heavy items, their counters, candidate buffers and chunk tasks
@@ -107,10 +94,13 @@ struct Plan {
            o_selq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
     int64_t selq_items[EG_MAX_HOPS] = {};
     int32_t scan_blocks[EG_MAX_HOPS] = {}, max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
-    int32_t sparse[EG_MAX_HOPS] = {};   // compaction variant per hop (1 = lane-per-slice)
+    // batch-local compaction state (compact.cuh): meta | kcnt | mcnt contiguous (one memset)
+    size_t o_partial = 0, o_kcnt = 0, o_mcnt = 0, o_kofs = 0, o_mofs = 0, o_tstart = 0, o_lb = 0, o_keys = 0,
+           o_kidx = 0, o_mg[2] = {}, o_mp[2] = {}, zero_bytes = 0;
+    int64_t cap_keys = 0, cap_members = 0;
     // link prediction (NEXT-3): n_cap = positives capacity; seeds <= n_cap * (2 + n_neg)
     bool lp = false;
-    int32_t n_neg = 0, lp_sparse = 0;
+    int32_t n_neg = 0;
     size_t o_lp_src = 0, o_lp_dst = 0, o_lp_neg = 0, o_lp_pairs = 0;
     size_t o_bd = 0, total = 0;      // BatchDev header, then B batch regions
     int32_t n_kernels = 0;
@@ -158,7 +148,6 @@ struct eg_ctx {
     std::vector<Lane> lanes;
     int next_lane = 0;
     int depth = 1, bundle = 1;
-    int32_t n_chunks = 0;
     std::vector<void *> ipc_bases;
     uint32_t attached = 0;                          // bit p: rank p's shard is mapped
     eg_shard_meta metas[EG_MAX_RANKS] = {};          // every rank's published shard metadata
@@ -173,7 +162,7 @@ struct eg_ctx {
     cudaStream_t cap_stream = nullptr;
     Fork fork{};                          // capture side stream + events (graph branches)
     bool trace = false;                   // EG_TRACE=1 at create: per-stage events in every graph
-    int compact = 0;                      // EG_COMPACT at create: 0 per hop, 1 dense, 2 sparse
+    int compact = 0;                      // EG_COMPACT at create: 0 default, 1 bitmap path for every bucket
     int prio = 1;                         // EG_PRIO at create: 0 none, 1 gather first, 2 sampling first
     int gather_mode = 2;                  // EG_GATHER at create: 0 tma, 1 ldg, 2 auto (gather.cu)
     std::vector<std::string> trace_names;
@@ -349,41 +338,15 @@ void fill_meta(const eg_ctx *c, ShardBlob *b)
     }
 }
 
-eg_status alloc_state(eg_ctx *c, BatchState *st)
+// At least `depth` lanes.
+eg_status ensure_lanes(eg_ctx *c, int depth)
 {
-    const int64_t nt = std::max<int64_t>(1, c->n_total);
-    const size_t words = (size_t)std::max<int64_t>(1, c->g.boff[c->g.n_vt] / 32);
-    EG_CUDA(c, cudaMalloc(&st->pos, sizeof(int32_t) * nt));
-    EG_CUDA(c, cudaMemset(st->pos, 0xFF, sizeof(int32_t) * nt));
-    EG_CUDA(c, cudaMalloc(&st->bitmap, 2 * sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMemset(st->bitmap, 0, 2 * sizeof(uint32_t) * words));
-    EG_CUDA(c, cudaMalloc(&st->summary, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
-    EG_CUDA(c, cudaMemset(st->summary, 0, sizeof(uint32_t) * std::max<size_t>(1, words / 32)));
-    EG_CUDA(c, cudaMalloc(&st->chunk_cnt, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMemset(st->chunk_cnt, 0, sizeof(int32_t) * std::max(1, c->n_chunks)));   // accumulated
-    EG_CUDA(c, cudaMalloc(&st->seg_cnt, sizeof(int32_t) * std::max(1, c->n_chunks) * (kChunkWords / 16)));
-    EG_CUDA(c, cudaMalloc(&st->chunk_pre, sizeof(int32_t) * std::max(1, c->n_chunks)));
-    EG_CUDA(c, cudaMalloc(&st->partial, sizeof(int32_t) * EG_MAX_REL * kMaxScanBlocks));
-    return EG_OK;
-}
-
-// At least `depth` lanes with at least `bundle` batch states each.
-eg_status ensure_lanes(eg_ctx *c, int depth, int bundle)
-{
-    eg_status st;
     while ((int)c->lanes.size() < depth) {
         Lane ln;
         EG_CUDA(c, cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
         EG_CUDA(c, cudaEventCreateWithFlags(&ln.ready, cudaEventDisableTiming));
         c->lanes.push_back(ln);
     }
-    for (Lane &ln : c->lanes)
-        while ((int)ln.st.size() < bundle) {
-            BatchState bs;
-            if ((st = alloc_state(c, &bs))) return st;
-            ln.st.push_back(bs);
-        }
-    EG_CUDA(c, cudaDeviceSynchronize());
     return EG_OK;
 }
 
@@ -588,9 +551,10 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
     {
         const char *tr = getenv("EG_TRACE");
         c->trace = tr && tr[0] == '1';
-        // EG_COMPACT=dense|sparse forces a compaction variant (tests); default per hop (plan)
+        // EG_COMPACT=bitmap: every compaction bucket is a task of its own, on the bitmap path
+        // (tests: both paths on the same inputs); default: runs of small buckets are sorted
         const char *cm = getenv("EG_COMPACT");
-        c->compact = !cm ? 0 : (cm[0] == 'd' ? 1 : (cm[0] == 's' ? 2 : 0));
+        c->compact = cm && cm[0] == 'b' ? 1 : 0;
         // EG_PRIO=gather|sample|none: per-node scheduling priority inside the batch graphs.
         // Default gather: measured (profiles/prio_sweep.sh) it shortens the gather's
         // duration in the pipelined run by 8-20 % at unchanged throughput (C2, C4).
@@ -653,10 +617,15 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
         for (int p = 0; p < c->world; ++p)
             if (g.bounds[t][p + 1] < g.bounds[t][p]) return fail(c, EG_EINVAL, "bounds must be non-decreasing");
     }
-    // bitmap layout: one chunk-aligned bit range per type
-    g.boff[0] = 0;
-    for (int t = 0; t < n_vt; ++t) g.boff[t + 1] = g.boff[t] + (int64_t)align_up((size_t)vt_counts[t], kChunkBits);
-    c->n_chunks = (int32_t)(g.boff[n_vt] / kChunkBits);
+    // compaction buckets (compact.cuh): type-aligned ranges of 2^bshift gids, bshift the
+    // smallest in [kMinBucketShift, kMaxBucketShift] that keeps the graph's buckets <= 2^16
+    g.bshift = kMinBucketShift;
+    while (g.bshift < kMaxBucketShift && (c->n_total >> g.bshift) > (1 << 16)) ++g.bshift;
+    g.bbase[0] = 0;
+    for (int t = 0; t < n_vt; ++t) g.bbase[t + 1] = g.bbase[t] + ((vt_counts[t] + (1ll << g.bshift) - 1) >> g.bshift);
+    if (g.bbase[n_vt] > kMaxBuckets) return fail(c, EG_EINVAL, "too many vertices for the compaction buckets");
+    g.nb = (int32_t)g.bbase[n_vt];
+    g.compact_bitmap = c->compact;
 
     unsigned long long *d_max = nullptr;
     EG_CUDA(c, cudaMalloc(&d_max, sizeof(unsigned long long) * EG_MAX_REL));
@@ -725,7 +694,7 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
                                           std::to_string(c->rel_max_degree[r]) + " exceeds 2^26");
     }
 
-    if ((st = ensure_lanes(c, 1, 1))) return st;
+    if ((st = ensure_lanes(c, 1))) return st;
     EG_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
     build_gather_maps(c);
@@ -922,15 +891,47 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         off = align_up(off + std::max<size_t>(bytes, 1), 256);
         return o;
     };
-    p->o_meta = take(sizeof(int32_t) * kMetaSize);
+    // meta, kcnt, mcnt are contiguous: one memset per batch and launch clears them
+    const int64_t NB = c->g.nb;
+    p->o_meta = off;
+    off += align_up(sizeof(int32_t) * kMetaSize, 16);
+    p->o_kcnt = off;
+    off += align_up(sizeof(uint32_t) * NB, 16);
+    p->o_mcnt = off;
+    off += align_up(sizeof(uint32_t) * NB, 16);
+    p->zero_bytes = off - p->o_meta;
+    off = align_up(off, 256);
     p->o_dyn = take(sizeof(uint64_t) * kDyn);
+    p->o_partial = take(sizeof(int32_t) * EG_MAX_REL * kMaxScanBlocks);
+    p->o_kofs = take(sizeof(uint32_t) * (NB + 1));
+    p->o_mofs = take(sizeof(uint32_t) * (NB + 1));
+    p->o_tstart = take(sizeof(uint32_t) * (NB + 1));
+    p->o_lb = take(sizeof(unsigned long long) * NB);
     p->o_seeds = take(sizeof(int64_t) * (lp ? 1 : n_cap));
     if (lp) {
         p->o_lp_src = take(sizeof(int64_t) * n_cap);
         p->o_lp_dst = take(sizeof(int64_t) * n_cap);
         p->o_lp_neg = take(sizeof(int64_t) * n_cap * n_neg);
         p->o_lp_pairs = take(sizeof(int32_t) * n_cap * (2 + 2 * (int64_t)n_neg));
-        p->lp_sparse = c->compact == 2 ? 1 : c->compact == 1 ? 0 : (seed_cap < c->g.boff[V] / 32 ? 1 : 0);
+    }
+    // keys of a level: its seeds / endpoints (level 0) or its hop's sampled edges; members:
+    // every vertex of the batch
+    p->cap_keys = seed_cap;
+    for (int h = 0; h < L; ++h) {
+        int64_t e = 0;
+        for (int r = 0; r < R; ++r) e += p->capE[h][r];
+        p->cap_keys = std::max(p->cap_keys, e);
+    }
+    for (int u = 0; u < V; ++u) p->cap_members += p->capF[L][u];
+    if (p->cap_keys >= INT32_MAX || p->cap_members >= INT32_MAX) {
+        delete p;
+        return fail(c, EG_EINVAL, "batch exceeds 2^31 keys / vertices");
+    }
+    p->o_keys = take(sizeof(uint32_t) * p->cap_keys);
+    p->o_kidx = take(sizeof(uint32_t) * p->cap_keys);
+    for (int i = 0; i < 2; ++i) {
+        p->o_mg[i] = take(sizeof(uint32_t) * p->cap_members);
+        p->o_mp[i] = take(sizeof(int32_t) * p->cap_members);
     }
     for (int u = 0; u < V; ++u) p->o_nodes[u] = take(sizeof(int64_t) * p->capF[L][u]);
     for (int h = 0; h < L; ++h)
@@ -956,14 +957,6 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         p->max_heavy[h] = (int32_t)std::min<int64_t>(65535, kMinHeavy + items / 2048);
         p->max_heavy_tasks[h] = (int32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)p->max_heavy[h] * kHeavyTasksPerItem);
         p->o_heavy[h] = take(heavy_bytes(p->max_heavy[h], p->max_heavy_tasks[h]));
-        // compaction variant: sparse (lane per 16-word slice) when the hop's edge bound is
-        // below one mark per bitmap word, else dense (lane per word); EG_COMPACT forces.
-        // (Measured: sparse wins at ~1 mark per 20 words -- C4 hop 2, bound ~6x actual --
-        // dense at 1.6 per word -- a 10^6-vertex frontier on C4 -- and on C2 / C3.)
-        int64_t edges = 0;
-        for (int r = 0; r < R; ++r) edges += p->capE[h][r];
-        const int64_t words = c->g.boff[V] / 32;
-        p->sparse[h] = c->compact == 2 ? 1 : c->compact == 1 ? 0 : (edges < words ? 1 : 0);
     }
     if (features)
         for (int u = 0; u < V; ++u)
@@ -997,11 +990,9 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     const GraphDev &g = c->g;
     const int V = g.n_vt, R = g.n_rel, L = p->n_hops, B = p->B;
     cudaStream_t cs = c->cap_stream;
-    const Lane &ln = c->lanes[sl->lane];
     BatchDev *bd = new BatchDev();
     memset(bd, 0, sizeof(BatchDev));
     bd->n_hops = L;
-    bd->n_chunks = c->n_chunks;
     bd->trace = c->trace ? 1 : 0;
     bd->B = B;
     bd->lp = p->lp ? 1 : 0;
@@ -1009,27 +1000,37 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     gs.nb = B;
     for (int b = 0; b < B; ++b) {
         char *base = p->batch_base(sl->mem, b);
-        const BatchState &st = ln.st[b];
         HopDev hd{};
         hd.dyn = (const uint64_t *)(base + p->o_dyn);
         hd.meta = (int32_t *)(base + p->o_meta);
-        hd.partial = st.partial;
-        hd.pos = st.pos;
-        hd.bitmap = st.bitmap;
-        hd.summary = st.summary;
-        hd.chunk_cnt = st.chunk_cnt;
-        hd.seg_cnt = st.seg_cnt;
-        hd.chunk_pre = st.chunk_pre;
+        hd.partial = (int32_t *)(base + p->o_partial);
+        CompactDev &cd = hd.cd;
+        cd.kcnt = (uint32_t *)(base + p->o_kcnt);
+        cd.mcnt = (uint32_t *)(base + p->o_mcnt);
+        cd.kofs = (uint32_t *)(base + p->o_kofs);
+        cd.mofs = (uint32_t *)(base + p->o_mofs);
+        cd.tstart = (uint32_t *)(base + p->o_tstart);
+        cd.lb = (unsigned long long *)(base + p->o_lb);
+        cd.keys = (uint32_t *)(base + p->o_keys);
+        cd.kidx = (uint32_t *)(base + p->o_kidx);
+        for (int i = 0; i < 2; ++i) {
+            cd.mg[i] = (uint32_t *)(base + p->o_mg[i]);
+            cd.mp[i] = (int32_t *)(base + p->o_mp[i]);
+        }
+        cd.cap_keys = (int32_t)p->cap_keys;
         for (int u = 0; u < V; ++u) {
             hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
             hd.cap_nodes[u] = (int32_t)p->capF[L][u];
         }
         bd->seeds[b] = (const int64_t *)(base + p->o_seeds);
-        if (p->lp) {
+        {   // the seeds' level: seed split / link-prediction targets + the level-0 compaction
             HopDev x = hd;
             x.h = -1;
-            x.summary_mark = p->lp_sparse ? x.summary : nullptr;
-            bd->lph[b] = x;
+            x.mode = p->lp ? kModeLp : kModeSeeds;
+            x.last = 0;
+            bd->seedh[b] = x;
+        }
+        if (p->lp) {
             LpDev &lp = bd->lpd[b];
             lp.n_neg = p->n_neg;
             lp.cap_pos = p->n_cap;
@@ -1050,7 +1051,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
                 x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
                 x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
             }
-            x.summary_mark = p->sparse[h] ? x.summary : nullptr;
+            x.mode = kModeHop;
+            x.last = h == L - 1;
             x.selq = (uint64_t *)(base + p->o_selq[h]);
             x.selq_cap = (int32_t)p->selq_items[h];
             char *hv = base + p->o_heavy[h];
@@ -1090,12 +1092,12 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     for (int b = 0; b < B; ++b) {
         char *base = p->batch_base(sl->mem, b);
         cudaMemcpyAsync(base + p->o_dyn, sl->h_dyn + kDyn * b, sizeof(uint64_t) * kDyn, cudaMemcpyHostToDevice, cs);
-        cudaMemsetAsync(base + p->o_meta, 0, sizeof(int32_t) * kMetaSize, cs);
     }
+    // counters + the compaction's bucket counts of every batch: one 2-D memset
+    cudaMemset2DAsync(p->batch_base(sl->mem, 0) + p->o_meta, p->stride, 0, p->zero_bytes, B, cs);
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->scan_blocks, p->sparse, c->n_chunks, B, cs,
-                       c->fork, c->trace, p->lp ? p->lp_sparse : -1);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->scan_blocks, B, cs, c->fork, c->trace, p->lp);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -1250,13 +1252,13 @@ void slot_finished(eg_ctx *c, Slot *sl)
         c->prof_n[1] += 1;
     }
     if (c->trace) {
-        // in-kernel phase stamps of batch 0: seed, per hop count/scan/select/copy/tiny/bitcount/cscan/emit, relabel, reset
+        // in-kernel phase stamps of batch 0 (batch.cu stamp indices): seed, level-0 compaction
+        // (kscan, scatter, compact), per hop count/scan/select/copy/tiny + its level's compaction
         const uint64_t *st = reinterpret_cast<const uint64_t *>(sl->h_meta + kMetaStamps);
-        std::vector<std::string> names = {"k.seed"};
+        std::vector<std::string> names = {"k.seed", "k.l0.kscan", "k.l0.scatter", "k.l0.compact"};
         for (int h = 0; h < sl->plan->n_hops; ++h)
-            for (const char *x : {"count", "scan", "select", "copy", "tiny", "bitcount", "cscan", "emit"})
+            for (const char *x : {"count", "scan", "select", "copy", "tiny", "kscan", "scatter", "compact"})
                 names.push_back("k.h" + std::to_string(h) + "." + x);
-        names.push_back("k.relabel");
         for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
             if (!st[k + 1] || !st[k]) break;
             trace_add(c, names[k], (double)(st[k + 1] - st[k]) * 1e-6);
@@ -1689,7 +1691,7 @@ eg_status eg_set_pipeline(eg_ctx *c, int32_t depth, int32_t bundle)
     if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
     if (depth < 1 || depth > 16) return fail(c, EG_EINVAL, "pipeline depth must be in [1, 16]");
     if (bundle < 1 || bundle > kMaxBundle) return fail(c, EG_EINVAL, "bundle size must be in [1, 16]");
-    if ((st = ensure_lanes(c, depth, bundle))) return st;
+    if ((st = ensure_lanes(c, depth))) return st;
     c->next_lane = 0;
     c->depth = depth;
     c->bundle = bundle;
@@ -1760,15 +1762,6 @@ eg_status eg_destroy(eg_ctx *c)
     for (void *p : c->ipc_bases) cudaIpcCloseMemHandle(p);
     for (Lane &ln : c->lanes) {
         if (ln.stream) cudaStreamSynchronize(ln.stream);
-        for (BatchState &bs : ln.st) {
-            cudaFree(bs.pos);
-            cudaFree(bs.bitmap);
-            cudaFree(bs.summary);
-            cudaFree(bs.chunk_cnt);
-            cudaFree(bs.seg_cnt);
-            cudaFree(bs.chunk_pre);
-            cudaFree(bs.partial);
-        }
         if (ln.ready) cudaEventDestroy(ln.ready);
         if (ln.stream) cudaStreamDestroy(ln.stream);
     }

@@ -25,11 +25,11 @@ struct GatherSet {
 };
 
 struct BatchDev {
-    int32_t n_hops, n_chunks, trace, B;
+    int32_t n_hops, trace, B;
     int32_t lp;                            // link-prediction batches (seeds from targets)
     const int64_t *seeds[kMaxBundle];
     HopDev hop[kMaxBundle][EG_MAX_HOPS];
-    HopDev lph[kMaxBundle];                // LP seed compaction ("hop -1")
+    HopDev seedh[kMaxBundle];              // the seeds' level ("hop -1": seed split + level-0 compaction)
     LpDev lpd[kMaxBundle];
 };
 
@@ -40,11 +40,9 @@ struct Fork {
 };
 
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
-// returns the number of kernels.
-// lp >= 0: link-prediction batches, seed compaction variant lp (1 = sparse).
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks,
-                 const int32_t *sparse_hop, int n_chunks, int B, cudaStream_t s,
-                 const Fork &fk, bool serial, int lp);
+// returns the number of kernels.  lp: link-prediction batches (seeds from targets).
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks, int B,
+                 cudaStream_t s, const Fork &fk, bool serial, bool lp);
 
 // TMA tensor maps of the feature tables the gather reads with cp.async.bulk.tensor
 // tile::gather4 (four rows per TMA operation): per vertex type one 2-D map over its full

@@ -10,8 +10,8 @@
 //   scan              block CSC indptr = exclusive prefix of c
 //   sample            d <= k: the whole in-neighbourhood in CSC order; d > k: the
 //                     k offsets with the smallest (key32 << 32 | j), ascending j P:284-285
-//   bitcount / emit   new sources of the hop in gid order after the dst prefix
-//   relabel           local src ids = positions in src_nodes
+//   compaction        new sources of the hop in gid order after the dst prefix,
+//                     local src ids = positions in src_nodes (compact.cuh)
 #pragma once
 #include "common.cuh"
 
@@ -21,8 +21,9 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 
 // ============================================================================ seed split
 
-// Seeds (caller order, mixed types) -> F_0[u] (stable per type) + pos[] for the
-// dst-prefix relabel; flags out-of-range and duplicate seeds.  One block.
+// Seeds (caller order, mixed types) -> F_0[u] (stable per type); every placed seed is a
+// key of the level-0 compaction (compact.cuh, kModeSeeds: sorted member list, duplicate
+// check).  Flags out-of-range seeds.  One block.
 __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds)
 {
     // the caller's buffer when it is device-accessible, else the slot's staged copy
@@ -31,7 +32,7 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
     __shared__ int32_t base[EG_MAX_VT];
     // pointers hoisted into registers: HopDev lives in global memory and every store
     // below could alias it, so reading fields inside the loops would reload them
-    int32_t *const pos = hd.pos;
+    uint32_t *const kcnt = hd.cd.kcnt;
     int32_t *const meta = hd.meta;
     const int64_t n = (int64_t)hd.dyn[1];
     const int w = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = lane_id();
@@ -74,12 +75,7 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
             const int32_t p = wcnt[w][vt] + rank;
             if (p < hd.cap_nodes[vt]) {
                 hd.nodes[vt][p] = gid;
-                pos[gid] = p;
-                // duplicate seed: its member bit is already set (pos[] is only ever read for
-                // members of the current batch, so it needs no reset between batches)
-                const int64_t bit = g.boff[vt] + (gid - g.off[vt]);
-                const uint32_t mb = 1u << (bit & 31);
-                if (atomicOr(hd.bitmap + 2 * (bit >> 5) + 1, mb) & mb) atomicOr(meta + kMetaErr, kErrSeedDup);
+                atomicAdd(kcnt + bucket_of(g, vt, gid), 1u);
             } else {
                 atomicOr(meta + kMetaErr, kErrCapacity);
             }
@@ -213,10 +209,9 @@ __device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb)
 // ============================================================================ sampling
 
 struct Item {
-    const int32_t *pos;     // the batch's gid -> position map (read only here)
-    uint32_t *bitmap;       // the batch's new-vertex bitmap
-    uint32_t *summary;      // and its summary (one bit per bitmap word)
-    int64_t bit_base;       // boff[s(r)] - off[s(r)]: bitmap bit of gid = bit_base + gid
+    uint32_t *kcnt;         // the batch's keys per compaction bucket
+    int32_t bbase;          // first bucket of s(r)
+    int32_t bshift;         // log2 gids per bucket
     uint32_t soff;          // off[s(r)]
     int64_t ebase;          // global CSC position of this dst's first edge
     const int32_t *ix;      // src tids of this dst's in-edges
@@ -224,19 +219,20 @@ struct Item {
     int64_t *eid_out;
 };
 
-// Mark the source in the hop's bitmap (the first step of the compaction, fused into
-// sampling).  Fire-and-forget RED.OR, no load: sources already in the batch are
-// cleared from the bitmap by phase_bitcount (one check per unique source instead of
-// a dependent pos[] load per sampled edge).
-//
-// The summary bit of the word is set too, so that the compaction visits only the words
-// that hold marks: at hop 2 of a 111M-vertex graph a batch marks ~1% of the words.
-__device__ __forceinline__ void mark_src(uint32_t *bitmap, uint32_t *summary, uint32_t gid, int64_t bit_base)
+// Count the source as a key of the hop's compaction (its first step, fused into sampling):
+// fire-and-forget RED.ADD on the batch's bucket counts (L2-resident, sized by the graph's
+// bucket count, ~2^16).
+__device__ __forceinline__ void mark_src(const Item &it, uint32_t gid)
 {
-    const int64_t bit = bit_base + gid;
-    const int64_t w = bit >> 5;
-    atomicOr(bitmap + 2 * w, 1u << (bit & 31));   // results unused: RED (word A of the pair)
-    if (summary) atomicOr(summary + (w >> 5), 1u << (w & 31));   // sparse hops only
+    atomicAdd(it.kcnt + it.bbase + ((gid - it.soff) >> it.bshift), 1u);   // result unused: RED
+}
+
+__device__ __forceinline__ void item_common(const GraphDev &g, const HopDev &hd, const RelDev &R, Item &it)
+{
+    it.kcnt = hd.cd.kcnt;
+    it.bbase = (int32_t)g.bbase[R.src_vt];
+    it.bshift = g.bshift;
+    it.soff = (uint32_t)g.off[R.src_vt];
 }
 
 __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_t slot, int64_t j)
@@ -244,7 +240,7 @@ __device__ __forceinline__ void emit_edge(const HopDev &, const Item &it, int32_
     const uint32_t gid = it.soff + (uint32_t)__ldg(it.ix + j);
     it.src_out[slot] = gid;
     it.eid_out[slot] = it.ebase + j;
-    mark_src(it.bitmap, it.summary, gid, it.bit_base);
+    mark_src(it, gid);
 }
 
 // Up to four selected edges of one lane: the source-id loads are issued together before
@@ -263,7 +259,7 @@ __device__ __forceinline__ void emit_edges4(const Item &it, uint32_t sel, const 
             const uint32_t gid = it.soff + ix[t];
             it.src_out[slot[t]] = gid;
             it.eid_out[slot[t]] = it.ebase + j[t];
-            mark_src(it.bitmap, it.summary, gid, it.bit_base);
+            mark_src(it, gid);
         }
 }
 
@@ -590,11 +586,7 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
     const int p = (int)(ib >> 56);
     const int64_t base0 = ib & ((1ll << 56) - 1);
     Item itm;
-    itm.pos = hd.pos;
-    itm.bitmap = hd.bitmap;
-    itm.summary = hd.summary_mark;
-    itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
-    itm.soff = (uint32_t)g.off[R.src_vt];
+    item_common(g, hd, R, itm);
     itm.ebase = R.edge_base[p] + base0;
     itm.ix = R.indices[p] + base0;
     itm.src_out = hd.src[r] + pos0;
@@ -673,8 +665,6 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
 {
     const int lane = lane_id();
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const int32_t *const pos = hd.pos;
-    uint32_t *const bitmap = hd.bitmap;
     const uint64_t *const selq = hd.selq;
     (void)bid;
     // ---- heavy chunk tasks
@@ -722,11 +712,7 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
             const int p = (int)(ib >> 56);
             const int64_t base = ib & ((1ll << 56) - 1);
             Item itm;
-            itm.pos = pos;
-            itm.bitmap = bitmap;
-            itm.summary = hd.summary_mark;
-            itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
-            itm.soff = (uint32_t)g.off[R.src_vt];
+            item_common(g, hd, R, itm);
             itm.ebase = R.edge_base[p] + base;
             itm.ix = R.indices[p] + base;
             itm.src_out = hd.src[r] + pos0;
@@ -812,11 +798,7 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
             const RelDev &R = g.rel[r];
             const int p = (int)(cur.ib >> 56);
             const int64_t base = cur.ib & ((1ll << 56) - 1);
-            itm.pos = hd.pos;
-            itm.bitmap = hd.bitmap;
-            itm.summary = hd.summary_mark;
-            itm.bit_base = g.boff[R.src_vt] - g.off[R.src_vt];
-            itm.soff = (uint32_t)g.off[R.src_vt];
+            item_common(g, hd, R, itm);
             itm.ebase = R.edge_base[p] + base;
             itm.ix = R.indices[p] + base;
             itm.src_out = hd.src[r] + cur.pos0;
@@ -895,8 +877,8 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
     const int warps = blockDim.x >> 5;
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
-    uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const summary = hd.summary_mark;
+    uint32_t *const kcnt = hd.cd.kcnt;
+    const int32_t bshift = g.bshift;
     // ---- full neighbourhoods: segmented copy over groups of 32 items
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
     int64_t cum[EG_MAX_REL + 1];
@@ -931,7 +913,7 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
         const int32_t excl = incl - c;
         constexpr int U = 4;   // slots per lane per round: U independent load chains in flight
         for (int32_t b0 = 0; b0 < tot; b0 += 32 * U) {
-            uint32_t gid[U];
+            uint32_t gid[U], goff[U];
             uint32_t *dsrc[U];
             int64_t *deid[U];
             int64_t eid[U], bb[U];
@@ -958,8 +940,8 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
                     const int32_t j = s - exL;
                     const RelDev &R = g.rel[rL];
                     ixp[q] = R.indices[p] + base + j;
-                    gid[q] = (uint32_t)g.off[R.src_vt];
-                    bb[q] = g.boff[R.src_vt] - g.off[R.src_vt];
+                    gid[q] = goff[q] = (uint32_t)g.off[R.src_vt];
+                    bb[q] = g.bbase[R.src_vt];
                     eid[q] = R.edge_base[p] + base + j;
                     dsrc[q] = srcL + j;
                     deid[q] = eidL + j;
@@ -973,302 +955,8 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
                 if (dsrc[q]) {
                     *dsrc[q] = gid[q];
                     *deid[q] = eid[q];
-                    mark_src(bitmap, summary, gid[q], bb[q]);
+                    atomicAdd(kcnt + bb[q] + ((gid[q] - goff[q]) >> bshift), 1u);   // mark_src: RED
                 }
-        }
-    }
-}
-
-// ============================================================================ compaction
-//
-// Work unit: a slice of kLaneWords bitmap words per lane (half a summary word), a warp
-// per 32 slices (half a chunk).  A lane loads only the words whose summary bits are
-// set, four at a time, so a sparse slice (the common case at 10^8 vertices) costs one
-// round of loads and a dense one (10^6 vertices) at most four.
-
-constexpr int kLaneWords = 16;
-constexpr int kSlices = kChunkWords / kLaneWords;     // slices per chunk (64)
-constexpr int kHalves = kSlices / 32;                 // warps per chunk (2)
-static_assert(kHalves == 2, "slice layout");
-
-// Summary bits of slice (c, hc, lane): bit t = word t of the slice may hold marks.
-__device__ __forceinline__ uint32_t slice_bits(const uint32_t *summary, int64_t c, int hc, int lane)
-{
-    const int sl = hc * 32 + lane;
-    return (__ldcg(summary + c * 32 + (sl >> 1)) >> ((sl & 1) * kLaneWords)) & 0xFFFFu;
-}
-
-// New vertices (A & ~M) per slice and chunk.  Words whose marks are all members are
-// cleared here, so that emit finds only words with new vertices.  chunk_cnt[] is zero
-// on entry (phase_chunk_scan consumes and clears it).
-__device__ void phase_bitcount_sparse(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
-{
-    const int lane = lane_id();
-    uint32_t *const bitmap = hd.bitmap;
-    const int64_t n_items = (int64_t)n_chunks * kHalves;
-    const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
-    int64_t it = (int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    uint32_t bits_next = it < n_items ? slice_bits(hd.summary, it / kHalves, (int)(it % kHalves), lane) : 0u;
-    for (; it < n_items; it += stride) {
-        const int64_t c = it / kHalves;
-        const int hc = (int)(it % kHalves);
-        uint32_t bits = bits_next;
-        if (it + stride < n_items)   // prefetch the next slice's summary
-            bits_next = slice_bits(hd.summary, (it + stride) / kHalves, (int)((it + stride) % kHalves), lane);
-        const int64_t w0 = c * kChunkWords + (hc * 32 + lane) * kLaneWords;
-        int32_t cnt = 0;
-        while (bits) {
-            int t[4];
-            uint32_t a[4], m[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                t[q] = -1;
-                a[q] = m[q] = 0u;
-                if (bits) {
-                    t[q] = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const uint2 am = __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w0 + t[q]);
-                    a[q] = am.x;
-                    m[q] = am.y;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t nw = a[q] & ~m[q];
-                cnt += __popc(nw);
-                if (a[q] && !nw) bitmap[2 * (w0 + t[q])] = 0u;   // only members marked: consumed here
-            }
-        }
-        hd.seg_cnt[c * kSlices + hc * 32 + lane] = cnt;
-        const int32_t total = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)cnt);
-        if (lane == 0 && total) atomicAdd(hd.chunk_cnt + c, total);
-    }
-}
-
-// Exclusive scan of the chunk counts within each vertex type (one 1024-thread block per
-// batch) -> chunk_pre[]; sets |S_h+1[u]| = |F_h[u]| + new[u] and clears chunk_cnt[].
-__device__ void phase_chunk_scan(const GraphDev &g, const HopDev &hd)
-{
-    __shared__ int32_t sh[33];
-    int32_t *const nn = meta_nodes(hd.meta, hd.h + 1);
-    const int32_t *const nF = nodes_before(hd);
-    for (int u = 0; u < g.n_vt; ++u) {
-        const int lo = (int)(g.boff[u] / kChunkBits), hi = (int)(g.boff[u + 1] / kChunkBits);
-        const int per = (hi - lo + (int)blockDim.x - 1) / (int)blockDim.x;
-        const int a = min(hi, lo + (int)threadIdx.x * per), b = min(hi, a + per);
-        int32_t s = 0;
-        for (int c = a; c < b; ++c) s += __ldcg(hd.chunk_cnt + c);
-        int32_t tot;
-        int32_t run = block_excl_scan(s, sh, &tot);
-        for (int c = a; c < b; ++c) {
-            const int32_t v = __ldcg(hd.chunk_cnt + c);
-            hd.chunk_pre[c] = run;
-            hd.chunk_cnt[c] = 0;
-            run += v;
-        }
-        if (threadIdx.x == 0) nn[u] = nF[u] + tot;
-        __syncthreads();   // sh reuse by the next type
-    }
-}
-
-// New vertices of each chunk, in gid order: append to the node array of their type,
-// set pos[], fold them into the members, clear the marks and the summary.  A lane
-// emits its slice's new vertices in ascending gid from its prefix position.
-__device__ void phase_emit_sparse(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
-{
-    const int lane = lane_id();
-    uint32_t *const bitmap = hd.bitmap;
-    int32_t *const pos = hd.pos;
-    const int64_t n_items = (int64_t)n_chunks * kHalves;
-    const int64_t stride = (int64_t)nb * (blockDim.x >> 5);
-    // The loads of an item are issued together (measured, ncu C4 hop 2: the serial chain
-    // summary -> counts -> chunk prefix -> word pairs was the kernel's stall): the next
-    // item's summary word is prefetched, and the first four word pairs are loaded beside
-    // the counts.
-    int64_t it = (int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    auto summary_of = [&](int64_t i) -> uint32_t {
-        const int64_t ci = i / kHalves;
-        const int sli = (int)(i % kHalves) * 32 + lane;
-        return __ldcg(hd.summary + ci * 32 + (sli >> 1));
-    };
-    uint32_t sw_next = it < n_items ? summary_of(it) : 0u;
-    for (; it < n_items; it += stride) {
-        const int64_t c = it / kHalves;
-        const int hc = (int)(it % kHalves);
-        const int sl = hc * 32 + lane;
-        const uint32_t sw = sw_next;
-        if (it + stride < n_items) sw_next = summary_of(it + stride);
-        uint32_t bits = (sw >> ((sl & 1) * kLaneWords)) & 0xFFFFu;
-        if (!__any_sync(0xffffffffu, bits != 0)) continue;
-        const int64_t w0 = c * kChunkWords + sl * kLaneWords;
-        int t[4];
-        uint2 am[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            t[q] = -1;
-            am[q] = make_uint2(0u, 0u);
-            if (bits) {
-                t[q] = __ffs(bits) - 1;
-                bits &= bits - 1;
-                am[q] = __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w0 + t[q]);
-            }
-        }
-        const int32_t cnt = __ldcg(hd.seg_cnt + c * kSlices + sl);
-        const int32_t cnt_lo = hc ? __ldcg(hd.seg_cnt + c * kSlices + lane) : 0;
-        const int32_t cpre = __ldcg(hd.chunk_pre + c);
-        if ((sl & 1) == 0 && sw) hd.summary[c * 32 + (sl >> 1)] = 0u;   // both halves of the word are read (this warp)
-        int32_t ex = warp_incl_scan(cnt) - cnt;
-        if (hc) ex += (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)cnt_lo);
-        if (t[0] < 0) continue;
-        const int64_t bit0 = c * kChunkBits;
-        int u = 0;
-        while (bit0 >= g.boff[u + 1]) ++u;
-        int32_t position = nodes_before(hd)[u] + cpre + ex;
-        const int32_t cap = hd.cap_nodes[u];
-        int64_t *const nodes = hd.nodes[u];
-        const int64_t gid0 = g.off[u] - g.boff[u] + w0 * 32;   // gid of bit b of word w0 + t: gid0 + 32t + b
-        while (true) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t a = am[q].x, m = am[q].y;
-                uint32_t word = a & ~m;
-                if (!a) continue;
-                // marks consumed, new vertices now members: one 8-B store of the pair
-                reinterpret_cast<uint2 *>(bitmap)[w0 + t[q]] = make_uint2(0u, m | word);
-                const int64_t gb = gid0 + 32 * t[q];
-                while (word) {
-                    const int b = __ffs(word) - 1;
-                    word &= word - 1;
-                    if (position < cap) {
-                        nodes[position] = gb + b;
-                        pos[gb + b] = position;
-                    } else {
-                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
-                    }
-                    ++position;
-                }
-            }
-            if (!bits) break;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                t[q] = -1;
-                am[q] = make_uint2(0u, 0u);
-                if (bits) {
-                    t[q] = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    am[q] = __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w0 + t[q]);
-                }
-            }
-        }
-    }
-}
-
-// ---- dense variant (hops that mark a large fraction of the words; they keep no summary,
-// every word is visited): a block of 8 warps per chunk = 32 units of 32 words; warp w
-// takes units w, w+8,
-// w+16, w+24, one word per lane, so that the emission of a dense word (up to 32 new
-// vertices) is spread over the lanes and the node-array stores of a warp are contiguous.
-constexpr int kUnitsPerWarp = kChunkWords / 32 / 8;   // 4 (blockDim.x == 256)
-constexpr int kPrefetch = 8;                          // chunks whose summary words one load fetches
-
-__device__ void phase_bitcount_dense(const GraphDev &, const HopDev &hd, int bid, int nb, int32_t n_chunks)
-{
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
-    uint32_t *const bitmap = hd.bitmap;
-    // rounds of 8 chunks c0 + j nb: lane 4j + q prefetches summary word q of chunk j
-    for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
-        const int cp = c0 + (lane >> 2) * nb;
-        const uint32_t swall = cp < n_chunks ? 0xFFFFFFFFu : 0u;   // dense hops keep no summary: every word
-        for (int j = 0; j < kPrefetch; ++j) {
-            const int c = c0 + j * nb;
-            if (c >= n_chunks) break;
-            const int64_t u0 = (int64_t)c * 32 + wid;      // unit of q = 0; unit q = u0 + 8q
-            const uint32_t sw = __shfl_sync(0xffffffffu, swall, 4 * j + (lane & 3));   // lanes q < 4
-            if (!__ballot_sync(0xffffffffu, lane < kUnitsPerWarp && sw != 0)) {
-                if (lane < kUnitsPerWarp) hd.seg_cnt[u0 + 8 * lane] = 0;
-                continue;
-            }
-            uint32_t a[kUnitsPerWarp], m[kUnitsPerWarp];
-#pragma unroll
-            for (int q = 0; q < kUnitsPerWarp; ++q) {
-                const bool b = (__shfl_sync(0xffffffffu, sw, q) >> lane) & 1u;
-                const int64_t w = (u0 + 8 * q) * 32 + lane;
-                const uint2 am = b ? __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w) : make_uint2(0u, 0u);
-                a[q] = am.x;
-                m[q] = am.y;
-            }
-            int32_t cnt_mine = 0, total = 0;
-#pragma unroll
-            for (int q = 0; q < kUnitsPerWarp; ++q) {
-                const uint32_t nw = a[q] & ~m[q];
-                if (a[q] && !nw) bitmap[2 * ((u0 + 8 * q) * 32 + lane)] = 0u;   // only members marked: consumed
-                const int32_t v = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)__popc(nw));
-                if (lane == q) cnt_mine = v;
-                total += v;
-            }
-            if (lane < kUnitsPerWarp) hd.seg_cnt[u0 + 8 * lane] = cnt_mine;
-            if (lane == 0 && total) atomicAdd(hd.chunk_cnt + c, total);
-        }
-    }
-}
-
-__device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, int nb, int32_t n_chunks)
-{
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
-    uint32_t *const bitmap = hd.bitmap;
-    int32_t *const pos = hd.pos;
-    for (int c0 = bid; c0 < n_chunks; c0 += kPrefetch * nb) {
-        const int cp = c0 + (lane >> 2) * nb;
-        const uint32_t swall = cp < n_chunks ? 0xFFFFFFFFu : 0u;   // dense hops keep no summary: every word
-        for (int j = 0; j < kPrefetch; ++j) {
-            const int c = c0 + j * nb;
-            if (c >= n_chunks) break;
-            const int64_t u0 = (int64_t)c * 32 + wid;
-            const uint32_t sw = __shfl_sync(0xffffffffu, swall, 4 * j + (lane & 3));   // lanes q < 4
-            if (!__ballot_sync(0xffffffffu, lane < kUnitsPerWarp && sw != 0)) continue;
-            const int64_t bit0 = (int64_t)c * kChunkBits;
-            int u = 0;
-            while (bit0 >= g.boff[u + 1]) ++u;
-            const int32_t uc = __ldcg(hd.seg_cnt + (int64_t)c * 32 + lane);   // unit `lane` of the chunk
-            const int32_t uex = warp_incl_scan(uc) - uc;
-            const int32_t base = nodes_before(hd)[u] + __ldcg(hd.chunk_pre + c);
-            const int32_t cap = hd.cap_nodes[u];
-            int64_t *const nodes = hd.nodes[u];
-            const int64_t gid0 = g.off[u] - g.boff[u];   // gid of bitmap bit b = gid0 + b
-            uint32_t su[kUnitsPerWarp], a[kUnitsPerWarp], m[kUnitsPerWarp];
-#pragma unroll
-            for (int q = 0; q < kUnitsPerWarp; ++q) {
-                su[q] = __shfl_sync(0xffffffffu, sw, q);
-                const int64_t w = (u0 + 8 * q) * 32 + lane;
-                const bool b = (su[q] >> lane) & 1u;
-                const uint2 am = b ? __ldcg(reinterpret_cast<const uint2 *>(bitmap) + w) : make_uint2(0u, 0u);
-                a[q] = am.x;
-                m[q] = am.y;
-            }
-#pragma unroll
-            for (int q = 0; q < kUnitsPerWarp; ++q) {
-                const int unit = wid + 8 * q;
-                const int32_t ubase = __shfl_sync(0xffffffffu, uex, unit);
-                if (!su[q]) continue;   // warp-uniform
-                uint32_t word = a[q] & ~m[q];
-                const int32_t pc = __popc(word);
-                int32_t position = base + ubase + (warp_incl_scan(pc) - pc);
-                const int64_t w = (u0 + 8 * q) * 32 + lane;
-                if (a[q]) reinterpret_cast<uint2 *>(bitmap)[w] = make_uint2(0u, m[q] | word);   // one 8-B store
-                if (!word) continue;
-                const int64_t gb = gid0 + w * 32;
-                while (word) {
-                    const int b = __ffs(word) - 1;
-                    word &= word - 1;
-                    if (position < cap) {
-                        nodes[position] = gb + b;
-                        pos[gb + b] = position;
-                    } else {
-                        atomicOr(hd.meta + kMetaErr, kErrCapacity);
-                    }
-                    ++position;
-                }
-            }
         }
     }
 }
@@ -1276,9 +964,9 @@ __device__ void phase_emit_dense(const GraphDev &g, const HopDev &hd, int bid, i
 // ============================================================================ link prediction
 
 // Link-prediction targets (NEXT-3, DESIGN.md §3 L1-L4): per positive (src_i, dst_i) of
-// relation r, n_neg corrupted dsts drawn uniformly from t(r)'s range; every endpoint is
-// marked in the bitmap so that the ordinary compaction (run as "hop -1" over an empty
-// frontier) yields the distinct endpoints in ascending gid as the seeds F_0.
+// relation r, n_neg corrupted dsts drawn uniformly from t(r)'s range; every endpoint is a
+// key of the level-0 compaction (compact.cuh, kModeLp), which yields the distinct
+// endpoints in ascending gid as the seeds F_0 and every pair in local ids.
 __device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
 {
     const int64_t n = (int64_t)hd.dyn[1];
@@ -1288,11 +976,9 @@ __device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &
     const int r = (int)hd.dyn[5];
     const int sv = g.rel[r].src_vt, tv = g.rel[r].dst_vt;
     const int64_t s_lo = g.off[sv], s_hi = g.off[sv + 1], t_lo = g.off[tv], t_hi = g.off[tv + 1];
-    const int64_t sb = g.boff[sv] - s_lo, tb = g.boff[tv] - t_lo;   // bitmap bit of gid = base + gid
     const uint64_t n_t = (uint64_t)(t_hi - t_lo);
     const int n_neg = lp.n_neg;
-    uint32_t *const bitmap = hd.bitmap;
-    uint32_t *const summary = hd.summary_mark;
+    uint32_t *const kcnt = hd.cd.kcnt;
     int64_t *const neg = lp.neg;
     for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
         const int64_t a = src[i], b = dst[i];
@@ -1300,84 +986,14 @@ __device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &
             atomicOr(hd.meta + kMetaErr, kErrSeedRange);
             continue;
         }
-        mark_src(bitmap, summary, (uint32_t)a, sb);
-        mark_src(bitmap, summary, (uint32_t)b, tb);
+        atomicAdd(kcnt + bucket_of(g, sv, a), 1u);
+        atomicAdd(kcnt + bucket_of(g, tv, b), 1u);
         for (int q = 0; q < n_neg; ++q) {
             uint32_t c0 = (uint32_t)i, c1 = (uint32_t)q, c2 = 0u, c3 = 0x4E454721u;   // 'NEG!'
             philox4x32_10(c0, c1, c2, c3, k0, k1);
             const int64_t x = t_lo + (int64_t)(((uint64_t)c0 * n_t) >> 32);
             neg[i * n_neg + q] = x;
-            mark_src(bitmap, summary, (uint32_t)x, tb);
-        }
-    }
-}
-
-// After the seed compaction: every pair in local ids (pos[] = index among the seeds of
-// the endpoint's type).
-__device__ void phase_lp_pairs(const GraphDev &, const HopDev &hd, const LpDev &lp, int bid, int nb)
-{
-    const int64_t n = (int64_t)hd.dyn[1];
-    const int64_t *__restrict__ src = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : lp.src_stage;
-    const int64_t *__restrict__ dst = hd.dyn[3] ? (const int64_t *)hd.dyn[3] : lp.dst_stage;
-    const int32_t *const pos = hd.pos;
-    const int n_neg = lp.n_neg;
-    const int64_t cap = lp.cap_pos;
-    int32_t *const pairs = lp.pairs;
-    const int64_t *const neg = lp.neg;
-    if (*(volatile int32_t *)(hd.meta + kMetaErr)) return;   // a range error: pos[] is not valid
-    for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
-        const int32_t ps = __ldcg(pos + src[i]);
-        pairs[i] = ps;
-        pairs[cap + i] = __ldcg(pos + dst[i]);
-        for (int q = 0; q < n_neg; ++q) {
-            pairs[2 * cap + i * n_neg + q] = ps;
-            pairs[2 * cap + cap * n_neg + i * n_neg + q] = __ldcg(pos + neg[i * n_neg + q]);
-        }
-    }
-}
-
-// indices = pos[src]: the local id of every sampled src in S_h[s(r)].
-__device__ void phase_relabel(const GraphDev &g, const HopDev &hd, int bid, int nb)
-{
-    const int32_t *const pos = hd.pos;
-    const int64_t stride = (int64_t)nb * blockDim.x;
-    for (int r = 0; r < g.n_rel; ++r) {
-        const int64_t n = meta_nnz(hd.meta, hd.h)[r];
-        const uint32_t *const src = hd.src[r];
-        int32_t *const idx = hd.indices[r];
-        // four independent src -> pos[] chains per thread in flight
-        int64_t e = bid * (int64_t)blockDim.x + threadIdx.x;
-        for (; e + 3 * stride < n; e += 4 * stride) {
-            uint32_t sv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) sv[q] = __ldcs(src + e + q * stride);
-            int32_t pv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) pv[q] = __ldcg(pos + sv[q]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) idx[e + q * stride] = pv[q];
-        }
-        for (; e < n; e += stride) idx[e] = __ldcg(pos + src[e]);
-    }
-}
-
-// End of batch: clear the member bitmap.  Every bit set in it belongs to this batch, so the
-// whole word of each vertex is zeroed with a plain store (idempotent across the vertices
-// sharing it); pos[] keeps stale values, which are never read (only members are looked up).
-__device__ void phase_reset(const GraphDev &g, const HopDev &hd, int32_t level, int bid, int nb)
-{
-    const int32_t *n = meta_nodes(hd.meta, level);
-    int64_t cum[EG_MAX_VT + 1];
-    cum[0] = 0;
-    for (int u = 0; u < g.n_vt; ++u) cum[u + 1] = cum[u] + min(n[u], hd.cap_nodes[u]);
-    uint32_t *const bitmap = hd.bitmap;
-    for (int u = 0; u < g.n_vt; ++u) {
-        const int64_t *const nodes = hd.nodes[u];
-        const int64_t n = cum[u + 1] - cum[u];
-        const int64_t lo = g.off[u], hi = g.off[u + 1], b0 = g.boff[u];
-        for (int64_t i = bid * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nb * blockDim.x) {
-            const int64_t gid = nodes[i];
-            if (gid >= lo && gid < hi) bitmap[2 * ((b0 + (gid - lo)) >> 5) + 1] = 0u;
+            atomicAdd(kcnt + bucket_of(g, tv, x), 1u);
         }
     }
 }

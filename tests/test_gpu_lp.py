@@ -98,7 +98,7 @@ def test_c1_node_batch_has_no_lp_view(c1):
     b.free()
 
 
-@pytest.mark.parametrize("mode", ["sparse", "dense"])
+@pytest.mark.parametrize("mode", ["default", "bitmap"])
 def test_c1_lp_compaction_variants(c1, mode, monkeypatch):
     cfg, g, rows, _ = c1
     monkeypatch.setenv("EG_COMPACT", mode)

@@ -376,11 +376,11 @@ def test_bench_launch_configuration(name, depth, bundle):
 
 # ----------------------------------------------------------------------------- compaction variants
 
-@pytest.mark.parametrize("mode", ["sparse", "dense"])
+@pytest.mark.parametrize("mode", ["default", "bitmap"])
 def test_compaction_variant_forced(c1, c2, mode, monkeypatch):
-    """Both compaction variants (lane-per-word blocks for hops that mark many words,
-    lane-per-slice warps for sparse hops; chosen per hop by the plan) give the oracle's blocks on C1
-    and C2, alone and in a bundle of 3 batches."""
+    """Both compaction paths (compact.cuh: runs of small buckets sorted in shared memory,
+    big buckets by a per-warp bitmap; EG_COMPACT=bitmap makes every bucket a task of its own
+    on the bitmap path) give the oracle's blocks on C1 and C2, alone and in a bundle of 3."""
     import torch
     monkeypatch.setenv("EG_COMPACT", mode)   # read at context creation
     for cfg, g, rows, _ in (c1, c2):
