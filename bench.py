@@ -584,12 +584,13 @@ def run_ours(args, cfg, rank, world, local_rank):
             return e, nbytes
 
         e2e_acc = {"edges": 0, "h2d": 0, "d2h": 0}
+        counter_b = __import__("paper_2112_15345_b200").counter_bytes()
 
         def e2e_count(bl):
             e, nb = e2e_retire(bl)
             e2e_acc["edges"] += e
             e2e_acc["h2d"] += cfg.batch * (16 if lp else 8)
-            e2e_acc["d2h"] += nb + 1440   # + the per-batch counters (kMetaSize = 360 int32, csrc/common.cuh)
+            e2e_acc["d2h"] += nb + counter_b   # + the per-batch counters read back (eg_counter_bytes)
 
         with torch.cuda.stream(stream):
             run(0, min(W, 2), pinned_seeds, e2e_retire)

@@ -111,6 +111,11 @@ typedef struct {
 /* Library version string. */
 EG_API const char *eg_version(void);
 
+/* Bytes of the per-batch device counters copied to the host at the end of every launch
+ * (sizes, error bits, trace stamps): the only device->host transfer of a batch whose
+ * features stay on the device. */
+EG_API int64_t eg_counter_bytes(void);
+
 /* Create a context for rank `rank` of `world` (1 <= world <= EG_MAX_RANKS) on CUDA
  * device `device`; `stream` is a cudaStream_t (NULL = legacy default stream).
  * Fails with EG_ECUDA when no usable sm_100 device is present. */

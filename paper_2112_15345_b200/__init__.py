@@ -5,4 +5,4 @@ for sm_100a from csrc/ and exposed through the C ABI in include/egonet.h;
 ``egonet`` is its ctypes binding.
 """
 from .egonet import (Block, Blocks, Context, EgError, batch_caps, lib, range_bounds,  # noqa: F401
-                     version, ABI_SYMBOLS, ShardMeta, shard_meta, check_shard_metas)
+                     version, counter_bytes, ABI_SYMBOLS, ShardMeta, shard_meta, check_shard_metas)

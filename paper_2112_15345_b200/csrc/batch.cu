@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(kBatchThreads, 4) k_tiny(const __grid_constant
 }
 
 // Compaction of level h + 1 (the keys produced by hop h; h = -1: the seeds' level).
-__global__ void __launch_bounds__(1024) k_kscan(const __grid_constant__ GraphDev g, const BatchDev *__restrict__ bd,
-                                                int h)
+__global__ void __launch_bounds__(kScanThreads) k_kscan(const __grid_constant__ GraphDev g,
+                                                        const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 1 + 8 * (h + 1));
     phase_kscan(g, hop_of(bd, h));
@@ -126,7 +126,7 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
     const int samp = (kSMs * 4 + B - 1) / B;
     int nk = 0;
     auto compaction = [&](int h) {   // level h + 1
-        k_kscan<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev, h);
+        k_kscan<<<dim3((g.nb + kScanTile - 1) / kScanTile, B), kScanThreads, 0, s>>>(g, bd_dev, h);
         k_scatter<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         k_compact<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
         nk += 3;

@@ -17,6 +17,8 @@ constexpr int kSMs = 148;                 // B200
 constexpr int kMinBucketShift = 10;
 constexpr int kMaxBucketShift = 14;
 constexpr int64_t kMaxBuckets = (int64_t)1 << 17;
+constexpr int kScanTile = 4096;                                   // buckets per kscan CTA (512 threads x 8)
+constexpr int kMaxScanTiles = (int)(kMaxBuckets / kScanTile);     // 32: one warp looks back over all
 // Virtual blocks per relation in the two-phase count / scan: per hop, one per
 // kScanItemsPerBlock frontier-capacity items, within [kMinScanBlocks, kMaxScanBlocks].
 // (Measured, profiles/r01/diag/scan_blocks_ab*.txt: a floor of 64 left most threads of
@@ -90,8 +92,9 @@ constexpr int kMetaTiny = kMetaHeavyNext + EG_MAX_HOPS;         // tiny selectio
 constexpr int kMetaTinyNext = kMetaTiny + EG_MAX_HOPS;            // dynamic fetch counter per hop
 constexpr int kMetaTasks = kMetaTinyNext + EG_MAX_HOPS;           // compaction tasks per level (0..L)
 constexpr int kMetaTicket = kMetaTasks + EG_MAX_HOPS + 1;         // compaction task tickets per level
-constexpr int kMetaErr = kMetaTicket + EG_MAX_HOPS + 1;
-constexpr int kMetaStamps = kMetaErr + 8;                  // 64-bit phase timestamps (tracing)
+constexpr int kMetaKTicket = kMetaTicket + EG_MAX_HOPS + 1;       // kscan tile tickets per level
+constexpr int kMetaErr = kMetaKTicket + EG_MAX_HOPS + 1;
+constexpr int kMetaStamps = (kMetaErr + 8 + 1) & ~1;       // 64-bit phase timestamps (tracing), 8-B aligned
 constexpr int kMaxStamps = 80;
 constexpr int kMetaSize = kMetaStamps + 2 * kMaxStamps;
 
@@ -119,9 +122,10 @@ enum : int32_t { kModeHop = 0, kModeSeeds = 1, kModeLp = 2 };
 
 // Batch-local compaction state (one per batch; sized by the batch's caps, not by the graph).
 struct CompactDev {
-    uint32_t *kcnt;                  // [nb] keys per bucket (counted by the marking kernels,
-                                     // counted back to 0 by the scatter)
-    uint32_t *mcnt;                  // [nb] members per bucket for the next level (zeroed by kscan)
+    uint32_t *kcnt;                  // [nb, padded to kScanTile] keys per bucket (counted by the
+                                     // marking kernels, counted back to 0 by the scatter)
+    uint32_t *mcnt;                  // [same] members per bucket for the next level (zeroed by kscan)
+    unsigned long long *tlb;         // [levels][2][kMaxScanTiles] kscan tile look-back words (zeroed per launch)
     uint32_t *kofs, *mofs;           // [nb + 1] exclusive prefixes of kcnt / mcnt
     uint32_t *tstart;                // [nb + 1] first bucket of each compaction task
     unsigned long long *lb;          // [nb] decoupled look-back words of the tasks

@@ -81,75 +81,148 @@ __device__ __forceinline__ int32_t level_nodes_before(const HopDev &hd, int u)
 
 // ============================================================================ kscan
 
-// One CTA per batch.  kofs / mofs = exclusive prefixes of the key / member counts per
-// bucket; tasks: bucket b starts a task if it is its type's first bucket, if it or its
-// predecessor is big (> kBigBucket elements), or if the elements before it crossed a
+// Tiles of kScanTile buckets, one CTA of 512 threads each (8 buckets per thread, 16-B
+// loads), tiles taken by ticket; each tile publishes its totals (keys, members, tasks) and
+// adds those of all earlier tiles (<= 32: one warp reads them at once).  Outputs: kofs /
+// mofs = exclusive prefixes of the key / member counts per bucket; the compaction TASKS:
+// bucket b starts a task if it is its tile's or its type's first bucket, if it or its
+// predecessor is big (> kBigBucket elements), or if the tile's elements before it crossed a
 // multiple of kTaskElems since its predecessor.  Clears mcnt (the compaction counts the
 // next level's members into it) and the tasks' look-back words.
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = kScanTile / kScanThreads;   // 8
+static_assert(kScanPer == 8, "two 16-B loads per array and thread");
+
+__device__ __forceinline__ unsigned long long tlb_word(uint32_t hi, uint32_t lo)
+{
+    return (1ull << 63) | ((unsigned long long)(hi & 0x7FFFFFFFu) << 32) | lo;
+}
+
 __device__ void phase_kscan(const GraphDev &g, const HopDev &hd)
 {
-    __shared__ unsigned long long sh64[33];
-    __shared__ int32_t sh32[33];
+    __shared__ unsigned long long sh64[kScanThreads / 32 + 1];
+    __shared__ int32_t sh32[kScanThreads / 32 + 1];
+    __shared__ uint32_t last_e[kScanThreads];
+    __shared__ int32_t s_tile;
+    __shared__ unsigned long long s_base;   // keys << 32 | members before this tile
+    __shared__ uint32_t s_tbase;            // tasks before this tile
     const CompactDev &cd = hd.cd;
     const int level = hd.h + 1;
     const int64_t NB = g.nb;
-    const int64_t per = (NB + blockDim.x - 1) / blockDim.x;
-    const int64_t a = min(NB, (int64_t)threadIdx.x * per), e = min(NB, a + per);
-    // pass 1: sums of this thread's buckets
-    unsigned long long loc = 0;   // keys << 32 | members
-    for (int64_t b = a; b < e; ++b) loc += ((unsigned long long)__ldcg(cd.kcnt + b) << 32) | __ldcg(cd.mcnt + b);
-    unsigned long long tot;
-    unsigned long long base = block_excl_scan(loc, sh64, &tot);
-    // pass 2: offsets and task flags
-    uint32_t ko = (uint32_t)(base >> 32), mo = (uint32_t)base;
-    int32_t nflag = 0;
-    uint32_t e_prev = 0;          // elements of bucket b - 1
-    if (a > 0 && a < e) e_prev = __ldcg(cd.kcnt + a - 1) + __ldcg(cd.mcnt + a - 1);
-    const int u_first = a < e ? type_of_bucket(g, a) : 0;
-    int u = u_first;
-    for (int64_t b = a; b < e; ++b) {
-        while (u + 1 < g.n_vt && b >= g.bbase[u + 1]) ++u;
-        const uint32_t kc = __ldcg(cd.kcnt + b), mc = __ldcg(cd.mcnt + b);
-        const uint32_t eb = kc + mc;
-        const uint32_t E = ko + mo;                       // elements before b
-        const bool flag = b == g.bbase[u] || eb > kBigBucket || e_prev > kBigBucket ||
-                          (E / kTaskElems) != ((E - e_prev) / kTaskElems) || g.compact_bitmap;
-        nflag += flag;
-        cd.kofs[b] = ko;
-        cd.mofs[b] = mo;
-        ko += kc;
-        mo += mc;
-        e_prev = eb;
+    const int ntiles = (int)((NB + kScanTile - 1) / kScanTile);
+    if (threadIdx.x == 0) s_tile = (int32_t)atomicAdd((uint32_t *)(hd.meta + kMetaKTicket + level), 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= ntiles) return;
+    const int64_t b0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanPer;
+    uint32_t kc[kScanPer], mc[kScanPer];
+    {
+        const uint4 *kp = reinterpret_cast<const uint4 *>(cd.kcnt + b0);
+        const uint4 *mp = reinterpret_cast<const uint4 *>(cd.mcnt + b0);
+        const uint4 k0 = __ldcg(kp), k1 = __ldcg(kp + 1), m0 = __ldcg(mp), m1 = __ldcg(mp + 1);
+        kc[0] = k0.x; kc[1] = k0.y; kc[2] = k0.z; kc[3] = k0.w; kc[4] = k1.x; kc[5] = k1.y; kc[6] = k1.z; kc[7] = k1.w;
+        mc[0] = m0.x; mc[1] = m0.y; mc[2] = m0.z; mc[3] = m0.w; mc[4] = m1.x; mc[5] = m1.y; mc[6] = m1.z; mc[7] = m1.w;
     }
-    int32_t ntask;
-    int32_t t = block_excl_scan(nflag, sh32, &ntask);
-    // pass 3: task starts (re-derive the flags), clear the member counts
-    e_prev = 0;
-    if (a > 0 && a < e) e_prev = __ldcg(cd.kcnt + a - 1) + __ldcg(cd.mcnt + a - 1);
-    u = u_first;
-    __syncthreads();   // kcnt of a - 1 read above before anyone clears mcnt (kcnt is not cleared here)
-    for (int64_t b = a; b < e; ++b) {
-        while (u + 1 < g.n_vt && b >= g.bbase[u + 1]) ++u;
-        const uint32_t eb = __ldcg(cd.kcnt + b) + __ldcg(cd.mcnt + b);
-        const uint32_t E = cd.kofs[b] + cd.mofs[b];
-        const bool flag = b == g.bbase[u] || eb > kBigBucket || e_prev > kBigBucket ||
-                          (E / kTaskElems) != ((E - e_prev) / kTaskElems) || g.compact_bitmap;
-        if (flag) cd.tstart[t++] = (uint32_t)b;
-        e_prev = eb;
+    // padded buckets (b >= NB) are zero (the launch memset covers the padding)
+    unsigned long long loc = 0;   // keys << 32 | members
+    uint32_t eloc = 0;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        loc += ((unsigned long long)kc[q] << 32) | mc[q];
+        eloc += kc[q] + mc[q];
+    }
+    last_e[threadIdx.x] = kc[kScanPer - 1] + mc[kScanPer - 1];
+    unsigned long long ttot;
+    const unsigned long long lbase = block_excl_scan(loc, sh64, &ttot);   // syncs: last_e visible
+    const uint32_t E0 = (uint32_t)(lbase >> 32) + (uint32_t)lbase;        // tile-local elements before b0
+    // task flags
+    uint32_t flags = 0;
+    {
+        uint32_t E = E0, e_prev = threadIdx.x ? last_e[threadIdx.x - 1] : 0u;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) {
+            const int64_t b = b0 + q;
+            const uint32_t eb = kc[q] + mc[q];
+            bool f = false;
+            if (b < NB) {
+                f = (threadIdx.x == 0 && q == 0) || eb > kBigBucket || e_prev > kBigBucket ||
+                    (E / kTaskElems) != ((E - e_prev) / kTaskElems) || g.compact_bitmap;
+                for (int u = 1; u < g.n_vt; ++u) f |= b == g.bbase[u];
+            }
+            flags |= (uint32_t)f << q;
+            E += eb;
+            e_prev = eb;
+        }
+    }
+    int32_t tflags;
+    const int32_t tl = block_excl_scan((int32_t)__popc(flags), sh32, &tflags);
+    // tile look-back: publish this tile's totals, add every earlier tile's
+    unsigned long long *tlb = cd.tlb + (size_t)level * 2 * kMaxScanTiles;
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) {
+            volatile unsigned long long *v = tlb;
+            v[kMaxScanTiles + tile] = tlb_word(0, (uint32_t)tflags);
+            __threadfence();
+            v[tile] = tlb_word((uint32_t)(ttot >> 32), (uint32_t)ttot);
+        }
+        __syncwarp();
+        unsigned long long kb = 0;
+        uint32_t tb = 0;
+        const int p = threadIdx.x;
+        if (p < tile) {
+            volatile unsigned long long *v = tlb;
+            unsigned long long w;
+            do {
+                w = v[p];
+            } while (!(w >> 63));
+            __threadfence();
+            const unsigned long long wt = v[kMaxScanTiles + p];
+            kb = (((w >> 32) & 0x7FFFFFFFull) << 32) | (w & 0xFFFFFFFFull);
+            tb = (uint32_t)wt;
+        }
+        kb = warp_sum(kb);
+        tb = warp_sum(tb);
+        if (threadIdx.x == 0) {
+            s_base = kb;
+            s_tbase = tb;
+        }
     }
     __syncthreads();
-    for (int64_t b = a; b < e; ++b) cd.mcnt[b] = 0u;
-    for (int i = threadIdx.x; i < ntask; i += blockDim.x) cd.lb[i] = 0ull;
-    if (threadIdx.x == 0) {
-        cd.tstart[ntask] = (uint32_t)NB;
-        cd.kofs[NB] = (uint32_t)(tot >> 32);
-        cd.mofs[NB] = (uint32_t)tot;
-        hd.meta[kMetaTasks + level] = ntask;
+    const unsigned long long base = s_base + lbase;
+    uint32_t ko = (uint32_t)(base >> 32), mo = (uint32_t)base;
+    uint32_t t = s_tbase + (uint32_t)tl;
+    const uint32_t ntask_before = s_tbase;
+    uint32_t kv[kScanPer], mv[kScanPer];
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        kv[q] = ko;
+        mv[q] = mo;
+        ko += kc[q];
+        mo += mc[q];
+        if (flags >> q & 1) cd.tstart[t++] = (uint32_t)(b0 + q);
     }
-    // |S_level[u]| defaults to |F_h[u]| (a type without new vertices); the last task of each
-    // type overwrites it
-    if (level > 0 && threadIdx.x < g.n_vt)
-        meta_nodes(hd.meta, level)[threadIdx.x] = meta_nodes(hd.meta, level - 1)[threadIdx.x];
+    uint4 *ko4 = reinterpret_cast<uint4 *>(cd.kofs + b0);
+    uint4 *mo4 = reinterpret_cast<uint4 *>(cd.mofs + b0);
+    uint4 *mz4 = reinterpret_cast<uint4 *>(cd.mcnt + b0);
+    ko4[0] = make_uint4(kv[0], kv[1], kv[2], kv[3]);
+    ko4[1] = make_uint4(kv[4], kv[5], kv[6], kv[7]);
+    mo4[0] = make_uint4(mv[0], mv[1], mv[2], mv[3]);
+    mo4[1] = make_uint4(mv[4], mv[5], mv[6], mv[7]);
+    mz4[0] = make_uint4(0u, 0u, 0u, 0u);
+    mz4[1] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < tflags; i += blockDim.x) cd.lb[ntask_before + i] = 0ull;
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const unsigned long long all = s_base + ttot;
+        const uint32_t ntask = s_tbase + (uint32_t)tflags;
+        cd.tstart[ntask] = (uint32_t)NB;
+        cd.kofs[NB] = (uint32_t)(all >> 32);
+        cd.mofs[NB] = (uint32_t)all;
+        hd.meta[kMetaTasks + level] = (int32_t)ntask;
+        // |S_level[u]| defaults to |F_h[u]| (a type without new vertices); the last task of
+        // each type overwrites it
+        if (level > 0)
+            for (int u = 0; u < g.n_vt; ++u) meta_nodes(hd.meta, level)[u] = meta_nodes(hd.meta, level - 1)[u];
+    }
 }
 
 // ============================================================================ scatter
@@ -266,40 +339,51 @@ __device__ __forceinline__ unsigned long long lb_word(unsigned long long st, uin
     return (st << 62) | ((unsigned long long)(glob & 0x7FFFFFFFu) << 31) | (typ & 0x7FFFFFFFu);
 }
 
-// Lane 0: publish task t's counts and find the exclusive prefixes.  glob = the task's
-// entries of the next level's member list that are not members yet (its new vertices; at
-// the seeds' level every distinct seed), counted over all earlier tasks; typ = its new
-// vertices to append to the type's node array, counted over the earlier tasks of the
-// same type.  Tasks are processed in ticket order, so every earlier task is held by a
-// running warp and publishes its aggregate before it waits itself.
+// Publish task t's counts and find the exclusive prefixes (whole warp; result in every
+// lane).  glob = the task's entries of the next level's member list that are not members
+// yet (its new vertices; at the seeds' level every distinct seed), summed over all earlier
+// tasks; typ = its new vertices to append to the type's node array, summed over the earlier
+// tasks of the same type.  Decoupled look-back with a window of 32 predecessors: lane i
+// reads task p = base - i; the window's aggregates are added down to the nearest inclusive
+// prefix.  Tasks are processed in ticket order, so every earlier task is held by a running
+// warp and publishes its aggregate before it waits itself.
 __device__ __forceinline__ void lookback(const GraphDev &g, const CompactDev &cd, int32_t t, int u, uint32_t glob,
                                          uint32_t typ, uint32_t &g_excl, uint32_t &t_excl)
 {
     volatile unsigned long long *lb = cd.lb;
-    lb[t] = lb_word(1, glob, typ);
-    uint32_t gs = 0, ts = 0;
-    bool same = true;
+    const int lane = lane_id();
+    if (lane == 0) lb[t] = lb_word(1, glob, typ);
     const uint32_t first_b = (uint32_t)g.bbase[u];
-    for (int32_t p = t - 1; p >= 0; --p) {
-        if (same && __ldcg(cd.tstart + p) < first_b) same = false;   // p belongs to an earlier type
-        unsigned long long w;
-        uint64_t t0 = 0;
-        for (uint32_t it = 0;; ++it) {   // bounded: a publication that never comes traps after ~2 s
-            w = lb[p];
-            if ((w >> 62) != 0) break;
-            if ((it & 1023) == 1023) {
-                uint64_t tn;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-                if (!t0) t0 = tn;
-                else if (tn - t0 > 2000000000ull) __trap();
+    uint32_t gs = 0, ts = 0;
+    for (int32_t top = t - 1; top >= 0; top -= 32) {
+        const int32_t p = top - lane;
+        unsigned long long w = 0;
+        bool same = false;
+        if (p >= 0) {
+            uint64_t t0 = 0;
+            for (uint32_t it = 0;; ++it) {   // bounded: a publication that never comes traps after ~2 s
+                w = lb[p];
+                if ((w >> 62) != 0) break;
+                if ((it & 1023) == 1023) {
+                    uint64_t tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                    if (!t0) t0 = tn;
+                    else if (tn - t0 > 2000000000ull) __trap();
+                }
             }
+            same = __ldcg(cd.tstart + p) >= first_b;   // p holds buckets of the same type
         }
-        gs += (uint32_t)(w >> 31) & 0x7FFFFFFFu;
-        if (same) ts += (uint32_t)w & 0x7FFFFFFFu;
-        if ((w >> 62) == 2) break;
+        const uint32_t incl = __ballot_sync(0xffffffffu, p >= 0 && (w >> 62) == 2);
+        const int lim = incl ? __ffs(incl) - 1 : 31;   // the nearest inclusive prefix ends the walk
+        const bool use = p >= 0 && lane <= lim;
+        gs += warp_sum(use ? (uint32_t)(w >> 31) & 0x7FFFFFFFu : 0u);
+        ts += warp_sum(use && same ? (uint32_t)w & 0x7FFFFFFFu : 0u);
+        if (incl) break;
     }
-    __threadfence();
-    lb[t] = lb_word(2, gs + glob, ts + typ);
+    if (lane == 0) {
+        __threadfence();
+        lb[t] = lb_word(2, gs + glob, ts + typ);
+    }
     g_excl = gs;
     t_excl = ts;
 }
@@ -338,38 +422,58 @@ __device__ void compact_sort(const GraphDev &g, const HopDev &hd, const LpDev &l
     const uint32_t *mg_in = level > 0 ? cd.mg[(level - 1) & 1] : nullptr;
     const int32_t *mp_in = level > 0 ? cd.mp[(level - 1) & 1] : nullptr;
     const int n = (int)(nk + nm);
-    // 1. elements in bucket order (per bucket: members, then keys)
+    // 1. keys (bucket order, any order inside a bucket) at e[0, nk), members (sorted) at
+    //    e[nk, n); bk = bucket relative to b0 (non-decreasing within each part)
     for (int i = lane; i < n; i += 32) {
         uint32_t gid, flag, pay;
-        int64_t b;
-        int idx;
         if (i < (int)nk) {
             gid = __ldcg(cd.keys + k0 + i);
             pay = __ldcg(cd.kidx + k0 + i);
             flag = hd.mode == kModeSeeds ? 0u : 1u;   // seeds: keys that carry their position
-            b = bucket_of(g, u, gid);
-            idx = i + (int)(__ldcg(cd.mofs + b + 1) - m0);
         } else {
-            const int j = i - (int)nk;
-            gid = __ldcg(mg_in + m0 + j);
-            pay = (uint32_t)__ldcg(mp_in + m0 + j);
+            gid = __ldcg(mg_in + m0 + (i - (int)nk));
+            pay = (uint32_t)__ldcg(mp_in + m0 + (i - (int)nk));
             flag = 0u;
-            b = bucket_of(g, u, gid);
-            idx = j + (int)(__ldcg(cd.kofs + b) - k0);
         }
-        sm.s.e[idx] = comp(gid, flag, pay);
-        sm.s.bk[idx] = (uint32_t)(b - b0);
+        sm.s.e[i] = comp(gid, flag, pay);
+        sm.s.bk[i] = (uint32_t)(bucket_of(g, u, gid) - b0);
     }
     __syncwarp();
-    // 2. rank inside the bucket (elements of a bucket are contiguous) -> sorted order
+    // 2. merged rank of every element: its rank among the keys (keys of earlier buckets +
+    //    the smaller keys of its bucket, <= kBigBucket of them) + among the members (binary
+    //    search: members are sorted) -- shared memory only
+    const int nki = (int)nk;
     for (int i = lane; i < n; i += 32) {
         const unsigned long long c = sm.s.e[i];
         const uint32_t bk = sm.s.bk[i];
-        int lo = i, hi = i + 1;
-        while (lo > 0 && sm.s.bk[lo - 1] == bk) --lo;   // buckets of runs hold <= kBigBucket elements
-        while (hi < n && sm.s.bk[hi] == bk) ++hi;
-        int r = lo;
-        for (int j = lo; j < hi; ++j) r += sm.s.e[j] < c;
+        // keys of bucket bk: [klo, khi)
+        int klo, khi;
+        if (i < nki) {
+            klo = i;
+            khi = i + 1;
+            while (klo > 0 && sm.s.bk[klo - 1] == bk) --klo;
+            while (khi < nki && sm.s.bk[khi] == bk) ++khi;
+        } else {   // lower bound of bk among the keys' buckets
+            int lo = 0, hi = nki;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sm.s.bk[mid] < bk) lo = mid + 1; else hi = mid;
+            }
+            klo = khi = lo;
+            while (khi < nki && sm.s.bk[khi] == bk) ++khi;
+        }
+        int r = klo;
+        for (int j = klo; j < khi; ++j) r += sm.s.e[j] < c;
+        if (i < nki) {   // + members below c (binary search; a key's own member entry sorts first)
+            int lo = nki, hi = n;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sm.s.e[mid] < c) lo = mid + 1; else hi = mid;
+            }
+            r += lo - nki;
+        } else {
+            r += i - nki;   // members below c: the sorted ones before it
+        }
         sm.s.srt[r] = c;
     }
     __syncwarp();
@@ -398,10 +502,7 @@ __device__ void compact_sort(const GraphDev &g, const HopDev &hd, const LpDev &l
     const uint32_t tot_new = tot & 0xFFFFu, tot_dist = tot >> 16;
     uint32_t g_excl = 0, t_excl = 0;
     // seeds: every distinct seed is new to the member list, none is appended (positions given)
-    if (lane == 0)
-        lookback(g, cd, t, u, hd.mode == kModeSeeds ? tot_dist : tot_new, tot_new, g_excl, t_excl);
-    g_excl = __shfl_sync(0xffffffffu, g_excl, 0);
-    t_excl = __shfl_sync(0xffffffffu, t_excl, 0);
+    lookback(g, cd, t, u, hd.mode == kModeSeeds ? tot_dist : tot_new, tot_new, g_excl, t_excl);
     const int32_t before = level_nodes_before(hd, u);
     // 4. heads: positions, new vertices, the merged member list of the next level
     for (int j = 0; j < R; ++j) {
@@ -498,9 +599,7 @@ __device__ void compact_bitmap(const GraphDev &g, const HopDev &hd, const LpDev 
     }
     const uint32_t tot_new = tot & 0xFFFFu, tot_all = tot >> 16;
     uint32_t g_excl = 0, t_excl = 0;
-    if (lane == 0) lookback(g, cd, t, u, tot_new, hd.mode == kModeSeeds ? 0u : tot_new, g_excl, t_excl);
-    g_excl = __shfl_sync(0xffffffffu, g_excl, 0);
-    t_excl = __shfl_sync(0xffffffffu, t_excl, 0);
+    lookback(g, cd, t, u, tot_new, hd.mode == kModeSeeds ? 0u : tot_new, g_excl, t_excl);
     __syncwarp();
     const int32_t before = level_nodes_before(hd, u);
     const uint32_t mo = m0 + g_excl;   // merged member list of the next level: this bucket's first slot

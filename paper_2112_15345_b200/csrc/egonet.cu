@@ -95,7 +95,7 @@ struct Plan {
     int64_t selq_items[EG_MAX_HOPS] = {};
     int32_t scan_blocks[EG_MAX_HOPS] = {}, max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
     // batch-local compaction state (compact.cuh): meta | kcnt | mcnt contiguous (one memset)
-    size_t o_partial = 0, o_kcnt = 0, o_mcnt = 0, o_kofs = 0, o_mofs = 0, o_tstart = 0, o_lb = 0, o_keys = 0,
+    size_t o_partial = 0, o_kcnt = 0, o_mcnt = 0, o_tlb = 0, o_kofs = 0, o_mofs = 0, o_tstart = 0, o_lb = 0, o_keys = 0,
            o_kidx = 0, o_mg[2] = {}, o_mp[2] = {}, zero_bytes = 0;
     int64_t cap_keys = 0, cap_members = 0;
     // link prediction (NEXT-3): n_cap = positives capacity; seeds <= n_cap * (2 + n_neg)
@@ -488,6 +488,8 @@ void build_gather_maps(eg_ctx *c)
 extern "C" {
 
 const char *eg_version(void) { return kVersion; }
+
+int64_t eg_counter_bytes(void) { return (int64_t)sizeof(int32_t) * kMetaSize; }
 
 const char *eg_last_error(const eg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
@@ -891,20 +893,24 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         off = align_up(off + std::max<size_t>(bytes, 1), 256);
         return o;
     };
-    // meta, kcnt, mcnt are contiguous: one memset per batch and launch clears them
+    // meta, kcnt, mcnt, the kscan tile look-back words are contiguous: one memset per batch
+    // and launch clears them.  Bucket arrays are padded to whole kscan tiles (16-B accesses).
     const int64_t NB = c->g.nb;
+    const int64_t NBp = (NB + kScanTile - 1) / kScanTile * kScanTile;
     p->o_meta = off;
     off += align_up(sizeof(int32_t) * kMetaSize, 16);
     p->o_kcnt = off;
-    off += align_up(sizeof(uint32_t) * NB, 16);
+    off += sizeof(uint32_t) * NBp;
     p->o_mcnt = off;
-    off += align_up(sizeof(uint32_t) * NB, 16);
+    off += sizeof(uint32_t) * NBp;
+    p->o_tlb = off;
+    off += sizeof(unsigned long long) * 2 * kMaxScanTiles * (L + 1);
     p->zero_bytes = off - p->o_meta;
     off = align_up(off, 256);
     p->o_dyn = take(sizeof(uint64_t) * kDyn);
     p->o_partial = take(sizeof(int32_t) * EG_MAX_REL * kMaxScanBlocks);
-    p->o_kofs = take(sizeof(uint32_t) * (NB + 1));
-    p->o_mofs = take(sizeof(uint32_t) * (NB + 1));
+    p->o_kofs = take(sizeof(uint32_t) * (NBp + 1));
+    p->o_mofs = take(sizeof(uint32_t) * (NBp + 1));
     p->o_tstart = take(sizeof(uint32_t) * (NB + 1));
     p->o_lb = take(sizeof(unsigned long long) * NB);
     p->o_seeds = take(sizeof(int64_t) * (lp ? 1 : n_cap));
@@ -1007,6 +1013,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         CompactDev &cd = hd.cd;
         cd.kcnt = (uint32_t *)(base + p->o_kcnt);
         cd.mcnt = (uint32_t *)(base + p->o_mcnt);
+        cd.tlb = (unsigned long long *)(base + p->o_tlb);
         cd.kofs = (uint32_t *)(base + p->o_kofs);
         cd.mofs = (uint32_t *)(base + p->o_mofs);
         cd.tstart = (uint32_t *)(base + p->o_tstart);

@@ -31,7 +31,7 @@ ABI_SYMBOLS = [
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
     "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer", "eg_set_feature_replica",
-    "eg_gather_path",
+    "eg_gather_path", "eg_counter_bytes",
 ]
 
 EG_FEATURES = 1
@@ -128,6 +128,7 @@ def lib(build_if_missing: bool = True):
         P = c.POINTER
         vp = c.c_void_p
         L.eg_version.restype = c.c_char_p
+        L.eg_counter_bytes.restype = c.c_int64
         L.eg_last_error.argtypes = [vp]
         L.eg_last_error.restype = c.c_char_p
         L.eg_create.argtypes = [c.c_int32, c.c_int32, c.c_int32, vp, P(vp)]
@@ -170,7 +171,7 @@ def lib(build_if_missing: bool = True):
         L.eg_batch_caps.argtypes = [c.c_int32, vp, c.c_int32, vp, vp, vp, vp, c.c_int64, c.c_int32, vp, vp, vp]
         for name in ABI_SYMBOLS:
             if name not in ("eg_version", "eg_last_error", "eg_blocks_n_hops", "eg_blocks_n_inputs",
-                            "eg_kernel_launches", "eg_trace_get"):
+                            "eg_kernel_launches", "eg_trace_get", "eg_counter_bytes"):
                 getattr(L, name).restype = c.c_int
         _lib = L
     return _lib
@@ -178,6 +179,11 @@ def lib(build_if_missing: bool = True):
 
 def version() -> str:
     return lib().eg_version().decode()
+
+
+def counter_bytes() -> int:
+    """Bytes of the per-batch counters read back to the host after every launch."""
+    return int(lib().eg_counter_bytes())
 
 
 def range_bounds(n: int, world: int) -> np.ndarray:
