@@ -69,8 +69,7 @@ def parse():
     ap.add_argument("--depth", type=int, default=None,
                     help="launches in flight per GPU (pipeline lanes); default 4")
     ap.add_argument("--bundle", type=int, default=None,
-                    help="mini-batches per launch (bundled kernels); default 16 (8 for C5, whose per-batch "
-                         "state is ~1 GB: 48 states + a 98 GB shard would not fit 180 GB at N = 2)")
+                    help="mini-batches per launch (bundled kernels); default 16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--diag-no-gather", action="store_true",
                     help="DIAGNOSTIC ONLY (not a bench line): sampling + compaction without the gather")
@@ -81,13 +80,12 @@ def parse():
                          "(default 8 for C4/C5, 16 otherwise; 0 = none)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     a = ap.parse_args()
-    # pipeline shape (profiles/r01/shape/): 4 lanes x bundles of 16 measured best
-    # once the count/scan block floor made sampling cheaper; C5 keeps 4 x 8 for memory
-    big = a.config.startswith("C5")
+    # pipeline shape: 4 lanes x bundles of 16 (since the compaction state is
+    # batch-sized, round 2, C5 fits this shape too)
     if a.depth is None:
         a.depth = 4
     if a.bundle is None:
-        a.bundle = 8 if big else 16
+        a.bundle = 16
     if a.replicate not in ("auto", "none"):
         a.replicate = [int(x) for x in a.replicate.split(",") if x != ""]
     return a

@@ -1,7 +1,7 @@
 // batch.cu -- the sampling + compaction of a bundle of mini-batches, one kernel per phase.
 //
 //   seed split | kscan scatter compact (level 0) |
-//   for h: count | scan | select + copy + tiny | kscan scatter compact (level h+1)
+//   for h: count | select + copy + tiny | kscan scatter compact (level h+1)
 //
 // Every phase kernel runs with grid.y = the batch of the bundle (each batch has its own
 // HopDev / compaction state), so B mini-batches cost about what one does: at batch ~1k
@@ -56,18 +56,11 @@ __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev 
     phase_seed_split(g, bd->seedh[blockIdx.y], bd->seeds[blockIdx.y]);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_count(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kCountThreads) k_count(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 4 + 8 * h);
-    phase_count(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
-}
-
-__global__ void __launch_bounds__(kBatchThreads) k_scan(const __grid_constant__ GraphDev g,
-                                                        const BatchDev *__restrict__ bd, int h)
-{
-    stamp(bd, 5 + 8 * h);
-    phase_scan(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x);
+    phase_count(g, bd->hop[blockIdx.y][h]);
 }
 
 #ifndef EG_SELECT_MIN_BLOCKS
@@ -110,15 +103,28 @@ __global__ void __launch_bounds__(kBatchThreads) k_scatter(const __grid_constant
     phase_scatter(g, hop_of(bd, h), bd->lpd[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_compact(const __grid_constant__ GraphDev g,
-                                                           const BatchDev *__restrict__ bd, int h)
+__global__ void __launch_bounds__(kBatchThreads) k_compact_count(const __grid_constant__ GraphDev g,
+                                                                 const BatchDev *__restrict__ bd, int h)
 {
     __shared__ CompactSmem sm[kBatchWarps];
     stamp(bd, 3 + 8 * (h + 1));
-    phase_compact(g, hop_of(bd, h), bd->lpd[blockIdx.y], sm);
+    phase_compact_count(g, hop_of(bd, h), sm, blockIdx.x, gridDim.x);
 }
 
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks, int B,
+__global__ void __launch_bounds__(kScanThreads) k_tscan(const __grid_constant__ GraphDev g,
+                                                        const BatchDev *__restrict__ bd, int h)
+{
+    phase_tscan(g, hop_of(bd, h));
+}
+
+__global__ void __launch_bounds__(kBatchThreads) k_compact_emit(const __grid_constant__ GraphDev g,
+                                                                const BatchDev *__restrict__ bd, int h)
+{
+    __shared__ CompactSmem sm[kBatchWarps];
+    phase_compact_emit(g, hop_of(bd, h), bd->lpd[blockIdx.y], sm, blockIdx.x, gridDim.x);
+}
+
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *count_tiles, int B,
                  cudaStream_t s, const Fork &fk, bool serial, bool lp)
 {
     // blocks per batch: about one wave of the chip in total
@@ -128,8 +134,10 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
     auto compaction = [&](int h) {   // level h + 1
         k_kscan<<<dim3((g.nb + kScanTile - 1) / kScanTile, B), kScanThreads, 0, s>>>(g, bd_dev, h);
         k_scatter<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_compact<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        nk += 3;
+        k_compact_count<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        k_tscan<<<dim3((g.nb + kScanTile - 1) / kScanTile, B), kScanThreads, 0, s>>>(g, bd_dev, h);
+        k_compact_emit<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        nk += 5;
     };
     if (lp) {   // link prediction: targets -> endpoint keys -> seeds + pairs
         k_lp_mark<<<dim3(per, B), kBatchThreads, 0, s>>>(g, bd_dev);
@@ -139,9 +147,8 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
     ++nk;
     compaction(-1);
     for (int h = 0; h < n_hops; ++h) {
-        const int wide = scan_blocks[h] * g.n_rel;   // count / scan: one block per virtual block
-        k_count<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
-        k_scan<<<dim3(wide, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
+        const int cb = count_tiles[h] < per ? count_tiles[h] : per;   // count: blocks take tiles by ticket
+        k_count<<<dim3(cb, B), kCountThreads, 0, s>>>(g, bd_dev, h);
         // selections and full-neighbourhood copies write disjoint slots: two graph branches
         // (EG_TRACE=1 serialises them so that each gets its own phase stamp)
         if (serial) {
@@ -157,7 +164,7 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
             k_select<<<dim3(samp, B), kBatchThreads, 0, s>>>(g, bd_dev, h);
             cudaStreamWaitEvent(s, fk.join, 0);
         }
-        nk += 5;
+        nk += 4;
         compaction(h);
     }
     return nk;

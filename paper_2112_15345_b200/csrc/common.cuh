@@ -13,25 +13,17 @@ constexpr int kSMs = 148;                 // B200
 // Compaction buckets (compact.cuh): each vertex type's id range is cut into fine buckets of
 // 2^bshift consecutive gids, bshift in [kMinBucketShift, kMaxBucketShift] chosen at load so
 // that a graph has at most ~2^16 buckets (C4: 2^11 gids, 54k buckets).  A bucket's bitmap is
-// 2^bshift / 32 words, at most 16 per lane of a warp.
+// 2^bshift / 32 words, at most 8 per lane of a warp.
 constexpr int kMinBucketShift = 10;
-constexpr int kMaxBucketShift = 14;
+constexpr int kMaxBucketShift = 13;
 constexpr int64_t kMaxBuckets = (int64_t)1 << 17;
 constexpr int kScanTile = 4096;                                   // buckets per kscan CTA (512 threads x 8)
 constexpr int kMaxScanTiles = (int)(kMaxBuckets / kScanTile);     // 32: one warp looks back over all
-// Virtual blocks per relation in the two-phase count / scan: per hop, one per
-// kScanItemsPerBlock frontier-capacity items, within [kMinScanBlocks, kMaxScanBlocks].
-// (Measured, profiles/r01/diag/scan_blocks_ab*.txt: a floor of 64 left most threads of
-// the hop-0 blocks idle -- 1024 seeds over 64 blocks per relation -- and 8 is C2 +8 %.)
-#ifndef EG_MIN_SCAN_BLOCKS
-#define EG_MIN_SCAN_BLOCKS 8
-#endif
-constexpr int kMinScanBlocks = EG_MIN_SCAN_BLOCKS;
-#ifndef EG_SCAN_ITEMS_PER_BLOCK
-#define EG_SCAN_ITEMS_PER_BLOCK 4096
-#endif
-constexpr int64_t kScanItemsPerBlock = EG_SCAN_ITEMS_PER_BLOCK;
-constexpr int kMaxScanBlocks = 1024;
+// Count tiles (single pass with a decoupled look-back per relation): kCountThreads threads
+// x kCountItems consecutive dst items each.
+constexpr int kCountThreads = 256;
+constexpr int kCountItems = 4;
+constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
 constexpr int kTinyD = 64;                // selections with d <= this: 8 lanes per item (phase_tiny)
@@ -90,7 +82,9 @@ constexpr int kMetaHeavyQ = kMetaHeavy + EG_MAX_HOPS;            // heavy tasks 
 constexpr int kMetaHeavyNext = kMetaHeavyQ + EG_MAX_HOPS;        // dynamic fetch counter per hop
 constexpr int kMetaTiny = kMetaHeavyNext + EG_MAX_HOPS;         // tiny selection items per hop
 constexpr int kMetaTinyNext = kMetaTiny + EG_MAX_HOPS;            // dynamic fetch counter per hop
-constexpr int kMetaTasks = kMetaTinyNext + EG_MAX_HOPS;           // compaction tasks per level (0..L)
+constexpr int kMetaCopy = kMetaTinyNext + EG_MAX_HOPS;            // full-neighbourhood items per hop
+constexpr int kMetaCntTicket = kMetaCopy + EG_MAX_HOPS;           // count tile tickets per hop
+constexpr int kMetaTasks = kMetaCntTicket + EG_MAX_HOPS;          // compaction tasks per level (0..L)
 constexpr int kMetaTicket = kMetaTasks + EG_MAX_HOPS + 1;         // compaction task tickets per level
 constexpr int kMetaKTicket = kMetaTicket + EG_MAX_HOPS + 1;       // kscan tile tickets per level
 constexpr int kMetaErr = kMetaKTicket + EG_MAX_HOPS + 1;
@@ -123,16 +117,28 @@ enum : int32_t { kModeHop = 0, kModeSeeds = 1, kModeLp = 2 };
 // Batch-local compaction state (one per batch; sized by the batch's caps, not by the graph).
 struct CompactDev {
     uint32_t *kcnt;                  // [nb, padded to kScanTile] keys per bucket (counted by the
-                                     // marking kernels, counted back to 0 by the scatter)
+                                     // marking kernels, cleared by kscan)
     uint32_t *mcnt;                  // [same] members per bucket for the next level (zeroed by kscan)
-    unsigned long long *tlb;         // [levels][2][kMaxScanTiles] kscan tile look-back words (zeroed per launch)
+    unsigned long long *tlb;         // [levels][3][kMaxScanTiles] kscan / tscan tile look-back words (zeroed per launch)
+    uint32_t *tnew;                  // [nb] per task: new entries of the member list, then their exclusive prefix
+    int32_t *ftask;                  // [EG_MAX_VT] first task of each vertex type
     uint32_t *kofs, *mofs;           // [nb + 1] exclusive prefixes of kcnt / mcnt
+    uint32_t *kcur;                  // [nb] scatter cursors: end of each bucket's keys in elems
     uint32_t *tstart;                // [nb + 1] first bucket of each compaction task
-    unsigned long long *lb;          // [nb] decoupled look-back words of the tasks
-    uint32_t *keys, *kidx;           // [cap_keys] keys (gids) in bucket order + payload
+    unsigned long long *elems;       // [cap_elems] the level's members + keys, bucket by bucket (compact.cuh)
     uint32_t *mg[2];                 // members (gids of the batch so far) sorted by gid, ping-pong by level
     int32_t *mp[2];                  // their positions in their type's node array
-    int32_t cap_keys;
+    int32_t cap_elems;
+};
+
+// A dst item of a hop, as the count phase hands it to the sampling kernels (queues of
+// full-neighbourhood copies and of selections): everything they need in one 24-B record.
+struct QEntry {
+    int64_t ib;      // (owner << 56) | CSC row start in the owner's shard
+    int32_t pos0;    // its first output slot in the block (= block indptr)
+    int32_t d;       // in-degree
+    int32_t v;       // gid of the dst (Philox counter words)
+    int32_t r;       // relation
 };
 
 // Everything a hop's kernels touch.
@@ -145,19 +151,18 @@ struct HopDev {
     int64_t *eids[EG_MAX_REL];
     uint32_t *src[EG_MAX_REL];       // sampled src gids (scratch)
     int32_t *meta;                   // batch counters
-    int32_t *partial;                // scan scratch [EG_MAX_REL][scan_blocks]
-    int32_t scan_blocks;             // virtual blocks per relation (count / scan)
+
     int32_t max_heavy;               // heavy item slots
     int32_t max_heavy_tasks;         // heavy task slots
     CompactDev cd;                   // the batch's compaction state
     int32_t mode;                    // compaction mode of the level this hop produces (kMode*)
     int32_t last;                    // 1: the last level (no member list for a next level)
-    int64_t *ibase[EG_MAX_REL];      // per dst item: (owner << 56) | CSC row start (from count)
-    int32_t *ideg[EG_MAX_REL];       // per dst item: in-degree d
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
-    uint64_t *selq;                  // items that need a selection: (r << 32) | i; tiny ones from the top
-    int32_t selq_cap;                // slots of selq
-    uint64_t *heavy_items;           // [max_heavy] (r << 32) | i
+    QEntry *selq;                    // items that need a selection (d > k); tiny ones (d <= 64) from the top
+    QEntry *copyq;                   // full-neighbourhood items (0 < d <= k, or k = -1)
+    int32_t selq_cap;                // slots of selq (= of copyq)
+    unsigned long long *clb;         // count tiles' look-back words (zeroed per launch)
+    QEntry *heavy_items;             // [max_heavy]
     uint32_t *heavy_cnt;             // [max_heavy] candidates found
     uint32_t *heavy_done;            // [max_heavy] finished tasks
     uint64_t *heavy_cand;            // [max_heavy][kHeavyCap] (key << 32) | j
@@ -270,6 +275,24 @@ __device__ __forceinline__ void philox4x32_10(uint32_t &c0, uint32_t &c1, uint32
         k1 += 0xBB67AE85u;
     }
 }
+
+// ------------------------------------------------------------------ spin guard
+
+// Call once per iteration of a spin-wait on another CTA's publication: after ~2 s the
+// kernel traps (an error the host reports) instead of hanging the GPU.
+struct SpinGuard {
+    uint32_t it = 0;
+    uint64_t t0 = 0;
+    __device__ __forceinline__ void step()
+    {
+        if ((++it & 1023) == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (!t0) t0 = t;
+            else if (t - t0 > 2000000000ull) __trap();
+        }
+    }
+};
 
 // ------------------------------------------------------------------ memory helpers
 

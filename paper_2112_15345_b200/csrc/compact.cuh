@@ -15,16 +15,18 @@
 //   kscan    one CTA per batch: prefixes kofs / mofs of the key and member counts, and the
 //            compaction TASKS: runs of consecutive buckets of one type holding < 256
 //            elements, or a single bucket with more ("big")
-//   scatter  each key -> keys[kofs[b] + (--kcnt[b])], with its payload (edge / seed slot)
-//   compact  a warp per task (dynamic tickets, in task order):
+//   scatter  each key -> elems[--kcur[b]] with its payload (edge / seed slot); each member
+//            of the previous level -> its bucket's member run
+//   count    a warp per task:
 //              sort path (runs): the task's keys and members (the batch's vertices so far,
-//              kept sorted by gid with their positions) go to shared memory in bucket order,
-//              each element is ranked inside its bucket, duplicates collapse to group heads;
+//              kept sorted by gid with their positions) go to shared memory, each element is
+//              ranked (inside its bucket among the keys, by binary search among the members),
+//              duplicates collapse to group heads; the sorted elements go to a scratch;
 //              bitmap path (big buckets): a 2^bshift-bit bitmap per warp in shared memory;
-//            the number of new vertices of the task -> decoupled look-back over the tasks
-//            (global and per-type prefixes in one word) -> the new vertices' positions; then
-//            new vertices are appended to their type's node array (in gid order), the merged
-//            member list of the next level is written, and every key is relabelled.
+//            -> the task's count of new vertices
+//   tscan    exclusive prefix of the task counts (tiles + a one-warp look-back over tiles)
+//   emit     a warp per task: new vertices appended to their type's node array (in gid
+//            order), the merged member list of the next level written, every key relabelled.
 //
 // Every step reads and writes batch-sized arrays that stay in L2; the old form (a gid ->
 // position map and bitmaps over all N vertices per batch in flight) paid a 32-B DRAM sector
@@ -46,7 +48,6 @@ struct CompactSmem {
         struct {
             unsigned long long e[kSortCap];      // elements in bucket order
             unsigned long long srt[kSortCap];    // sorted
-            uint32_t bk[kSortCap];               // bucket of e[i], relative to the task's first
             int32_t pos[kSortCap];               // position of group heads (by sorted index)
         } s;
         struct {
@@ -64,6 +65,13 @@ struct CompactSmem {
 __device__ __forceinline__ unsigned long long comp(uint32_t gid, uint32_t flag, uint32_t pay)
 {
     return ((unsigned long long)gid << 32) | ((unsigned long long)flag << 31) | (pay & 0x7FFFFFFFu);
+}
+
+__device__ __forceinline__ int type_of_bucket_gid(const GraphDev &g, int64_t gid)
+{
+    int u = 0;
+    while (u + 1 < g.n_vt && gid >= g.off[u + 1]) ++u;
+    return u;
 }
 
 __device__ __forceinline__ int type_of_bucket(const GraphDev &g, int64_t b)
@@ -88,7 +96,7 @@ __device__ __forceinline__ int32_t level_nodes_before(const HopDev &hd, int u)
 // bucket b starts a task if it is its tile's or its type's first bucket, if it or its
 // predecessor is big (> kBigBucket elements), or if the tile's elements before it crossed a
 // multiple of kTaskElems since its predecessor.  Clears mcnt (the compaction counts the
-// next level's members into it) and the tasks' look-back words.
+// next level's members into it); records each type's first task (ftask).
 constexpr int kScanThreads = 512;
 constexpr int kScanPer = kScanTile / kScanThreads;   // 8
 static_assert(kScanPer == 8, "two 16-B loads per array and thread");
@@ -98,7 +106,7 @@ __device__ __forceinline__ unsigned long long tlb_word(uint32_t hi, uint32_t lo)
     return (1ull << 63) | ((unsigned long long)(hi & 0x7FFFFFFFu) << 32) | lo;
 }
 
-__device__ void phase_kscan(const GraphDev &g, const HopDev &hd)
+__device__ __forceinline__ void phase_kscan(const GraphDev &g, const HopDev &hd)
 {
     __shared__ unsigned long long sh64[kScanThreads / 32 + 1];
     __shared__ int32_t sh32[kScanThreads / 32 + 1];
@@ -157,7 +165,7 @@ __device__ void phase_kscan(const GraphDev &g, const HopDev &hd)
     int32_t tflags;
     const int32_t tl = block_excl_scan((int32_t)__popc(flags), sh32, &tflags);
     // tile look-back: publish this tile's totals, add every earlier tile's
-    unsigned long long *tlb = cd.tlb + (size_t)level * 2 * kMaxScanTiles;
+    unsigned long long *tlb = cd.tlb + (size_t)level * 3 * kMaxScanTiles;
     if (threadIdx.x < 32) {
         if (threadIdx.x == 0) {
             volatile unsigned long long *v = tlb;
@@ -172,8 +180,10 @@ __device__ void phase_kscan(const GraphDev &g, const HopDev &hd)
         if (p < tile) {
             volatile unsigned long long *v = tlb;
             unsigned long long w;
+            SpinGuard sg;
             do {
                 w = v[p];
+                sg.step();
             } while (!(w >> 63));
             __threadfence();
             const unsigned long long wt = v[kMaxScanTiles + p];
@@ -191,26 +201,35 @@ __device__ void phase_kscan(const GraphDev &g, const HopDev &hd)
     const unsigned long long base = s_base + lbase;
     uint32_t ko = (uint32_t)(base >> 32), mo = (uint32_t)base;
     uint32_t t = s_tbase + (uint32_t)tl;
-    const uint32_t ntask_before = s_tbase;
-    uint32_t kv[kScanPer], mv[kScanPer];
+    uint32_t kv[kScanPer], mv[kScanPer], cv[kScanPer];
 #pragma unroll
     for (int q = 0; q < kScanPer; ++q) {
         kv[q] = ko;
         mv[q] = mo;
         ko += kc[q];
         mo += mc[q];
-        if (flags >> q & 1) cd.tstart[t++] = (uint32_t)(b0 + q);
+        cv[q] = ko + mo;   // end of bucket b's keys in the element array: the scatter's cursor
+        if (flags >> q & 1) {
+            for (int u = 0; u < g.n_vt; ++u)
+                if (b0 + q == g.bbase[u]) cd.ftask[u] = (int32_t)t;   // the type's first task
+            cd.tstart[t++] = (uint32_t)(b0 + q);
+        }
     }
     uint4 *ko4 = reinterpret_cast<uint4 *>(cd.kofs + b0);
     uint4 *mo4 = reinterpret_cast<uint4 *>(cd.mofs + b0);
     uint4 *mz4 = reinterpret_cast<uint4 *>(cd.mcnt + b0);
+    uint4 *kz4 = reinterpret_cast<uint4 *>(cd.kcnt + b0);
+    uint4 *cu4 = reinterpret_cast<uint4 *>(cd.kcur + b0);
     ko4[0] = make_uint4(kv[0], kv[1], kv[2], kv[3]);
     ko4[1] = make_uint4(kv[4], kv[5], kv[6], kv[7]);
     mo4[0] = make_uint4(mv[0], mv[1], mv[2], mv[3]);
     mo4[1] = make_uint4(mv[4], mv[5], mv[6], mv[7]);
-    mz4[0] = make_uint4(0u, 0u, 0u, 0u);
+    cu4[0] = make_uint4(cv[0], cv[1], cv[2], cv[3]);
+    cu4[1] = make_uint4(cv[4], cv[5], cv[6], cv[7]);
+    mz4[0] = make_uint4(0u, 0u, 0u, 0u);   // counted again by the compaction (next level's members)
     mz4[1] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = threadIdx.x; i < tflags; i += blockDim.x) cd.lb[ntask_before + i] = 0ull;
+    kz4[0] = make_uint4(0u, 0u, 0u, 0u);   // counted again by the next hop's sampling
+    kz4[1] = make_uint4(0u, 0u, 0u, 0u);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         const unsigned long long all = s_base + ttot;
         const uint32_t ntask = s_tbase + (uint32_t)tflags;
@@ -294,13 +313,79 @@ __device__ __forceinline__ int64_t level_keys(const GraphDev &g, const HopDev &h
     return n * (2 + lp.n_neg);
 }
 
-__device__ void phase_scatter(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
+// The level's elements in ONE array, bucket by bucket: for bucket b, its members (sorted,
+// copied in order) at [kofs[b] + mofs[b], kofs[b] + mofs[b + 1]), then its keys (any order)
+// up to kofs[b + 1] + mofs[b + 1].  Composite elements (comp): gid, flag (0 member or seed,
+// 1 key), payload (a member's position, a key's slot).
+__device__ __forceinline__ void phase_scatter(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
 {
     int64_t cum[EG_MAX_REL + 1];
     const int64_t n = level_keys(g, hd, lp, cum);
     const CompactDev &cd = hd.cd;
     const int64_t stride = (int64_t)nb * blockDim.x;
-    constexpr int U = 4;   // independent key -> slot chains per thread
+    constexpr int U = 4;   // independent element -> slot chains per thread
+    // pointers hoisted into registers (HopDev lives in global memory; the stores below could
+    // alias it as far as the compiler knows)
+    const uint32_t *const kofs = cd.kofs;
+    const uint32_t *const mofs = cd.mofs;
+    uint32_t *const kcur = cd.kcur;   // per bucket: the end of its keys, counted down (kscan)
+    unsigned long long *const el = cd.elems;
+    const uint32_t cap = (uint32_t)cd.cap_elems;
+    const uint32_t kflag = hd.mode == kModeSeeds ? 0u : 1u;   // seeds: keys that carry their position
+    const int level = hd.h + 1;
+    // members of the previous level (sorted by gid): member j of bucket b -> kofs[b] + j
+    if (level > 0) {
+        const uint32_t nm = __ldcg(mofs + g.nb);
+        const uint32_t *const mg = cd.mg[(level - 1) & 1];
+        const int32_t *const mp = cd.mp[(level - 1) & 1];
+        for (int64_t j0 = (int64_t)bid * blockDim.x + threadIdx.x; j0 < nm; j0 += U * stride) {
+            uint32_t gid[U];
+            int32_t pos[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int64_t j = j0 + q * stride;
+                gid[q] = j < nm ? __ldcs(mg + j) : 0u;
+                pos[q] = j < nm ? __ldcs(mp + j) : 0;
+            }
+            uint32_t slot[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int64_t j = j0 + q * stride;
+                if (j < nm) slot[q] = __ldcg(kofs + bucket_of(g, type_of_bucket_gid(g, gid[q]), gid[q])) + (uint32_t)j;
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (j0 + q * stride < nm) el[slot[q]] = comp(gid[q], 0u, (uint32_t)pos[q]);
+        }
+    }
+    if (hd.mode == kModeHop && g.n_rel == 1) {   // homogeneous hop (C3, C4): no relation lookup
+        const uint32_t *const src = hd.src[0];
+        const int64_t bb = g.bbase[g.rel[0].src_vt];
+        const uint32_t goff = (uint32_t)g.off[g.rel[0].src_vt];
+        const int sh = g.bshift;
+        for (int64_t i0 = (int64_t)bid * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+            uint32_t gid[U], slot[U];
+            int64_t b[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int64_t i = i0 + q * stride;
+                gid[q] = i < n ? __ldcs(src + i) : goff;
+                b[q] = bb + ((gid[q] - goff) >> sh);
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (i0 + q * stride < n) slot[q] = atomicSub(kcur + b[q], 1u) - 1u;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int64_t i = i0 + q * stride;
+                if (i < n) {
+                    if (slot[q] < cap) el[slot[q]] = comp(gid[q], kflag, (uint32_t)i);
+                    else atomicOr(hd.meta + kMetaErr, kErrCapacity);
+                }
+            }
+        }
+        return;
+    }
     for (int64_t i0 = (int64_t)bid * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
         uint32_t gid[U], pay[U];
         int64_t b[U];
@@ -315,78 +400,27 @@ __device__ void phase_scatter(const GraphDev &g, const HopDev &hd, const LpDev &
         uint32_t slot[U];
 #pragma unroll
         for (int q = 0; q < U; ++q)
-            if (ok[q]) slot[q] = __ldcg(cd.kofs + b[q]) + atomicSub(cd.kcnt + b[q], 1u) - 1u;
+            if (ok[q]) slot[q] = atomicSub(kcur + b[q], 1u) - 1u;
 #pragma unroll
         for (int q = 0; q < U; ++q)
             if (ok[q]) {
-                if (slot[q] < (uint32_t)cd.cap_keys) {
-                    cd.keys[slot[q]] = gid[q];
-                    cd.kidx[slot[q]] = pay[q];
-                } else {
-                    atomicOr(hd.meta + kMetaErr, kErrCapacity);
-                }
+                if (slot[q] < cap) el[slot[q]] = comp(gid[q], kflag, pay[q]);
+                else atomicOr(hd.meta + kMetaErr, kErrCapacity);
             }
     }
 }
 
 // ============================================================================ compact
 
-// Decoupled look-back word: status (bits 63..62: 1 aggregate, 2 inclusive prefix), the
-// count over all earlier tasks (bits 61..31) and over the earlier tasks of the same type
-// (bits 30..0).
-__device__ __forceinline__ unsigned long long lb_word(unsigned long long st, uint32_t glob, uint32_t typ)
-{
-    return (st << 62) | ((unsigned long long)(glob & 0x7FFFFFFFu) << 31) | (typ & 0x7FFFFFFFu);
-}
-
-// Publish task t's counts and find the exclusive prefixes (whole warp; result in every
-// lane).  glob = the task's entries of the next level's member list that are not members
-// yet (its new vertices; at the seeds' level every distinct seed), summed over all earlier
-// tasks; typ = its new vertices to append to the type's node array, summed over the earlier
-// tasks of the same type.  Decoupled look-back with a window of 32 predecessors: lane i
-// reads task p = base - i; the window's aggregates are added down to the nearest inclusive
-// prefix.  Tasks are processed in ticket order, so every earlier task is held by a running
-// warp and publishes its aggregate before it waits itself.
-__device__ __forceinline__ void lookback(const GraphDev &g, const CompactDev &cd, int32_t t, int u, uint32_t glob,
-                                         uint32_t typ, uint32_t &g_excl, uint32_t &t_excl)
-{
-    volatile unsigned long long *lb = cd.lb;
-    const int lane = lane_id();
-    if (lane == 0) lb[t] = lb_word(1, glob, typ);
-    const uint32_t first_b = (uint32_t)g.bbase[u];
-    uint32_t gs = 0, ts = 0;
-    for (int32_t top = t - 1; top >= 0; top -= 32) {
-        const int32_t p = top - lane;
-        unsigned long long w = 0;
-        bool same = false;
-        if (p >= 0) {
-            uint64_t t0 = 0;
-            for (uint32_t it = 0;; ++it) {   // bounded: a publication that never comes traps after ~2 s
-                w = lb[p];
-                if ((w >> 62) != 0) break;
-                if ((it & 1023) == 1023) {
-                    uint64_t tn;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-                    if (!t0) t0 = tn;
-                    else if (tn - t0 > 2000000000ull) __trap();
-                }
-            }
-            same = __ldcg(cd.tstart + p) >= first_b;   // p holds buckets of the same type
-        }
-        const uint32_t incl = __ballot_sync(0xffffffffu, p >= 0 && (w >> 62) == 2);
-        const int lim = incl ? __ffs(incl) - 1 : 31;   // the nearest inclusive prefix ends the walk
-        const bool use = p >= 0 && lane <= lim;
-        gs += warp_sum(use ? (uint32_t)(w >> 31) & 0x7FFFFFFFu : 0u);
-        ts += warp_sum(use && same ? (uint32_t)w & 0x7FFFFFFFu : 0u);
-        if (incl) break;
-    }
-    if (lane == 0) {
-        __threadfence();
-        lb[t] = lb_word(2, gs + glob, ts + typ);
-    }
-    g_excl = gs;
-    t_excl = ts;
-}
+// Two passes over the tasks with a scan of their counts in between (no task waits for
+// another: a decoupled look-back over thousands of tiny concurrent tasks walked back over
+// every task in flight, measured 121 us for C4's level 3).
+//   compact_count  per task: its elements sorted in place (sort path) or put in a bitmap
+//                  (big buckets) -> tnew[t] = entries of the next level's member list that
+//                  are not members yet (new vertices; at the seeds' level every distinct seed)
+//   tscan          tnew -> exclusive prefix G (in place), per batch
+//   compact_emit   per task: new vertices at before[u] + G(t) - G(first task of u) + rank,
+//                  the merged member list at m0 + G(t) + rank, every key relabelled
 
 // Relabelled output of key (slot pay) at position pos.
 __device__ __forceinline__ void key_out(const GraphDev &g, const HopDev &hd, const LpDev &lp, const int64_t *cum,
@@ -412,172 +446,176 @@ __device__ __forceinline__ void emit_node(const HopDev &hd, int u, int32_t pos, 
         atomicOr(hd.meta + kMetaErr, kErrCapacity);
 }
 
-// Sort path: a run of buckets [b0, b1) with n = nk + nm <= kSortCap elements.
-__device__ void compact_sort(const GraphDev &g, const HopDev &hd, const LpDev &lp, const int64_t *cum, CompactSmem &sm,
-                             int32_t t, int u, int64_t b0, uint32_t k0, uint32_t nk, uint32_t m0, uint32_t nm)
+struct TaskRange {
+    int64_t b0, b1;
+    uint32_t e0, n;          // the task's elements: elems[e0, e0 + n)
+    uint32_t m0;             // members before the task (= its first slot of the member list - G)
+    uint32_t km, nm, nk;     // bitmap path (single bucket): members at [e0, e0 + nm), keys after
+    int u;
+    bool bitmap;
+};
+
+__device__ __forceinline__ TaskRange task_range(const GraphDev &g, const CompactDev &cd, int32_t t)
 {
-    const CompactDev &cd = hd.cd;
+    TaskRange r;
+    r.b0 = __ldcg(cd.tstart + t);
+    r.b1 = __ldcg(cd.tstart + t + 1);
+    const uint32_t k0 = __ldcg(cd.kofs + r.b0), k1 = __ldcg(cd.kofs + r.b1);
+    r.m0 = __ldcg(cd.mofs + r.b0);
+    const uint32_t m1 = __ldcg(cd.mofs + r.b1);
+    r.e0 = k0 + r.m0;
+    r.n = (k1 - k0) + (m1 - r.m0);
+    r.nm = m1 - r.m0;
+    r.nk = k1 - k0;
+    r.u = type_of_bucket(g, r.b0);
+    r.bitmap = r.b1 - r.b0 == 1 && (r.n > (uint32_t)kBigBucket || g.compact_bitmap);
+    return r;
+}
+
+// ---------------------------------------------------------------------------- sort path
+
+// A run of buckets with n <= kSortCap elements (bucket by bucket: members sorted, then keys)
+// -> sm.s.srt sorted by composite.  Blocked layout: lane owns elements [R lane, R lane + R);
+// an element's bucket segment comes from segmented scans over the lanes (no search), its
+// rank from the elements of its segment (<= kBigBucket of them).
+__device__ __forceinline__ void sort_build(const GraphDev &g, const HopDev &hd, CompactSmem &sm, const TaskRange &T)
+{
     const int lane = lane_id();
-    const int level = hd.h + 1;
-    const uint32_t *mg_in = level > 0 ? cd.mg[(level - 1) & 1] : nullptr;
-    const int32_t *mp_in = level > 0 ? cd.mp[(level - 1) & 1] : nullptr;
-    const int n = (int)(nk + nm);
-    // 1. keys (bucket order, any order inside a bucket) at e[0, nk), members (sorted) at
-    //    e[nk, n); bk = bucket relative to b0 (non-decreasing within each part)
-    for (int i = lane; i < n; i += 32) {
-        uint32_t gid, flag, pay;
-        if (i < (int)nk) {
-            gid = __ldcg(cd.keys + k0 + i);
-            pay = __ldcg(cd.kidx + k0 + i);
-            flag = hd.mode == kModeSeeds ? 0u : 1u;   // seeds: keys that carry their position
-        } else {
-            gid = __ldcg(mg_in + m0 + (i - (int)nk));
-            pay = (uint32_t)__ldcg(mp_in + m0 + (i - (int)nk));
-            flag = 0u;
-        }
-        sm.s.e[i] = comp(gid, flag, pay);
-        sm.s.bk[i] = (uint32_t)(bucket_of(g, u, gid) - b0);
-    }
-    __syncwarp();
-    // 2. merged rank of every element: its rank among the keys (keys of earlier buckets +
-    //    the smaller keys of its bucket, <= kBigBucket of them) + among the members (binary
-    //    search: members are sorted) -- shared memory only
-    const int nki = (int)nk;
-    for (int i = lane; i < n; i += 32) {
-        const unsigned long long c = sm.s.e[i];
-        const uint32_t bk = sm.s.bk[i];
-        // keys of bucket bk: [klo, khi)
-        int klo, khi;
-        if (i < nki) {
-            klo = i;
-            khi = i + 1;
-            while (klo > 0 && sm.s.bk[klo - 1] == bk) --klo;
-            while (khi < nki && sm.s.bk[khi] == bk) ++khi;
-        } else {   // lower bound of bk among the keys' buckets
-            int lo = 0, hi = nki;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (sm.s.bk[mid] < bk) lo = mid + 1; else hi = mid;
-            }
-            klo = khi = lo;
-            while (khi < nki && sm.s.bk[khi] == bk) ++khi;
-        }
-        int r = klo;
-        for (int j = klo; j < khi; ++j) r += sm.s.e[j] < c;
-        if (i < nki) {   // + members below c (binary search; a key's own member entry sorts first)
-            int lo = nki, hi = n;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (sm.s.e[mid] < c) lo = mid + 1; else hi = mid;
-            }
-            r += lo - nki;
-        } else {
-            r += i - nki;   // members below c: the sorted ones before it
-        }
-        sm.s.srt[r] = c;
-    }
-    __syncwarp();
-    // 3. group heads; blocked layout: lane owns sorted elements [R lane, R lane + R)
+    const int n = (int)T.n;
+    const unsigned long long *const el = hd.cd.elems + T.e0;
     const int R = (n + 31) >> 5;
-    uint32_t newm = 0, headm = 0, keym = 0;
-    int last_head = -1;   // sorted index of the last head at or before this lane's elements
-    for (int j = 0; j < R; ++j) {
+    const int64_t goff = g.off[T.u];
+    const int sh = g.bshift;
+    unsigned long long c[kSortCap / 32];
+#pragma unroll
+    for (int j = 0; j < kSortCap / 32; ++j) {
         const int i = lane * R + j;
-        if (i >= n) break;
-        const unsigned long long c = sm.s.srt[i];
-        const bool head = i == 0 || (uint32_t)(sm.s.srt[i - 1] >> 32) != (uint32_t)(c >> 32);
-        const bool key = (c >> 31) & 1;
-        if (head) {
-            headm |= 1u << j;
-            last_head = i;
-            if (key) newm |= 1u << j;
-        }
-        if (key) keym |= 1u << j;
-        if (hd.mode == kModeSeeds && !head) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+        c[j] = j < R && i < n ? __ldcg(el + i) : ~0ull;
     }
-    const uint32_t cnt = ((uint32_t)__popc(headm) << 16) | (uint32_t)__popc(newm);   // n <= 256: 16-bit fields
-    const uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    uint32_t d_rank = (incl - cnt) >> 16, n_rank = (incl - cnt) & 0xFFFFu;
-    const uint32_t tot_new = tot & 0xFFFFu, tot_dist = tot >> 16;
-    uint32_t g_excl = 0, t_excl = 0;
-    // seeds: every distinct seed is new to the member list, none is appended (positions given)
-    lookback(g, cd, t, u, hd.mode == kModeSeeds ? tot_dist : tot_new, tot_new, g_excl, t_excl);
-    const int32_t before = level_nodes_before(hd, u);
-    // 4. heads: positions, new vertices, the merged member list of the next level
-    for (int j = 0; j < R; ++j) {
-        if (!(headm >> j & 1)) continue;
+#pragma unroll
+    for (int j = 0; j < kSortCap / 32; ++j) {
         const int i = lane * R + j;
-        const unsigned long long c = sm.s.srt[i];
-        const uint32_t gid = (uint32_t)(c >> 32);
-        int32_t pos;
-        if (newm >> j & 1) {
-            pos = before + (int32_t)(t_excl + n_rank);
-            emit_node(hd, u, pos, gid);
-            ++n_rank;
-        } else {
-            pos = (int32_t)(c & 0x7FFFFFFFu);   // a member's position, or a seed's own
-        }
-        sm.s.pos[i] = pos;
-        if (!hd.last) {
-            const uint32_t o = m0 + g_excl + d_rank;
-            cd.mg[level & 1][o] = gid;
-            cd.mp[level & 1][o] = pos;
-            atomicAdd(cd.mcnt + bucket_of(g, u, gid), 1u);
-        }
-        ++d_rank;
+        if (j < R && i < n) sm.s.e[i] = c[j];
     }
-    // the last head before each lane's first element: exclusive max-scan of last_head over
-    // the lanes (segmented broadcast of the group heads' positions)
-    int lh = last_head;
+    // the bucket of the element before the lane's first one (segment starts)
+    uint32_t bprev = 0xFFFFFFFFu;
+    if (lane * R > 0 && lane * R < n) bprev = (uint32_t)((__ldcg(el + lane * R - 1) >> 32) - goff) >> sh;
+    __syncwarp();
+    // segment start (first element of the bucket) of each of the lane's elements: running
+    // within the lane + the last start of the lanes before (max-scan)
+    constexpr int RM = kSortCap / 32;
+    uint32_t startm = 0;   // bit j: element R lane + j starts a bucket segment
+#pragma unroll
+    for (int j = 0; j < RM; ++j) {
+        const int i = lane * R + j;
+        if (j < R && i < n) {
+            const uint32_t bk = (uint32_t)(((c[j] >> 32) - goff) >> sh);
+            if (bk != bprev) startm |= 1u << j;
+            bprev = bk;
+        }
+    }
+    const int last = startm ? lane * R + 31 - __clz(startm) : -1;
+    int lo_run = -1;
+    int ls = last;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, lh, o);
-        if (lane >= o) lh = max(lh, x);
+        const int x = __shfl_up_sync(0xffffffffu, ls, o);
+        if (lane >= o) ls = max(ls, x);
     }
-    int carry = __shfl_up_sync(0xffffffffu, lh, 1);
-    if (lane == 0) carry = -1;
-    __syncwarp();
-    if (hd.mode == kModeSeeds) return;   // seeds carry their positions: nothing to relabel
-    // 5. relabel every key with its group head's position
-    int hidx = carry;
-    for (int j = 0; j < R; ++j) {
+    lo_run = __shfl_up_sync(0xffffffffu, ls, 1);
+    if (lane == 0) lo_run = -1;
+    // segment end: the first start after the lane's elements (min-scan from the right)
+    int fs = startm ? lane * R + __ffs(startm) - 1 : n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_down_sync(0xffffffffu, fs, o);
+        if (lane + o < 32) fs = min(fs, x);
+    }
+    int hi_run = __shfl_down_sync(0xffffffffu, fs, 1);
+    if (lane == 31) hi_run = n;
+    // the lane's elements: segment [lo, hi): lo = the last start at or before it, hi = the
+    // first start after it (inside the lane, else from the lanes before / after)
+    int lo = lo_run;
+#pragma unroll
+    for (int j = 0; j < RM; ++j) {
         const int i = lane * R + j;
-        if (i >= n) break;
-        if (headm >> j & 1) hidx = i;
-        if (keym >> j & 1) {
-            const unsigned long long c = sm.s.srt[i];
-            key_out(g, hd, lp, cum, (uint32_t)(c & 0x7FFFFFFFu), sm.s.pos[hidx]);
+        if (j < R && i < n) {
+            if (startm >> j & 1) lo = i;
+            const uint32_t after = startm & ~((2u << j) - 1u);
+            const int hi = after ? lane * R + __ffs(after) - 1 : hi_run;
+            const unsigned long long x = c[j];
+            int r = lo;
+            for (int k = lo; k < hi; ++k) r += sm.s.e[k] < x;
+            sm.s.srt[r] = x;
         }
     }
     __syncwarp();
 }
 
-// Bitmap path: one bucket b (2^bshift gids from gid0) with any number of elements.
-__device__ void compact_bitmap(const GraphDev &g, const HopDev &hd, const LpDev &lp, const int64_t *cum,
-                               CompactSmem &sm, int32_t t, int u, int64_t b, uint32_t k0, uint32_t nk, uint32_t m0,
-                               uint32_t nm)
+// Group heads of sorted elements [0, n) in the blocked layout (lane owns [R lane, R lane + R)):
+// bit j of headm / newm / keym for element R lane + j.
+struct Heads {
+    int R;
+    uint32_t headm, newm, keym;
+    int last_head;   // sorted index of the last head among this lane's elements, or -1
+};
+
+__device__ __forceinline__ Heads sort_heads(const CompactSmem &sm, int n)
 {
-    const CompactDev &cd = hd.cd;
     const int lane = lane_id();
-    const int level = hd.h + 1;
-    const uint32_t *mg_in = level > 0 ? cd.mg[(level - 1) & 1] : nullptr;
-    const int32_t *mp_in = level > 0 ? cd.mp[(level - 1) & 1] : nullptr;
+    Heads H;
+    H.R = (n + 31) >> 5;
+    H.headm = H.newm = H.keym = 0;
+    H.last_head = -1;
+    for (int j = 0; j < H.R; ++j) {
+        const int i = lane * H.R + j;
+        if (i >= n) break;
+        const unsigned long long c = sm.s.srt[i];
+        const bool head = i == 0 || (uint32_t)(sm.s.srt[i - 1] >> 32) != (uint32_t)(c >> 32);
+        const bool key = (c >> 31) & 1;
+        if (head) {
+            H.headm |= 1u << j;
+            H.last_head = i;
+            if (key) H.newm |= 1u << j;
+        }
+        if (key) H.keym |= 1u << j;
+    }
+    return H;
+}
+
+// ---------------------------------------------------------------------------- bitmap path
+
+// One big bucket -> sm.b: key bits a, member bits m, per-word exclusive prefixes of
+// popc(a | m) (pa) and popc(a & ~m) (pn); returns (distinct << 16) | new.
+__device__ __forceinline__ uint32_t bitmap_build(const GraphDev &g, const HopDev &hd, CompactSmem &sm, const TaskRange &T,
+                                 bool check_dup)
+{
+    const int lane = lane_id();
     const int WL = 1 << (g.bshift - 10);   // words per lane (blocked: lane owns [WL lane, WL lane + WL))
-    const int64_t gid0 = g.off[u] + ((b - g.bbase[u]) << g.bshift);
+    const uint32_t gid0 = (uint32_t)(g.off[T.u] + ((T.b0 - g.bbase[T.u]) << g.bshift));
+    const unsigned long long *const el = hd.cd.elems + T.e0;
     for (int q = 0; q < WL; ++q) {
         sm.b.a[lane * WL + q] = 0u;
         sm.b.m[lane * WL + q] = 0u;
     }
     __syncwarp();
-    for (uint32_t i = lane; i < nm; i += 32) {
-        const uint32_t x = __ldcg(mg_in + m0 + i) - (uint32_t)gid0;
-        atomicOr(sm.b.m + (x >> 5), 1u << (x & 31));
-    }
-    for (uint32_t i = lane; i < nk; i += 32) {
-        const uint32_t x = __ldcg(cd.keys + k0 + i) - (uint32_t)gid0;
-        const uint32_t old = atomicOr(sm.b.a + (x >> 5), 1u << (x & 31));
-        if (hd.mode == kModeSeeds && (old >> (x & 31) & 1)) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+    // four loads in flight per lane before their shared-memory atomics; members first in el
+    for (uint32_t i0 = lane; i0 < T.n; i0 += 128) {
+        unsigned long long x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = i0 + 32 * q < T.n ? __ldcg(el + i0 + 32 * q) : 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t i = i0 + 32 * q;
+            if (i >= T.n) continue;
+            const uint32_t b = (uint32_t)(x[q] >> 32) - gid0;
+            if (i < T.nm) {
+                atomicOr(sm.b.m + (b >> 5), 1u << (b & 31));
+            } else {
+                const uint32_t old = atomicOr(sm.b.a + (b >> 5), 1u << (b & 31));
+                if (check_dup && (old >> (b & 31) & 1)) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+            }
+        }
     }
     __syncwarp();
     uint32_t ca = 0, cn = 0;
@@ -586,9 +624,8 @@ __device__ void compact_bitmap(const GraphDev &g, const HopDev &hd, const LpDev 
         ca += __popc(a | m);
         cn += __popc(a & ~m);
     }
-    const uint32_t cnt = (ca << 16) | cn;   // <= 4096 per bucket
+    const uint32_t cnt = (ca << 16) | cn;   // <= 2^14 per bucket
     const uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     uint32_t pa = (incl - cnt) >> 16, pn = (incl - cnt) & 0xFFFFu;
     for (int q = 0; q < WL; ++q) {
         const uint32_t a = sm.b.a[lane * WL + q], m = sm.b.m[lane * WL + q];
@@ -597,102 +634,274 @@ __device__ void compact_bitmap(const GraphDev &g, const HopDev &hd, const LpDev 
         pa += __popc(a | m);
         pn += __popc(a & ~m);
     }
-    const uint32_t tot_new = tot & 0xFFFFu, tot_all = tot >> 16;
-    uint32_t g_excl = 0, t_excl = 0;
-    lookback(g, cd, t, u, tot_new, hd.mode == kModeSeeds ? 0u : tot_new, g_excl, t_excl);
     __syncwarp();
-    const int32_t before = level_nodes_before(hd, u);
-    const uint32_t mo = m0 + g_excl;   // merged member list of the next level: this bucket's first slot
-    if (hd.mode == kModeSeeds) {
-        // the seeds carry their positions: each (unique) key writes its merged entry
-        if (!hd.last)
-            for (uint32_t i = lane; i < nk; i += 32) {
-                const uint32_t gid = __ldcg(cd.keys + k0 + i);
-                const uint32_t x = gid - (uint32_t)gid0;
-                const uint32_t w = x >> 5, low = (1u << (x & 31)) - 1u;
-                const uint32_t r = sm.b.pa[w] + __popc((sm.b.a[w] | sm.b.m[w]) & low);
-                cd.mg[level & 1][mo + r] = gid;
-                cd.mp[level & 1][mo + r] = (int32_t)__ldcg(cd.kidx + k0 + i);
-            }
-    } else {
-        for (int q = 0; q < WL; ++q) {
-            const int w = lane * WL + q;
-            const uint32_t a = sm.b.a[w], m = sm.b.m[w];
-            uint32_t all = a | m;
-            const uint32_t nw = a & ~m;
-            uint32_t r = sm.b.pa[w];
-            while (all) {
-                const int bit = __ffs(all) - 1;
-                all &= all - 1;
-                const uint32_t gid = (uint32_t)gid0 + (uint32_t)(32 * w + bit);
-                const uint32_t low = (1u << bit) - 1u;
-                int32_t pos;
-                if (nw >> bit & 1) {
-                    pos = before + (int32_t)(t_excl + sm.b.pn[w] + __popc(nw & low));
-                    emit_node(hd, u, pos, gid);
-                } else {
-                    pos = __ldcg(mp_in + m0 + (r - sm.b.pn[w] - __popc(nw & low)));
-                }
-                if (!hd.last) {
-                    cd.mg[level & 1][mo + r] = gid;
-                    cd.mp[level & 1][mo + r] = pos;
-                }
-                ++r;
-            }
-        }
-    }
-    if (!hd.last && lane == 0 && tot_all) atomicAdd(cd.mcnt + b, tot_all);
-    if (hd.mode == kModeSeeds) return;
-    // relabel every key
-    for (uint32_t i = lane; i < nk; i += 32) {
-        const uint32_t gid = __ldcg(cd.keys + k0 + i);
-        const uint32_t pay = __ldcg(cd.kidx + k0 + i);
-        const uint32_t x = gid - (uint32_t)gid0;
-        const uint32_t w = x >> 5, bit = x & 31, low = (1u << bit) - 1u;
-        const uint32_t a = sm.b.a[w], m = sm.b.m[w];
-        int32_t pos;
-        if (m >> bit & 1) {
-            const uint32_t mem_rank = (sm.b.pa[w] - sm.b.pn[w]) + __popc(m & low);
-            pos = __ldcg(mp_in + m0 + mem_rank);
-        } else {
-            pos = before + (int32_t)(t_excl + sm.b.pn[w] + __popc((a & ~m) & low));
-        }
-        key_out(g, hd, lp, cum, pay, pos);
-    }
-    __syncwarp();
+    return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-// A warp per task, in ticket order.  The last task of each type records |S_level[u]|.
-__device__ void phase_compact(const GraphDev &g, const HopDev &hd, const LpDev &lp, CompactSmem *smem)
+// ---------------------------------------------------------------------------- one task
+
+// Pass A of a task: its elements deduplicated -> the task's count of entries of the next
+// level's member list that are not members yet (new vertices; at the seeds' level every
+// distinct seed).  Sort-path tasks leave their elements sorted in place (elems).
+__device__ __forceinline__ uint32_t count_task(const GraphDev &g, const HopDev &hd, CompactSmem &sm,
+                                               const TaskRange &T)
+{
+    const int lane = lane_id();
+    const bool seeds = hd.mode == kModeSeeds;
+    if (T.bitmap) return bitmap_build(g, hd, sm, T, seeds) & 0xFFFFu;   // a & ~m (seeds: m = 0)
+    sort_build(g, hd, sm, T);
+    const int n = (int)T.n;
+    const Heads H = sort_heads(sm, n);
+    // seeds: every distinct seed counts (they are all new to the member list); a repeated
+    // gid is a duplicate seed
+    if (seeds && __popc(H.headm) != min(H.R, max(0, n - lane * H.R))) atomicOr(hd.meta + kMetaErr, kErrSeedDup);
+    unsigned long long *const el = hd.cd.elems + T.e0;   // sorted, in place
+    for (int i = lane; i < n; i += 32) el[i] = sm.s.srt[i];
+    __syncwarp();
+    return warp_sum((uint32_t)__popc(seeds ? H.headm : H.newm));
+}
+
+// Pass B of a task: G = new entries of the earlier tasks (all types), Gu = those before its
+// type's first task: new vertices at before[u] + G - Gu + rank, the merged member list at
+// m0 + G + rank, every key relabelled.  Returns the task's new vertices.
+__device__ __forceinline__ uint32_t emit_task(const GraphDev &g, const HopDev &hd, const LpDev &lp,
+                                              const int64_t *cum, CompactSmem &sm, const TaskRange &T, uint32_t G,
+                                              uint32_t Gu)
 {
     const CompactDev &cd = hd.cd;
     const int lane = lane_id();
+    const int level = hd.h + 1;
+    const int32_t *mp_in = level > 0 ? cd.mp[(level - 1) & 1] : nullptr;
+    uint32_t *const mg_out = cd.mg[level & 1];
+    int32_t *const mp_out = cd.mp[level & 1];
+    const bool seeds = hd.mode == kModeSeeds;
+        const int32_t before = level_nodes_before(hd, T.u);
+        const int32_t tbase = before + (int32_t)(G - Gu);              // position of the task's first new vertex
+        const uint32_t mo = T.m0 + G;                                  // its first entry of the member list
+        const unsigned long long *const el = cd.elems + T.e0;
+        uint32_t tot_new;
+        if (T.bitmap) {
+            const uint32_t tot = bitmap_build(g, hd, sm, T, false);
+            tot_new = tot & 0xFFFFu;
+            const int WL = 1 << (g.bshift - 10);
+            const uint32_t gid0 = (uint32_t)(g.off[T.u] + ((T.b0 - g.bbase[T.u]) << g.bshift));
+            if (seeds) {   // positions given by the keys
+                if (!hd.last)
+                    for (uint32_t i = lane; i < T.n; i += 32) {
+                        const unsigned long long c = __ldcg(el + i);
+                        const uint32_t gid = (uint32_t)(c >> 32), x = gid - gid0;
+                        const uint32_t w = x >> 5, low = (1u << (x & 31)) - 1u;
+                        const uint32_t r = sm.b.pa[w] + __popc((sm.b.a[w] | sm.b.m[w]) & low);
+                        mg_out[mo + r] = gid;
+                        mp_out[mo + r] = (int32_t)(c & 0x7FFFFFFFu);
+                    }
+            } else {
+                // new vertices: the bits of a & ~m, in gid order
+                for (int q = 0; q < WL; ++q) {
+                    const int w = lane * WL + q;
+                    const uint32_t a = sm.b.a[w], m = sm.b.m[w];
+                    uint32_t nwd = a & ~m;
+                    while (nwd) {
+                        const int bit = __ffs(nwd) - 1;
+                        nwd &= nwd - 1;
+                        const uint32_t low = (1u << bit) - 1u;
+                        const uint32_t gid = gid0 + (uint32_t)(32 * w + bit);
+                        const int32_t pos = tbase + (int32_t)(sm.b.pn[w] + __popc(a & ~m & low));
+                        emit_node(hd, T.u, pos, gid);
+                        if (!hd.last) {
+                            const uint32_t r = sm.b.pa[w] + __popc((a | m) & low);
+                            mg_out[mo + r] = gid;
+                            mp_out[mo + r] = pos;
+                        }
+                    }
+                }
+                // members (el[0, nm), sorted): copied to their merged slots
+                if (!hd.last)
+                    for (uint32_t i0 = lane; i0 < T.nm; i0 += 128) {
+                        unsigned long long cm[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) cm[q] = i0 + 32 * q < T.nm ? __ldcg(el + i0 + 32 * q) : 0ull;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (i0 + 32 * q < T.nm) {
+                                const uint32_t gid = (uint32_t)(cm[q] >> 32);
+                                const uint32_t x = gid - gid0, w = x >> 5, low = (1u << (x & 31)) - 1u;
+                                const uint32_t r = sm.b.pa[w] + __popc((sm.b.a[w] | sm.b.m[w]) & low);
+                                mg_out[mo + r] = gid;
+                                mp_out[mo + r] = (int32_t)(cm[q] & 0x7FFFFFFFu);
+                            }
+                    }
+            }
+            if (!hd.last && lane == 0 && (tot >> 16)) atomicAdd(cd.mcnt + T.b0, tot >> 16);
+            if (!seeds)
+                for (uint32_t i0 = T.nm + lane; i0 < T.n; i0 += 128) {   // relabel every key, 4 in flight per lane
+                    unsigned long long ck[4];
+                    int32_t pos[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ck[q] = i0 + 32 * q < T.n ? __ldcg(el + i0 + 32 * q) : ((unsigned long long)gid0 << 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t x = (uint32_t)(ck[q] >> 32) - gid0;
+                        const uint32_t w = x >> 5, bit = x & 31, low = (1u << bit) - 1u;
+                        const uint32_t a = sm.b.a[w], m = sm.b.m[w];
+                        if (m >> bit & 1)
+                            pos[q] = __ldcg(mp_in + T.m0 + (sm.b.pa[w] - sm.b.pn[w]) + __popc(m & low));
+                        else
+                            pos[q] = tbase + (int32_t)(sm.b.pn[w] + __popc((a & ~m) & low));
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (i0 + 32 * q < T.n) key_out(g, hd, lp, cum, (uint32_t)(ck[q] & 0x7FFFFFFFu), pos[q]);
+                }
+        } else {
+            const int n = (int)T.n;
+            unsigned long long v[kSortCap / 32];
+#pragma unroll
+            for (int j = 0; j < kSortCap / 32; ++j) v[j] = lane + 32 * j < n ? __ldcg(el + lane + 32 * j) : 0ull;
+#pragma unroll
+            for (int j = 0; j < kSortCap / 32; ++j)
+                if (lane + 32 * j < n) sm.s.srt[lane + 32 * j] = v[j];
+            __syncwarp();
+            const Heads H = sort_heads(sm, n);
+            const uint32_t cnt = ((uint32_t)__popc(H.headm) << 16) | (uint32_t)__popc(H.newm);   // n <= 256
+            const uint32_t incl = warp_incl_scan(cnt);
+            tot_new = __shfl_sync(0xffffffffu, incl, 31) & 0xFFFFu;
+            uint32_t d_rank = (incl - cnt) >> 16, n_rank = (incl - cnt) & 0xFFFFu;
+            for (int j = 0; j < H.R; ++j) {   // heads: positions, new vertices, the next member list
+                if (!(H.headm >> j & 1)) continue;
+                const int i = lane * H.R + j;
+                const unsigned long long c = sm.s.srt[i];
+                const uint32_t gid = (uint32_t)(c >> 32);
+                int32_t pos;
+                if (H.newm >> j & 1) {
+                    pos = tbase + (int32_t)n_rank;
+                    emit_node(hd, T.u, pos, gid);
+                    ++n_rank;
+                } else {
+                    pos = (int32_t)(c & 0x7FFFFFFFu);   // a member's position, or a seed's own
+                }
+                sm.s.pos[i] = pos;
+                if (!hd.last) {
+                    mg_out[mo + d_rank] = gid;
+                    mp_out[mo + d_rank] = pos;
+                    atomicAdd(cd.mcnt + bucket_of(g, T.u, gid), 1u);
+                }
+                ++d_rank;
+            }
+            // the last head before each lane's first element: exclusive max-scan over lanes
+            int lh = H.last_head;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, lh, o);
+                if (lane >= o) lh = max(lh, x);
+            }
+            int hidx = __shfl_up_sync(0xffffffffu, lh, 1);
+            if (lane == 0) hidx = -1;
+            __syncwarp();
+            if (!seeds)
+                for (int j = 0; j < H.R; ++j) {   // relabel every key with its group head's position
+                    const int i = lane * H.R + j;
+                    if (i >= n) break;
+                    if (H.headm >> j & 1) hidx = i;
+                    if (H.keym >> j & 1)
+                        key_out(g, hd, lp, cum, (uint32_t)(sm.s.srt[i] & 0x7FFFFFFFu), sm.s.pos[hidx]);
+                }
+        }
+    return tot_new;
+}
+
+// ---------------------------------------------------------------------------- the kernels
+
+// Pass A: a warp per task (static stride over the batch's tasks) -> tnew[t].
+__device__ __forceinline__ void phase_compact_count(const GraphDev &g, const HopDev &hd, CompactSmem *smem, int bid,
+                                                    int nb)
+{
+    const CompactDev &cd = hd.cd;
+    const int level = hd.h + 1;
+    CompactSmem &sm = smem[threadIdx.x >> 5];
+    const int32_t ntask = *(volatile int32_t *)(hd.meta + kMetaTasks + level);
+    const int32_t nw = nb * (blockDim.x >> 5);
+    for (int32_t t = bid * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask; t += nw) {
+        const TaskRange T = task_range(g, cd, t);
+        const uint32_t cnt = count_task(g, hd, sm, T);
+        if (lane_id() == 0) cd.tnew[t] = cnt;
+        __syncwarp();
+    }
+}
+
+// tnew -> exclusive prefix, in place (tiles of kScanTile tasks, one CTA of 512 threads
+// each, taken by ticket; one warp adds the totals of every earlier tile).
+__device__ __forceinline__ void phase_tscan(const GraphDev &g, const HopDev &hd)
+{
+    __shared__ uint32_t sh[kScanThreads / 32 + 1];
+    __shared__ int32_t s_tile;
+    __shared__ uint32_t s_base;
+    const CompactDev &cd = hd.cd;
+    const int level = hd.h + 1;
+    const int32_t ntask = *(volatile int32_t *)(hd.meta + kMetaTasks + level);
+    const int ntiles = (ntask + kScanTile - 1) / kScanTile;
+    if (threadIdx.x == 0) s_tile = (int32_t)atomicAdd((uint32_t *)(hd.meta + kMetaTicket + level), 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= ntiles) return;
+    const int64_t t0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanPer;
+    uint32_t v[kScanPer], loc = 0;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        v[q] = t0 + q < ntask ? __ldcg(cd.tnew + t0 + q) : 0u;
+        loc += v[q];
+    }
+    uint32_t ttot;
+    const uint32_t lbase = block_excl_scan(loc, sh, &ttot);
+    unsigned long long *tlb = cd.tlb + (size_t)level * 3 * kMaxScanTiles + 2 * kMaxScanTiles;
+    if (threadIdx.x < 32) {
+        volatile unsigned long long *w = tlb;
+        if (threadIdx.x == 0) w[tile] = (1ull << 63) | ttot;
+        uint32_t b = 0;
+        const int p = threadIdx.x;
+        if (p < tile) {
+            unsigned long long x;
+            SpinGuard sg;
+            do {
+                x = w[p];
+                sg.step();
+            } while (!(x >> 63));
+            b = (uint32_t)x;
+        }
+        b = warp_sum(b);
+        if (threadIdx.x == 0) s_base = b;
+    }
+    __syncthreads();
+    uint32_t run = s_base + lbase;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        if (t0 + q < ntask) cd.tnew[t0 + q] = run;
+        run += v[q];
+    }
+}
+
+// Pass B: a warp per task; the last task of each type records |S_level[u]|.
+__device__ __forceinline__ void phase_compact_emit(const GraphDev &g, const HopDev &hd, const LpDev &lp,
+                                                   CompactSmem *smem, int bid, int nb)
+{
+    const CompactDev &cd = hd.cd;
     const int level = hd.h + 1;
     CompactSmem &sm = smem[threadIdx.x >> 5];
     int64_t cum[EG_MAX_REL + 1];
     level_keys(g, hd, lp, cum);
     const int32_t ntask = *(volatile int32_t *)(hd.meta + kMetaTasks + level);
-    uint32_t *ticket = (uint32_t *)(hd.meta + kMetaTicket + level);
-    for (;;) {
-        int32_t t = 0;
-        if (lane == 0) t = (int32_t)atomicAdd(ticket, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= ntask) break;
-        const int64_t b0 = __ldcg(cd.tstart + t), b1 = __ldcg(cd.tstart + t + 1);
-        const uint32_t k0 = __ldcg(cd.kofs + b0), k1 = __ldcg(cd.kofs + b1);
-        const uint32_t m0 = __ldcg(cd.mofs + b0), m1 = __ldcg(cd.mofs + b1);
-        const int u = type_of_bucket(g, b0);
-        const uint32_t nk = k1 - k0, nm = m1 - m0;
-        if (b1 - b0 == 1 && (nk + nm > (uint32_t)kBigBucket || g.compact_bitmap))
-            compact_bitmap(g, hd, lp, cum, sm, t, u, b0, k0, nk, m0, nm);
-        else
-            compact_sort(g, hd, lp, cum, sm, t, u, b0, k0, nk, m0, nm);
-        // the last task of its type: |S_level[u]| = |F[u]| + new vertices of the type (its own
-        // inclusive look-back word; the seeds' sizes come from the seed split)
-        if (lane == 0 && b1 == g.bbase[u + 1] && hd.mode != kModeSeeds) {
-            const unsigned long long w = ((volatile unsigned long long *)cd.lb)[t];
-            meta_nodes(hd.meta, level)[u] = level_nodes_before(hd, u) + (int32_t)((uint32_t)w & 0x7FFFFFFFu);
-        }
+    const int32_t nw = nb * (blockDim.x >> 5);
+    const bool seeds = hd.mode == kModeSeeds;
+    for (int32_t t = bid * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask; t += nw) {
+        const TaskRange T = task_range(g, cd, t);
+        const uint32_t G = __ldcg(cd.tnew + t);                                    // earlier tasks' new entries
+        const uint32_t Gu = seeds ? 0u : __ldcg(cd.tnew + __ldcg(cd.ftask + T.u));  // ... before the type's first task
+        const uint32_t tot_new = emit_task(g, hd, lp, cum, sm, T, G, Gu);
+        // the last task of its type: |S_level[u]| = |F[u]| + the type's new vertices (the
+        // seeds' sizes come from the seed split)
+        if (lane_id() == 0 && T.b1 == g.bbase[T.u + 1] && !seeds)
+            meta_nodes(hd.meta, level)[T.u] = level_nodes_before(hd, T.u) + (int32_t)(G - Gu + tot_new);
+        __syncwarp();
     }
 }
 

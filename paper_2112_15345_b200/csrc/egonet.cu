@@ -71,7 +71,7 @@ struct Lane {
 // per (batch, hop): heavy items, their counters, candidate buffers and chunk tasks
 size_t heavy_bytes(int64_t mh, int64_t mt)
 {
-    return sizeof(uint64_t) * mh + 2 * sizeof(uint32_t) * mh + sizeof(uint64_t) * mh * kHeavyCap +
+    return sizeof(QEntry) * mh + 2 * sizeof(uint32_t) * mh + sizeof(uint64_t) * mh * kHeavyCap +
            sizeof(uint32_t) * mt;
 }
 
@@ -90,13 +90,15 @@ struct Plan {
     size_t o_meta = 0, o_dyn = 0, o_seeds = 0, stride = 0;
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_src[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ib[EG_MAX_HOPS][EG_MAX_REL] = {}, o_id[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_selq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
+           o_src[EG_MAX_HOPS][EG_MAX_REL] = {},
+           o_selq[EG_MAX_HOPS] = {}, o_copyq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
     int64_t selq_items[EG_MAX_HOPS] = {};
-    int32_t scan_blocks[EG_MAX_HOPS] = {}, max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
+    int32_t max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
     // batch-local compaction state (compact.cuh): meta | kcnt | mcnt contiguous (one memset)
-    size_t o_partial = 0, o_kcnt = 0, o_mcnt = 0, o_tlb = 0, o_kofs = 0, o_mofs = 0, o_tstart = 0, o_lb = 0, o_keys = 0,
-           o_kidx = 0, o_mg[2] = {}, o_mp[2] = {}, zero_bytes = 0;
+    size_t o_elems = 0, o_tnew = 0, o_ftask = 0, o_kcur = 0;
+    size_t o_clb[EG_MAX_HOPS] = {};
+    int32_t count_tiles[EG_MAX_HOPS] = {};
+    size_t o_kcnt = 0, o_mcnt = 0, o_tlb = 0, o_kofs = 0, o_mofs = 0, o_tstart = 0, o_mg[2] = {}, o_mp[2] = {}, zero_bytes = 0;
     int64_t cap_keys = 0, cap_members = 0;
     // link prediction (NEXT-3): n_cap = positives capacity; seeds <= n_cap * (2 + n_neg)
     bool lp = false;
@@ -904,15 +906,23 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
     p->o_mcnt = off;
     off += sizeof(uint32_t) * NBp;
     p->o_tlb = off;
-    off += sizeof(unsigned long long) * 2 * kMaxScanTiles * (L + 1);
+    off += sizeof(unsigned long long) * 3 * kMaxScanTiles * (L + 1);
+    for (int h = 0; h < L; ++h) {   // count tiles' look-back words
+        int64_t tiles = 0;
+        for (int r = 0; r < R; ++r) tiles += (p->capF[h][dst_vt[r]] + kCountTile - 1) / kCountTile;
+        p->count_tiles[h] = (int32_t)std::max<int64_t>(1, tiles);
+        p->o_clb[h] = off;
+        off += sizeof(unsigned long long) * p->count_tiles[h];
+    }
     p->zero_bytes = off - p->o_meta;
     off = align_up(off, 256);
     p->o_dyn = take(sizeof(uint64_t) * kDyn);
-    p->o_partial = take(sizeof(int32_t) * EG_MAX_REL * kMaxScanBlocks);
     p->o_kofs = take(sizeof(uint32_t) * (NBp + 1));
     p->o_mofs = take(sizeof(uint32_t) * (NBp + 1));
+    p->o_kcur = take(sizeof(uint32_t) * NBp);
     p->o_tstart = take(sizeof(uint32_t) * (NB + 1));
-    p->o_lb = take(sizeof(unsigned long long) * NB);
+    p->o_tnew = take(sizeof(uint32_t) * (NB + 1));
+    p->o_ftask = take(sizeof(int32_t) * EG_MAX_VT);
     p->o_seeds = take(sizeof(int64_t) * (lp ? 1 : n_cap));
     if (lp) {
         p->o_lp_src = take(sizeof(int64_t) * n_cap);
@@ -929,12 +939,11 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         p->cap_keys = std::max(p->cap_keys, e);
     }
     for (int u = 0; u < V; ++u) p->cap_members += p->capF[L][u];
-    if (p->cap_keys >= INT32_MAX || p->cap_members >= INT32_MAX) {
+    if (p->cap_keys + p->cap_members >= INT32_MAX) {
         delete p;
         return fail(c, EG_EINVAL, "batch exceeds 2^31 keys / vertices");
     }
-    p->o_keys = take(sizeof(uint32_t) * p->cap_keys);
-    p->o_kidx = take(sizeof(uint32_t) * p->cap_keys);
+    p->o_elems = take(sizeof(unsigned long long) * (p->cap_keys + p->cap_members));
     for (int i = 0; i < 2; ++i) {
         p->o_mg[i] = take(sizeof(uint32_t) * p->cap_members);
         p->o_mp[i] = take(sizeof(int32_t) * p->cap_members);
@@ -947,19 +956,14 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
             p->o_ix[h][r] = take(sizeof(int32_t) * p->capE[h][r]);
             p->o_ei[h][r] = take(sizeof(int64_t) * p->capE[h][r]);
             p->o_src[h][r] = take(sizeof(uint32_t) * p->capE[h][r]);
-            p->o_ib[h][r] = take(sizeof(int64_t) * nd);
-            p->o_id[h][r] = take(sizeof(int32_t) * nd);
         }
     for (int h = 0; h < L; ++h) {
         int64_t items = 0;
         for (int r = 0; r < R; ++r) items += p->capF[h][dst_vt[r]];
         p->selq_items[h] = items;
-        p->o_selq[h] = take(sizeof(uint64_t) * items);
-        // scan virtual blocks: ~one per 4096 items of the largest relation's frontier;
+        p->o_selq[h] = take(sizeof(QEntry) * items);
+        p->o_copyq[h] = take(sizeof(QEntry) * items);
         // heavy slots: one per 2048 frontier items beyond the first kMinHeavy
-        int64_t most = 0;
-        for (int r = 0; r < R; ++r) most = std::max<int64_t>(most, p->capF[h][dst_vt[r]]);
-        p->scan_blocks[h] = (int32_t)std::min<int64_t>(kMaxScanBlocks, std::max<int64_t>(kMinScanBlocks, (most + kScanItemsPerBlock - 1) / kScanItemsPerBlock));
         p->max_heavy[h] = (int32_t)std::min<int64_t>(65535, kMinHeavy + items / 2048);
         p->max_heavy_tasks[h] = (int32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)p->max_heavy[h] * kHeavyTasksPerItem);
         p->o_heavy[h] = take(heavy_bytes(p->max_heavy[h], p->max_heavy_tasks[h]));
@@ -1009,22 +1013,22 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
         HopDev hd{};
         hd.dyn = (const uint64_t *)(base + p->o_dyn);
         hd.meta = (int32_t *)(base + p->o_meta);
-        hd.partial = (int32_t *)(base + p->o_partial);
         CompactDev &cd = hd.cd;
         cd.kcnt = (uint32_t *)(base + p->o_kcnt);
         cd.mcnt = (uint32_t *)(base + p->o_mcnt);
         cd.tlb = (unsigned long long *)(base + p->o_tlb);
+        cd.elems = (unsigned long long *)(base + p->o_elems);
+        cd.tnew = (uint32_t *)(base + p->o_tnew);
+        cd.ftask = (int32_t *)(base + p->o_ftask);
         cd.kofs = (uint32_t *)(base + p->o_kofs);
         cd.mofs = (uint32_t *)(base + p->o_mofs);
+        cd.kcur = (uint32_t *)(base + p->o_kcur);
         cd.tstart = (uint32_t *)(base + p->o_tstart);
-        cd.lb = (unsigned long long *)(base + p->o_lb);
-        cd.keys = (uint32_t *)(base + p->o_keys);
-        cd.kidx = (uint32_t *)(base + p->o_kidx);
         for (int i = 0; i < 2; ++i) {
             cd.mg[i] = (uint32_t *)(base + p->o_mg[i]);
             cd.mp[i] = (int32_t *)(base + p->o_mp[i]);
         }
-        cd.cap_keys = (int32_t)p->cap_keys;
+        cd.cap_elems = (int32_t)(p->cap_keys + p->cap_members);
         for (int u = 0; u < V; ++u) {
             hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
             hd.cap_nodes[u] = (int32_t)p->capF[L][u];
@@ -1055,22 +1059,21 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
                 x.indices[r] = (int32_t *)(base + p->o_ix[h][r]);
                 x.eids[r] = (int64_t *)(base + p->o_ei[h][r]);
                 x.src[r] = (uint32_t *)(base + p->o_src[h][r]);
-                x.ibase[r] = (int64_t *)(base + p->o_ib[h][r]);
-                x.ideg[r] = (int32_t *)(base + p->o_id[h][r]);
             }
             x.mode = kModeHop;
             x.last = h == L - 1;
-            x.selq = (uint64_t *)(base + p->o_selq[h]);
+            x.selq = (QEntry *)(base + p->o_selq[h]);
+            x.copyq = (QEntry *)(base + p->o_copyq[h]);
             x.selq_cap = (int32_t)p->selq_items[h];
+            x.clb = (unsigned long long *)(base + p->o_clb[h]);
             char *hv = base + p->o_heavy[h];
-            x.heavy_items = (uint64_t *)hv;
+            x.heavy_items = (QEntry *)hv;
             const int64_t mh = p->max_heavy[h];
             x.max_heavy = p->max_heavy[h];
             x.max_heavy_tasks = p->max_heavy_tasks[h];
-            x.scan_blocks = p->scan_blocks[h];
-            x.heavy_cnt = (uint32_t *)(hv + sizeof(uint64_t) * mh);
+            x.heavy_cnt = (uint32_t *)(hv + sizeof(QEntry) * mh);
             x.heavy_done = x.heavy_cnt + mh;
-            x.heavy_cand = (uint64_t *)(hv + sizeof(uint64_t) * mh + 2 * sizeof(uint32_t) * mh);
+            x.heavy_cand = (uint64_t *)(hv + sizeof(QEntry) * mh + 2 * sizeof(uint32_t) * mh);
             x.heavyq = (uint32_t *)(x.heavy_cand + (size_t)mh * kHeavyCap);
             bd->hop[b][h] = x;
         }
@@ -1104,7 +1107,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     cudaMemset2DAsync(p->batch_base(sl->mem, 0) + p->o_meta, p->stride, 0, p->zero_bytes, B, cs);
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->scan_blocks, B, cs, c->fork, c->trace, p->lp);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->count_tiles, B, cs, c->fork, c->trace, p->lp);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {
@@ -1264,11 +1267,14 @@ void slot_finished(eg_ctx *c, Slot *sl)
         const uint64_t *st = reinterpret_cast<const uint64_t *>(sl->h_meta + kMetaStamps);
         std::vector<std::string> names = {"k.seed", "k.l0.kscan", "k.l0.scatter", "k.l0.compact"};
         for (int h = 0; h < sl->plan->n_hops; ++h)
-            for (const char *x : {"count", "scan", "select", "copy", "tiny", "kscan", "scatter", "compact"})
+            for (const char *x : {"count", "(unused)", "select", "copy", "tiny", "kscan", "scatter", "compact"})
                 names.push_back("k.h" + std::to_string(h) + "." + x);
-        for (size_t k = 0; k < names.size() && k + 1 < (size_t)kMaxStamps; ++k) {
-            if (!st[k + 1] || !st[k]) break;
-            trace_add(c, names[k], (double)(st[k + 1] - st[k]) * 1e-6);
+        for (size_t k = 0; k < names.size() && k < (size_t)kMaxStamps; ++k) {   // a stage runs until the next stamp
+            if (!st[k]) continue;
+            size_t k2 = k + 1;
+            while (k2 < names.size() && k2 < (size_t)kMaxStamps && !st[k2]) ++k2;
+            if (k2 >= names.size() || k2 >= (size_t)kMaxStamps) break;
+            trace_add(c, names[k], (double)(st[k2] - st[k]) * 1e-6);
         }
         for (size_t k = 1; k < sl->tev.size(); ++k) {
             float e = 0;

@@ -41,7 +41,7 @@ struct Fork {
 
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
 // returns the number of kernels.  lp: link-prediction batches (seeds from targets).
-int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *scan_blocks, int B,
+int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *count_tiles, int B,
                  cudaStream_t s, const Fork &fk, bool serial, bool lp);
 
 // TMA tensor maps of the feature tables the gather reads with cp.async.bulk.tensor

@@ -24,7 +24,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 // Seeds (caller order, mixed types) -> F_0[u] (stable per type); every placed seed is a
 // key of the level-0 compaction (compact.cuh, kModeSeeds: sorted member list, duplicate
 // check).  Flags out-of-range seeds.  One block.
-__device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds)
+__device__ __forceinline__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds)
 {
     // the caller's buffer when it is device-accessible, else the slot's staged copy
     const int64_t *__restrict__ seeds = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : slot_seeds;
@@ -87,122 +87,190 @@ __device__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int6
     __syncthreads();
 }
 
-// ============================================================================ count + scan
+// ============================================================================ count
 
-// Virtual blocks (r, b), b < hd.scan_blocks: count c for the dst items of chunk b of
-// F_h[t(r)] into the block indptr slots, record (owner, CSC row start) and d for
-// the sampler, enqueue the items that need a selection; per-chunk sums -> partial.
-__device__ void phase_count(const GraphDev &g, const HopDev &hd, int bid, int nb)
+// Single pass per hop: tiles of kCountTile consecutive dst items of one relation, taken by
+// ticket (relation-major).  Per item: c = min(d, k) (all d if k == -1 or d <= k) from the
+// owner's CSC row bounds; the tile's exclusive prefix comes from a decoupled look-back over
+// the relation's earlier tiles (window of 32), so the block indptr is final here and every
+// item that needs sampling is queued with its output slot: full neighbourhoods to copyq,
+// selections to selq (d > kTinyD from the bottom, the rest from the top), hubs as chunk
+// tasks.  The last tile of a relation writes indptr[n] and nnz(h, r).
+__device__ __forceinline__ unsigned long long clb_word(unsigned long long st, uint32_t v)
 {
-    __shared__ int32_t sh[33];
+    return (st << 62) | v;
+}
+
+__device__ __forceinline__ void phase_count(const GraphDev &g, const HopDev &hd)
+{
+    __shared__ int32_t sh[kCountThreads / 32 + 1];
+    __shared__ int32_t s_vt;
+    __shared__ int32_t s_excl;
     const int32_t *nF = meta_nodes(hd.meta, hd.h);
-    const int SB = hd.scan_blocks;
-    for (int vb = bid; vb < SB * g.n_rel; vb += nb) {
-        const int r = vb / SB, b = vb % SB;
+    int32_t cumT[EG_MAX_REL + 1];
+    cumT[0] = 0;
+    for (int r = 0; r < g.n_rel; ++r) cumT[r + 1] = cumT[r] + (nF[g.rel[r].dst_vt] + kCountTile - 1) / kCountTile;
+    const int lane = lane_id();
+    uint32_t *const selc = (uint32_t *)(hd.meta + kMetaSel + hd.h);
+    uint32_t *const tinyc = (uint32_t *)(hd.meta + kMetaTiny + hd.h);
+    uint32_t *const copyc = (uint32_t *)(hd.meta + kMetaCopy + hd.h);
+    QEntry *const selq = hd.selq;
+    QEntry *const copyq = hd.copyq;
+    volatile unsigned long long *const clb = hd.clb;
+    for (;;) {
+        if (threadIdx.x == 0) s_vt = (int32_t)atomicAdd((uint32_t *)(hd.meta + kMetaCntTicket + hd.h), 1u);
+        __syncthreads();
+        const int32_t vt = s_vt;
+        if (vt >= cumT[g.n_rel]) break;
+        int r = 0;
+        while (vt >= cumT[r + 1]) ++r;
+        const int32_t tile = vt - cumT[r];
         const RelDev &R = g.rel[r];
         const int t = R.dst_vt;
         const int k = hd.fanout[r];
         const int64_t n = nF[t];
-        const int64_t chunk = (n + SB - 1) / SB;
-        const int64_t lo = b * chunk, hi = min(n, lo + chunk);
+        const int64_t i0 = (int64_t)tile * kCountTile + (int64_t)threadIdx.x * kCountItems;
         const int64_t *const nodes = hd.nodes[t];
-        int64_t *const ibase = hd.ibase[r];
-        int32_t *const ideg = hd.ideg[r];
-        int32_t *const bip = hd.indptr[r];
-        uint64_t *const selq = hd.selq;
-        uint32_t *const selc = (uint32_t *)(hd.meta + kMetaSel + hd.h);
-        uint32_t *const tinyc = (uint32_t *)(hd.meta + kMetaTiny + hd.h);
-        int32_t sum = 0;
-        for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {   // block-uniform trip count
-            const int64_t i = t0 + threadIdx.x;
-            bool sel = false;
-            int64_t dd = 0;
-            if (i < hi) {
-                int32_t c = 0;
-                if (k != 0) {
-                    const int64_t tid = nodes[i] - g.off[t];
-                    const int p = owner_of(g, t, tid);
-                    const int64_t x = tid - g.bounds[t][p];
-                    const int64_t *ip = R.indptr[p];
-                    const int64_t b0 = ip[x], d = ip[x + 1] - b0;
-                    const bool all = (k < 0 || d <= k);
-                    c = (int32_t)(all ? d : k);
-                    sel = !all;
-                    dd = d;
-                    ibase[i] = ((int64_t)p << 56) | b0;
-                    ideg[i] = (int32_t)d;
-                }
-                bip[i] = c;
-                sum += c;
+        int32_t c[kCountItems], d[kCountItems], v[kCountItems];
+        int64_t ib[kCountItems];
+        int64_t b0[kCountItems];
+        const int64_t *ip[kCountItems];
+#pragma unroll
+        for (int q = 0; q < kCountItems; ++q) {
+            c[q] = d[q] = v[q] = 0;
+            ib[q] = 0;
+            ip[q] = nullptr;
+            const int64_t i = i0 + q;
+            if (i < n && k != 0) {
+                const int64_t gid = nodes[i];
+                const int64_t tid = gid - g.off[t];
+                const int p = owner_of(g, t, tid);
+                const int64_t x = tid - g.bounds[t][p];
+                ip[q] = R.indptr[p] + x;
+                v[q] = (int32_t)gid;
+                ib[q] = (int64_t)p << 56;
             }
+        }
+#pragma unroll
+        for (int q = 0; q < kCountItems; ++q)
+            if (ip[q]) {
+                b0[q] = ip[q][0];
+                d[q] = (int32_t)(ip[q][1] - b0[q]);
+            }
+        int32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < kCountItems; ++q)
+            if (ip[q]) {
+                ib[q] |= b0[q];
+                c[q] = (k < 0 || d[q] <= k) ? d[q] : k;
+                sum += c[q];
+            }
+        int32_t ttot;
+        const int32_t texcl = block_excl_scan(sum, sh, &ttot);
+        // decoupled look-back over the relation's earlier tiles (warp 0)
+        if (threadIdx.x < 32) {
+            if (lane == 0) clb[vt] = clb_word(tile == 0 ? 2 : 1, (uint32_t)ttot);
+            uint32_t excl = 0;
+            for (int32_t top = vt - 1; top >= cumT[r]; top -= 32) {
+                const int32_t p = top - lane;
+                unsigned long long w = 0;
+                if (p >= cumT[r]) {
+                    SpinGuard sg;
+                    do {
+                        w = clb[p];
+                        sg.step();
+                    } while ((w >> 62) == 0);
+                }
+                const uint32_t incl = __ballot_sync(0xffffffffu, p >= cumT[r] && (w >> 62) == 2);
+                const int lim = incl ? __ffs(incl) - 1 : 31;
+                excl += warp_sum(p >= cumT[r] && lane <= lim ? (uint32_t)w : 0u);
+                if (incl) break;
+            }
+            if (lane == 0) {
+                if (tile > 0) {
+                    __threadfence();
+                    clb[vt] = clb_word(2, excl + (uint32_t)ttot);
+                }
+                s_excl = (int32_t)excl;
+            }
+        }
+        __syncthreads();
+        int32_t pos = s_excl + texcl;
+        int32_t *const bip = hd.indptr[r];
+        // classify the lane's items; queue slots are reserved once per warp for all of them
+        // (three independent atomics instead of one dependent round trip per item and queue)
+        QEntry e[kCountItems];
+        uint32_t mc[kCountItems], ms[kCountItems], mt[kCountItems];
+        uint32_t nc = 0, ns = 0, ntn = 0;
+#pragma unroll
+        for (int q = 0; q < kCountItems; ++q) {
+            const int64_t i = i0 + q;
+            const bool ok = i < n;
+            e[q].ib = ib[q];
+            e[q].pos0 = pos;
+            e[q].d = d[q];
+            e[q].v = v[q];
+            e[q].r = r;
+            if (ok) bip[i] = pos;
+            const bool all = ok && c[q] > 0 && c[q] == d[q];
+            bool sel = ok && c[q] > 0 && c[q] < d[q];
             // heavy items (d > kHeavyD): split into tasks of kHeavyChunk keys for several warps
-            if (sel && k <= kHeavyMaxK && ideg[i] > kHeavyD) {
-                const int64_t d = ideg[i];
-                const uint32_t nch = (uint32_t)((d + kHeavyChunk - 1) / kHeavyChunk);
+            if (sel && k <= kHeavyMaxK && d[q] > kHeavyD) {
+                const uint32_t nch = (uint32_t)((d[q] + kHeavyChunk - 1) / kHeavyChunk);
                 const uint32_t hs = atomicAdd((uint32_t *)(hd.meta + kMetaHeavy + hd.h), 1u);
                 if (hs < (uint32_t)hd.max_heavy) {
                     const uint32_t t0 = atomicAdd((uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), nch);
                     if (t0 + nch <= (uint32_t)hd.max_heavy_tasks) {
-                        hd.heavy_items[hs] = ((uint64_t)r << 32) | (uint64_t)i;
+                        hd.heavy_items[hs] = e[q];
                         hd.heavy_cnt[hs] = 0;
                         hd.heavy_done[hs] = 0;
-                        for (uint32_t c = 0; c < nch; ++c) hd.heavyq[t0 + c] = (hs << 16) | c;
+                        for (uint32_t ch = 0; ch < nch; ++ch) hd.heavyq[t0 + ch] = (hs << 16) | ch;
                         sel = false;
                     } else {   // task list full: mark the reserved entries void, item goes to the normal queue
-                        for (uint32_t c = 0; c < nch && t0 + c < (uint32_t)hd.max_heavy_tasks; ++c)
-                            hd.heavyq[t0 + c] = 0xFFFFFFFFu;
+                        for (uint32_t ch = 0; ch < nch && t0 + ch < (uint32_t)hd.max_heavy_tasks; ++ch)
+                            hd.heavyq[t0 + ch] = 0xFFFFFFFFu;
                     }
                 }
             }
-            const bool tiny = sel && dd <= kTinyD;   // 8 lanes per item (phase_tiny)
-            const uint32_t m = __ballot_sync(0xffffffffu, sel && !tiny);
-            if (m) {
-                uint32_t q = 0;
-                if (lane_id() == 0) q = atomicAdd(selc, (uint32_t)__popc(m));
-                q = __shfl_sync(0xffffffffu, q, 0);
-                if (sel && !tiny) selq[q + __popc(m & lanemask_lt())] = ((uint64_t)r << 32) | (uint64_t)i;
-            }
-            const uint32_t mt = __ballot_sync(0xffffffffu, tiny);
-            if (mt) {
-                uint32_t q = 0;
-                if (lane_id() == 0) q = atomicAdd(tinyc, (uint32_t)__popc(mt));
-                q = __shfl_sync(0xffffffffu, q, 0);
-                if (tiny) selq[hd.selq_cap - 1 - (q + __popc(mt & lanemask_lt()))] = ((uint64_t)r << 32) | (uint64_t)i;
-            }
+            const bool tiny = sel && d[q] <= kTinyD;   // 8 lanes per item (phase_tiny)
+            mc[q] = __ballot_sync(0xffffffffu, all);
+            ms[q] = __ballot_sync(0xffffffffu, sel && !tiny);
+            mt[q] = __ballot_sync(0xffffffffu, tiny);
+            nc += __popc(mc[q]);
+            ns += __popc(ms[q]);
+            ntn += __popc(mt[q]);
+            pos += c[q];
         }
-        sum = block_sum(sum, sh);
-        if (threadIdx.x == 0) hd.partial[r * SB + b] = sum;
+        uint32_t oc = 0, os = 0, ot = 0;
+        if (lane == 0) {
+            if (nc) oc = atomicAdd(copyc, nc);
+            if (ns) os = atomicAdd(selc, ns);
+            if (ntn) ot = atomicAdd(tinyc, ntn);
+        }
+        oc = __shfl_sync(0xffffffffu, oc, 0);
+        os = __shfl_sync(0xffffffffu, os, 0);
+        ot = __shfl_sync(0xffffffffu, ot, 0);
+        const uint32_t lt = lanemask_lt();
+#pragma unroll
+        for (int q = 0; q < kCountItems; ++q) {
+            if (mc[q] >> lane & 1) copyq[oc + __popc(mc[q] & lt)] = e[q];
+            if (ms[q] >> lane & 1) selq[os + __popc(ms[q] & lt)] = e[q];
+            if (mt[q] >> lane & 1) selq[hd.selq_cap - 1 - (ot + __popc(mt[q] & lt))] = e[q];
+            oc += __popc(mc[q]);
+            os += __popc(ms[q]);
+            ot += __popc(mt[q]);
+        }
+        if (threadIdx.x == 0 && tile == cumT[r + 1] - cumT[r] - 1) {   // the relation's last tile
+            const int32_t tot = s_excl + ttot;
+            bip[n] = tot;
+            meta_nnz(hd.meta, hd.h)[r] = tot;
+        }
+        __syncthreads();   // s_vt / s_excl reuse
     }
-}
-
-// Exclusive scan of the counts in place -> block indptr; nnz(h, r).
-__device__ void phase_scan(const GraphDev &g, const HopDev &hd, int bid, int nb)
-{
-    __shared__ int32_t sh[33];
-    const int SB = hd.scan_blocks;
-    for (int vb = bid; vb < SB * g.n_rel; vb += nb) {
-        const int r = vb / SB, b = vb % SB;
-        const int t = g.rel[r].dst_vt;
-        const int64_t n = meta_nodes(hd.meta, hd.h)[t];
-        const int64_t chunk = (n + SB - 1) / SB;
-        const int64_t lo = b * chunk, hi = min(n, lo + chunk);
-        int32_t s = 0;
-        const int32_t *const partial = hd.partial + r * SB;
-        for (int j = threadIdx.x; j < b; j += blockDim.x) s += partial[j];
-        int32_t carry = block_sum(s, sh);
-        int32_t *const ip = hd.indptr[r];
-        for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
-            const int64_t i = t0 + threadIdx.x;
-            const int32_t v = i < hi ? ip[i] : 0;
-            int32_t tot;
-            const int32_t ex = block_excl_scan(v, sh, &tot);
-            if (i < hi) ip[i] = carry + ex;
-            carry += tot;
-        }
-        if (b == SB - 1 && threadIdx.x == 0) {
-            ip[n] = carry;
-            meta_nnz(hd.meta, hd.h)[r] = carry;
-        }
+    // relations whose dst frontier is empty: indptr = [0], nnz = 0
+    if (blockIdx.x == 0 && threadIdx.x < g.n_rel && nF[g.rel[threadIdx.x].dst_vt] == 0) {
+        hd.indptr[threadIdx.x][0] = 0;
+        meta_nnz(hd.meta, hd.h)[threadIdx.x] = 0;
     }
 }
 
@@ -384,7 +452,7 @@ __device__ __noinline__ void select_generic(const HopDev &hd, const Item &it, in
 // one Philox call), so the k-th smallest key is found by a radix select over them
 // directly, ties broken by ascending j, and the selected offsets are emitted in
 // ascending j (j = 4 lane + t).
-__device__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
+__device__ __forceinline__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
                              uint32_t hr, uint32_t k0, uint32_t k1)
 {
     const int lane = lane_id();
@@ -428,7 +496,7 @@ __device__ void select_small(const HopDev &hd, const Item &it, int64_t d, int k,
 // the k smallest composites among them are found by a register radix select (m <= 128)
 // or rank counting, and emitted in ascending j.  Falls back to select_generic if the candidate count is < k or
 // exceeds the slots (both astronomically rare; the result is identical).
-__device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
+__device__ __forceinline__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, uint32_t v_lo, uint32_t v_hi,
                             uint32_t hr, uint32_t k0, uint32_t k1, uint64_t *cand)
 {
     // any threshold gives the same result (the selection below is exact; too few or too
@@ -530,18 +598,17 @@ __device__ void select_fast(const HopDev &hd, const Item &it, int64_t d, int k, 
 // One chunk of a heavy item (d > kHeavyD): keys of offsets [c * kHeavyChunk, ...) below
 // the item's threshold go to the item's candidate buffer; the warp that finishes the
 // item's last chunk selects the k smallest composites and emits them in ascending j.
-__device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, uint32_t seed_lo, uint32_t seed_hi,
+__device__ __forceinline__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, uint32_t seed_lo, uint32_t seed_hi,
                            uint64_t *cand)
 {
     const int lane = lane_id();
     const uint32_t hs = task >> 16, c = task & 0xFFFFu;
-    const uint64_t e = hd.heavy_items[hs];
-    const int r = (int)(e >> 32);
-    const int64_t i = (int64_t)(e & 0xFFFFFFFFu);
+    const QEntry e = hd.heavy_items[hs];
+    const int r = e.r;
     const RelDev &R = g.rel[r];
-    const int64_t ib = hd.ibase[r][i];
-    const int64_t d = hd.ideg[r][i];
-    const int64_t v = hd.nodes[R.dst_vt][i];
+    const int64_t ib = e.ib;
+    const int64_t d = e.d;
+    const int64_t v = e.v;
     const int k = hd.fanout[r];
     const uint32_t hr = ((uint32_t)hd.h << 16) | (uint32_t)r;
     const uint32_t v_lo = (uint32_t)v, v_hi = (uint32_t)((uint64_t)v >> 32);
@@ -582,7 +649,7 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
     if (done != nch - 1) return;
     // ---- last chunk: finalize the item
     __threadfence();
-    const int32_t pos0 = hd.indptr[r][i];
+    const int32_t pos0 = e.pos0;
     const int p = (int)(ib >> 56);
     const int64_t base0 = ib & ((1ll << 56) - 1);
     Item itm;
@@ -661,11 +728,11 @@ __device__ void heavy_task(const GraphDev &g, const HopDev &hd, uint32_t task, u
 // Sampling of one hop, part 1: the selection items (d > k, queued by phase_count):
 // heavy items as chunk tasks first (largest work first), then one warp per item;
 // both fetched dynamically.  cand: kSelCap slots of this warp in shared memory.
-__device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
+__device__ __forceinline__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int nb, uint64_t *cand)
 {
     const int lane = lane_id();
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const uint64_t *const selq = hd.selq;
+    const QEntry *const selq = hd.selq;
     (void)bid;
     // ---- heavy chunk tasks
     const uint32_t ntask = min(*(const volatile uint32_t *)(hd.meta + kMetaHeavyQ + hd.h), (uint32_t)hd.max_heavy_tasks);
@@ -689,17 +756,16 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
         if (lane == 0) w0 = atomicAdd(snext, (uint32_t)kGrab);
         w0 = __shfl_sync(0xffffffffu, w0, 0);
         if (w0 >= nsel) break;
-        uint32_t my_r = 0, my_i = 0;
+        uint32_t my_r = 0;
         int32_t my_pos0 = 0, my_d = 0;
         int64_t my_ib = 0, my_v = 0;
         if (lane < kGrab && w0 + lane < nsel) {
-            const uint64_t e = selq[w0 + lane];
-            my_r = (uint32_t)(e >> 32);
-            my_i = (uint32_t)e;
-            my_pos0 = hd.indptr[my_r][my_i];
-            my_ib = hd.ibase[my_r][my_i];
-            my_d = hd.ideg[my_r][my_i];
-            my_v = hd.nodes[g.rel[my_r].dst_vt][my_i];
+            const QEntry e = selq[w0 + lane];
+            my_r = (uint32_t)e.r;
+            my_pos0 = e.pos0;
+            my_ib = e.ib;
+            my_d = e.d;
+            my_v = e.v;
         }
         const int cnt = (int)min((uint32_t)kGrab, nsel - w0);
         for (int q = 0; q < cnt; ++q) {
@@ -738,41 +804,41 @@ __device__ void phase_select(const GraphDev &g, const HopDev &hd, int bid, int n
 // are loaded while this round computes.  (Measured: items with 32 < d <= 64 took a whole
 // warp each in select_small, with 3/4 of its 128 key slots empty.)
 struct TinyItem {
-    uint32_t r, i;
+    uint32_t r;
     int32_t pos0, d;
     int64_t ib, v;
 };
 
-__device__ __forceinline__ void tiny_load(const GraphDev &g, const HopDev &hd, uint64_t e, bool ok, TinyItem &t)
+__device__ __forceinline__ void tiny_load(const QEntry *e, bool ok, TinyItem &t)
 {
-    t.r = (uint32_t)(e >> 32);
-    t.i = (uint32_t)e;
+    t.r = 0;
     t.pos0 = 0;
     t.d = 0;
     t.ib = 0;
     t.v = 0;
     if (ok) {
-        t.pos0 = hd.indptr[t.r][t.i];
-        t.ib = hd.ibase[t.r][t.i];
-        t.d = hd.ideg[t.r][t.i];
-        t.v = hd.nodes[g.rel[t.r].dst_vt][t.i];
+        const QEntry x = *e;
+        t.r = (uint32_t)x.r;
+        t.pos0 = x.pos0;
+        t.ib = x.ib;
+        t.d = x.d;
+        t.v = x.v;
     }
 }
 
-__device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
+__device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
     static_assert(kTinyD == 64, "8 lanes x (4 + 4) keys");
     const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
     const int64_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
     const int64_t nw = (int64_t)nb * (blockDim.x >> 5);
-    const uint64_t *const selq_top = hd.selq + (hd.selq_cap - 1);   // item q at selq_top[-q]
+    const QEntry *const selq_top = hd.selq + (hd.selq_cap - 1);   // item q at selq_top[-q]
     int64_t q = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + gi;
     if (q - gi >= ntiny) return;   // warp-uniform
     TinyItem cur;
-    tiny_load(g, hd, q < ntiny ? selq_top[-q] : 0ull, q < ntiny, cur);
+    tiny_load(selq_top - q, q < ntiny, cur);
     const int64_t step = nw * 4;
-    uint64_t e_next = q + step < ntiny ? selq_top[-(q + step)] : 0ull;
     // exclusive scan / total over the 8 lanes of the item
     auto group_excl = [&](int x, int &tot) {
         int y = x;
@@ -787,8 +853,7 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
     for (; q - gi < ntiny; q += step) {
         const bool act = q < ntiny;
         TinyItem nxt;
-        tiny_load(g, hd, e_next, q + step < ntiny, nxt);   // next round's data in flight
-        e_next = q + 2 * step < ntiny ? selq_top[-(q + 2 * step)] : 0ull;
+        tiny_load(selq_top - (q + step), q + step < ntiny, nxt);   // next round's item in flight
         Item itm;
         int k = 0;
         const int32_t d = cur.d;
@@ -872,42 +937,32 @@ __device__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
 
 // Sampling of one hop, part 2: the full-neighbourhood items (d <= k or k = -1) as
 // segmented copies, 32 items per warp, 4 independent load chains per lane.
-__device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
+__device__ __forceinline__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
 {
     const int warps = blockDim.x >> 5;
     const int lane = lane_id();
     const int64_t gw = (int64_t)bid * warps + (threadIdx.x >> 5), nw = (int64_t)nb * warps;
     uint32_t *const kcnt = hd.cd.kcnt;
     const int32_t bshift = g.bshift;
-    // ---- full neighbourhoods: segmented copy over groups of 32 items
-    const int32_t *nF = meta_nodes(hd.meta, hd.h);
-    int64_t cum[EG_MAX_REL + 1];
-    cum[0] = 0;
-    for (int r = 0; r < g.n_rel; ++r) cum[r + 1] = cum[r] + (hd.fanout[r] != 0 ? nF[g.rel[r].dst_vt] : 0);
-    const int64_t total = cum[g.n_rel];
+    // ---- full neighbourhoods (copyq, queued by phase_count with their output slots):
+    // segmented copy over groups of 32 items
+    const int64_t total = *(const volatile uint32_t *)(hd.meta + kMetaCopy + hd.h);
+    const QEntry *const copyq = hd.copyq;
     for (int64_t g0 = gw * 32; g0 < total; g0 += nw * 32) {
         const int64_t it = g0 + lane;
         int r = 0;
-        int32_t pos0 = 0, cnt = 0, d = 0;
+        int32_t c = 0;
         int64_t ib = 0;
         uint32_t *srcp = nullptr;
         int64_t *eidp = nullptr;
         if (it < total) {
-            while (it >= cum[r + 1]) ++r;
-            const int64_t i = it - cum[r];
-            const int32_t *bip = hd.indptr[r];
-            pos0 = bip[i];
-            cnt = bip[i + 1] - pos0;
-            if (cnt > 0) {
-                ib = hd.ibase[r][i];
-                d = hd.ideg[r][i];
-            }
-            srcp = hd.src[r] + pos0;
-            eidp = hd.eids[r] + pos0;
+            const QEntry e = copyq[it];
+            r = e.r;
+            c = e.d;
+            ib = e.ib;
+            srcp = hd.src[r] + e.pos0;
+            eidp = hd.eids[r] + e.pos0;
         }
-        const int k = hd.fanout[r];
-        const bool copy = cnt > 0 && !(k >= 0 && d > k);
-        const int32_t c = copy ? cnt : 0;
         const int32_t incl = warp_incl_scan(c);
         const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const int32_t excl = incl - c;
@@ -967,7 +1022,7 @@ __device__ void phase_copy(const GraphDev &g, const HopDev &hd, int bid, int nb)
 // relation r, n_neg corrupted dsts drawn uniformly from t(r)'s range; every endpoint is a
 // key of the level-0 compaction (compact.cuh, kModeLp), which yields the distinct
 // endpoints in ascending gid as the seeds F_0 and every pair in local ids.
-__device__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
+__device__ __forceinline__ void phase_lp_mark(const GraphDev &g, const HopDev &hd, const LpDev &lp, int bid, int nb)
 {
     const int64_t n = (int64_t)hd.dyn[1];
     const int64_t *__restrict__ src = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : lp.src_stage;

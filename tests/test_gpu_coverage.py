@@ -206,3 +206,29 @@ def test_in_degree_limit_rejected():
             assert e.value.code == -1 and "2^26" in str(e.value)
         ctx.close()
         del ix, ip
+
+
+# ----------------------------------------------------------------------------- skewed keys
+
+def test_c4l_world4_confined_seeds():
+    """C4L (planted communities: a source from its dst's community with p = 0.9) at emulated
+    world 4 with each rank's seeds confined to its own range: a rank's sampled sources
+    concentrate in its two communities, so the compaction sees buckets 4x denser than C4's
+    (more big buckets on the bitmap path, longer sorted runs).  Blocks bit-exact, features
+    vs the generator formula."""
+    import torch
+    cfg = synth.config("C4L")
+    g = synth.build_host_graph(cfg)
+    rows = {0: synth.LazyRows(cfg, 0)}
+    ctxs = _world(g, 4)
+    for p in (0, 3):
+        for b in range(2):
+            seeds = synth.batch_seeds_confined(cfg, b, p, 4)
+            rs = synth.rng_seed(cfg, 4 * b + p)
+            res = oracle.sample(g, seeds, cfg.fanouts, rs)
+            bl = ctxs[p].sample_minibatch(torch.from_numpy(seeds).cuda(), cfg.fanouts, rs, features=True)
+            assert_same_batch(res, bl, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, _features_of(bl, cfg), cfg, rows)
+            bl.free()
+    for c in ctxs:
+        c.close()
