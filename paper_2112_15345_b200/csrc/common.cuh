@@ -27,6 +27,7 @@ constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this
 constexpr int kTinyD = 64;                // selections with d <= this: 8 lanes per item (phase_tiny)
+constexpr int kTinyD16 = 16;              // ... with d <= this: 4 lanes per item
 // Heavy items (d > kHeavyD, k <= kHeavyMaxK) are split into tasks of kHeavyChunk keys
 // sampled by different warps; their candidates meet in a per-item buffer.
 constexpr int kHeavyD = 2048;
@@ -83,7 +84,8 @@ constexpr int kMetaHeavyNext = kMetaHeavyQ + EG_MAX_HOPS;        // dynamic fetc
 constexpr int kMetaTiny = kMetaHeavyNext + EG_MAX_HOPS;         // tiny selection items per hop
 constexpr int kMetaTinyNext = kMetaTiny + EG_MAX_HOPS;            // dynamic fetch counter per hop
 constexpr int kMetaCopy = kMetaTinyNext + EG_MAX_HOPS;            // full-neighbourhood items per hop
-constexpr int kMetaCntTicket = kMetaCopy + EG_MAX_HOPS;           // count tile tickets per hop
+constexpr int kMetaTiny16 = kMetaCopy + EG_MAX_HOPS;              // tiny selection items with d <= 16 per hop
+constexpr int kMetaCntTicket = kMetaTiny16 + EG_MAX_HOPS;         // count tile tickets per hop
 constexpr int kMetaTasks = kMetaCntTicket + EG_MAX_HOPS;          // compaction tasks per level (0..L)
 constexpr int kMetaTicket = kMetaTasks + EG_MAX_HOPS + 1;         // compaction task tickets per level
 constexpr int kMetaKTicket = kMetaTicket + EG_MAX_HOPS + 1;       // kscan tile tickets per level
@@ -160,6 +162,7 @@ struct HopDev {
     const uint64_t *dyn;             // device: {rng_seed, n_seeds} of the batch
     QEntry *selq;                    // items that need a selection (d > k); tiny ones (d <= 64) from the top
     QEntry *copyq;                   // full-neighbourhood items (0 < d <= k, or k = -1)
+    QEntry *tinyq16;                 // selections with d <= kTinyD16 (from the top)
     int32_t selq_cap;                // slots of selq (= of copyq)
     unsigned long long *clb;         // count tiles' look-back words (zeroed per launch)
     QEntry *heavy_items;             // [max_heavy]

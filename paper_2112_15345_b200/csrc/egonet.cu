@@ -91,7 +91,7 @@ struct Plan {
     size_t o_nodes[EG_MAX_VT] = {}, o_feat[EG_MAX_VT] = {};
     size_t o_ip[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ix[EG_MAX_HOPS][EG_MAX_REL] = {}, o_ei[EG_MAX_HOPS][EG_MAX_REL] = {},
            o_src[EG_MAX_HOPS][EG_MAX_REL] = {},
-           o_selq[EG_MAX_HOPS] = {}, o_copyq[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
+           o_selq[EG_MAX_HOPS] = {}, o_copyq[EG_MAX_HOPS] = {}, o_tiny16[EG_MAX_HOPS] = {}, o_heavy[EG_MAX_HOPS] = {};
     int64_t selq_items[EG_MAX_HOPS] = {};
     int32_t max_heavy[EG_MAX_HOPS] = {}, max_heavy_tasks[EG_MAX_HOPS] = {};
     // batch-local compaction state (compact.cuh): meta | kcnt | mcnt contiguous (one memset)
@@ -963,6 +963,7 @@ eg_status get_plan(eg_ctx *c, int32_t L, const int32_t *fanouts, int64_t n_cap, 
         p->selq_items[h] = items;
         p->o_selq[h] = take(sizeof(QEntry) * items);
         p->o_copyq[h] = take(sizeof(QEntry) * items);
+        p->o_tiny16[h] = take(sizeof(QEntry) * items);
         // heavy slots: one per 2048 frontier items beyond the first kMinHeavy
         p->max_heavy[h] = (int32_t)std::min<int64_t>(65535, kMinHeavy + items / 2048);
         p->max_heavy_tasks[h] = (int32_t)std::min<int64_t>(INT32_MAX / 2, (int64_t)p->max_heavy[h] * kHeavyTasksPerItem);
@@ -1064,6 +1065,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             x.last = h == L - 1;
             x.selq = (QEntry *)(base + p->o_selq[h]);
             x.copyq = (QEntry *)(base + p->o_copyq[h]);
+            x.tinyq16 = (QEntry *)(base + p->o_tiny16[h]);
             x.selq_cap = (int32_t)p->selq_items[h];
             x.clb = (unsigned long long *)(base + p->o_clb[h]);
             char *hv = base + p->o_heavy[h];

@@ -114,7 +114,9 @@ __device__ __forceinline__ void phase_count(const GraphDev &g, const HopDev &hd)
     uint32_t *const selc = (uint32_t *)(hd.meta + kMetaSel + hd.h);
     uint32_t *const tinyc = (uint32_t *)(hd.meta + kMetaTiny + hd.h);
     uint32_t *const copyc = (uint32_t *)(hd.meta + kMetaCopy + hd.h);
+    uint32_t *const tiny16c = (uint32_t *)(hd.meta + kMetaTiny16 + hd.h);
     QEntry *const selq = hd.selq;
+    QEntry *const tinyq16 = hd.tinyq16;
     QEntry *const copyq = hd.copyq;
     volatile unsigned long long *const clb = hd.clb;
     for (;;) {
@@ -200,8 +202,8 @@ __device__ __forceinline__ void phase_count(const GraphDev &g, const HopDev &hd)
         // classify the lane's items; queue slots are reserved once per warp for all of them
         // (three independent atomics instead of one dependent round trip per item and queue)
         QEntry e[kCountItems];
-        uint32_t mc[kCountItems], ms[kCountItems], mt[kCountItems];
-        uint32_t nc = 0, ns = 0, ntn = 0;
+        uint32_t mc[kCountItems], ms[kCountItems], mt[kCountItems], m16[kCountItems];
+        uint32_t nc = 0, ns = 0, ntn = 0, n16 = 0;
 #pragma unroll
         for (int q = 0; q < kCountItems; ++q) {
             const int64_t i = i0 + q;
@@ -232,33 +234,40 @@ __device__ __forceinline__ void phase_count(const GraphDev &g, const HopDev &hd)
                     }
                 }
             }
-            const bool tiny = sel && d[q] <= kTinyD;   // 8 lanes per item (phase_tiny)
+            const bool tiny16 = sel && d[q] <= kTinyD16;             // 4 lanes per item (phase_tiny)
+            const bool tiny = sel && !tiny16 && d[q] <= kTinyD;     // 8 lanes per item
             mc[q] = __ballot_sync(0xffffffffu, all);
-            ms[q] = __ballot_sync(0xffffffffu, sel && !tiny);
+            ms[q] = __ballot_sync(0xffffffffu, sel && !tiny && !tiny16);
             mt[q] = __ballot_sync(0xffffffffu, tiny);
+            m16[q] = __ballot_sync(0xffffffffu, tiny16);
             nc += __popc(mc[q]);
             ns += __popc(ms[q]);
             ntn += __popc(mt[q]);
+            n16 += __popc(m16[q]);
             pos += c[q];
         }
-        uint32_t oc = 0, os = 0, ot = 0;
+        uint32_t oc = 0, os = 0, ot = 0, o16 = 0;
         if (lane == 0) {
             if (nc) oc = atomicAdd(copyc, nc);
             if (ns) os = atomicAdd(selc, ns);
             if (ntn) ot = atomicAdd(tinyc, ntn);
+            if (n16) o16 = atomicAdd(tiny16c, n16);
         }
         oc = __shfl_sync(0xffffffffu, oc, 0);
         os = __shfl_sync(0xffffffffu, os, 0);
         ot = __shfl_sync(0xffffffffu, ot, 0);
+        o16 = __shfl_sync(0xffffffffu, o16, 0);
         const uint32_t lt = lanemask_lt();
 #pragma unroll
         for (int q = 0; q < kCountItems; ++q) {
             if (mc[q] >> lane & 1) copyq[oc + __popc(mc[q] & lt)] = e[q];
             if (ms[q] >> lane & 1) selq[os + __popc(ms[q] & lt)] = e[q];
             if (mt[q] >> lane & 1) selq[hd.selq_cap - 1 - (ot + __popc(mt[q] & lt))] = e[q];
+            if (m16[q] >> lane & 1) tinyq16[hd.selq_cap - 1 - (o16 + __popc(m16[q] & lt))] = e[q];
             oc += __popc(mc[q]);
             os += __popc(ms[q]);
             ot += __popc(mt[q]);
+            o16 += __popc(m16[q]);
         }
         if (threadIdx.x == 0 && tile == cumT[r + 1] - cumT[r] - 1) {   // the relation's last tile
             const int32_t tot = s_excl + ttot;
@@ -826,38 +835,40 @@ __device__ __forceinline__ void tiny_load(const QEntry *e, bool ok, TinyItem &t)
     }
 }
 
-__device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
+// G lanes per item (G = 8: d <= 64, two key words per lane when d > 32; G = 4: d <= 16),
+// 32 / G items per warp, static stride over the queue (item q at top[-q]).
+template <int G>
+__device__ __forceinline__ void tiny_items(const GraphDev &g, const HopDev &hd, const QEntry *top, int64_t ntiny,
+                                           int bid, int nb)
 {
-    static_assert(kTinyD == 64, "8 lanes x (4 + 4) keys");
-    const int lane = lane_id(), gi = lane >> 3, sl = lane & 7;
+    constexpr int IPW = 32 / G;   // items per warp
+    const int lane = lane_id(), gi = lane / G, sl = lane % G;
     const uint32_t seed_lo = (uint32_t)hd.dyn[0], seed_hi = (uint32_t)(hd.dyn[0] >> 32);
-    const int64_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
     const int64_t nw = (int64_t)nb * (blockDim.x >> 5);
-    const QEntry *const selq_top = hd.selq + (hd.selq_cap - 1);   // item q at selq_top[-q]
-    int64_t q = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + gi;
+    int64_t q = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * IPW + gi;
     if (q - gi >= ntiny) return;   // warp-uniform
     TinyItem cur;
-    tiny_load(selq_top - q, q < ntiny, cur);
-    const int64_t step = nw * 4;
-    // exclusive scan / total over the 8 lanes of the item
+    tiny_load(top - q, q < ntiny, cur);
+    const int64_t step = nw * IPW;
+    // exclusive scan / total over the G lanes of the item
     auto group_excl = [&](int x, int &tot) {
         int y = x;
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            const int z = __shfl_up_sync(0xffffffffu, y, o, 8);
+        for (int o = 1; o < G; o <<= 1) {
+            const int z = __shfl_up_sync(0xffffffffu, y, o, G);
             if (sl >= o) y += z;
         }
-        tot = __shfl_sync(0xffffffffu, y, 7, 8);
+        tot = __shfl_sync(0xffffffffu, y, G - 1, G);
         return y - x;
     };
     for (; q - gi < ntiny; q += step) {
         const bool act = q < ntiny;
         TinyItem nxt;
-        tiny_load(selq_top - (q + step), q + step < ntiny, nxt);   // next round's item in flight
+        tiny_load(top - (q + step), q + step < ntiny, nxt);   // next round's item in flight
         Item itm;
         int k = 0;
         const int32_t d = cur.d;
-        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vm = 0;   // bit t < 4: j = 4 sl + t; t >= 4: j = 32 + 4 sl + t - 4
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vm = 0;   // bit t < 4: j = 4 sl + t; t >= 4: j = 4 G + 4 sl + t - 4
         if (act) {
             const int r = (int)cur.r;
             const RelDev &R = g.rel[r];
@@ -876,13 +887,13 @@ __device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, 
 #pragma unroll
                 for (int t = 0; t < 4; ++t) vm |= (uint32_t)(4 * sl + t < d) << t;
             }
-            if (32 + 4 * sl < d) {
+            if (G == 8 && 32 + 4 * sl < d) {
                 keys4((uint32_t)(8 + sl), vlo, vhi, hr, seed_lo, seed_hi, w + 4);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) vm |= (uint32_t)(32 + 4 * sl + t < d) << (4 + t);
             }
         }
-        const bool upper = __any_sync(0xffffffffu, (vm >> 4) != 0);   // warp-uniform: any d > 32
+        const bool upper = G == 8 && __any_sync(0xffffffffu, (vm >> 4) != 0);   // warp-uniform: any d > 32
         uint32_t P = 0;
         int krem = k, s = 32;
         bool done = !act;
@@ -896,9 +907,8 @@ __device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, 
                     for (int t = 4; t < 8; ++t) pk += radix2_count(w[t], vm >> t & 1, P, s);
                 }
             }
-            pk += __shfl_xor_sync(0xffffffffu, pk, 1);
-            pk += __shfl_xor_sync(0xffffffffu, pk, 2);
-            pk += __shfl_xor_sync(0xffffffffu, pk, 4);
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
             if (!done) done = radix2_decide(pk, krem, P, s);
         }
         uint32_t ltm = 0, eqm = 0;
@@ -908,10 +918,10 @@ __device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, 
             ltm |= (uint32_t)((vm >> t & 1) && hi < ph) << t;
             eqm |= (uint32_t)((vm >> t & 1) && hi == ph) << t;
         }
-        // ascending j: the lower halves of the item's 8 lanes (j < 32), then the upper halves
-        int te0, te1, tc0, tc1;
+        // ascending j: the lower halves of the item's lanes (j < 4 G), then the upper halves
+        int te0, te1 = 0, tc0, tc1;
         int er0 = group_excl(__popc(eqm & 0xFu), te0);
-        int er1 = te0 + group_excl(__popc(eqm >> 4), te1);
+        int er1 = G == 8 ? te0 + group_excl(__popc(eqm >> 4), te1) : 0;
         uint32_t sel = ltm;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -919,20 +929,33 @@ __device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, 
                 if (er0 < krem) sel |= 1u << t;
                 ++er0;
             }
+        if (G == 8) {
 #pragma unroll
-        for (int t = 4; t < 8; ++t)
-            if (eqm >> t & 1) {
-                if (er1 < krem) sel |= 1u << t;
-                ++er1;
-            }
+            for (int t = 4; t < 8; ++t)
+                if (eqm >> t & 1) {
+                    if (er1 < krem) sel |= 1u << t;
+                    ++er1;
+                }
+        }
         const int slot0 = group_excl(__popc(sel & 0xFu), tc0);
-        const int slot1 = tc0 + group_excl(__popc(sel >> 4), tc1);
+        const int slot1 = G == 8 ? tc0 + group_excl(__popc(sel >> 4), tc1) : 0;
         if (act) {
             emit_run4(itm, sel & 0xFu, slot0, 4 * sl);
-            if (sel >> 4) emit_run4(itm, sel >> 4, slot1, 32 + 4 * sl);
+            if (G == 8 && (sel >> 4)) emit_run4(itm, sel >> 4, slot1, 32 + 4 * sl);
         }
         cur = nxt;
     }
+}
+
+// Selections of tiny items: k < d <= kTinyD16 with 4 lanes per item (their own queue), the
+// rest of k < d <= kTinyD with 8 lanes (the top of the selection queue).
+__device__ __forceinline__ void phase_tiny(const GraphDev &g, const HopDev &hd, int bid, int nb)
+{
+    static_assert(kTinyD == 64 && kTinyD16 == 16, "8 lanes x (4 + 4) keys, 4 lanes x 4 keys");
+    const int64_t n16 = *(const volatile uint32_t *)(hd.meta + kMetaTiny16 + hd.h);
+    tiny_items<4>(g, hd, hd.tinyq16 + (hd.selq_cap - 1), n16, bid, nb);
+    const int64_t ntiny = *(const volatile uint32_t *)(hd.meta + kMetaTiny + hd.h);
+    tiny_items<8>(g, hd, hd.selq + (hd.selq_cap - 1), ntiny, bid, nb);
 }
 
 // Sampling of one hop, part 2: the full-neighbourhood items (d <= k or k = -1) as
