@@ -29,26 +29,31 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _stale() -> bool:
-    if not os.path.exists(SO):
+def _stale(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + HEADERS
-    return os.path.getmtime(SO) < max(os.path.getmtime(d) for d in deps)
+    return os.path.getmtime(so) < max(os.path.getmtime(d) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = ["nvcc", *NVCC_FLAGS, "-shared", "-o", tmp, *sources()]
+SO_CHECK = os.path.join(PKG, "libegonet_check.so")
+
+
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
+    """check: the bounds-checked variant libegonet_check.so (-DEG_CHECK=1: device-side
+    asserts on the hot paths' indices; load it with EG_LIB=<path>)."""
+    so = SO_CHECK if check else SO
+    if not force and not _stale(so):
+        return so
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = ["nvcc", *NVCC_FLAGS, *(["-DEG_CHECK=1"] if check else []), "-shared", "-o", tmp, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, check="--check" in sys.argv))

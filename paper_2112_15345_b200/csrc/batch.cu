@@ -1,6 +1,6 @@
 // batch.cu -- the sampling + compaction of a bundle of mini-batches, one kernel per phase.
 //
-//   seed split | kscan scatter compact (level 0) |
+//   seed split (+ sort: batches of <= 1024 seeds) | [kscan scatter compact (level 0)] |
 //   for h: count | select + copy + tiny | kscan scatter compact (level h+1)
 //
 // Every phase kernel runs with grid.y = the batch of the bundle (each batch has its own
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev 
                                                         const BatchDev *__restrict__ bd)
 {
     stamp(bd, 0);
-    phase_seed_split(g, bd->seedh[blockIdx.y], bd->seeds[blockIdx.y]);
+    phase_seed_split(g, bd->seedh[blockIdx.y], bd->seeds[blockIdx.y], bd->seed_sort != 0);
 }
 
 __global__ void __launch_bounds__(kCountThreads) k_count(const __grid_constant__ GraphDev g,
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kBatchThreads) k_compact_emit(const __grid_con
 }
 
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *count_tiles, int B,
-                 cudaStream_t s, const Fork &fk, bool serial, bool lp)
+                 cudaStream_t s, const Fork &fk, bool serial, bool lp, bool seed_sort)
 {
     // blocks per batch: about one wave of the chip in total
     const int per = (kSMs * 8 + B - 1) / B;
@@ -145,7 +145,7 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
         k_seed<<<dim3(1, B), 1024, 0, s>>>(g, bd_dev);
     }
     ++nk;
-    compaction(-1);
+    if (!seed_sort) compaction(-1);   // else the seed split sorted the seeds itself
     for (int h = 0; h < n_hops; ++h) {
         const int cb = count_tiles[h] < per ? count_tiles[h] : per;   // count: blocks take tiles by ticket
         k_count<<<dim3(cb, B), kCountThreads, 0, s>>>(g, bd_dev, h);

@@ -6,6 +6,27 @@
 
 #include "../../include/egonet.h"
 
+// Bounds-checked build (paper_2112_15345_b200/build.py --check -> libegonet_check.so,
+// loaded with EG_LIB=...): every EG_DCHECK traps with the failing line.  compute-sanitizer
+// is not available on the GPU pool used here (profiles/r02/sanitize/), so the GPU suite is
+// run against this build instead.
+#ifndef EG_CHECK
+#define EG_CHECK 0
+#endif
+#if EG_CHECK
+#include <cstdio>
+#define EG_DCHECK(c)                                                                                \
+    do {                                                                                            \
+        if (!(c)) {                                                                                 \
+            printf("EG_CHECK failed: %s:%d: %s (block %d,%d thread %d)\n", __FILE__, __LINE__, #c,     \
+                   blockIdx.x, blockIdx.y, threadIdx.x);                                            \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define EG_DCHECK(c) do { } while (0)
+#endif
+
 namespace eg {
 
 constexpr int kWarp = 32;
@@ -131,6 +152,8 @@ struct CompactDev {
     uint32_t *mg[2];                 // members (gids of the batch so far) sorted by gid, ping-pong by level
     int32_t *mp[2];                  // their positions in their type's node array
     int32_t cap_elems;
+    int32_t cap_members;             // entries of mg / mp (bounds checks)
+    int32_t nb_pad;                  // entries of the bucket arrays (bounds checks)
 };
 
 // A dst item of a hop, as the count phase hands it to the sampling kernels (queues of
@@ -203,6 +226,7 @@ __device__ __forceinline__ int owner_of(const GraphDev &g, int t, int64_t tid)
 // else the owner's shard (local HBM, or a peer's over NVLink).
 __device__ __forceinline__ const uint8_t *feature_row(const GraphDev &g, const FeatDev &f, int u, int64_t tid)
 {
+    EG_DCHECK(tid >= 0 && tid < g.off[u + 1] - g.off[u]);
     if (f.replica[u]) return f.replica[u] + tid * f.row_bytes[u];
     const int p = owner_of(g, u, tid);
     return f.rows[u][p] + (tid - g.bounds[u][p]) * f.row_bytes[u];

@@ -123,6 +123,7 @@ __device__ __forceinline__ void phase_kscan(const GraphDev &g, const HopDev &hd)
     const int tile = s_tile;
     if (tile >= ntiles) return;
     const int64_t b0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanPer;
+    EG_DCHECK(b0 + kScanPer <= cd.nb_pad);
     uint32_t kc[kScanPer], mc[kScanPer];
     {
         const uint4 *kp = reinterpret_cast<const uint4 *>(cd.kcnt + b0);
@@ -210,6 +211,7 @@ __device__ __forceinline__ void phase_kscan(const GraphDev &g, const HopDev &hd)
         mo += mc[q];
         cv[q] = ko + mo;   // end of bucket b's keys in the element array: the scatter's cursor
         if (flags >> q & 1) {
+            EG_DCHECK(t < (uint32_t)NB);
             for (int u = 0; u < g.n_vt; ++u)
                 if (b0 + q == g.bbase[u]) cd.ftask[u] = (int32_t)t;   // the type's first task
             cd.tstart[t++] = (uint32_t)(b0 + q);
@@ -355,7 +357,10 @@ __device__ __forceinline__ void phase_scatter(const GraphDev &g, const HopDev &h
             }
 #pragma unroll
             for (int q = 0; q < U; ++q)
-                if (j0 + q * stride < nm) el[slot[q]] = comp(gid[q], 0u, (uint32_t)pos[q]);
+                if (j0 + q * stride < nm) {
+                    EG_DCHECK(slot[q] < cap);
+                    el[slot[q]] = comp(gid[q], 0u, (uint32_t)pos[q]);
+                }
         }
     }
     if (hd.mode == kModeHop && g.n_rel == 1) {   // homogeneous hop (C3, C4): no relation lookup
@@ -428,7 +433,8 @@ __device__ __forceinline__ void key_out(const GraphDev &g, const HopDev &hd, con
 {
     if (hd.mode == kModeHop) {
         int r = 0;
-        while ((int64_t)pay >= cum[r + 1]) ++r;
+        while (r + 1 < g.n_rel && (int64_t)pay >= cum[r + 1]) ++r;
+        EG_DCHECK((int64_t)pay < cum[r + 1] && pos >= 0);
         hd.indices[r][pay - cum[r]] = pos;
     } else if (hd.mode == kModeLp) {
         lp.pairs[pay] = pos;
@@ -469,6 +475,8 @@ __device__ __forceinline__ TaskRange task_range(const GraphDev &g, const Compact
     r.nk = k1 - k0;
     r.u = type_of_bucket(g, r.b0);
     r.bitmap = r.b1 - r.b0 == 1 && (r.n > (uint32_t)kBigBucket || g.compact_bitmap);
+    EG_DCHECK(r.b0 < r.b1 && r.b1 <= g.nb && (int64_t)r.e0 + r.n <= cd.cap_elems);
+    EG_DCHECK(r.bitmap || r.n <= (uint32_t)kSortCap);
     return r;
 }
 
@@ -546,6 +554,7 @@ __device__ __forceinline__ void sort_build(const GraphDev &g, const HopDev &hd, 
             const unsigned long long x = c[j];
             int r = lo;
             for (int k = lo; k < hi; ++k) r += sm.s.e[k] < x;
+            EG_DCHECK(lo >= 0 && hi <= n && r < hi);
             sm.s.srt[r] = x;
         }
     }
@@ -609,6 +618,7 @@ __device__ __forceinline__ uint32_t bitmap_build(const GraphDev &g, const HopDev
             const uint32_t i = i0 + 32 * q;
             if (i >= T.n) continue;
             const uint32_t b = (uint32_t)(x[q] >> 32) - gid0;
+            EG_DCHECK(b < (1u << g.bshift));
             if (i < T.nm) {
                 atomicOr(sm.b.m + (b >> 5), 1u << (b & 31));
             } else {

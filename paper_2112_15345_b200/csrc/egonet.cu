@@ -1007,6 +1007,7 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     bd->trace = c->trace ? 1 : 0;
     bd->B = B;
     bd->lp = p->lp ? 1 : 0;
+    bd->seed_sort = (!p->lp && p->n_cap <= 1024) ? 1 : 0;
     GatherSet gs{};
     gs.nb = B;
     for (int b = 0; b < B; ++b) {
@@ -1030,6 +1031,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
             cd.mp[i] = (int32_t *)(base + p->o_mp[i]);
         }
         cd.cap_elems = (int32_t)(p->cap_keys + p->cap_members);
+        cd.cap_members = (int32_t)p->cap_members;
+        cd.nb_pad = (int32_t)((g.nb + kScanTile - 1) / kScanTile * kScanTile);
         for (int u = 0; u < V; ++u) {
             hd.nodes[u] = (int64_t *)(base + p->o_nodes[u]);
             hd.cap_nodes[u] = (int32_t)p->capF[L][u];
@@ -1109,7 +1112,8 @@ eg_status capture_slot(eg_ctx *c, Plan *p, Slot *sl)
     cudaMemset2DAsync(p->batch_base(sl->mem, 0) + p->o_meta, p->stride, 0, p->zero_bytes, B, cs);
     cudaEventRecordWithFlags(sl->s0, cs, cudaEventRecordExternal);
     mark("start");
-    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->count_tiles, B, cs, c->fork, c->trace, p->lp);
+    nk += launch_batch(g, (const BatchDev *)(sl->mem + p->o_bd), L, p->count_tiles, B, cs, c->fork, c->trace, p->lp,
+                       !p->lp && p->n_cap <= 1024);
     mark("sample");
     cudaEventRecordWithFlags(sl->s1, cs, cudaEventRecordExternal);
     if (p->features) {

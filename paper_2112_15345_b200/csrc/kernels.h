@@ -27,6 +27,7 @@ struct GatherSet {
 struct BatchDev {
     int32_t n_hops, trace, B;
     int32_t lp;                            // link-prediction batches (seeds from targets)
+    int32_t seed_sort;                     // the seed split sorts the seeds (<= 1024 per batch)
     const int64_t *seeds[kMaxBundle];
     HopDev hop[kMaxBundle][EG_MAX_HOPS];
     HopDev seedh[kMaxBundle];              // the seeds' level ("hop -1": seed split + level-0 compaction)
@@ -42,7 +43,7 @@ struct Fork {
 // batch.cu: enqueue the sampling + compaction of the B batches of bd_dev (capturable);
 // returns the number of kernels.  lp: link-prediction batches (seeds from targets).
 int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const int32_t *count_tiles, int B,
-                 cudaStream_t s, const Fork &fk, bool serial, bool lp);
+                 cudaStream_t s, const Fork &fk, bool serial, bool lp, bool seed_sort);
 
 // TMA tensor maps of the feature tables the gather reads with cp.async.bulk.tensor
 // tile::gather4 (four rows per TMA operation): per vertex type one 2-D map over its full

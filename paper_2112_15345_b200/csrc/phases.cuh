@@ -24,7 +24,12 @@ __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1
 // Seeds (caller order, mixed types) -> F_0[u] (stable per type); every placed seed is a
 // key of the level-0 compaction (compact.cuh, kModeSeeds: sorted member list, duplicate
 // check).  Flags out-of-range seeds.  One block.
-__device__ __forceinline__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds)
+// sort: batches of at most blockDim.x seeds (one round) skip the level-0 compaction kernels:
+// the seeds are sorted here by a block-wide bitonic sort of (gid << 32 | position), which
+// gives the level-0 member list (mg[0], mp[0]) and its bucket counts, and a repeated gid
+// is a duplicate seed.  Otherwise every placed seed is a key of the level-0 compaction.
+__device__ __forceinline__ void phase_seed_split(const GraphDev &g, const HopDev &hd, const int64_t *__restrict__ slot_seeds,
+                                                 bool sort)
 {
     // the caller's buffer when it is device-accessible, else the slot's staged copy
     const int64_t *__restrict__ seeds = hd.dyn[2] ? (const int64_t *)hd.dyn[2] : slot_seeds;
@@ -71,13 +76,47 @@ __device__ __forceinline__ void phase_seed_split(const GraphDev &g, const HopDev
             base[u] = run;
         }
         __syncthreads();
+        unsigned long long key = ~0ull;   // (gid << 32) | position, or none
         if (vt >= 0) {
             const int32_t p = wcnt[w][vt] + rank;
             if (p < hd.cap_nodes[vt]) {
                 hd.nodes[vt][p] = gid;
-                atomicAdd(kcnt + bucket_of(g, vt, gid), 1u);
+                if (sort)
+                    key = ((unsigned long long)gid << 32) | (uint32_t)p;
+                else
+                    atomicAdd(kcnt + bucket_of(g, vt, gid), 1u);
             } else {
                 atomicOr(meta + kMetaErr, kErrCapacity);
+            }
+        }
+        if (sort) {   // n <= blockDim.x: this is the only round
+            __shared__ unsigned long long sk[1024];
+            const int tid = threadIdx.x;
+            for (int k = 2; k <= (int)blockDim.x; k <<= 1)
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    unsigned long long y;
+                    if (j >= 32) {
+                        sk[tid] = key;
+                        __syncthreads();
+                        y = sk[tid ^ j];
+                        __syncthreads();
+                    } else {
+                        y = __shfl_xor_sync(0xffffffffu, key, j);
+                    }
+                    const bool up = (tid & k) == 0, low = (tid & j) == 0;
+                    key = (low == up) ? min(key, y) : max(key, y);
+                }
+            sk[tid] = key;
+            __syncthreads();
+            if (key != ~0ull) {
+                const uint32_t sg = (uint32_t)(key >> 32);
+                EG_DCHECK(tid < hd.cd.cap_members);
+                if (tid > 0 && (uint32_t)(sk[tid - 1] >> 32) == sg) atomicOr(meta + kMetaErr, kErrSeedDup);
+                hd.cd.mg[0][tid] = sg;
+                hd.cd.mp[0][tid] = (int32_t)(uint32_t)key;
+                int u = 0;
+                while (u + 1 < g.n_vt && (int64_t)sg >= g.off[u + 1]) ++u;
+                atomicAdd(hd.cd.mcnt + bucket_of(g, u, sg), 1u);   // members of level 1's buckets
             }
         }
         __syncthreads();
@@ -258,6 +297,8 @@ __device__ __forceinline__ void phase_count(const GraphDev &g, const HopDev &hd)
         ot = __shfl_sync(0xffffffffu, ot, 0);
         o16 = __shfl_sync(0xffffffffu, o16, 0);
         const uint32_t lt = lanemask_lt();
+        EG_DCHECK(oc + nc <= (uint32_t)hd.selq_cap && os + ns + ot + ntn <= (uint32_t)hd.selq_cap &&
+                  o16 + n16 <= (uint32_t)hd.selq_cap);
 #pragma unroll
         for (int q = 0; q < kCountItems; ++q) {
             if (mc[q] >> lane & 1) copyq[oc + __popc(mc[q] & lt)] = e[q];
