@@ -169,13 +169,13 @@ EG_API eg_status eg_set_feature_replica(eg_ctx *ctx, int32_t vt, const void *row
 
 /* Which feature-gather kernel the last enqueued gather used (instrumentation; the
  * kernel captured into the launched batch graph, or of the last eg_gather_features): 0 =
- * gather_tma_kernel (TMA: cp.async.bulk.tensor tile::gather4, four rows per operation,
- * for types whose full table is local with rows <= 1 KB and a multiple of 32 B; per-row
- * bulk copies otherwise, e.g. rows in peer shards read over NVLink), 1 = gather_ldg_kernel
- * (16-B vector loads), -1 = none yet.  Default (EG_GATHER=auto): TMA, except at world 1
- * when a requested type has no gather4 map (local per-row bulk copies are issue-bound);
- * EG_GATHER=tma|ldg forces one.  Rows wider than one 16 KB TMA stage always take the
- * LDG kernel. */
+ * gather_tma_kernel (TMA: cp.async.bulk.tensor tile::gather4, four rows per operation, from
+ * one tensor map per vertex type and owner shard -- the own table, or the IPC-mapped peer
+ * shards read over NVLink -- for rows <= 1 KB and a multiple of 16 B; per-row bulk copies
+ * otherwise), 1 = gather_ldg_kernel (16-B vector loads), -1 = none yet.  Default
+ * (EG_GATHER=auto, read at eg_create): TMA, except at world 1 when a requested type has no
+ * gather4 map (local per-row bulk copies are issue-bound); EG_GATHER=tma|ldg forces one.
+ * Rows wider than one 16 KB TMA stage always take the LDG kernel. */
 EG_API int32_t eg_gather_path(const eg_ctx *ctx);
 
 /* Sample L = n_hops blocks from `seeds` (gids, unique, any vertex types, caller

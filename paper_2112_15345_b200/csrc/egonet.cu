@@ -423,12 +423,15 @@ eg_status check_peer(eg_ctx *c, const ShardBlob &b, int p)
 }
 
 // All ranks mapped: validate the partition, global edge counts / max degrees.
+void build_gather_maps(eg_ctx *c);
+
 eg_status finalize_peers(eg_ctx *c)
 {
     std::string why;
     if (!check_metas(c->world, c->metas, c->rel_edges_total, c->rel_max_degree, &why))
         return fail(c, EG_EPEER, why);
     c->peers_ready = true;
+    build_gather_maps(c);   // per-owner maps over the peer shards, now mapped
     return EG_OK;
 }
 }  // namespace
@@ -459,29 +462,44 @@ EncodeTiledFn encode_tiled()
     return fn;
 }
 
-// gather4 tensor maps for the types whose full table is local (world 1, or a replica):
-// [N_t][row_bytes / 4] u32, box {row_bytes / 4, 1}.  Rows must be <= 1 KB (box <= 256
-// elements); the kernel places each 4-row group at a 128-B aligned stage offset.
-// A type without a map is gathered by the other paths (same bytes).
+// gather4 tensor maps (kernels.h GatherMaps): a type whose full table is on this GPU (world
+// 1, or a replica) gets one map over it; otherwise, once every peer is mapped, one map per
+// owner shard (own and peers').  Rows must be <= 1 KB (box <= 256 elements) and a multiple
+// of 16 B; the kernel places each 4-row group at a 128-B aligned stage offset.  A type
+// without maps is gathered by the other paths (same bytes).
+bool encode_map(EncodeTiledFn fn, CUtensorMap *m, const void *base, int64_t rb, int64_t n)
+{
+    if (!base || rb <= 0 || rb > 1024 || rb % 16 || n < 1 || n > INT32_MAX || ((uintptr_t)base & 15)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)(rb / 4), (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)rb};
+    cuuint32_t box[2] = {(cuuint32_t)(rb / 4), 1u};
+    cuuint32_t es[2] = {1u, 1u};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void build_gather_maps(eg_ctx *c)
 {
     EncodeTiledFn fn = encode_tiled();
-    for (int u = 0; u < EG_MAX_VT; ++u) c->gmaps.ok[u] = 0;
+    for (int u = 0; u < EG_MAX_VT; ++u) c->gmaps.grp[u] = c->gmaps.whole[u] = 0;
     if (!fn) return;
     for (int u = 0; u < c->g.n_vt; ++u) {
         const int64_t rb = c->f.row_bytes[u];
-        const void *base = c->f.replica[u];
-        if (!base && c->world == 1 && !c->host_feat[u]) base = c->f.rows[u][c->rank];
-        const int64_t n = c->vt_counts[u];
-        if (!base || rb <= 0 || rb > 1024 || rb % 16 || n < 1 || n > INT32_MAX || ((uintptr_t)base & 15)) continue;
-        cuuint64_t dims[2] = {(cuuint64_t)(rb / 4), (cuuint64_t)n};
-        cuuint64_t strides[1] = {(cuuint64_t)rb};
-        cuuint32_t box[2] = {(cuuint32_t)(rb / 4), 1u};
-        cuuint32_t es[2] = {1u, 1u};
-        if (fn(&c->gmaps.map[u], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-            c->gmaps.ok[u] = 1;
+        if (c->host_feat[u] || !rb) continue;
+        const void *whole = c->f.replica[u];
+        if (!whole && c->world == 1) whole = c->f.rows[u][c->rank];
+        if (whole) {
+            if (encode_map(fn, &c->gmaps.map[u][0], whole, rb, c->vt_counts[u])) c->gmaps.grp[u] = c->gmaps.whole[u] = 1;
+            continue;
+        }
+        if (c->attached != (1u << c->world) - 1) continue;   // peers not mapped yet
+        bool all = true;
+        for (int p = 0; p < c->world && all; ++p) {
+            const int64_t n = c->g.bounds[u][p + 1] - c->g.bounds[u][p];
+            all = n == 0 || encode_map(fn, &c->gmaps.map[u][p], c->f.rows[u][p], rb, n);
+        }
+        c->gmaps.grp[u] = all ? 1 : 0;
     }
 }
 

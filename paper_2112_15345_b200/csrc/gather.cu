@@ -233,7 +233,7 @@ __device__ __forceinline__ int64_t group_stride(const FeatDev &f, int u)
 __device__ __forceinline__ int32_t rows_per_tile(const FeatDev &f, const GatherMaps &m, int u)
 {
     const int64_t rb = f.row_bytes[u];
-    if (m.ok[u]) return (int32_t)min((int64_t)kMaxRowsPerTile, 4 * ((int64_t)kStageBytes / group_stride(f, u)));
+    if (m.grp[u]) return (int32_t)min((int64_t)kMaxRowsPerTile, 4 * ((int64_t)kStageBytes / group_stride(f, u)));
     const int32_t r = rb ? (int32_t)min((int64_t)kMaxRowsPerTile, (int64_t)kStageBytes / rb) : 1;
     return r > 0 ? r : 1;
 }
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
         auto prefetch = [&](int64_t j, Pre &p) {
             tile_of(gs, f, m, V, cur, blockIdx.x + j * gridDim.x, p.b, p.u, p.row0, p.nrows);
             const int64_t *ids = gs.b[p.b].nodes[p.u] + p.row0;
-            const bool grp = m.ok[p.u] != 0;
+            const bool grp = m.grp[p.u] != 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int rr = grp ? min(4 * lane + q, p.nrows - 1) : lane + 32 * q;
@@ -316,17 +316,35 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             const int32_t nrows = cu.nrows;
             const int64_t rb = f.row_bytes[u];
             uint8_t *dst = stage_mem + s * kStageBytes;
-            if (m.ok[u]) {
+            if (m.grp[u]) {
                 // groups of 4 rows, one gather4 each, at 128-B aligned group strides (a
                 // ragged last group repeats its last row: 4 rows always land, inside the
-                // stage since rows_per_tile counts whole groups)
+                // stage since rows_per_tile counts whole groups).  A group whose rows span
+                // two owner shards is fetched row by row into the same layout.
                 const int ng = (nrows + 3) >> 2;
                 if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(ng * 4 * rb));
                 __syncwarp();
                 if (lane < ng) {
-                    const int32_t o = (int32_t)g.off[u];
-                    gather4_g2s(dst + lane * group_stride(f, u), &m.map[u], (int32_t)cu.id[0] - o,
-                                (int32_t)cu.id[1] - o, (int32_t)cu.id[2] - o, (int32_t)cu.id[3] - o, &full[s]);
+                    uint8_t *gdst = dst + lane * group_stride(f, u);
+                    int64_t tid[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tid[q] = cu.id[q] - g.off[u];
+                    int p0 = 0;
+                    bool same = true;
+                    if (!m.whole[u]) {
+                        p0 = owner_of(g, u, tid[0]);
+#pragma unroll
+                        for (int q = 1; q < 4; ++q) same &= tid[q] >= g.bounds[u][p0] && tid[q] < g.bounds[u][p0 + 1];
+                    }
+                    if (same) {
+                        const int64_t lo = m.whole[u] ? 0 : g.bounds[u][p0];
+                        gather4_g2s(gdst, &m.map[u][p0], (int32_t)(tid[0] - lo), (int32_t)(tid[1] - lo),
+                                    (int32_t)(tid[2] - lo), (int32_t)(tid[3] - lo), &full[s]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            bulk_g2s(gdst + q * rb, feature_row(g, f, u, tid[q]), (uint32_t)rb, &full[s]);
+                    }
                 }
             } else {
                 if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(nrows * rb));
@@ -352,7 +370,7 @@ __global__ void __launch_bounds__(64, 1) gather_tma_kernel(const __grid_constant
             const int64_t rb = f.row_bytes[u];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             const int64_t gsz = group_stride(f, u);
-            if (!m.ok[u] || gsz == 4 * rb) {   // rows contiguous in the stage: one store
+            if (!m.grp[u] || gsz == 4 * rb) {   // rows contiguous in the stage: one store
                 bulk_s2g(gs.b[b].out[u] + row0 * rb, stage_mem + s * kStageBytes, (uint32_t)(nrows * rb));
             } else {                             // padded groups: one store per group
                 for (int q = 0; 4 * q < nrows; ++q)
@@ -385,7 +403,7 @@ int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gd, cons
         bool ldg = false;
         for (int b = 0; b < gd.nb; ++b)
             for (int u = 0; u < g.n_vt; ++u)
-                if (gd.b[b].out[u] && !m.ok[u] && g.world == 1) ldg = true;
+                if (gd.b[b].out[u] && !m.grp[u] && g.world == 1) ldg = true;
         mode = ldg ? 1 : 0;
     }
     if (mode == 1) {

@@ -46,12 +46,16 @@ int launch_batch(const GraphDev &g, const BatchDev *bd_dev, int n_hops, const in
                  cudaStream_t s, const Fork &fk, bool serial, bool lp, bool seed_sort);
 
 // TMA tensor maps of the feature tables the gather reads with cp.async.bulk.tensor
-// tile::gather4 (four rows per TMA operation): per vertex type one 2-D map over its full
-// local table ([n_rows][row_bytes / 4] u32, box {row_bytes / 4, 1}).  ok[u] == 0: the
-// type's rows are read otherwise (owner shards at world > 1, rows > 1 KB, host memory).
+// tile::gather4 (four rows per TMA operation): per vertex type and owner rank one 2-D map
+// over that owner's table ([n_rows][row_bytes / 4] u32, box {row_bytes / 4, 1}) -- the own
+// shard, the IPC-mapped peer shards (read over NVLink), or, for a type whose full table is
+// on this GPU (world 1, a replica), one map over it (owner 0, rows by type-local id).
+// grp[u]: the type's rows are staged in 4-row groups (every owner has a map); a group whose
+// four rows span two owners is fetched by per-row copies into the same layout.
 struct __align__(64) GatherMaps {
-    CUtensorMap map[EG_MAX_VT];
-    int32_t ok[EG_MAX_VT];
+    CUtensorMap map[EG_MAX_VT][EG_MAX_RANKS];
+    int32_t grp[EG_MAX_VT];
+    int32_t whole[EG_MAX_VT];   // one map over the full table (owner 0)
 };
 
 // gather.cu

@@ -11,3 +11,7 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
     bench.py --gpus 2 --steps 20 --warmup 5 --no-e2e --out $D/bench_c4_n2.json > $D/bench_n2.log 2>&1; echo bench2=$?
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 \
     bench.py --gpus 2 --config C3 --steps 20 --warmup 5 --no-e2e --out $D/bench_c3_n2.json > $D/bench_c3_n2.log 2>&1; echo bench3=$?
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29535 \
+    bench.py --gpus 2 --config C2 --steps 20 --warmup 5 --no-e2e --out $D/bench_c2_n2.json > $D/bench_c2_n2.log 2>&1; echo bench2c2=$?
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29536 \
+    tests/dist_gpu_parity.py --config C4 --batches 2 --depth 2 --bundle 4 > $D/dist_parity_c4.log 2>&1; echo distc4=$?
