@@ -298,6 +298,14 @@ EG_API eg_status eg_blocks_wait(eg_blocks *blocks);
 EG_API eg_status eg_blocks_features(const eg_blocks *blocks, int32_t u, const void **rows, int64_t *n_rows,
                                     int64_t *row_bytes);
 
+/* Copy the feature rows gathered in the batch's launch (EG_FEATURES) to caller memory:
+ * host[u] (host array [n_vt]; NULL skips u) receives n_inputs(u) x row_bytes(u) bytes,
+ * pinned host memory for an asynchronous DMA (pageable memory works, synchronously).
+ * Stream-ordered on the context's stream after the batch's launch (waits for its sizes
+ * first); flags & EG_ASYNC: returns after enqueueing, else synchronizes the stream.
+ * EG_EINVAL: null pointers, a type without gathered rows; EG_ESTATE: orphaned handle. */
+EG_API eg_status eg_blocks_copy_features(const eg_blocks *blocks, void *const *host, int32_t flags);
+
 /* Host view of block `hop` (0 <= hop < n_hops).  Pointers stay valid until
  * eg_blocks_free. */
 EG_API eg_status eg_block_view_get(const eg_blocks *blocks, int32_t hop, eg_block_view *out);

@@ -167,6 +167,7 @@ struct eg_ctx {
     int compact = 0;                      // EG_COMPACT at create: 0 default, 1 bitmap path for every bucket
     int prio = 1;                         // EG_PRIO at create: 0 none, 1 gather first, 2 sampling first
     int gather_mode = 2;                  // EG_GATHER at create: 0 tma, 1 ldg, 2 auto (gather.cu)
+    bool peer_maps = true;                // EG_PEER_MAPS=0 at create: no gather4 maps over peer shards (A/B)
     std::vector<std::string> trace_names;
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
@@ -493,7 +494,7 @@ void build_gather_maps(eg_ctx *c)
             if (encode_map(fn, &c->gmaps.map[u][0], whole, rb, c->vt_counts[u])) c->gmaps.grp[u] = c->gmaps.whole[u] = 1;
             continue;
         }
-        if (c->attached != (1u << c->world) - 1) continue;   // peers not mapped yet
+        if (!c->peer_maps || c->attached != (1u << c->world) - 1) continue;   // peers not mapped yet
         bool all = true;
         for (int p = 0; p < c->world && all; ++p) {
             const int64_t n = c->g.bounds[u][p + 1] - c->g.bounds[u][p];
@@ -582,6 +583,8 @@ eg_status eg_create(int32_t rank, int32_t world, int32_t device, void *stream, e
         // duration in the pipelined run by 8-20 % at unchanged throughput (C2, C4).
         const char *pr = getenv("EG_PRIO");
         c->prio = !pr ? 1 : (pr[0] == 'g' ? 1 : (pr[0] == 's' ? 2 : 0));
+        const char *pm = getenv("EG_PEER_MAPS");
+        c->peer_maps = !(pm && pm[0] == '0');
         const char *ga = getenv("EG_GATHER");
         c->gather_mode = !ga ? 2 : (!strcmp(ga, "tma") ? 0 : (!strcmp(ga, "ldg") ? 1 : 2));
     }
@@ -1660,6 +1663,25 @@ eg_status eg_blocks_features(const eg_blocks *cb, int32_t u, const void **rows, 
     *rows = b->feat[u];
     *n_rows = b->feat[u] ? b->n_nodes[b->n_hops][u] : 0;
     *row_bytes = b->feat[u] ? b->ctx->f.row_bytes[u] : 0;
+    return EG_OK;
+}
+
+eg_status eg_blocks_copy_features(const eg_blocks *cb, void *const *host, int32_t flags)
+{
+    if (!cb || !host) return EG_EINVAL;
+    eg_blocks *b = const_cast<eg_blocks *>(cb);
+    if (!b->ctx) return EG_ESTATE;
+    eg_ctx *c = b->ctx;
+    eg_status st = enter(c);
+    if (st) return st;
+    if ((st = finish(b))) return st;   // sizes (the launch has completed on its lane)
+    for (int u = 0; u < b->n_vt; ++u) {
+        if (!host[u]) continue;
+        if (!b->feat[u]) return fail(c, EG_EINVAL, "vertex type " + std::to_string(u) + " has no gathered rows");
+        const int64_t bytes = b->n_nodes[b->n_hops][u] * c->f.row_bytes[u];
+        if (bytes) EG_CUDA(c, cudaMemcpyAsync(host[u], b->feat[u], (size_t)bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (!(flags & EG_ASYNC)) EG_CUDA(c, cudaStreamSynchronize(c->stream));
     return EG_OK;
 }
 

@@ -31,7 +31,7 @@ ABI_SYMBOLS = [
     "eg_range_bounds", "eg_batch_caps", "eg_attach_peer", "eg_sample_minibatch", "eg_blocks_wait",
     "eg_blocks_features", "eg_check_shard_metas", "eg_trace_get", "eg_set_pipeline", "eg_sample_bundle",
     "eg_blocks_stats", "eg_sample_lp_bundle", "eg_lp_view_get", "eg_sage_mean_layer", "eg_set_feature_replica",
-    "eg_gather_path", "eg_counter_bytes",
+    "eg_gather_path", "eg_counter_bytes", "eg_blocks_copy_features",
 ]
 
 EG_FEATURES = 1
@@ -156,6 +156,7 @@ def lib(build_if_missing: bool = True):
         L.eg_blocks_wait.argtypes = [vp]
         L.eg_blocks_stats.argtypes = [vp, P(c.c_int64), vp]
         L.eg_blocks_features.argtypes = [vp, c.c_int32, P(vp), P(c.c_int64), P(c.c_int64)]
+        L.eg_blocks_copy_features.argtypes = [vp, vp, c.c_int32]
         L.eg_blocks_n_hops.argtypes = [vp]
         L.eg_blocks_n_hops.restype = c.c_int32
         L.eg_blocks_n_inputs.argtypes = [vp, c.c_int32]
@@ -356,6 +357,20 @@ class Blocks:
             return torch.empty((0,) + shape, dtype=dt, device=self._ctx.device)
         raw = _wrap(ptr.value, n.value * rb.value // 4, "<i4", self, self._ctx.device)
         return raw.view(dt).view((n.value,) + shape)
+
+    def copy_features(self, host, async_: bool = False):
+        """eg_blocks_copy_features: the rows gathered in this batch's launch into caller
+        memory, host[u] (pinned CPU tensors / numpy arrays with room for n_inputs(u) rows;
+        None skips u).  async_: stream-ordered on the context's stream, not synchronized."""
+        V = len(self._ctx.vt_counts)
+        ptrs = (ctypes.c_void_p * V)()
+        for u in range(V):
+            o = host[u] if u < len(host) else None
+            ptrs[u] = None if o is None else (o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data)
+        rc = lib().eg_blocks_copy_features(self._h, ptrs, EG_ASYNC if async_ else 0)
+        if rc:
+            raise EgError(rc, lib().eg_last_error(self._ctx._h).decode())
+        self._inputs = None
 
     @property
     def handle(self):

@@ -232,3 +232,37 @@ def test_c4l_world4_confined_seeds():
             bl.free()
     for c in ctxs:
         c.close()
+
+
+# ----------------------------------------------------------------------------- host copies
+
+def test_copy_features_to_host():
+    """eg_blocks_copy_features: the rows gathered in a bundle's launch copied to pinned host
+    tensors through the C ABI (the e2e path of bench.py), async + one synchronize, equal the
+    oracle's gather; orphaned / featureless handles are rejected."""
+    import torch
+    from paper_2112_15345_b200 import EgError
+    cfg = synth.config("C2")
+    g = synth.build_host_graph(cfg)
+    rows = {u: synth.host_features(cfg, u) for u in cfg.feats}
+    ctx = _ctx(g)
+    ctx.set_pipeline(2, 4)
+    gis = [300, 301, 302]
+    dev = [torch.from_numpy(synth.batch_seeds(cfg, x)).cuda() for x in gis]
+    bls = ctx.sample_bundle(dev, cfg.fanouts, [synth.rng_seed(cfg, x) for x in gis], features=True, async_=True)
+    outs = []
+    for bl in bls:
+        _, n = bl.stats()
+        host = [torch.empty((n[u], cfg.feats[u][0]), dtype=torch.float32).pin_memory() for u in range(cfg.n_vt)]
+        bl.copy_features(host, async_=True)
+        outs.append(host)
+    torch.cuda.synchronize()
+    for x, host in zip(gis, outs):
+        res = oracle.sample(g, synth.batch_seeds(cfg, x), cfg.fanouts, synth.rng_seed(cfg, x))
+        assert_same_features(res, host, cfg, rows)
+    b = ctx.sample_minibatch(dev[0], cfg.fanouts, 1, features=False)
+    with pytest.raises(EgError):
+        b.copy_features([torch.empty(1).pin_memory()] * cfg.n_vt)
+    for bl in bls + [b]:
+        bl.free()
+    ctx.close()
