@@ -55,5 +55,19 @@ def build(force: bool = False, verbose: bool = False, check: bool = False) -> st
     return so
 
 
+def build_variant(name: str, defines) -> str:
+    """A/B builds: libegonet_<name>.so with extra -D defines (load with EG_LIB=<path>)."""
+    so = os.path.join(PKG, f"libegonet_{name}.so")
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp, *sources()]
+    subprocess.check_call(cmd)
+    os.replace(tmp, so)
+    return so
+
+
 if __name__ == "__main__":
+    if "--variant" in sys.argv:   # build.py --variant NAME DEF=VAL ...
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, check="--check" in sys.argv))

@@ -56,7 +56,16 @@ __global__ void __launch_bounds__(1024) k_seed(const __grid_constant__ GraphDev 
     phase_seed_split(g, bd->seedh[blockIdx.y], bd->seeds[blockIdx.y], bd->seed_sort != 0);
 }
 
-__global__ void __launch_bounds__(kCountThreads) k_count(const __grid_constant__ GraphDev g,
+#ifndef EG_COUNT_MINB
+#define EG_COUNT_MINB 4
+#endif
+#ifndef EG_COPY_MINB
+#define EG_COPY_MINB 4
+#endif
+#ifndef EG_SCATTER_MINB
+#define EG_SCATTER_MINB 6
+#endif
+__global__ void __launch_bounds__(kCountThreads, EG_COUNT_MINB) k_count(const __grid_constant__ GraphDev g,
                                                          const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 4 + 8 * h);
@@ -74,7 +83,7 @@ __global__ void __launch_bounds__(kBatchThreads, EG_SELECT_MIN_BLOCKS) k_select(
     phase_select(g, bd->hop[blockIdx.y][h], blockIdx.x, gridDim.x, s_cand[threadIdx.x >> 5]);
 }
 
-__global__ void __launch_bounds__(kBatchThreads, 3) k_copy(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, EG_COPY_MINB) k_copy(const __grid_constant__ GraphDev g,
                                                         const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 7 + 8 * h);
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(kScanThreads) k_kscan(const __grid_constant__ 
     phase_kscan(g, hop_of(bd, h));
 }
 
-__global__ void __launch_bounds__(kBatchThreads) k_scatter(const __grid_constant__ GraphDev g,
+__global__ void __launch_bounds__(kBatchThreads, EG_SCATTER_MINB) k_scatter(const __grid_constant__ GraphDev g,
                                                            const BatchDev *__restrict__ bd, int h)
 {
     stamp(bd, 2 + 8 * (h + 1));

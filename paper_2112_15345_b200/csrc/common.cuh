@@ -43,7 +43,10 @@ constexpr int kMaxScanTiles = (int)(kMaxBuckets / kScanTile);     // 32: one war
 // Count tiles (single pass with a decoupled look-back per relation): kCountThreads threads
 // x kCountItems consecutive dst items each.
 constexpr int kCountThreads = 256;
-constexpr int kCountItems = 4;
+#ifndef EG_COUNT_ITEMS
+#define EG_COUNT_ITEMS 4
+#endif
+constexpr int kCountItems = EG_COUNT_ITEMS;
 constexpr int kCountTile = kCountThreads * kCountItems;
 constexpr int kSelCap = 512;              // candidate slots per warp (selection)
 constexpr int kSelMaxK = 112;             // fast selection path for k <= this

@@ -36,8 +36,14 @@
 
 namespace eg {
 
-constexpr int kTaskElems = 224;    // T: a run of small buckets closes once its elements cross a multiple of T
-constexpr int kBigBucket = 32;     // buckets with more elements are tasks of their own (bitmap path)
+#ifndef EG_TASK_ELEMS
+#define EG_TASK_ELEMS 224
+#endif
+#ifndef EG_BIG_BUCKET
+#define EG_BIG_BUCKET 32
+#endif
+constexpr int kTaskElems = EG_TASK_ELEMS;   // T: a run of small buckets closes once its elements cross a multiple of T
+constexpr int kBigBucket = EG_BIG_BUCKET;   // buckets with more elements are tasks of their own (bitmap path)
 constexpr int kSortCap = 256;      // elements of a sort-path task: 8 per lane
 static_assert(kTaskElems + kBigBucket <= kSortCap, "a run holds < T + kBigBucket elements");
 constexpr int kMaxWordsPerLane = 1 << (kMaxBucketShift - 10);   // bitmap words of a bucket per lane
