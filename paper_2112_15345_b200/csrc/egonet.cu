@@ -172,8 +172,6 @@ struct eg_ctx {
     std::vector<double> trace_ms;
     std::vector<int64_t> trace_n;
     std::set<eg_blocks *> live;           // handles not yet freed (orphaned by eg_destroy)
-    void *sage_buf = nullptr;             // eg_sage_mean_layer's A scratch (grown on demand)
-    size_t sage_cap = 0;
 };
 
 struct eg_blocks {
@@ -1592,35 +1590,8 @@ eg_status eg_sage_mean_layer(eg_ctx *c, const eg_blocks *cb, int32_t hop, int32_
     uint32_t cols = 32;
     while ((int)cols < H) cols <<= 1;
     a.tmem_cols = cols;
-    if (a.n_dst == 0) return EG_OK;
-    // the aggregation kernel's output A = [x_dst | mean] (bf16 [n_dst][Kp]) and its TMA map
-    const int Kp = sage_kp(F, x_dst != nullptr);
-    const size_t abytes = (size_t)a.n_dst * Kp * 2;
-    if (abytes > c->sage_cap) {
-        if (c->sage_buf) {
-            EG_CUDA(c, cudaStreamSynchronize(c->stream));
-            EG_CUDA(c, cudaFree(c->sage_buf));
-            c->sage_buf = nullptr;
-            c->sage_cap = 0;
-        }
-        EG_CUDA(c, cudaMalloc(&c->sage_buf, abytes));
-        c->sage_cap = abytes;
-    }
-    a.abuf = c->sage_buf;
-    EncodeTiledFn fn = encode_tiled();
-    if (!fn) return fail(c, EG_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    {
-        cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)a.n_dst};
-        cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
-        cuuint32_t box[2] = {64u, 128u};
-        cuuint32_t es[2] = {1u, 1u};
-        if (fn(&a.amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->sage_buf, dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return fail(c, EG_ECUDA, "sage: A tensor map encode failed");
-    }
     EG_CUDA(c, launch_sage(a, x_dtype, c->stream));
-    c->launches += 2;
+    ++c->launches;
     return EG_OK;
 }
 
@@ -1854,7 +1825,6 @@ eg_status eg_destroy(eg_ctx *c)
         if (ln.stream) cudaStreamDestroy(ln.stream);
     }
     c->lanes.clear();
-    if (c->sage_buf) cudaFree(c->sage_buf);
     delete c;
     return EG_OK;
 }

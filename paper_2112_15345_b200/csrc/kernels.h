@@ -65,9 +65,7 @@ int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cons
                   int mode);
 
 // sage.cu: one GraphSAGE-mean layer over a block relation on the tensor cores (NEXT-4 i).
-struct __align__(64) SageArgs {
-    CUtensorMap amap;           // A = [x_dst | mean] bf16 [n_dst][Kp] (abuf), box {64, 128}, 128-B swizzle
-    void *abuf;                 // scratch of the aggregation kernel (n_dst x Kp bf16)
+struct SageArgs {
     const int32_t *indptr;      // block CSC over the dst vertices (n_dst + 1)
     const int32_t *indices;     // local src ids
     const void *x_src;          // [n_src][ld_src] input rows of the relation's src nodes
@@ -81,7 +79,6 @@ struct __align__(64) SageArgs {
 };
 cudaError_t launch_sage(const SageArgs &a, int x_dtype, cudaStream_t s);   // x_dtype 0 f32, 1 f16, 2 bf16
 size_t sage_smem_bytes(int F, int H, bool self_term);
-inline int sage_kp(int F, bool self_term) { return (self_term ? 2 : 1) * ((F + 63) / 64 * 64); }
 
 // store.cu
 void launch_max_degree(const int64_t *indptr, int64_t n, unsigned long long *out, cudaStream_t s);

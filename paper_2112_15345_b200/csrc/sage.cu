@@ -19,8 +19,6 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
-#include <algorithm>
-
 #include "kernels.h"
 
 namespace eg {
@@ -45,6 +43,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr)
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int n)
 {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init1(uint64_t *bar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity)
@@ -125,170 +129,133 @@ __device__ __forceinline__ void store_bf16(uint8_t *base, int rows, int row, int
 }
 
 constexpr int kTileM = 128;
+// warps per CTA (A-operand builders; TMEM lane group = warp % 4): as many as the
+// registers allow -- the A build is a latency-bound gather (ncu: 16 warps, 25 %
+// occupancy, stalls on the row loads)
+template <int CPL> __host__ __device__ constexpr int warps_for() { return CPL <= 4 ? 32 : 16; }
 
-// ---------------------------------------------------------------------------- kernel 1
-
-// A = [bf16(x_dst) | bf16(mean of the sampled in-neighbours' rows)] as a row-major bf16
-// matrix [n_dst][Kp] (columns >= F of each part are 0).  A warp per pair of dst rows,
-// CPL consecutive columns per lane, four neighbour-row reads in flight; full occupancy
-// (the mean is a latency-bound gather: round 1 built it inside the GEMM kernel, one CTA per
-// SM, 25 % occupancy).  The mean is accumulated in fp32 (reading C2).
+// CPL = Fp / 32 columns per lane (Fp = F rounded up to 64).
 template <typename T, int CPL>
-__global__ void __launch_bounds__(256) sage_aggregate(const __grid_constant__ SageArgs a)
+__global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __grid_constant__ SageArgs a)
 {
-    constexpr int Fp = CPL * 32;
-    const int parts = a.x_dst ? 2 : 1;
-    const int Kp = parts * Fp;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const T *xs = static_cast<const T *>(a.x_src);
-    const T *xd = static_cast<const T *>(a.x_dst);
-    __nv_bfloat16 *A = static_cast<__nv_bfloat16 *>(a.abuf);
-    const int c = lane * CPL;
-    auto store = [&](int64_t row, int col, const float (&v)[CPL]) {
-        uint32_t p[CPL / 2];
-#pragma unroll
-        for (int e = 0; e < CPL / 2; ++e) {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-            p[e] = *reinterpret_cast<const uint32_t *>(&h);
-        }
-        __nv_bfloat16 *dst = A + row * Kp + col;
-        if constexpr (CPL == 8) *reinterpret_cast<uint4 *>(dst) = make_uint4(p[0], p[1], p[2], p[3]);
-        else if constexpr (CPL == 4) *reinterpret_cast<uint2 *>(dst) = make_uint2(p[0], p[1]);
-        else *reinterpret_cast<uint32_t *>(dst) = p[0];
-    };
-    for (int64_t pr = warp; 2 * pr < a.n_dst; pr += nw) {
-        const int64_t v0 = 2 * pr, v1 = v0 + 1;
-        const bool has1 = v1 < a.n_dst;
-        int j = 0;
-        if (lane < 3) j = __ldg(a.indptr + min(v0 + lane, (int64_t)a.n_dst));
-        const int a0 = __shfl_sync(0xffffffffu, j, 0), a1 = __shfl_sync(0xffffffffu, j, 1);
-        const int b0 = has1 ? a1 : 0, b1 = has1 ? __shfl_sync(0xffffffffu, j, 2) : 0;
-        if (xd) {
-            float s0[CPL], s1[CPL];
-            load_cols<T, CPL>(xd + v0 * a.ld_dst, c, a.F, s0);
-            if (has1) load_cols<T, CPL>(xd + v1 * a.ld_dst, c, a.F, s1);
-            store(v0, c, s0);
-            if (has1) store(v1, c, s1);
-        }
-        float acc0[CPL], acc1[CPL];
-#pragma unroll
-        for (int e = 0; e < CPL; ++e) acc0[e] = acc1[e] = 0.f;
-        for (int ja = a0, jb = b0; ja < a1 || jb < b1; ja += 2, jb += 2) {   // four rows in flight
-            int ix[4];
-            ix[0] = ja < a1 ? __ldg(a.indices + ja) : -1;
-            ix[1] = ja + 1 < a1 ? __ldg(a.indices + ja + 1) : -1;
-            ix[2] = jb < b1 ? __ldg(a.indices + jb) : -1;
-            ix[3] = jb + 1 < b1 ? __ldg(a.indices + jb + 1) : -1;
-            float t[4][CPL];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (ix[q] >= 0) load_cols<T, CPL>(xs + (int64_t)ix[q] * a.ld_src, c, a.F, t[q]);
-                else
-#pragma unroll
-                    for (int e = 0; e < CPL; ++e) t[q][e] = 0.f;
-            }
-#pragma unroll
-            for (int e = 0; e < CPL; ++e) {
-                acc0[e] += t[0][e] + t[1][e];
-                acc1[e] += t[2][e] + t[3][e];
-            }
-        }
-        const float i0 = a1 > a0 ? 1.f / (float)(a1 - a0) : 0.f, i1 = b1 > b0 ? 1.f / (float)(b1 - b0) : 0.f;
-#pragma unroll
-        for (int e = 0; e < CPL; ++e) {
-            acc0[e] *= i0;
-            acc1[e] *= i1;
-        }
-        store(v0, (parts - 1) * Fp + c, acc0);
-        if (has1) store(v1, (parts - 1) * Fp + c, acc1);
-    }
-}
-
-// ---------------------------------------------------------------------------- kernel 2
-
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int32_t c0, int32_t c1, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-            "r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-
-// z = A [W_self | W_neigh]^T on the tensor cores: persistent CTAs of 4 warps; W (H x Kp)
-// staged once per CTA in the canonical K-major 128-B-swizzled layout; per tile of 128 rows
-// the A tile arrives by TMA (Kp / 64 boxes of 128 rows x 128 B, the same layout), one thread
-// issues Kp / 16 tcgen05.mma (M = 128, N = H) into TMEM and commits; as soon as the MMAs
-// are done the next tile's A is requested, so its load overlaps this tile's epilogue
-// (tcgen05.ld of the accumulator, fp32 rows out).
-__global__ void __launch_bounds__(128, 1) sage_gemm(const __grid_constant__ SageArgs a, int Kp)
-{
+    constexpr int kWarps = warps_for<CPL>();
+    constexpr int kRowsPerWarp = kTileM / kWarps;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    constexpr int Fp = CPL * 32;
+    const int parts = a.x_dst ? 2 : 1;                // [self | neigh] or [neigh]
+    const int Kp = parts * Fp;
     uint8_t *sB = smem;                               // H x Kp
     uint8_t *sA = smem + (size_t)a.H * Kp * 2;        // 128 x Kp
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sA + (size_t)kTileM * Kp * 2);
-    uint64_t *a_full = bars, *mma_done = bars + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sA + (size_t)kTileM * Kp * 2);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = (a.n_dst + kTileM - 1) / kTileM;
-    const uint32_t a_bytes = (uint32_t)kTileM * Kp * 2;
+
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
                      "r"(a.tmem_cols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (threadIdx.x == 32) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(a_full)) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mma_done)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // the first A tile in flight while W is staged
-    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&a.amap) : "memory");
-        mbar_expect(a_full, a_bytes);
-        for (int kb = 0; kb < Kp / 64; ++kb)
-            tma_load_2d(sA + (size_t)kb * kTileM * 128, &a.amap, kb * 64, (int)blockIdx.x * kTileM, a_full);
-    }
-    const int parts = a.x_dst ? 2 : 1;
-    const int Fp = Kp / parts;
+    if (threadIdx.x == 32) mbar_init1(mbar);
+    // W -> sB: padded column kp of part p maps to W column p * F + (kp - p * Fp)
     const int K = parts * a.F;
     const __nv_bfloat16 *wt = static_cast<const __nv_bfloat16 *>(a.w);
     const bool wvec = (a.F % 8) == 0 && ((uintptr_t)a.w % 16) == 0;   // 16-B chunks of W rows
     for (int i = threadIdx.x; i < a.H * (Kp / 8); i += blockDim.x) {
         const int n = i / (Kp / 8), kp = (i % (Kp / 8)) * 8;
-        const int p = kp / Fp, cc = kp - p * Fp;
+        const int p = kp / Fp, c = kp - p * Fp;
         uint8_t *dst = sB + sw128_off(a.H, n, kp);
-        if (wvec) {
-            const uint4 v = cc < a.F ? __ldg(reinterpret_cast<const uint4 *>(wt + (int64_t)n * K + p * a.F + cc))
-                                     : make_uint4(0, 0, 0, 0);
+        if (wvec) {   // bf16 bits copied as they are
+            const uint4 v = c < a.F ? __ldg(reinterpret_cast<const uint4 *>(wt + (int64_t)n * K + p * a.F + c))
+                                    : make_uint4(0, 0, 0, 0);
             *reinterpret_cast<uint4 *>(dst) = v;
         } else {
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-                v[e] = cc + e < a.F ? __bfloat162float(wt[(int64_t)n * K + p * a.F + cc + e]) : 0.f;
+                v[e] = c + e < a.F ? __bfloat162float(wt[(int64_t)n * K + p * a.F + c + e]) : 0.f;
             store_bf16<8>(sB, a.H, n, kp, v);
         }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // W (generic stores) -> tensor core
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     const uint32_t idesc = idesc_bf16_f32(a.H);
+    const T *xs = static_cast<const T *>(a.x_src);
+    const T *xd = static_cast<const T *>(a.x_dst);
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+
+    for (int tile = blockIdx.x; tile * kTileM < a.n_dst; tile += gridDim.x) {
         const int row0 = tile * kTileM;
-        mbar_wait_parity(a_full, phase);
+        // ---- A operand: warp w builds rows w + kWarps q, two rows at a time with
+        // independent accumulators; the rows' CSC bounds are loaded up front (lane q)
+        const int c = lane * CPL;
+        int jq0 = 0, jq1 = 0;
+        if (lane < kRowsPerWarp) {
+            const int v = row0 + warp + kWarps * lane;
+            if (v < a.n_dst) {
+                jq0 = __ldg(a.indptr + v);
+                jq1 = __ldg(a.indptr + v + 1);
+            }
+        }
+#pragma unroll 1
+        for (int rp = 0; rp < kRowsPerWarp; rp += 2) {
+            const int r0 = warp + kWarps * rp, r1 = r0 + kWarps;
+            const int v0 = row0 + r0, v1 = row0 + r1;
+            const int a0 = __shfl_sync(0xffffffffu, jq0, rp), a1 = __shfl_sync(0xffffffffu, jq1, rp);
+            const int b0 = __shfl_sync(0xffffffffu, jq0, rp + 1), b1 = __shfl_sync(0xffffffffu, jq1, rp + 1);
+            float acc0[CPL], acc1[CPL];
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc0[e] = acc1[e] = 0.f;
+            if (xd) {
+                float s0[CPL], s1[CPL];
+                if (v0 < a.n_dst) load_cols<T, CPL>(xd + (int64_t)v0 * a.ld_dst, c, a.F, s0);
+                else
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) s0[e] = 0.f;
+                if (v1 < a.n_dst) load_cols<T, CPL>(xd + (int64_t)v1 * a.ld_dst, c, a.F, s1);
+                else
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) s1[e] = 0.f;
+                store_bf16<CPL>(sA, kTileM, r0, c, s0);
+                store_bf16<CPL>(sA, kTileM, r1, c, s1);
+            }
+            // two edges of each row per step: four independent row reads in flight
+            for (int ja = a0, jb = b0; ja < a1 || jb < b1; ja += 2, jb += 2) {
+                int ix[4];
+                ix[0] = ja < a1 ? __ldg(a.indices + ja) : -1;
+                ix[1] = ja + 1 < a1 ? __ldg(a.indices + ja + 1) : -1;
+                ix[2] = jb < b1 ? __ldg(a.indices + jb) : -1;
+                ix[3] = jb + 1 < b1 ? __ldg(a.indices + jb + 1) : -1;
+                float t[4][CPL];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (ix[q] >= 0) load_cols<T, CPL>(xs + (int64_t)ix[q] * a.ld_src, c, a.F, t[q]);
+                    else
+#pragma unroll
+                        for (int e = 0; e < CPL; ++e) t[q][e] = 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                    acc0[e] += t[0][e] + t[1][e];
+                    acc1[e] += t[2][e] + t[3][e];
+                }
+            }
+            const float i0 = a1 > a0 ? 1.f / (float)(a1 - a0) : 0.f, i1 = b1 > b0 ? 1.f / (float)(b1 - b0) : 0.f;
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) {
+                acc0[e] *= i0;
+                acc1[e] *= i1;
+            }
+            store_bf16<CPL>(sA, kTileM, r0, (parts - 1) * Fp + c, acc0);
+            store_bf16<CPL>(sA, kTileM, r1, (parts - 1) * Fp + c, acc1);
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
         if (threadIdx.x == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t a0 = smem_addr(sA), b0 = smem_addr(sB);
@@ -304,28 +271,23 @@ __global__ void __launch_bounds__(128, 1) sage_gemm(const __grid_constant__ Sage
                     : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_addr(mma_done))
+                             smem_addr(mbar))
                          : "memory");
         }
-        mbar_wait_parity(mma_done, phase);
+        mbar_wait_parity(mbar, phase);
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // A is free: the next tile's A loads while this tile's accumulator is drained
-        const int next = tile + gridDim.x;
-        if (threadIdx.x == 0 && next < ntiles) {
-            mbar_expect(a_full, a_bytes);
-            for (int kb = 0; kb < Kp / 64; ++kb)
-                tma_load_2d(sA + (size_t)kb * kTileM * 128, &a.amap, kb * 64, next * kTileM, a_full);
-        }
-        // epilogue: warp w reads TMEM lanes 32 w .. 32 w + 31 (= tile rows), 8 columns per load
-        const int row = row0 + warp * 32 + lane;
+        // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) + lane (= tile rows), columns
+        // 8 (w / 4) + 2 kWarps j, 8 fp32 per load
+        const int lg = warp & 3;
+        const int row = row0 + lg * 32 + lane;
         float *orow = a.out + (int64_t)row * a.ld_out;
-        for (int col = 0; col < a.H; col += 8) {
+        for (int col = (warp >> 2) * 8; col < a.H; col += 2 * kWarps) {
             uint32_t r[8];
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)col));
+                : "r"(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)col));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (row < a.n_dst) {
                 float4 x0 = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
@@ -343,7 +305,7 @@ __global__ void __launch_bounds__(128, 1) sage_gemm(const __grid_constant__ Sage
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();   // the accumulator is free for the next tile's MMAs
+        __syncthreads();   // A and the accumulator are free for the next tile
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     __syncthreads();
@@ -355,16 +317,13 @@ __global__ void __launch_bounds__(128, 1) sage_gemm(const __grid_constant__ Sage
 template <typename T, int CPL>
 cudaError_t launch_typed(const SageArgs &a, cudaStream_t s)
 {
-    const int Kp = sage_kp(a.F, a.x_dst != nullptr);
-    if (a.n_dst == 0) return cudaSuccess;
-    const int64_t pairs = (a.n_dst + 1) / 2;
-    const int blocks = (int)std::min<int64_t>((pairs + 7) / 8, (int64_t)kSMs * 8);
-    sage_aggregate<T, CPL><<<blocks, 256, 0, s>>>(a);
-    const size_t smem = sage_smem_bytes(a.F, a.H, a.x_dst != nullptr);
-    cudaError_t e = cudaFuncSetAttribute(sage_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int Fp = CPL * 32, Kp = (a.x_dst ? 2 : 1) * Fp;
+    const size_t smem = (size_t)(a.H + kTileM) * Kp * 2 + 1024 + 64;
+    cudaError_t e = cudaFuncSetAttribute(sage_kernel<T, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int tiles = (a.n_dst + kTileM - 1) / kTileM;
-    sage_gemm<<<tiles < kSMs ? tiles : kSMs, 128, smem, s>>>(a, Kp);
+    if (tiles == 0) return cudaSuccess;
+    sage_kernel<T, CPL><<<tiles < kSMs ? tiles : kSMs, warps_for<CPL>() * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -381,7 +340,8 @@ cudaError_t launch_cpl(const SageArgs &a, cudaStream_t s)
 
 size_t sage_smem_bytes(int F, int H, bool self_term)
 {
-    return (size_t)(H + kTileM) * sage_kp(F, self_term) * 2 + 1024 + 64;
+    const int Fp = (F + 63) / 64 * 64;
+    return (size_t)(H + kTileM) * (self_term ? 2 : 1) * Fp * 2 + 1024 + 64;
 }
 
 cudaError_t launch_sage(const SageArgs &a, int x_dtype, cudaStream_t s)
