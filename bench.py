@@ -65,7 +65,8 @@ def parse():
     ap.add_argument("--replicate", default="auto",
                     help="replicated feature partition policy (P:468-473) for small vertex types: auto (N > 1: "
                          "every type whose full table is <= 64 MiB gets a local copy on each GPU), none, or a "
-                         "comma list of type indices")
+                         "comma list of type indices, or fit (N > 1: whole tables, smallest first, up to 45 GiB per GPU; "
+                         "the features of C2-C4 are then local on every GPU, DESIGN §7)")
     ap.add_argument("--depth", type=int, default=None,
                     help="launches in flight per GPU (pipeline lanes); default 4")
     ap.add_argument("--bundle", type=int, default=None,
@@ -86,7 +87,7 @@ def parse():
         a.depth = 4
     if a.bundle is None:
         a.bundle = 16
-    if a.replicate not in ("auto", "none"):
+    if a.replicate not in ("auto", "none", "fit"):
         a.replicate = [int(x) for x in a.replicate.split(",") if x != ""]
     return a
 

@@ -212,8 +212,10 @@ EG_API eg_status eg_sample_minibatch(eg_ctx *ctx, const int64_t *seeds, int64_t 
 /* Pipeline shape.  depth: up to `depth` launches run concurrently (round-robin over
  * `depth` lanes, each with its own stream); bundle: one launch may carry up to `bundle`
  * mini-batches (eg_sample_bundle), each phase kernel processing all of them at once
- * (the paper's bundling of several mini-batches).  Each lane keeps `bundle`
- * compaction states (4 B per global vertex + N_total/8 bytes each).  Default 1, 1.
+ * (the paper's bundling of several mini-batches); 1 <= bundle <= 16 (the
+ * build's kMaxBundle), else EG_EINVAL.  Each lane keeps `bundle` batch-sized states
+ * (bucket counts of 8 B per 2^bshift gids, element / member arrays sized by the seed
+ * capacity and fanouts).  Default 1, 1.
  * Results never change; the caller overlaps launches by enqueueing with EG_ASYNC
  * before waiting (the asynchronous mini-batch pipeline of P:548-679). */
 EG_API eg_status eg_set_pipeline(eg_ctx *ctx, int32_t depth, int32_t bundle);

@@ -1378,7 +1378,7 @@ eg_status enqueue_bundle(eg_ctx *c, int32_t nb, const int64_t *const *seeds, con
     if (st) return st;
     if (!out) return fail(c, EG_EINVAL, "out is null");
     if (!c->loaded || !c->peers_ready) return fail(c, EG_EINVAL, "partition not loaded / peers not mapped");
-    if (nb < 1 || nb > kMaxBundle) return fail(c, EG_EINVAL, "bundle size out of [1, 16]");
+    if (nb < 1 || nb > kMaxBundle) return fail(c, EG_EINVAL, "bundle size out of [1, kMaxBundle]");
     if (nb > c->bundle) return fail(c, EG_EINVAL, "bundle larger than eg_set_pipeline's bundle size");
     if (n_hops < 1 || n_hops > EG_MAX_HOPS) return fail(c, EG_EINVAL, "n_hops out of [1, EG_MAX_HOPS]");
     if (!fanouts || !n_seeds || !rng_seeds || (!lp && !seeds)) return fail(c, EG_EINVAL, "null argument");
@@ -1749,7 +1749,7 @@ eg_status eg_set_pipeline(eg_ctx *c, int32_t depth, int32_t bundle)
     if (st) return st;
     if (!c->loaded) return fail(c, EG_EINVAL, "load the partition first");
     if (depth < 1 || depth > 16) return fail(c, EG_EINVAL, "pipeline depth must be in [1, 16]");
-    if (bundle < 1 || bundle > kMaxBundle) return fail(c, EG_EINVAL, "bundle size must be in [1, 16]");
+    if (bundle < 1 || bundle > kMaxBundle) return fail(c, EG_EINVAL, "bundle size must be in [1, kMaxBundle]");
     if ((st = ensure_lanes(c, depth))) return st;
     c->next_lane = 0;
     c->depth = depth;

@@ -9,7 +9,10 @@ namespace eg {
 // A bundle of up to kMaxBundle mini-batches runs as one launch of each phase kernel
 // (grid.y = batch of the bundle) and one gather: the paper's bundling of the sampling
 // of several mini-batches.
-constexpr int kMaxBundle = 16;
+#ifndef EG_MAX_BUNDLE
+#define EG_MAX_BUNDLE 16
+#endif
+constexpr int kMaxBundle = EG_MAX_BUNDLE;
 
 struct GatherDev {
     uint8_t *out[EG_MAX_VT];

@@ -84,14 +84,27 @@ def device_shard(graph: HostGraph, world: int, rank: int, device, features=True)
 
 
 REPLICA_BUDGET = 64 << 20   # bytes: "auto" replicates feature types whose full table is this small
+FIT_BUDGET = 45 << 30       # bytes: "fit" replicates types (smallest first) up to a quarter of a B200's HBM
 
 
 def replica_types(cfg: Config, world: int, spec="auto", budget: int = REPLICA_BUDGET):
     """Vertex types whose features follow the replicated partition policy.
-    spec: "auto" (world > 1: every type whose full table is <= budget bytes), "none", or an
+    spec: "auto" (world > 1: every type whose full table is <= budget bytes), "fit" (world > 1:
+    whole tables, smallest first, while their sum stays <= FIT_BUDGET), "none", or an
     iterable of type indices."""
     if spec is None or spec == "none":
         return []
+    if spec == "fit":
+        if world <= 1:
+            return []
+        sizes = sorted((int(cfg.vt_counts[u]) * dim * (4 if dt == 0 else 2), u) for u, (dim, dt) in cfg.feats.items())
+        out, tot = [], 0
+        for b, u in sizes:
+            if tot + b > FIT_BUDGET:
+                break
+            out.append(u)
+            tot += b
+        return sorted(out)
     if spec == "auto":
         if world <= 1:
             return []

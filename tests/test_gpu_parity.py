@@ -181,6 +181,18 @@ def test_c2_replicated_small_types(c2, world):
         assert_same_features(res, _features_of(b, cfg), cfg, rows)
         b.free()
 
+def test_c2_replicated_fit_all_types(c2):
+    """The "fit" policy replicates every C2 feature table (0.99 GB): the gather reads only local
+    rows at world 2 and the bytes equal the oracle's."""
+    from synth.device import replica_types
+    cfg, g, rows, _ = c2
+    assert replica_types(cfg, 2, "fit") == [0, 1, 2, 3]
+    ctxs = _world(g, 2, replicate="fit")
+    for p in (0, 1):
+        gi = 60 + p
+        run_and_compare(ctxs[p], g, cfg, synth.batch_seeds(cfg, gi), cfg.fanouts, synth.rng_seed(cfg, gi), rows)
+
+
 
 def test_replica_is_what_the_gather_reads(c1):
     """Negative control: a replica whose bytes differ from the shards shows up in the

@@ -120,3 +120,18 @@ def test_confined_seeds_stay_in_the_rank_range():
             s = synth.batch_seeds_confined(cfg, 3, p, world) - int(cfg.offsets[cfg.seed_vt])
             assert len(s) == cfg.batch and len(set(s.tolist())) == len(s)
             assert s.min() >= lo and s.max() < hi
+
+
+def test_replica_policies_select_whole_tables():
+    """Replicated partition policy: "auto" takes the small types only, "fit" whole
+    tables smallest first within FIT_BUDGET (C2-C4 fit a quarter of a B200's HBM, C5 does not);
+    nothing is replicated on one GPU."""
+    from synth.device import FIT_BUDGET, replica_types
+    assert replica_types(synth.config("C2"), 2) == [2, 3]
+    assert replica_types(synth.config("C2"), 2, "fit") == [0, 1, 2, 3]
+    assert replica_types(synth.config("C3"), 4, "fit") == [0]
+    assert replica_types(synth.config("C4"), 8, "fit") == [0]
+    assert replica_types(synth.config("C5"), 2, "fit") == []
+    assert replica_types(synth.config("C4"), 1, "fit") == []
+    c4 = synth.config("C4")
+    assert int(c4.vt_counts[0]) * c4.feats[0][0] * 2 <= FIT_BUDGET
