@@ -6,10 +6,10 @@
 Workload (N=1 default): C4, the ogbn-papers100M-shaped graph (111M vertices, 1.6B
 edges, 128-d fp16) -- the largest BASELINE config that fits one B200 (C5 needs two).
 
-A step = one launch of the whole hot path over a bundle of `--bundle` (16)
+A step = one launch of the whole hot path over a bundle of `--bundle` (32)
 mini-batches per rank: sample every hop (sampling + compaction kernels) and gather
 the input vertices' feature rows, as one CUDA graph; `--depth` (4) launches are in
-flight per GPU.  So `--steps 20` times 320 mini-batches per rank, and every timed
+flight per GPU.  So `--steps 20` times 640 mini-batches per rank, and every timed
 launch carries a full bundle (steady state: the warm-up captures every lane's graph).
 Inputs (graph shard, feature shard, the seeds of every step) are resident in HBM
 before the timed region.  Each rank samples its own batches (global batch
@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--depth", type=int, default=None,
                     help="launches in flight per GPU (pipeline lanes); default 4")
     ap.add_argument("--bundle", type=int, default=None,
-                    help="mini-batches per launch (bundled kernels); default 16")
+                    help="mini-batches per launch (bundled kernels); default 32")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--diag-no-gather", action="store_true",
                     help="DIAGNOSTIC ONLY (not a bench line): sampling + compaction without the gather")
@@ -81,12 +81,12 @@ def parse():
                          "(default 8 for C4/C5, 16 otherwise; 0 = none)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     a = ap.parse_args()
-    # pipeline shape: 4 lanes x bundles of 16 (since the compaction state is
-    # batch-sized, round 2, C5 fits this shape too)
+    # pipeline shape: 4 lanes x bundles of 32 (round-2 sweep, profiles/r02/bundle32/,
+    # bundle64/: 4 x 32 is +5-10 % over 4 x 16, 4 x 64 another +2 %)
     if a.depth is None:
         a.depth = 4
-    if a.bundle is None:
-        a.bundle = 16
+    if a.bundle is None:   # C5: 4 x 32 batches of feature outputs (~84 GB) + a 98 GB shard at N = 2 exceed HBM
+        a.bundle = 16 if a.config == "C5" else 32
     if a.replicate not in ("auto", "none", "fit"):
         a.replicate = [int(x) for x in a.replicate.split(",") if x != ""]
     return a

@@ -212,7 +212,7 @@ EG_API eg_status eg_sample_minibatch(eg_ctx *ctx, const int64_t *seeds, int64_t 
 /* Pipeline shape.  depth: up to `depth` launches run concurrently (round-robin over
  * `depth` lanes, each with its own stream); bundle: one launch may carry up to `bundle`
  * mini-batches (eg_sample_bundle), each phase kernel processing all of them at once
- * (the paper's bundling of several mini-batches); 1 <= bundle <= 16 (the
+ * (the paper's bundling of several mini-batches); 1 <= bundle <= 32 (the
  * build's kMaxBundle), else EG_EINVAL.  Each lane keeps `bundle` batch-sized states
  * (bucket counts of 8 B per 2^bshift gids, element / member arrays sized by the seed
  * capacity and fanouts).  Default 1, 1.

@@ -10,7 +10,7 @@ namespace eg {
 // (grid.y = batch of the bundle) and one gather: the paper's bundling of the sampling
 // of several mini-batches.
 #ifndef EG_MAX_BUNDLE
-#define EG_MAX_BUNDLE 16
+#define EG_MAX_BUNDLE 32
 #endif
 constexpr int kMaxBundle = EG_MAX_BUNDLE;
 
