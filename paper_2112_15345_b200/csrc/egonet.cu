@@ -1590,6 +1590,21 @@ eg_status eg_sage_mean_layer(eg_ctx *c, const eg_blocks *cb, int32_t hop, int32_
     uint32_t cols = 32;
     while ((int)cols < H) cols <<= 1;
     a.tmem_cols = cols;
+    // W by the TMA when its [H][parts][F] view has 16-B strides (EG_SAGE_W_TMA=0: by the warps)
+    static const bool w_tma_env = !getenv("EG_SAGE_W_TMA") || atoi(getenv("EG_SAGE_W_TMA")) != 0;
+    a.w_tma = 0;
+    if (w_tma_env && F % 8 == 0 && ((uintptr_t)w % 16) == 0) {
+        if (EncodeTiledFn fn = encode_tiled()) {
+            const int parts = x_dst ? 2 : 1;
+            cuuint64_t dims[3] = {(cuuint64_t)F, (cuuint64_t)parts, (cuuint64_t)H};
+            cuuint64_t strides[2] = {(cuuint64_t)F * 2, (cuuint64_t)parts * F * 2};
+            cuuint32_t box[3] = {64u, 1u, (cuuint32_t)H};
+            cuuint32_t es[3] = {1u, 1u, 1u};
+            a.w_tma = fn(&a.wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(w), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+    }
     EG_CUDA(c, launch_sage(a, x_dtype, c->stream));
     ++c->launches;
     return EG_OK;

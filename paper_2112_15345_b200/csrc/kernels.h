@@ -69,6 +69,8 @@ int launch_gather(const GraphDev &g, const FeatDev &f, const GatherSet &gs, cons
 
 // sage.cu: one GraphSAGE-mean layer over a block relation on the tensor cores (NEXT-4 i).
 struct SageArgs {
+    CUtensorMap wmap;           // W as a [H][parts][F] bf16 view (3-D, SWIZZLE_128B boxes {64, 1, H}), if w_tma
+    int32_t w_tma;              // 1: W staged by the TMA (F % 8 == 0); 0: by the warps
     const int32_t *indptr;      // block CSC over the dst vertices (n_dst + 1)
     const int32_t *indices;     // local src ids
     const void *x_src;          // [n_src][ld_src] input rows of the relation's src nodes

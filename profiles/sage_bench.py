@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--hidden", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--batches", type=int, default=8, help="mini-batches whose input layers are timed")
+    ap.add_argument("--trace", action="store_true",
+                    help="with an EG_SAGE_TRACE build: print the phase stamps of CTAs 0 / 100 of the last call")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -66,6 +68,11 @@ def main():
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(e) / 1e3)
         sec = float(np.median(ts))
+        if args.trace:
+            st = out[:2, :20].contiguous().view(torch.int64).cpu().numpy()
+            for cta, row in zip((0, 100), st):
+                d = (row - row[0]) / 1e3
+                print(json.dumps({"trace_cta": cta, "us": [round(float(x), 2) for x in d]}), file=sys.stderr)
         esz = xs.element_size()
         alg = nnz * F * esz + n_dst * F * esz + n_dst * H * 4 + nnz * 4 + (n_dst + 1) * 4
         flops = 2 * ((n_dst + 127) // 128 * 128) * H * 2 * ((F + 63) // 64 * 64)
