@@ -370,6 +370,22 @@ __global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __
     const T *xd = static_cast<const T *>(a.x_dst);
     uint32_t phase = 0;
 
+    // the row bounds and the first 32 edge indices of this warp's rows in the NEXT tile are
+    // loaded while the current tile finishes (its MMA and epilogue), which takes two of the
+    // A build's dependent memory round trips off every tile but the first
+    const int c = lane * CPL;
+    const int rbase = warp * R;
+    auto load_bounds = [&](int t) {
+        int v = 0;
+        if (lane <= R && t * kTileM < a.n_dst) v = __ldg(a.indptr + min(t * kTileM + rbase + lane, a.n_dst));
+        return v;
+    };
+    auto load_first_idx = [&](int bounds) {
+        const int b0 = __shfl_sync(0xffffffffu, bounds, 0), b1 = __shfl_sync(0xffffffffu, bounds, R);
+        return lane < min(32, b1 - b0) ? __ldg(a.indices + b0 + lane) : 0;
+    };
+    int pv_next = load_bounds(blockIdx.x);
+    int idx_next = load_first_idx(pv_next);
     for (int tile = blockIdx.x; tile * kTileM < a.n_dst; tile += gridDim.x) {
         const int row0 = tile * kTileM;
         ++tile_no;
@@ -379,10 +395,8 @@ __global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __
         // of S = 32 / NW edges with every load of a group in flight before the first is
         // summed (round 2: the round-1 build issued index -> row chains for 4 rows at a time,
         // ~14 dependent memory round trips per tile; this one needs ~4).
-        const int c = lane * CPL;
-        const int rbase = warp * R;
-        int pv = 0;
-        if (lane <= R) pv = __ldg(a.indptr + min(row0 + rbase + lane, a.n_dst));
+        const int pv = pv_next, idx0 = idx_next;
+        pv_next = load_bounds(tile + gridDim.x);
         const int e0 = __shfl_sync(0xffffffffu, pv, 0), e1 = __shfl_sync(0xffffffffu, pv, R);
         if (xd) {
             uint32_t sr[R][NW];
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __
             };
             for (int base = e0; base < e1; base += 32) {
                 const int ne = min(32, e1 - base);
-                const int myidx = lane < ne ? __ldg(a.indices + base + lane) : 0;
+                const int myidx = base == e0 ? idx0 : (lane < ne ? __ldg(a.indices + base + lane) : 0);
                 for (int s0 = 0; s0 < ne; s0 += S) {
                     uint32_t raw[S][NW];
 #pragma unroll
@@ -442,6 +456,7 @@ __global__ void __launch_bounds__(warps_for<CPL>() * 32, 1) sage_kernel(const __
             }
             while (cur < R) flush();
         }
+        idx_next = load_first_idx(pv_next);
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
