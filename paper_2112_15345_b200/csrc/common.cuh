@@ -32,8 +32,9 @@ namespace eg {
 constexpr int kWarp = 32;
 constexpr int kSMs = 148;                 // B200
 // Compaction buckets (compact.cuh): each vertex type's id range is cut into fine buckets of
-// 2^bshift consecutive gids, bshift in [kMinBucketShift, kMaxBucketShift] chosen at load so
-// that a graph has at most ~2^16 buckets (C4: 2^11 gids, 54k buckets).  A bucket's bitmap is
+// 2^bshift consecutive gids, bshift in [12, kMaxBucketShift] chosen at load so that a graph
+// has at most ~2^14 buckets (C4: 2^13 gids, 13.6k buckets; kMinBucketShift is the smallest an
+// A/B override may set).  A bucket's bitmap is
 // 2^bshift / 32 words, at most 8 per lane of a warp.
 constexpr int kMinBucketShift = 10;
 constexpr int kMaxBucketShift = 13;

@@ -643,9 +643,18 @@ eg_status eg_load_partition(eg_ctx *c, int32_t n_vt, const int64_t *vt_counts, c
             if (g.bounds[t][p + 1] < g.bounds[t][p]) return fail(c, EG_EINVAL, "bounds must be non-decreasing");
     }
     // compaction buckets (compact.cuh): type-aligned ranges of 2^bshift gids, bshift the
-    // smallest in [kMinBucketShift, kMaxBucketShift] that keeps the graph's buckets <= 2^16
-    g.bshift = kMinBucketShift;
-    while (g.bshift < kMaxBucketShift && (c->n_total >> g.bshift) > (1 << 16)) ++g.bshift;
+    // smallest in [12, kMaxBucketShift] (graphs under 2^20 vertices: from kMinBucketShift) that
+    // keeps the graph's buckets <= 2^14 (C4: 2^13 gids per bucket, 13.6k buckets; C2 / C3:
+    // 2^12; C1: 2^10).  Measured against the first rule (<= 2^16 buckets from 2^10: C4 2^11,
+    // C2 / C3 2^10): the bucket scans halve, C4 +4.7 %, C2 +3.0 %, C3 +1.2 %; C1 prefers 2^10
+    // (profiles/r02/bshift/).  EG_BSHIFT (A/B runs) sets it in [kMinBucketShift,
+    // kMaxBucketShift]; results never depend on it.
+    g.bshift = c->n_total >= (1ll << 20) ? 12 : kMinBucketShift;
+    while (g.bshift < kMaxBucketShift && (c->n_total >> g.bshift) > (1 << 14)) ++g.bshift;
+    if (const char *e = getenv("EG_BSHIFT")) {
+        const int v = atoi(e);
+        if (v >= kMinBucketShift && v <= kMaxBucketShift) g.bshift = v;
+    }
     g.bbase[0] = 0;
     for (int t = 0; t < n_vt; ++t) g.bbase[t + 1] = g.bbase[t] + ((vt_counts[t] + (1ll << g.bshift) - 1) >> g.bshift);
     if (g.bbase[n_vt] > kMaxBuckets) return fail(c, EG_EINVAL, "too many vertices for the compaction buckets");

@@ -414,6 +414,30 @@ def test_compaction_variant_forced(c1, c2, mode, monkeypatch):
         ctx.close()
 
 
+@pytest.mark.parametrize("bshift", ["10", "11", "13"])
+def test_bucket_width_override(c1, c2, bshift, monkeypatch):
+    """Compaction bucket widths other than the load-time rule's (C1 2^10, C2 2^12): narrow
+    buckets (many per type, most tasks on the sort path) and wide ones (2^13, more big buckets
+    on the bitmap path) give the oracle's blocks, alone and in a bundle of 3 (EG_BSHIFT)."""
+    import torch
+    monkeypatch.setenv("EG_BSHIFT", bshift)   # read at eg_load_partition
+    for cfg, g, rows, _ in (c1, c2):
+        ctx = _ctx(g)
+        for gi in (0, 1):
+            run_and_compare(ctx, g, cfg, synth.batch_seeds(cfg, 120 + gi), cfg.fanouts, synth.rng_seed(cfg, 120 + gi),
+                            rows, check_invariants=(gi == 0))
+        ctx.set_pipeline(1, 4)
+        idx = [130, 131, 132]
+        dev = [torch.from_numpy(synth.batch_seeds(cfg, i)).cuda() for i in idx]
+        bls = ctx.sample_bundle(dev, cfg.fanouts, [synth.rng_seed(cfg, i) for i in idx], features=True)
+        for i, b in zip(idx, bls):
+            res = oracle.sample(g, synth.batch_seeds(cfg, i), cfg.fanouts, synth.rng_seed(cfg, i))
+            assert_same_batch(res, b, cfg.n_vt, cfg.n_rel)
+            assert_same_features(res, _features_of(b, cfg), cfg, rows)
+            b.free()
+        ctx.close()
+
+
 # ----------------------------------------------------------------------------- planted communities (NEXT-2)
 
 def test_c1l_planted_world2_confined_seeds():
