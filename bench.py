@@ -742,6 +742,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                                 "after the timed region, equal the oracle's element by element (node lists, block "
                                 "CSCs, eids, feature bytes)" % parity) if parity else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                # lanes co-running (nsys is not in the image): the device time of one launch
+                # (its sampling + compaction nodes and its gather node, CUDA events recorded
+                # inside the launch's graph) against the step period
+                "overlap": {"launch_device_ms": sample_ms + gather_ms, "ms_per_step": ms / K,
+                            "launches_in_flight_avg": (sample_ms + gather_ms) / (ms / K) if ms > 0 else None,
+                            "gather_busy_frac": gather_ms / (ms / K) if ms > 0 else None,
+                            "source": "CUDA events inside each launch's graph (rank 0)"},
                 "clocks": clk, "load_seconds": t_load, "stage_us": trace or None,
                 "pipeline_depth": args.depth, "bundle": B, "host_us_per_batch": host_us,
                 "host": {"cores": host_cores(), "cpu": cpu_model()}}
