@@ -9,3 +9,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file $D/launches_default.csv python bench.py --no-cpu-baseline > $D/ncu_list.log 2>&1; echo ncu=$?
 python profiles/launch_table.py $D/launches_default.csv > $D/launches_default_table.txt 2>&1
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 --out $D/reference.json > $D/reference.out 2> $D/reference.err; echo ref=$?
+EG_LIB=$PWD/paper_2112_15345_b200/libegonet_check.so timeout 1800 python -m pytest tests -m gpu -q --timeout 300 \
+    > $D/pytest_gpu_checked.log 2>&1; echo checked=$?; tail -1 $D/pytest_gpu_checked.log
