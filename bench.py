@@ -148,8 +148,10 @@ def workload(cfg, world, task="nc"):
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region.
 
-    NVML polled every 5 ms from a thread (the timed region of a default run is tens of
-    ms, too short for nvidia-smi's loop); nvidia-smi -lms 50 when NVML is unavailable."""
+    NVML polled every millisecond from a thread (the timed region of a default run is
+    tens of ms, too short for nvidia-smi's loop); nvidia-smi -lms 50 when NVML is
+    unavailable."""
+    POLL_S = 0.001
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -191,7 +193,7 @@ class ClockSampler:
                         self.samples.append((sm, rs))
                     except Exception:
                         pass
-                    time.sleep(0.005)
+                    time.sleep(self.POLL_S)
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
             return
@@ -218,7 +220,7 @@ class ClockSampler:
                 return None
             reasons = sorted({n for _, rs in self.samples for n, b in self.BITS.items() if rs & b})
             return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                    "reasons": reasons, "samples": len(self.samples), "source": "NVML, 5 ms polling"}
+                    "reasons": reasons, "samples": len(self.samples), "source": "NVML, 1 ms polling"}
         if not self.proc:
             return None
         time.sleep(0.1)
