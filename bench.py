@@ -614,6 +614,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             ems, e_edges = float(m[0]), float(t[1])
         e2e = {"value": e_edges / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
                "d2h_bytes_per_step": d2h // K,
+               # the bound: one GPU's PCIe link (D2H of the gathered rows, ~55-57 GB/s on Gen5 x16)
+               "d2h_GBps_per_gpu": (d2h / K) / (ems / K / 1e3) / 1e9 if ems > 0 else None,
                "note": "per step (one launch of %d mini-batches): seeds from pinned host memory in (read in place "
                        "by the seed split over PCIe), gathered feature rows out to pinned host memory (D2H), "
                        "per-batch counters read back; blocks stay device-resident" % B}
