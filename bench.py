@@ -8,7 +8,7 @@ edges, 128-d fp16) -- the largest BASELINE config that fits one B200 (C5 needs t
 
 A step = one launch of the whole hot path over a bundle of `--bundle` (32)
 mini-batches per rank: sample every hop (sampling + compaction kernels) and gather
-the input vertices' feature rows, as one CUDA graph; `--depth` (4) launches are in
+the input vertices' feature rows, as one CUDA graph; `--depth` (6) launches are in
 flight per GPU.  So `--steps 20` times 640 mini-batches per rank, and every timed
 launch carries a full bundle (steady state: the warm-up captures every lane's graph).
 Inputs (graph shard, feature shard, the seeds of every step) are resident in HBM
@@ -68,7 +68,7 @@ def parse():
                          "comma list of type indices, or fit (N > 1: whole tables, smallest first, up to 45 GiB per GPU; "
                          "the features of C2-C4 are then local on every GPU, DESIGN §7)")
     ap.add_argument("--depth", type=int, default=None,
-                    help="launches in flight per GPU (pipeline lanes); default 4")
+                    help="launches in flight per GPU (pipeline lanes); default 6 (C5: 4)")
     ap.add_argument("--bundle", type=int, default=None,
                     help="mini-batches per launch (bundled kernels); default 32")
     ap.add_argument("--no-e2e", action="store_true")
@@ -83,8 +83,8 @@ def parse():
     a = ap.parse_args()
     # pipeline shape: 4 lanes x bundles of 32 (round-2 sweep, profiles/r02/bundle32/,
     # bundle64/: 4 x 32 is +5-10 % over 4 x 16, 4 x 64 another +2 %)
-    if a.depth is None:
-        a.depth = 4
+    if a.depth is None:   # 6 lanes hide the peer (NVLink) latency at N > 1: C4 +5 % at N = 2, +2 % at N = 4,
+        a.depth = 4 if a.config == "C5" else 6   # ~+1 % at N = 1 (profiles/r02/depth/, knobs/); C5: memory
     if a.bundle is None:   # C5: 4 x 32 batches of feature outputs (~84 GB) + a 98 GB shard at N = 2 exceed HBM
         a.bundle = 16 if a.config == "C5" else 32
     if a.replicate not in ("auto", "none", "fit"):

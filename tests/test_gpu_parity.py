@@ -355,7 +355,7 @@ def test_c2_pipeline_depth4_concurrent_lanes(c2):
 # ----------------------------------------------------------------------------- the bench's launch configuration
 
 @pytest.mark.parametrize("name", ["C2", "C4"])
-@pytest.mark.parametrize("depth,bundle", [(4, 8), (4, 16), (4, 32)])
+@pytest.mark.parametrize("depth,bundle", [(4, 8), (4, 32), (6, 32)])
 def test_bench_launch_configuration(name, depth, bundle):
     """Exactly what bench.py times: `depth` lanes x bundles of `bundle`, async, `depth`
     launches in flight; batches g = 0..depth*bundle-1 as the bench draws them (rank 0 of
