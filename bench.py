@@ -68,7 +68,7 @@ def parse():
                          "comma list of type indices, or fit (N > 1: whole tables, smallest first, up to 45 GiB per GPU; "
                          "the features of C2-C4 are then local on every GPU, DESIGN §7)")
     ap.add_argument("--depth", type=int, default=None,
-                    help="launches in flight per GPU (pipeline lanes); default 6 (C5: 4)")
+                    help="launches in flight per GPU (pipeline lanes); default 6 (C5 and --task lp: 4)")
     ap.add_argument("--bundle", type=int, default=None,
                     help="mini-batches per launch (bundled kernels); default 32")
     ap.add_argument("--no-e2e", action="store_true")
@@ -84,7 +84,9 @@ def parse():
     # pipeline shape: 4 lanes x bundles of 32 (round-2 sweep, profiles/r02/bundle32/,
     # bundle64/: 4 x 32 is +5-10 % over 4 x 16, 4 x 64 another +2 %)
     if a.depth is None:   # 6 lanes hide the peer (NVLink) latency at N > 1: C4 +5 % at N = 2, +2 % at N = 4,
-        a.depth = 4 if a.config == "C5" else 6   # ~+1 % at N = 1 (profiles/r02/depth/, knobs/); C5: memory
+        # ~+1 % at N = 1 (profiles/r02/depth/, knobs/).  C5 and link-prediction batches keep 4: their
+        # worst-case slot sizes (C2 LP: fanout [25, 15] over 3 seeds per positive) exhaust HBM at 6 x 32
+        a.depth = 4 if (a.config == "C5" or a.task == "lp") else 6
     if a.bundle is None:   # C5: 4 x 32 batches of feature outputs (~84 GB) + a 98 GB shard at N = 2 exceed HBM
         a.bundle = 16 if a.config == "C5" else 32
     if a.replicate not in ("auto", "none", "fit"):
